@@ -1,0 +1,177 @@
+/*
+ * kiops.h -- C ABI of the B200-native KIOPS hot path (fp64, one GPU, sm_100a).
+ *
+ * Computes, for every requested output time T_l (KIOPS, Gaudreault, Rainwater &
+ * Tokman, JCP 2018 = arXiv 1804.05126; P:n = line n of the paper text):
+ *
+ *     w_l = sum_{k=0..p} T_l^k phi_k(T_l A) u_k             Eq. 12, Alg. 1
+ *
+ * through the exponential of the augmented matrix A~ = [[A, B],[0, K]],
+ * B = [u_p, ..., u_1] (Theorem 1), with adaptive substepping (Eqs. 23-28),
+ * the incomplete orthogonalisation procedure of window q (Alg. 2), the
+ * projected exponential exp(tau H~) (Eqs. 33, 37-38), the error estimate
+ * and acceptance test (Eqs. 36, 39), the adaptivity of Alg. 4 and the
+ * output update of Alg. 3.  Readings of silent or garbled passages:
+ * DESIGN.md section 3 (R1-R27).
+ *
+ * Every step runs on the device: after kiops_apply's single host->device copy of
+ * its call block, one CUDA-graph launch (device-side WHILE/IF conditional nodes)
+ * runs the whole adaptive loop; one device->host copy returns the statistics.
+ *
+ * Conventions for every entry point:
+ *  - No C++ exceptions cross the ABI; every call returns a kiops_status.
+ *  - "DEVICE" pointers are CUDA global-memory pointers on the ctx's device;
+ *    "HOST" pointers are ordinary (or pinned) host memory.
+ *  - Borrowed pointers are never freed by the library and must outlive their use.
+ *  - A ctx serves one kiops_apply at a time (single owner, not thread-safe).
+ *    Distinct ctxs may run concurrently on distinct streams.
+ */
+#ifndef KIOPS_H
+#define KIOPS_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define KIOPS_MAX_P 8        /* maximum number of phi terms beyond phi_0 (p)            */
+#define KIOPS_MAX_OUT 64     /* maximum number of output times per call                 */
+#define KIOPS_MAX_M 128      /* maximum Krylov dimension m_max (exp of <= 129^2 on one CTA) */
+#define KIOPS_MAX_FORCED 256 /* maximum length of a forced (test) schedule               */
+#define KIOPS_TRACE_CAP 16384
+
+typedef struct kiops_ctx_s *kiops_ctx; /* opaque; created by kiops_create */
+
+typedef enum {
+  KIOPS_OK = 0,
+  KIOPS_ERR_INVALID_ARG = 1,    /* argument outside the domain of R21; nothing launched     */
+  KIOPS_ERR_UNSUPPORTED = 2,    /* valid for the method, not implemented here (e.g. q != 2) */
+  KIOPS_ERR_CUDA = 3,           /* a CUDA call failed; text in kiops_last_error             */
+  KIOPS_ERR_NO_CONVERGENCE = 4, /* > max_attempts attempts (R22); stats filled, w undefined */
+  KIOPS_ERR_NONFINITE = 5,      /* NaN/Inf in a reduced dot, beta, H, eps or omega (R22)    */
+  KIOPS_ERR_WORKSPACE = 6       /* workspace pointer NULL, misaligned or too small          */
+} kiops_status;
+
+typedef enum {
+  KIOPS_OP_STENCIL1D3 = 1,          /* periodic 1D 3-point: (Ax)_i = W x_{i-1} + C x_i + E x_{i+1} + d_i x_i */
+  KIOPS_OP_STENCIL2D5 = 2,          /* periodic 2D 5-point: W x_{i-1,j} + E x_{i+1,j} + S x_{i,j-1} + N x_{i,j+1} + (C + d_ij) x_ij */
+  KIOPS_OP_STENCIL3D7_VARKAPPA = 3, /* periodic 3D 7-point: sum_faces (kappa_i + kappa_nb)/2 (x_nb - x_i) inv_h2 */
+  KIOPS_OP_CSR = 4                  /* general CSR: int64 row_ptr[N+1], int32 col_idx[nnz], fp64 vals[nnz] */
+} kiops_op_kind;
+
+/* Operator A ("the action of the matrix A ... provided by an external
+ * subroutine"; here built-in kinds).  Vectors are lexicographic, x fastest:
+ * i = x + nx*(y + ny*z).  All array pointers are DEVICE, borrowed, and must
+ * outlive the ctx. */
+typedef struct {
+  int32_t kind;           /* kiops_op_kind                                             */
+  int32_t periodic;       /* stencils: must be 1 (periodic wrap)                       */
+  int64_t nx, ny, nz;     /* grid; N = nx*ny*nz.  1D: ny = nz = 1; 2D: nz = 1; CSR: nx = N */
+  double w[5];            /* 1D: {W, C, E}; 2D: {W, E, S, N, C}; unused for 3D and CSR  */
+  const double *diag;     /* optional additive diagonal d (length N) for 1D/2D, or NULL */
+  const double *kappa;    /* 3D: cell conductivity (length N)                          */
+  double inv_h2;          /* 3D: 1/h^2                                                 */
+  const int64_t *row_ptr; /* CSR                                                       */
+  const int32_t *col_idx; /* CSR                                                       */
+  const double *vals;     /* CSR                                                       */
+  int64_t nnz;            /* CSR                                                       */
+} kiops_operator_desc;
+
+/* Alg. 1 inputs plus the IOP window.  Defaults (kiops_options_default):
+ * tol 1e-7, m_init 10, m_min 10, m_max 128, iop_q 2, task1 0, max_attempts 10000,
+ * host_staging 0, max_outputs 4. */
+typedef struct {
+  double tol;             /* Eq. 39 tolerance (absolute, 2-norm of the scaled augmented vector, R18) */
+  int32_t m_init, m_min, m_max; /* 1 <= m_min <= m_max <= KIOPS_MAX_M                   */
+  int32_t iop_q;          /* IOP window; this build supports 2 (Alg. 2 as printed)       */
+  int32_t task1;          /* 1 => output l scaled by 1/T_l^p (Alg. 1 l.31-35) */
+  int64_t max_attempts;   /* accepted + rejected attempts before KIOPS_ERR_NO_CONVERGENCE */
+  int32_t host_staging;   /* 1 => workspace also holds device staging for kiops_apply_host */
+  int32_t max_outputs;    /* largest n_out kiops_apply_host will be called with (staging)  */
+} kiops_options;
+
+/* Statistics of one kiops_apply. */
+typedef struct {
+  int64_t substeps;       /* accepted substeps                                         */
+  int64_t rejections;     /* rejected attempts                                         */
+  int64_t krylov_vectors; /* Alg. 2 iterations (augmented matvecs of the method)       */
+  int64_t expm_calls;     /* dense exponentials (F of Alg. 1 l.18 and F2 of Alg. 3 l.14) */
+  int64_t passes;         /* fused device passes launched (krylov_vectors + one look-ahead per basis) */
+  int32_t final_m;        /* m after the last Alg. 4 update (R25): warm start for the next call */
+  int32_t happy_breakdowns;
+  double t_reached;       /* T_end on success                                          */
+  double nu, mu;          /* Eqs. 48-49 normalisation constants used                    */
+} kiops_stats;
+
+/* One row per attempt (accepted or rejected), for oracle <-> GPU trace parity. */
+typedef struct {
+  int64_t attempt;
+  int32_t j, happy, accept, m_new;
+  double t_now, tau, beta, h_next, eps, omega, tau_new;
+} kiops_trace_row;
+
+/* Fills *o with the defaults above.  o: HOST, non-NULL. */
+void kiops_options_default(kiops_options *o);
+
+/* Bytes of DEVICE workspace kiops_create needs for this operator, p and options.
+ * Returns KIOPS_ERR_INVALID_ARG / KIOPS_ERR_UNSUPPORTED like kiops_create would. */
+kiops_status kiops_workspace_bytes(const kiops_operator_desc *op, int p, const kiops_options *o,
+                                   size_t *bytes);
+
+/* Creates a context: validates op, p and o (R21), carves the caller-owned DEVICE
+ * workspace (>= kiops_workspace_bytes, 256-byte aligned; the library never calls
+ * cudaMalloc for it) and instantiates the CUDA graph on `cuda_stream` (a
+ * cudaStream_t; NULL = legacy default stream).  The ctx keeps op's arrays
+ * borrowed.  On error *out is NULL. */
+kiops_status kiops_create(const kiops_operator_desc *op, int p, const kiops_options *o,
+                          void *cuda_stream, void *workspace, size_t workspace_bytes,
+                          kiops_ctx *out);
+
+/* Runs Alg. 1 on the ctx stream and returns after one stream synchronisation.
+ *  u:      HOST array of p+1 DEVICE pointers u_0..u_p (N doubles each; u_0 may be
+ *          all zeros).  u[k] multiplies T^k phi_k (Eq. 12).
+ *  tau_out: HOST array of n_out output times, 0 < T_1 < ... < T_n (R21).
+ *  w:      HOST array of n_out DEVICE pointers (N doubles each), written with
+ *          w(T_l); must not alias any u[k] or each other.
+ *  stats:  HOST, nullable.
+ * Errors: INVALID_ARG (bad times, n_out outside 1..KIOPS_MAX_OUT, NULL pointers),
+ * NO_CONVERGENCE / NONFINITE (stats filled, w undefined), CUDA. */
+kiops_status kiops_apply(kiops_ctx c, const double *const *u, const double *tau_out, int n_out,
+                         double *const *w, kiops_stats *stats);
+
+/* Same computation from HOST vectors: u is a HOST array of p+1 HOST pointers, w a
+ * HOST array of n_out HOST pointers.  Needs options.host_staging = 1 and
+ * n_out <= options.max_outputs at create.  The host<->device copies are part of
+ * the call (cudaMemcpyAsync on the ctx stream; pinned host memory is fastest). */
+kiops_status kiops_apply_host(kiops_ctx c, const double *const *u, const double *tau_out, int n_out,
+                              double *const *w, kiops_stats *stats);
+
+/* Copies the decision trace of the last apply (one kiops_trace_row per attempt,
+ * at most KIOPS_TRACE_CAP) into host_buf (HOST, `bytes` long); *rows = rows
+ * available (may exceed what fit). */
+kiops_status kiops_get_trace(kiops_ctx c, void *host_buf, size_t bytes, int64_t *rows);
+
+/* TEST HOOK (not for users): force the next applies to run attempt i with
+ * (tau[i], m[i]) and accept it, bypassing Alg. 4 (n = 0 clears).  tau, m: HOST,
+ * n <= KIOPS_MAX_FORCED.  Used for step-level parity and the semigroup pin. */
+kiops_status kiops_set_forced_schedule(kiops_ctx c, const double *tau, const int32_t *m, int n);
+
+/* TEST HOOK: copies the projected matrix H (column-major, leading dimension
+ * m_max+2, H(i,j) 1-based at h[(i-1) + (j-1)*(m_max+2)]) and the norms
+ * sigma_k = ||x_k|| of the unnormalised basis vectors of the current substep.
+ * h: HOST (m_max+2)^2 doubles; sig: HOST m_max+2 doubles (sig[k-1] = sigma_k);
+ * *npass: number of basis vectors formed in the current substep. */
+kiops_status kiops_debug_basis(kiops_ctx c, double *h, double *sig, int32_t *npass);
+
+/* Destroys the ctx (graph, host state).  The workspace stays owned by the caller. */
+kiops_status kiops_destroy(kiops_ctx c);
+
+/* Static strings; never NULL. */
+const char *kiops_status_string(kiops_status s);
+const char *kiops_last_error(kiops_ctx c);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,521 @@
+// controller.cuh -- SURVEY 8(a) rows a5-a8: the single-CTA controller kernel
+// (projected exponential, error estimate, acceptance, Alg. 4 adaptivity, Alg. 3
+// output bookkeeping) and the multi-RHS GEMV over the basis.  sm_100a, fp64.
+#pragma once
+#include "kiops_internal.cuh"
+#include "passes.cuh"
+
+#define CTRL_THREADS 512
+#define MM_KP 8  // k-panel depth of the CTA matmul
+
+// ---------------------------------------------------------------------------
+// Dense n x n (n <= KMAXM+1) helpers for ONE CTA.  Matrices are column-major with
+// leading dimension LDH in global scratch (L2-resident); shared memory holds the
+// matmul panels and, during the solve, the coefficient matrix.
+// ---------------------------------------------------------------------------
+__device__ void cta_matmul(int n, const double *__restrict__ A, const double *__restrict__ B,
+                           double *__restrict__ C, double *sm) {
+  // C = A B (C must not alias A or B).  4x4 register micro-tiles, KP-deep smem panels.
+  const int np = (n + 3) & ~3, tr = np >> 2, ntiles = tr * tr;
+  double *sA = sm;             // np x KP   sA[i + np*kk]
+  double *sB = sm + np * MM_KP; // KP x np  sB[kk + KP*j]
+  for (int t0 = 0; t0 < ntiles; t0 += blockDim.x) {
+    const int t = t0 + threadIdx.x;
+    const bool act = t < ntiles;
+    const int ti = (t % tr) * 4, tj = (t / tr) * 4;
+    double acc[4][4];
+#pragma unroll
+    for (int a = 0; a < 4; a++)
+#pragma unroll
+      for (int b = 0; b < 4; b++) acc[a][b] = 0.0;
+    for (int k0 = 0; k0 < n; k0 += MM_KP) {
+      __syncthreads();
+      for (int e = threadIdx.x; e < np * MM_KP; e += blockDim.x) {
+        const int i = e % np, kk = e / np;
+        sA[e] = (i < n && k0 + kk < n) ? A[i + (size_t)LDH * (k0 + kk)] : 0.0;
+      }
+      for (int e = threadIdx.x; e < np * MM_KP; e += blockDim.x) {
+        const int kk = e % MM_KP, j = e / MM_KP;
+        sB[e] = (j < n && k0 + kk < n) ? B[(k0 + kk) + (size_t)LDH * j] : 0.0;
+      }
+      __syncthreads();
+      if (act) {
+#pragma unroll
+        for (int kk = 0; kk < MM_KP; kk++) {
+          double a[4], b[4];
+#pragma unroll
+          for (int q = 0; q < 4; q++) { a[q] = sA[ti + q + np * kk]; b[q] = sB[kk + MM_KP * (tj + q)]; }
+#pragma unroll
+          for (int x = 0; x < 4; x++)
+#pragma unroll
+            for (int y = 0; y < 4; y++) acc[x][y] = fma(a[x], b[y], acc[x][y]);
+        }
+      }
+    }
+    if (act)
+#pragma unroll
+      for (int x = 0; x < 4; x++)
+#pragma unroll
+        for (int y = 0; y < 4; y++)
+          if (ti + x < n && tj + y < n) C[(ti + x) + (size_t)LDH * (tj + y)] = acc[x][y];
+  }
+  __syncthreads();
+}
+
+__device__ double cta_norm1(int n, const double *A, double *red) {
+  // max column abs sum, broadcast to all threads
+  double best = 0.0;
+  for (int j = threadIdx.x; j < n; j += blockDim.x) {
+    double s = 0.0;
+    for (int i = 0; i < n; i++) s += fabs(A[i + (size_t)LDH * j]);
+    best = (s > best || s != s) ? s : best;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const double x = __shfl_xor_sync(0xffffffffu, best, o);
+    best = (x > best || x != x) ? x : best;
+  }
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = best;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double b = 0.0;
+    for (int w = 0; w < (int)((blockDim.x + 31) >> 5); w++) b = (red[w] > b || red[w] != red[w]) ? red[w] : b;
+    red[32] = b;
+  }
+  __syncthreads();
+  const double r = red[32];
+  __syncthreads();
+  return r;
+}
+
+// Solve Q X = R in place (R <- X) by Gaussian elimination with partial pivoting
+// (first maximal |pivot|) applied to the right-hand sides, then back
+// substitution.  Q is copied to shared memory; R stays in global scratch.
+// Returns 0, or -1 for a zero pivot (all threads).
+__device__ int cta_solve(int n, const double *Qg, double *R, double *sm) {
+  double *sQ = sm;  // n x n, ld = n
+  __shared__ int s_piv;
+  __shared__ int s_bad;
+  for (int e = threadIdx.x; e < n * n; e += blockDim.x) sQ[e] = Qg[(e % n) + (size_t)LDH * (e / n)];
+  if (threadIdx.x == 0) s_bad = 0;
+  __syncthreads();
+  for (int k = 0; k < n; k++) {
+    if (threadIdx.x < 32) {
+      double best = -1.0;
+      int bi = n;
+      for (int r = k + threadIdx.x; r < n; r += 32) {
+        const double a = fabs(sQ[r + n * k]);
+        if (a > best) { best = a; bi = r; }
+      }
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+      }
+      if (threadIdx.x == 0) {
+        s_piv = bi;
+        if (!(best > 0.0)) s_bad = 1;
+      }
+    }
+    __syncthreads();
+    if (s_bad) return -1;
+    const int pv = s_piv;
+    if (pv != k) {
+      for (int c = threadIdx.x; c < n; c += blockDim.x) {
+        double t = sQ[k + n * c]; sQ[k + n * c] = sQ[pv + n * c]; sQ[pv + n * c] = t;
+        t = R[k + (size_t)LDH * c]; R[k + (size_t)LDH * c] = R[pv + (size_t)LDH * c]; R[pv + (size_t)LDH * c] = t;
+      }
+      __syncthreads();
+    }
+    const double piv = sQ[k + n * k];
+    for (int r = k + 1 + threadIdx.x; r < n; r += blockDim.x) sQ[r + n * k] = sQ[r + n * k] / piv;
+    __syncthreads();
+    const int rows = n - k - 1;
+    if (rows > 0) {
+      // trailing update of Q (columns > k) and of every RHS column
+      const int tot = rows * (n - k - 1 + n);
+      for (int e = threadIdx.x; e < tot; e += blockDim.x) {
+        const int r = k + 1 + e % rows, cc = e / rows;
+        const double f = sQ[r + n * k];
+        if (cc < n - k - 1) {
+          const int c = k + 1 + cc;
+          sQ[r + n * c] -= f * sQ[k + n * c];
+        } else {
+          const int c = cc - (n - k - 1);
+          R[r + (size_t)LDH * c] -= f * R[k + (size_t)LDH * c];
+        }
+      }
+    }
+    __syncthreads();
+  }
+  for (int k = n - 1; k >= 0; k--) {
+    const double d = sQ[k + n * k];
+    for (int c = threadIdx.x; c < n; c += blockDim.x) R[k + (size_t)LDH * c] = R[k + (size_t)LDH * c] / d;
+    __syncthreads();
+    const int tot = k * n;
+    for (int e = threadIdx.x; e < tot; e += blockDim.x) {
+      const int r = e % k, c = e / k;
+      R[r + (size_t)LDH * c] -= sQ[r + n * k] * R[k + (size_t)LDH * c];
+    }
+    __syncthreads();
+  }
+  return 0;
+}
+
+// F = exp(scale * M) for n <= KMAXM+1: diagonal Pade approximant with scaling and
+// squaring ("[47]" = Higham 2005, Algorithm 2.3; R17).  Degree cascade
+// {3,5,7,9,13} by the 1-norm thresholds theta_m of Higham's Table 2.3; above
+// theta_13, X is scaled by 2^-s and squared back s times.  Returns the number of
+// dense products (or -1 on a zero pivot / non-finite norm).
+__device__ int cta_expm(int n, const double *M, double scale, double *F, double *scr, double *sm) {
+  double *X = scr + 0 * (size_t)LDH * LDH, *X2 = scr + 1 * (size_t)LDH * LDH, *X4 = scr + 2 * (size_t)LDH * LDH,
+         *X6 = scr + 3 * (size_t)LDH * LDH, *X8 = scr + 4 * (size_t)LDH * LDH, *U = scr + 5 * (size_t)LDH * LDH,
+         *V = scr + 6 * (size_t)LDH * LDH, *T = scr + 7 * (size_t)LDH * LDH;
+  // [m/m] Pade numerator coefficients p_m(x) = sum b_j x^j, b_j proportional to
+  // (2m-j)! m! / ((2m)! j! (m-j)!), integer-scaled as tabulated by Higham (2005).
+  const double c3[4] = {120.0, 60.0, 12.0, 1.0};
+  const double c5[6] = {30240.0, 15120.0, 3360.0, 420.0, 30.0, 1.0};
+  const double c7[8] = {17297280.0, 8648640.0, 1995840.0, 277200.0, 25200.0, 1512.0, 56.0, 1.0};
+  const double c9[10] = {17643225600.0, 8821612800.0, 2075673600.0, 302702400.0, 30270240.0,
+                         2162160.0, 110880.0, 3960.0, 90.0, 1.0};
+  const double c13[14] = {64764752532480000.0, 32382376266240000.0, 7771770303897600.0,
+                          1187353796428800.0, 129060195264000.0, 10559470521600.0, 670442572800.0,
+                          33522128640.0, 1323241920.0, 40840800.0, 960960.0, 16380.0, 182.0, 1.0};
+  const int nn = n * n;
+  for (int e = threadIdx.x; e < nn; e += blockDim.x) {
+    const int i = e % n, j = e / n;
+    X[i + (size_t)LDH * j] = scale * M[i + (size_t)LDH * j];
+  }
+  __syncthreads();
+  const double nrm = cta_norm1(n, X, sm);
+  if (!isfinite(nrm)) return -1;
+  int deg, s = 0;
+  if (nrm <= 1.495585217958292e-2) deg = 3;
+  else if (nrm <= 2.539398330063230e-1) deg = 5;
+  else if (nrm <= 9.504178996162932e-1) deg = 7;
+  else if (nrm <= 2.097847961257068e0) deg = 9;
+  else {
+    deg = 13;
+    s = ceil_log2_exact(nrm / 5.371920351148152e0);
+    if (s < 0) s = 0;
+    const double f = ldexp(1.0, -s);
+    for (int e = threadIdx.x; e < nn; e += blockDim.x) X[(e % n) + (size_t)LDH * (e / n)] *= f;
+    __syncthreads();
+  }
+  int mult = 0;
+  cta_matmul(n, X, X, X2, sm); mult++;
+  if (deg >= 5) { cta_matmul(n, X2, X2, X4, sm); mult++; }
+  if (deg >= 7) { cta_matmul(n, X2, X4, X6, sm); mult++; }
+  if (deg == 9) { cta_matmul(n, X4, X4, X8, sm); mult++; }
+  if (deg < 13) {
+    const double *b = deg == 3 ? c3 : deg == 5 ? c5 : deg == 7 ? c7 : c9;
+    for (int e = threadIdx.x; e < nn; e += blockDim.x) {
+      const int i = e % n, j = e / n;
+      const size_t q = i + (size_t)LDH * j;
+      const double id = (i == j) ? 1.0 : 0.0;
+      double odd = b[1] * id + b[3] * X2[q], even = b[0] * id + b[2] * X2[q];
+      if (deg >= 5) { odd += b[5] * X4[q]; even += b[4] * X4[q]; }
+      if (deg >= 7) { odd += b[7] * X6[q]; even += b[6] * X6[q]; }
+      if (deg >= 9) { odd += b[9] * X8[q]; even += b[8] * X8[q]; }
+      T[q] = odd;
+      V[q] = even;
+    }
+    __syncthreads();
+    cta_matmul(n, X, T, U, sm); mult++;   // U = X * odd part
+  } else {
+    const double *b = c13;
+    for (int e = threadIdx.x; e < nn; e += blockDim.x) {
+      const size_t q = (e % n) + (size_t)LDH * (e / n);
+      T[q] = b[13] * X6[q] + b[11] * X4[q] + b[9] * X2[q];
+      X8[q] = b[12] * X6[q] + b[10] * X4[q] + b[8] * X2[q];
+    }
+    __syncthreads();
+    cta_matmul(n, X6, T, U, sm); mult++;
+    cta_matmul(n, X6, X8, V, sm); mult++;
+    for (int e = threadIdx.x; e < nn; e += blockDim.x) {
+      const int i = e % n, j = e / n;
+      const size_t q = i + (size_t)LDH * j;
+      const double id = (i == j) ? 1.0 : 0.0;
+      U[q] += b[7] * X6[q] + b[5] * X4[q] + b[3] * X2[q] + b[1] * id;
+      V[q] += b[6] * X6[q] + b[4] * X4[q] + b[2] * X2[q] + b[0] * id;
+    }
+    __syncthreads();
+    cta_matmul(n, X, U, T, sm); mult++;   // odd part: X [ ... ]
+    for (int e = threadIdx.x; e < nn; e += blockDim.x) {
+      const size_t q = (e % n) + (size_t)LDH * (e / n);
+      U[q] = T[q];
+    }
+    __syncthreads();
+  }
+  // (V - U) F = (V + U)
+  for (int e = threadIdx.x; e < nn; e += blockDim.x) {
+    const size_t q = (e % n) + (size_t)LDH * (e / n);
+    T[q] = V[q] - U[q];
+    F[q] = V[q] + U[q];
+  }
+  __syncthreads();
+  if (cta_solve(n, T, F, sm) != 0) return -1;
+  for (int k = 0; k < s; k++) {
+    cta_matmul(n, F, F, T, sm); mult++;
+    for (int e = threadIdx.x; e < nn; e += blockDim.x) {
+      const size_t q = (e % n) + (size_t)LDH * (e / n);
+      F[q] = T[q];
+    }
+    __syncthreads();
+  }
+  return mult;
+}
+
+// ---------------------------------------------------------------------------
+// Alg. 4 with readings R4-R10.  Thread 0 only.
+// ---------------------------------------------------------------------------
+__device__ int alg4_adapt(bool happy, bool accept, int j, int m, int m_min, int m_max, double tau,
+                          double omega, double t_now, double t_end, const DevState *st, double *tau_new) {
+  const double gam = 0.9, gam_max = 0.6, delta = 1.4;
+  const double rem = accept ? t_end - (t_now + tau) : t_end - t_now;  // R8
+  const double om = fmax(omega, 1e-300);
+  double ord = (double)j / 4.0;  // R4: model exponent, q + 1 with q = m/4 - 1
+  double kap = 2.0;
+  if (st->hist_valid) {          // only the preceding rejected attempt of this substep (R5)
+    const double omo = fmax(st->omega_old, 1e-300);
+    if (j == st->j_old && tau != st->tau_old) {  // Eq. 43 un-inverted (R4)
+      const double o = log(om / omo) / log(tau / st->tau_old);
+      if (isfinite(o) && o > 0.0) ord = fmax(o, 1.0);
+    } else if (j != st->j_old && tau == st->tau_old) {  // Eq. 45 (R6)
+      double kk = pow(om / omo, 1.0 / (double)(st->j_old - j));
+      if (!(kk >= 1.1)) kk = 1.1;
+      if (!(kk <= 10.0)) kk = 10.0;
+      kap = kk;
+    }
+  }
+  if (happy) {                   // Alg. 4 l.4-8
+    *tau_new = fmin(tau, rem);
+    return m;
+  }
+  if (j == m_max) {
+    if (omega > delta) {         // l.10-13
+      const double t = fmax(tau / 5.0, tau * pow(gam_max / om, 1.0 / ord));
+      *tau_new = fmin(rem, t);
+      return j;
+    }
+    // l.15 -> Sec. 3.6.1, Eq. 44 with gamma = 0.9, clip [tau/5, 5 tau]
+    const double t = fmax(tau / 5.0, fmin(5.0 * tau, tau * pow(gam / om, 1.0 / ord)));
+    *tau_new = fmin(rem, t);
+    return m;
+  }
+  // l.18 -> Sec. 3.6.2, Eq. 46 with the -25%/+33% clip of P:510 (R7)
+  const double x = (double)j + log(om / gam) / log(kap);
+  int lo = (3 * j) / 4, hi = (4 * j + 2) / 3;
+  lo = lo < m_min ? m_min : lo;
+  hi = hi > m_max ? m_max : hi;
+  lo = lo > hi ? hi : lo;
+  int mn = x >= (double)hi ? hi : (x <= (double)lo ? lo : (int)ceil(x));
+  mn = mn < lo ? lo : (mn > hi ? hi : mn);
+  *tau_new = fmin(tau, rem);
+  return mn;
+}
+
+// ---------------------------------------------------------------------------
+// The controller: one CTA per attempt (Alg. 1 l.17-29 + Alg. 3 bookkeeping).
+// ---------------------------------------------------------------------------
+struct CtrlShared {
+  int j, happy, accept, final_, n_tau, stop, l0;
+  double tau, beta, eps, omega, h_next, t_now;
+};
+
+__global__ void __launch_bounds__(CTRL_THREADS, 1) k_ctrl(KParams P) {
+  extern __shared__ double sm[];
+  __shared__ CtrlShared C;
+  DevState *st = P.st;
+  const CallBlock *call = P.call;
+  double *Mh = P.scratch + 8 * (size_t)LDH * LDH;  // H~ / H_j input
+  double *F = P.scratch + 9 * (size_t)LDH * LDH;   // exponential output
+  double *scr = P.scratch;                          // 8 work matrices
+
+  if (threadIdx.x == 0) {
+    C.stop = 0;
+    if (st->status != 0) C.stop = 1;
+    else if (st->zero_start) C.stop = 2;
+    C.t_now = st->t_now;
+    const double rem0 = st->t_end - st->t_now;      // R11: never step past T_end
+    double tau = st->tau;
+    C.final_ = 0;
+    if (tau >= rem0) { tau = rem0; C.final_ = 1; }
+    st->tau = tau;
+    C.tau = tau;
+    C.j = st->npass - 1;
+    C.happy = st->happy;
+    C.beta = st->beta;
+    C.l0 = st->l;
+  }
+  __syncthreads();
+  if (C.stop == 1) {
+    if (threadIdx.x == 0) {
+      set_cond(P.h_outer, 0u); set_cond(P.h_inner, 0u); set_cond(P.h_accept, 0u);
+    }
+    return;
+  }
+  if (C.stop == 2) {  // R27: zero start vector => every remaining output is 0
+    if (threadIdx.x == 0) {
+      int o = 0;
+      for (int l = st->l; l < call->n_out; l++) st->gemv_out[o++] = call->w[l];
+      st->gemv_nout = o;
+      st->gemv_j = 0;
+      st->gemv_x1 = st->x1;
+      st->l = call->n_out - 1;
+      st->t_now = st->t_end;
+      st->substeps++;
+      st->attempt++;
+      set_cond(P.h_outer, 0u); set_cond(P.h_inner, 0u); set_cond(P.h_accept, 1u);
+    }
+    return;
+  }
+  const int j = C.j, n1 = j + 1;
+  // R1 / Eq. 37: H~ = [[H(1:j,1:j), e_1],[0, 0]] from the IOP band (q = 2)
+  for (int e = threadIdx.x; e < n1 * n1; e += blockDim.x) {
+    const int r = e % n1, c = e / n1;
+    double v = 0.0;
+    if (r < j && c < j && r >= c - 1 && r <= c + 1) v = P.H[r + (size_t)LDH * c];
+    if (r == 0 && c == j) v = 1.0;
+    Mh[r + (size_t)LDH * c] = v;
+  }
+  __syncthreads();
+  const int nm = cta_expm(n1, Mh, C.tau, F, scr, sm);  // Alg. 1 l.18
+  if (threadIdx.x == 0) {
+    st->expm_calls++;
+    double eps = 0.0, omega = 0.0, h_next = 0.0;
+    if (nm < 0) st->status = KIOPS_ERR_NONFINITE;
+    if (!C.happy) {  // Eq. 36 via Eq. 38: entry (j, j+1); Eq. 39
+      h_next = P.H[j + (size_t)LDH * (j - 1)];
+      eps = C.beta * h_next * fabs(F[(j - 1) + (size_t)LDH * j]);
+      omega = st->t_end * eps / (C.tau * P.tol);
+    }
+    if (!isfinite(omega)) st->status = KIOPS_ERR_NONFINITE;
+    const long long att = st->attempt;
+    const bool forced = att < call->n_forced;
+    const bool accept = forced ? true : (omega <= 1.4);  // P:425 (R10)
+    double tau_new = C.tau;
+    int m_new = st->m;
+    if (!forced)
+      m_new = alg4_adapt(C.happy, accept, j, st->m, P.m_min, P.m_max, C.tau, omega, st->t_now, st->t_end, st,
+                         &tau_new);
+    if (att < KIOPS_TRACE_CAP) {
+      kiops_trace_row &tr = P.trace[att];
+      tr.attempt = att; tr.j = j; tr.happy = C.happy; tr.accept = accept; tr.m_new = m_new;
+      tr.t_now = st->t_now; tr.tau = C.tau; tr.beta = C.beta; tr.h_next = h_next; tr.eps = eps;
+      tr.omega = omega; tr.tau_new = tau_new;
+    }
+    C.accept = accept && st->status == 0;
+    C.eps = eps; C.omega = omega; C.h_next = h_next;
+    // Alg. 3 l.2-9: outputs crossed by this substep (strict <, R16; all tasks, R15)
+    int n_tau = 0;
+    if (C.accept) {
+      const double T_next = st->t_now + C.tau;
+      for (int k = st->l; k < call->n_out; k++)
+        if (fabs(call->T[k]) < fabs(T_next)) n_tau++;
+    }
+    C.n_tau = n_tau;
+    // advance the controller state
+    if (C.accept) {
+      st->substeps++;
+      if (C.happy) st->happy_count++;
+      st->hist_valid = 0;
+    } else if (st->status == 0) {
+      st->rejections++;
+      st->hist_valid = 1;
+      st->omega_old = omega; st->tau_old = C.tau; st->j_old = j;
+    }
+    st->attempt = att + 1;
+    if (att + 1 < call->n_forced) {
+      tau_new = call->forced_tau[att + 1];
+      const int fm = call->forced_m[att + 1];
+      m_new = fm < 1 ? 1 : (fm > P.m_max ? P.m_max : fm);
+    }
+    st->tau = tau_new;
+    st->m = m_new;
+    st->final_m = m_new;
+  }
+  __syncthreads();
+  if (C.accept) {
+    // Alg. 3: coefficients of the one-pass GEMV.  Output rows 0..n_tau-1 are the
+    // crossed T_{l+k} (F2 = exp((T_{l+k} - T_now) H_j), l.13-15); the last row is
+    // the running solution (F, l.20).  coef[o][c-1] = beta F(c,1) / s_c.
+    const int n_tau = C.n_tau, l0 = C.l0;
+    const double sc_final = P.task1 ? pow(1.0 / call->T[call->n_out - 1], (double)P.p) : 1.0;
+    for (int c = threadIdx.x; c < j; c += blockDim.x) {
+      const double sg = (c == 0) ? C.beta : P.sig[c + 1];
+      P.coef[(size_t)n_tau * LDH + c] = C.beta * F[c] / sg * (C.final_ ? sc_final : 1.0);
+    }
+    __syncthreads();
+    for (int k = 0; k < n_tau; k++) {
+      for (int e = threadIdx.x; e < j * j; e += blockDim.x) {
+        const int r = e % j, c = e / j;
+        Mh[r + (size_t)LDH * c] = (r >= c - 1 && r <= c + 1) ? P.H[r + (size_t)LDH * c] : 0.0;
+      }
+      __syncthreads();
+      const double tt = call->T[l0 + k] - C.t_now;
+      const int nm2 = cta_expm(j, Mh, tt, F, scr, sm);
+      const double sc = P.task1 ? pow(1.0 / call->T[l0 + k], (double)P.p) : 1.0;
+      for (int c = threadIdx.x; c < j; c += blockDim.x) {
+        const double sg = (c == 0) ? C.beta : P.sig[c + 1];
+        P.coef[(size_t)k * LDH + c] = C.beta * F[c] / sg * sc;
+      }
+      if (threadIdx.x == 0) {
+        st->expm_calls++;
+        if (nm2 < 0) st->status = KIOPS_ERR_NONFINITE;
+      }
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+      for (int k = 0; k < n_tau; k++) st->gemv_out[k] = call->w[l0 + k];
+      const int lnew = l0 + n_tau;
+      st->gemv_out[n_tau] = C.final_ ? call->w[call->n_out - 1] : P.V;  // V slot 1 = running solution
+      st->gemv_nout = n_tau + 1;
+      st->gemv_j = j;
+      st->gemv_x1 = st->x1;
+      st->x1 = P.V;
+      st->l = lnew;
+      const double T_next = C.t_now + C.tau;
+      st->t_now = C.final_ ? st->t_end : T_next;  // Alg. 1 l.24, R11
+      st->npass = 0;                              // l.25
+      st->happy = 0;
+      write_exact_tail(P, st->t_now, st->mu, P.tails + 1 * KMAXP);  // next substep's exact tail (Eq. 47)
+    }
+  }
+  if (threadIdx.x == 0) {
+    const bool more = st->status == 0 && st->t_now < st->t_end;
+    bool cont = more && st->attempt < P.max_attempts;
+    if (more && !cont) st->status = KIOPS_ERR_NO_CONVERGENCE;
+    set_cond(P.h_outer, cont ? 1u : 0u);
+    set_cond(P.h_inner, (cont && st->npass < st->m + 1) ? 1u : 0u);
+    set_cond(P.h_accept, C.accept ? 1u : 0u);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Alg. 3 l.15 and l.20 (Eq. 33): out_o = sum_c coef[o][c] x_c, all outputs of an
+// accepted substep in ONE pass over the basis.  The running-solution row (which
+// may overwrite x_1 in place) is the last chunk.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_gemv(KParams P) {
+  const DevState *st = P.st;
+  const int j = st->gemv_j, nout = st->gemv_nout;
+  const double *x1 = st->gemv_x1;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < P.N;
+       i += (long long)gridDim.x * blockDim.x) {
+    for (int o0 = 0; o0 < nout; o0 += GEMV_OCHUNK) {
+      double acc[GEMV_OCHUNK];
+#pragma unroll
+      for (int o = 0; o < GEMV_OCHUNK; o++) acc[o] = 0.0;
+      for (int c = 0; c < j; c++) {
+        const double x = (c == 0) ? x1[i] : P.V[(size_t)c * P.ldN + i];
+#pragma unroll
+        for (int o = 0; o < GEMV_OCHUNK; o++)
+          if (o0 + o < nout) acc[o] = fma(P.coef[(size_t)(o0 + o) * LDH + c], x, acc[o]);
+      }
+#pragma unroll
+      for (int o = 0; o < GEMV_OCHUNK; o++)
+        if (o0 + o < nout) st->gemv_out[o0 + o][i] = acc[o];
+    }
+  }
+}

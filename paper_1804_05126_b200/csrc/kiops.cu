@@ -1,0 +1,478 @@
+// kiops.cu -- host side of the C ABI declared in include/kiops.h, plus the single
+// translation unit that instantiates every device kernel (sm_100a).
+//
+// One kiops_apply = one H2D copy of the call block, ONE cudaGraphLaunch, one D2H
+// copy of the device state, one stream synchronisation.  The graph is
+//
+//   k_setup                                  a1 (Eqs. 48-49), Alg. 1 l.2-8
+//   WHILE (outer)                            Alg. 1 l.9   T_now < T_end
+//     WHILE (inner)                          Alg. 2 l.2   j < m and not happy
+//       k_pass_*  (CSR: k_csr_form, k_csr_spmv)      a2-a4
+//     k_ctrl                                 a5-a7, Alg. 3 bookkeeping (one CTA)
+//     IF (accept)
+//       k_gemv                               a8, Alg. 3 l.15, l.20
+//
+// with the three conditional handles set from device code (no host round trip per
+// step, no CPU fallback).
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+
+#include "controller.cuh"
+#include "kiops_internal.cuh"
+#include "passes.cuh"
+
+namespace {
+
+constexpr int SM_COUNT_HINT = 148;
+
+// v1 stencil tiles
+#define T1D 1, 256, 1, 1
+#define T2D 2, 64, 16, 1
+#define T3D 3, 32, 8, 4
+
+struct Layout {
+  size_t V, r, staging, state, call, H, sig, R2, tails, partials, npart, scratch, coef, trace, total;
+  long long ldN;
+  int grid_pass, grid_setup, grid_gemv, grid_form, grid_max;
+  size_t smem_pass;
+};
+
+inline size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
+
+long long op_n(const kiops_operator_desc *op) { return op->nx * op->ny * op->nz; }
+
+kiops_status validate(const kiops_operator_desc *op, int p, const kiops_options *o, std::string &err) {
+  if (!op || !o) { err = "NULL operator or options"; return KIOPS_ERR_INVALID_ARG; }
+  if (op->nx < 1 || op->ny < 1 || op->nz < 1) { err = "grid extents must be >= 1"; return KIOPS_ERR_INVALID_ARG; }
+  if (p < 0 || p > KIOPS_MAX_P) { err = "p must be in [0, KIOPS_MAX_P]"; return KIOPS_ERR_INVALID_ARG; }
+  if (!(o->tol > 0.0) || !std::isfinite(o->tol)) { err = "tol must be > 0"; return KIOPS_ERR_INVALID_ARG; }
+  if (o->m_min < 1 || o->m_min > o->m_max) { err = "need 1 <= m_min <= m_max"; return KIOPS_ERR_INVALID_ARG; }
+  if (o->m_max > KIOPS_MAX_M) { err = "m_max > KIOPS_MAX_M (single-CTA exponential of (m_max+1)^2)"; return KIOPS_ERR_UNSUPPORTED; }
+  if (o->m_init < 1) { err = "m_init must be >= 1"; return KIOPS_ERR_INVALID_ARG; }
+  if (o->iop_q < 1 || o->iop_q > o->m_max) { err = "need 1 <= iop_q <= m_max"; return KIOPS_ERR_INVALID_ARG; }
+  if (o->iop_q != 2) { err = "this build implements the IOP window q = 2 (Alg. 2 as printed)"; return KIOPS_ERR_UNSUPPORTED; }
+  if (o->max_attempts < 1) { err = "max_attempts must be >= 1"; return KIOPS_ERR_INVALID_ARG; }
+  if (o->host_staging && (o->max_outputs < 1 || o->max_outputs > KIOPS_MAX_OUT)) {
+    err = "max_outputs must be in [1, KIOPS_MAX_OUT]"; return KIOPS_ERR_INVALID_ARG;
+  }
+  switch (op->kind) {
+    case KIOPS_OP_STENCIL1D3:
+      if (op->ny != 1 || op->nz != 1) { err = "1D stencil needs ny = nz = 1"; return KIOPS_ERR_INVALID_ARG; }
+      break;
+    case KIOPS_OP_STENCIL2D5:
+      if (op->nz != 1) { err = "2D stencil needs nz = 1"; return KIOPS_ERR_INVALID_ARG; }
+      break;
+    case KIOPS_OP_STENCIL3D7_VARKAPPA:
+      if (!op->kappa) { err = "3D stencil needs kappa"; return KIOPS_ERR_INVALID_ARG; }
+      break;
+    case KIOPS_OP_CSR:
+      if (op->ny != 1 || op->nz != 1) { err = "CSR needs ny = nz = 1 (nx = rows)"; return KIOPS_ERR_INVALID_ARG; }
+      if (!op->row_ptr || !op->col_idx || !op->vals) { err = "CSR arrays must be non-NULL"; return KIOPS_ERR_INVALID_ARG; }
+      if (op_n(op) > 2147483647LL) { err = "CSR with more than 2^31-1 rows (int32 col_idx)"; return KIOPS_ERR_UNSUPPORTED; }
+      break;
+    default:
+      err = "unknown operator kind";
+      return KIOPS_ERR_INVALID_ARG;
+  }
+  if (op->kind != KIOPS_OP_CSR && op->periodic != 1) { err = "stencils are periodic only"; return KIOPS_ERR_UNSUPPORTED; }
+  return KIOPS_OK;
+}
+
+Layout layout(const kiops_operator_desc *op, int p, const kiops_options *o) {
+  Layout L{};
+  const long long N = op_n(op);
+  L.ldN = (N + 31) & ~31LL;
+  const long long blocks256 = (N + 255) / 256;
+  L.grid_setup = (int)std::min<long long>(blocks256, SM_COUNT_HINT * 8);
+  L.grid_gemv = (int)std::min<long long>(blocks256, SM_COUNT_HINT * 8);
+  L.grid_form = L.grid_gemv;
+  switch (op->kind) {
+    case KIOPS_OP_STENCIL1D3:
+      L.grid_pass = (int)((op->nx + 255) / 256);
+      L.smem_pass = stencil_smem_bytes<T1D>();
+      break;
+    case KIOPS_OP_STENCIL2D5:
+      L.grid_pass = (int)(((op->nx + 63) / 64) * ((op->ny + 15) / 16));
+      L.smem_pass = stencil_smem_bytes<T2D>();
+      break;
+    case KIOPS_OP_STENCIL3D7_VARKAPPA:
+      L.grid_pass = (int)(((op->nx + 31) / 32) * ((op->ny + 7) / 8) * ((op->nz + 3) / 4));
+      L.smem_pass = stencil_smem_bytes<T3D>();
+      break;
+    default:
+      L.grid_pass = (int)std::min<long long>((8 * N + 255) / 256, SM_COUNT_HINT * 8);
+      L.smem_pass = 0;
+  }
+  L.grid_max = std::max(L.grid_pass, L.grid_setup);
+  size_t off = 0;
+  const size_t vec = (size_t)L.ldN * sizeof(double);
+  L.V = off; off += al((size_t)(o->m_max + 1) * vec);
+  L.r = off; off += (op->kind == KIOPS_OP_CSR) ? al(vec) : 0;
+  L.staging = off; off += o->host_staging ? al((size_t)(p + 1 + o->max_outputs) * vec) : 0;
+  L.state = off; off += al(sizeof(DevState));
+  L.call = off; off += al(sizeof(CallBlock));
+  L.H = off; off += al(sizeof(double) * LDH * LDH);
+  L.sig = off; off += al(sizeof(double) * (LDH + 2));
+  L.R2 = off; off += al(sizeof(double) * (LDH + 2));
+  L.tails = off; off += al(sizeof(double) * (LDH + 2) * KMAXP);
+  L.partials = off; off += al(sizeof(double) * NDOT * (size_t)L.grid_max);
+  L.npart = off; off += al(sizeof(double) * KMAXP * (size_t)L.grid_max);
+  L.scratch = off; off += al(sizeof(double) * NSCR * (size_t)LDH * LDH);
+  L.coef = off; off += al(sizeof(double) * (KMAXO + 1) * (size_t)LDH);
+  L.trace = off; off += al(sizeof(kiops_trace_row) * (size_t)KIOPS_TRACE_CAP);
+  L.total = off;
+  return L;
+}
+
+size_t ctrl_smem_bytes() {
+  const size_t solve = sizeof(double) * (size_t)(KMAXM + 1) * (KMAXM + 1);
+  const size_t mm = sizeof(double) * 2 * (size_t)((KMAXM + 1 + 3) & ~3) * MM_KP;
+  return std::max(solve, mm);
+}
+
+}  // namespace
+
+struct kiops_ctx_s {
+  KParams P{};
+  Layout L{};
+  kiops_operator_desc op{};
+  kiops_options o{};
+  int p = 0;
+  cudaStream_t stream = nullptr;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  CallBlock *h_call = nullptr;   // pinned
+  DevState *h_state = nullptr;   // pinned
+  unsigned char *ws = nullptr;
+  int n_forced = 0;
+  double forced_tau[KIOPS_MAX_FORCED];
+  int forced_m[KIOPS_MAX_FORCED];
+  long long last_attempts = 0;
+  std::string err;
+};
+
+static kiops_status cuda_fail(kiops_ctx c, cudaError_t e, const char *what) {
+  if (c) {
+    c->err = std::string(what) + ": " + cudaGetErrorString(e);
+  }
+  return KIOPS_ERR_CUDA;
+}
+
+#define CK(call, what)                                  \
+  do {                                                  \
+    cudaError_t e_ = (call);                            \
+    if (e_ != cudaSuccess) return cuda_fail(c, e_, what); \
+  } while (0)
+
+static cudaError_t add_kernel(cudaGraph_t g, cudaGraphNode_t *node, const cudaGraphNode_t *deps, size_t nd,
+                              void *func, int grid, int block, size_t smem, KParams *P) {
+  cudaGraphNodeParams np = {};
+  np.type = cudaGraphNodeTypeKernel;
+  void *args[] = {P};
+  np.kernel.func = func;
+  np.kernel.gridDim = dim3(grid);
+  np.kernel.blockDim = dim3(block);
+  np.kernel.sharedMemBytes = (unsigned)smem;
+  np.kernel.kernelParams = args;
+  return cudaGraphAddNode(node, g, deps, nd, &np);
+}
+
+static cudaError_t add_cond(cudaGraph_t g, cudaGraphNode_t *node, const cudaGraphNode_t *deps, size_t nd,
+                            cudaGraphConditionalHandle h, cudaGraphConditionalNodeType type, cudaGraph_t *body) {
+  cudaGraphNodeParams np = {};
+  np.type = cudaGraphNodeTypeConditional;
+  np.conditional.handle = h;
+  np.conditional.type = type;
+  np.conditional.size = 1;
+  cudaError_t e = cudaGraphAddNode(node, g, deps, nd, &np);
+  if (e == cudaSuccess) *body = np.conditional.phGraph_out[0];
+  return e;
+}
+
+static kiops_status build_graph(kiops_ctx c) {
+  KParams &P = c->P;
+  CK(cudaGraphCreate(&c->graph, 0), "cudaGraphCreate");
+  CK(cudaGraphConditionalHandleCreate(&P.h_outer, c->graph, 1, cudaGraphCondAssignDefault), "handle outer");
+  CK(cudaGraphConditionalHandleCreate(&P.h_inner, c->graph, 1, cudaGraphCondAssignDefault), "handle inner");
+  CK(cudaGraphConditionalHandleCreate(&P.h_accept, c->graph, 0, cudaGraphCondAssignDefault), "handle accept");
+
+  void *fpass = nullptr;
+  switch (c->op.kind) {
+    case KIOPS_OP_STENCIL1D3: fpass = (void *)k_pass_stencil<T1D>; break;
+    case KIOPS_OP_STENCIL2D5: fpass = (void *)k_pass_stencil<T2D>; break;
+    case KIOPS_OP_STENCIL3D7_VARKAPPA: fpass = (void *)k_pass_stencil<T3D>; break;
+    default: break;
+  }
+  if (fpass && c->L.smem_pass > 48 * 1024)
+    CK(cudaFuncSetAttribute(fpass, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->L.smem_pass), "smem attr pass");
+  CK(cudaFuncSetAttribute((void *)k_ctrl, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctrl_smem_bytes()),
+     "smem attr ctrl");
+
+  cudaGraphNode_t n_setup, n_outer, n_inner, n_ctrl, n_if, n_a, n_b, n_gemv;
+  cudaGraph_t b_outer, b_inner, b_if;
+  CK(add_kernel(c->graph, &n_setup, nullptr, 0, (void *)k_setup, c->L.grid_setup, 256, 0, &P), "node setup");
+  CK(add_cond(c->graph, &n_outer, &n_setup, 1, P.h_outer, cudaGraphCondTypeWhile, &b_outer), "node outer");
+  CK(add_cond(b_outer, &n_inner, nullptr, 0, P.h_inner, cudaGraphCondTypeWhile, &b_inner), "node inner");
+  if (c->op.kind == KIOPS_OP_CSR) {
+    CK(add_kernel(b_inner, &n_a, nullptr, 0, (void *)k_csr_form, c->L.grid_form, 256, 0, &P), "node form");
+    CK(add_kernel(b_inner, &n_b, &n_a, 1, (void *)k_csr_spmv, c->L.grid_pass, 256, 0, &P), "node spmv");
+  } else {
+    CK(add_kernel(b_inner, &n_a, nullptr, 0, fpass, c->L.grid_pass, 256, c->L.smem_pass, &P), "node pass");
+  }
+  CK(add_kernel(b_outer, &n_ctrl, &n_inner, 1, (void *)k_ctrl, 1, CTRL_THREADS, ctrl_smem_bytes(), &P), "node ctrl");
+  CK(add_cond(b_outer, &n_if, &n_ctrl, 1, P.h_accept, cudaGraphCondTypeIf, &b_if), "node if");
+  CK(add_kernel(b_if, &n_gemv, nullptr, 0, (void *)k_gemv, c->L.grid_gemv, 256, 0, &P), "node gemv");
+  CK(cudaGraphInstantiate(&c->exec, c->graph, 0), "cudaGraphInstantiate");
+  return KIOPS_OK;
+}
+
+extern "C" {
+
+void kiops_options_default(kiops_options *o) {
+  if (!o) return;
+  o->tol = 1e-7;
+  o->m_init = 10;
+  o->m_min = 10;
+  o->m_max = 128;
+  o->iop_q = 2;
+  o->task1 = 0;
+  o->max_attempts = 10000;
+  o->host_staging = 0;
+  o->max_outputs = 4;
+}
+
+kiops_status kiops_workspace_bytes(const kiops_operator_desc *op, int p, const kiops_options *o, size_t *bytes) {
+  std::string err;
+  kiops_status s = validate(op, p, o, err);
+  if (s != KIOPS_OK) return s;
+  if (!bytes) return KIOPS_ERR_INVALID_ARG;
+  *bytes = layout(op, p, o).total;
+  return KIOPS_OK;
+}
+
+kiops_status kiops_create(const kiops_operator_desc *op, int p, const kiops_options *o, void *cuda_stream,
+                          void *workspace, size_t workspace_bytes, kiops_ctx *out) {
+  if (!out) return KIOPS_ERR_INVALID_ARG;
+  *out = nullptr;
+  std::string err;
+  kiops_status s = validate(op, p, o, err);
+  if (s != KIOPS_OK) return s;
+  const Layout L = layout(op, p, o);
+  if (!workspace || ((uintptr_t)workspace & 255) || workspace_bytes < L.total) return KIOPS_ERR_WORKSPACE;
+  kiops_ctx c = new (std::nothrow) kiops_ctx_s();
+  if (!c) return KIOPS_ERR_CUDA;
+  c->op = *op;
+  c->o = *o;
+  c->p = p;
+  c->L = L;
+  c->stream = (cudaStream_t)cuda_stream;
+  c->ws = (unsigned char *)workspace;
+  KParams &P = c->P;
+  P.kind = op->kind;
+  P.nx = op->nx; P.ny = op->ny; P.nz = op->nz;
+  P.N = op_n(op);
+  P.ldN = L.ldN;
+  for (int i = 0; i < 5; i++) P.w[i] = op->w[i];
+  P.diag = op->diag;
+  P.kappa = op->kappa;
+  P.inv_h2 = op->inv_h2;
+  P.row_ptr = (const long long *)op->row_ptr;
+  P.col_idx = op->col_idx;
+  P.vals = op->vals;
+  P.p = p;
+  P.tol = o->tol;
+  P.m_init = o->m_init; P.m_min = o->m_min; P.m_max = o->m_max;
+  P.task1 = o->task1;
+  P.max_attempts = o->max_attempts;
+  unsigned char *w = c->ws;
+  P.V = (double *)(w + L.V);
+  P.r = (double *)(w + L.r);
+  P.st = (DevState *)(w + L.state);
+  P.call = (CallBlock *)(w + L.call);
+  P.H = (double *)(w + L.H);
+  P.sig = (double *)(w + L.sig);
+  P.R2 = (double *)(w + L.R2);
+  P.tails = (double *)(w + L.tails);
+  P.partials = (double *)(w + L.partials);
+  P.npart = (double *)(w + L.npart);
+  P.scratch = (double *)(w + L.scratch);
+  P.coef = (double *)(w + L.coef);
+  P.trace = (kiops_trace_row *)(w + L.trace);
+  P.grid_pass = L.grid_pass;
+  P.grid_max = L.grid_max;
+  kiops_status st = KIOPS_OK;
+  cudaError_t e = cudaMallocHost((void **)&c->h_call, sizeof(CallBlock));
+  if (e == cudaSuccess) e = cudaMallocHost((void **)&c->h_state, sizeof(DevState));
+  if (e != cudaSuccess) st = cuda_fail(c, e, "cudaMallocHost");
+  if (st == KIOPS_OK) {
+    memset(c->h_call, 0, sizeof(CallBlock));
+    e = cudaMemsetAsync(P.st, 0, sizeof(DevState), c->stream);
+    if (e == cudaSuccess) e = cudaMemsetAsync(P.H, 0, sizeof(double) * LDH * LDH, c->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+    if (e != cudaSuccess) st = cuda_fail(c, e, "workspace init");
+  }
+  if (st == KIOPS_OK) st = build_graph(c);
+  if (st != KIOPS_OK) {
+    fprintf(stderr, "kiops_create: %s\n", c->err.c_str());
+    kiops_destroy(c);
+    return st;
+  }
+  *out = c;
+  return KIOPS_OK;
+}
+
+static kiops_status check_call(kiops_ctx c, const double *const *u, const double *T, int n_out, double *const *w) {
+  if (!c || !u || !T || !w) return KIOPS_ERR_INVALID_ARG;
+  if (n_out < 1 || n_out > KIOPS_MAX_OUT) { c->err = "n_out must be in [1, KIOPS_MAX_OUT]"; return KIOPS_ERR_INVALID_ARG; }
+  for (int l = 0; l < n_out; l++) {
+    if (!std::isfinite(T[l]) || !(T[l] > 0.0) || (l > 0 && !(T[l] > T[l - 1]))) {
+      c->err = "output times must satisfy 0 < T_1 < ... < T_n (R21)";
+      return KIOPS_ERR_INVALID_ARG;
+    }
+    if (!w[l]) { c->err = "NULL output pointer"; return KIOPS_ERR_INVALID_ARG; }
+  }
+  for (int k = 0; k <= c->p; k++)
+    if (!u[k]) { c->err = "NULL input vector"; return KIOPS_ERR_INVALID_ARG; }
+  return KIOPS_OK;
+}
+
+static kiops_status launch_and_finish(kiops_ctx c, kiops_stats *stats) {
+  CK(cudaMemcpyAsync(c->P.call, c->h_call, sizeof(CallBlock), cudaMemcpyHostToDevice, c->stream), "H2D call block");
+  CK(cudaGraphLaunch(c->exec, c->stream), "cudaGraphLaunch");
+  CK(cudaMemcpyAsync(c->h_state, c->P.st, sizeof(DevState), cudaMemcpyDeviceToHost, c->stream), "D2H state");
+  return KIOPS_OK;
+}
+
+static kiops_status finish(kiops_ctx c, kiops_stats *stats) {
+  CK(cudaStreamSynchronize(c->stream), "stream sync");
+  CK(cudaGetLastError(), "kernel error");
+  const DevState &S = *c->h_state;
+  c->last_attempts = S.attempt;
+  if (stats) {
+    stats->substeps = S.substeps;
+    stats->rejections = S.rejections;
+    stats->krylov_vectors = S.kv;
+    stats->expm_calls = S.expm_calls;
+    stats->passes = S.passes;
+    stats->final_m = S.final_m;
+    stats->happy_breakdowns = (int)S.happy_count;
+    stats->t_reached = S.t_now;
+    stats->nu = S.nu;
+    stats->mu = S.mu;
+  }
+  if (S.status == KIOPS_ERR_NONFINITE) { c->err = "non-finite value in the Krylov recurrence or estimate"; return KIOPS_ERR_NONFINITE; }
+  if (S.status == KIOPS_ERR_NO_CONVERGENCE) { c->err = "max_attempts exceeded"; return KIOPS_ERR_NO_CONVERGENCE; }
+  if (S.status != 0) { c->err = "device status"; return (kiops_status)S.status; }
+  return KIOPS_OK;
+}
+
+static void fill_call(kiops_ctx c, const double *const *u, const double *T, int n_out, double *const *w) {
+  CallBlock &B = *c->h_call;
+  for (int k = 0; k <= KMAXP; k++) B.u[k] = k <= c->p ? u[k] : nullptr;
+  for (int l = 0; l < KMAXO; l++) {
+    B.w[l] = l < n_out ? w[l] : nullptr;
+    B.T[l] = l < n_out ? T[l] : 0.0;
+  }
+  B.n_out = n_out;
+  B.n_forced = c->n_forced;
+  for (int i = 0; i < c->n_forced; i++) { B.forced_tau[i] = c->forced_tau[i]; B.forced_m[i] = c->forced_m[i]; }
+}
+
+kiops_status kiops_apply(kiops_ctx c, const double *const *u, const double *tau_out, int n_out, double *const *w,
+                         kiops_stats *stats) {
+  kiops_status s = check_call(c, u, tau_out, n_out, w);
+  if (s != KIOPS_OK) return s;
+  fill_call(c, u, tau_out, n_out, w);
+  s = launch_and_finish(c, stats);
+  if (s != KIOPS_OK) return s;
+  return finish(c, stats);
+}
+
+kiops_status kiops_apply_host(kiops_ctx c, const double *const *u, const double *tau_out, int n_out, double *const *w,
+                              kiops_stats *stats) {
+  kiops_status s = check_call(c, u, tau_out, n_out, w);
+  if (s != KIOPS_OK) return s;
+  if (!c->o.host_staging || n_out > c->o.max_outputs) {
+    c->err = "kiops_apply_host needs host_staging and n_out <= max_outputs";
+    return KIOPS_ERR_WORKSPACE;
+  }
+  const size_t vb = (size_t)c->P.N * sizeof(double);
+  double *stg = (double *)(c->ws + c->L.staging);
+  const double *ud[KMAXP + 1];
+  double *wd[KMAXO];
+  for (int k = 0; k <= c->p; k++) {
+    ud[k] = stg + (size_t)k * c->L.ldN;
+    CK(cudaMemcpyAsync((void *)ud[k], u[k], vb, cudaMemcpyHostToDevice, c->stream), "H2D u");
+  }
+  for (int l = 0; l < n_out; l++) wd[l] = stg + (size_t)(c->p + 1 + l) * c->L.ldN;
+  fill_call(c, ud, tau_out, n_out, wd);
+  s = launch_and_finish(c, stats);
+  if (s != KIOPS_OK) return s;
+  for (int l = 0; l < n_out; l++) CK(cudaMemcpyAsync(w[l], wd[l], vb, cudaMemcpyDeviceToHost, c->stream), "D2H w");
+  return finish(c, stats);
+}
+
+kiops_status kiops_get_trace(kiops_ctx c, void *host_buf, size_t bytes, int64_t *rows) {
+  if (!c || !rows) return KIOPS_ERR_INVALID_ARG;
+  const long long avail = std::min<long long>(c->last_attempts, KIOPS_TRACE_CAP);
+  *rows = avail;
+  const size_t n = std::min<size_t>((size_t)avail, bytes / sizeof(kiops_trace_row));
+  if (n && host_buf) {
+    CK(cudaMemcpyAsync(host_buf, c->P.trace, n * sizeof(kiops_trace_row), cudaMemcpyDeviceToHost, c->stream), "D2H trace");
+    CK(cudaStreamSynchronize(c->stream), "stream sync");
+  }
+  return KIOPS_OK;
+}
+
+kiops_status kiops_set_forced_schedule(kiops_ctx c, const double *tau, const int32_t *m, int n) {
+  if (!c || n < 0 || n > KIOPS_MAX_FORCED || (n > 0 && (!tau || !m))) return KIOPS_ERR_INVALID_ARG;
+  for (int i = 0; i < n; i++) {
+    if (!(tau[i] > 0.0)) return KIOPS_ERR_INVALID_ARG;
+    c->forced_tau[i] = tau[i];
+    c->forced_m[i] = m[i];
+  }
+  c->n_forced = n;
+  return KIOPS_OK;
+}
+
+kiops_status kiops_debug_basis(kiops_ctx c, double *h, double *sig, int32_t *npass) {
+  if (!c) return KIOPS_ERR_INVALID_ARG;
+  if (h) CK(cudaMemcpyAsync(h, c->P.H, sizeof(double) * LDH * LDH, cudaMemcpyDeviceToHost, c->stream), "D2H H");
+  if (sig) CK(cudaMemcpyAsync(sig, c->P.sig + 1, sizeof(double) * LDH, cudaMemcpyDeviceToHost, c->stream), "D2H sig");
+  CK(cudaMemcpyAsync(c->h_state, c->P.st, sizeof(DevState), cudaMemcpyDeviceToHost, c->stream), "D2H state");
+  CK(cudaStreamSynchronize(c->stream), "stream sync");
+  if (npass) *npass = c->h_state->npass;
+  return KIOPS_OK;
+}
+
+kiops_status kiops_destroy(kiops_ctx c) {
+  if (!c) return KIOPS_ERR_INVALID_ARG;
+  if (c->exec) cudaGraphExecDestroy(c->exec);
+  if (c->graph) cudaGraphDestroy(c->graph);
+  if (c->h_call) cudaFreeHost(c->h_call);
+  if (c->h_state) cudaFreeHost(c->h_state);
+  delete c;
+  return KIOPS_OK;
+}
+
+const char *kiops_status_string(kiops_status s) {
+  switch (s) {
+    case KIOPS_OK: return "KIOPS_OK";
+    case KIOPS_ERR_INVALID_ARG: return "KIOPS_ERR_INVALID_ARG";
+    case KIOPS_ERR_UNSUPPORTED: return "KIOPS_ERR_UNSUPPORTED";
+    case KIOPS_ERR_CUDA: return "KIOPS_ERR_CUDA";
+    case KIOPS_ERR_NO_CONVERGENCE: return "KIOPS_ERR_NO_CONVERGENCE";
+    case KIOPS_ERR_NONFINITE: return "KIOPS_ERR_NONFINITE";
+    case KIOPS_ERR_WORKSPACE: return "KIOPS_ERR_WORKSPACE";
+  }
+  return "KIOPS_ERR_UNKNOWN";
+}
+
+const char *kiops_last_error(kiops_ctx c) { return c ? c->err.c_str() : "NULL ctx"; }
+
+}  // extern "C"

@@ -1,0 +1,109 @@
+// kiops_internal.cuh -- device-side data layout shared by the kernels of the
+// B200 KIOPS path (sm_100a).  See DESIGN.md section 6 for the HBM layout.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/kiops.h"
+
+#define KMAXP KIOPS_MAX_P
+#define KMAXO KIOPS_MAX_OUT
+#define KMAXM KIOPS_MAX_M
+#define LDH (KMAXM + 2)          // leading dimension of H and of every controller matrix
+#define NSCR 10                  // controller scratch matrices (LDH x LDH each)
+#define NDOT 5                   // dots reduced per pass: S, G, E1, E2, R
+#define GEMV_OCHUNK 4            // outputs accumulated per GEMV chunk
+
+// Per-call block: written by the host with ONE cudaMemcpyAsync per kiops_apply.
+struct CallBlock {
+  const double *u[KMAXP + 1];    // u_0..u_p (DEVICE)
+  double *w[KMAXO];              // outputs (DEVICE)
+  double T[KMAXO];               // output times
+  int n_out;
+  int n_forced;                  // test hook: forced schedule
+  double forced_tau[KIOPS_MAX_FORCED];
+  int forced_m[KIOPS_MAX_FORCED];
+};
+
+// Controller / pass state, resident in device memory for the whole call.
+struct DevState {
+  double tau, t_now, t_end, beta, nu, mu;
+  double omega_old, tau_old;
+  int m, npass, happy, l, hist_valid, j_old, status, zero_start;
+  int accept, final_m;
+  // pending GEMV (Alg. 3), set by the controller, consumed by k_gemv
+  int gemv_j, gemv_nout;
+  const double *gemv_x1;         // x_1 of the substep being projected
+  double *gemv_out[KMAXO + 1];   // targets (user outputs, running slot last)
+  const double *x1;              // x_1 source for the current substep (u_0, then V slot 1)
+  long long attempt, substeps, rejections, kv, expm_calls, passes, happy_count;
+  unsigned int ticket;           // last-CTA counter of the grid reductions
+  unsigned int ticket2;
+};
+
+// Frozen per-ctx parameters, passed BY VALUE to every kernel (graph node params).
+struct KParams {
+  int kind;
+  long long nx, ny, nz, N, ldN;
+  double w[5];
+  const double *diag, *kappa;
+  double inv_h2;
+  const long long *row_ptr;
+  const int *col_idx;
+  const double *vals;
+  int p;
+  double tol;
+  int m_init, m_min, m_max, task1;
+  long long max_attempts;
+  double *V;          // basis slots: x_k at V + (k-1)*ldN, k = 1..m_max+1 (slot 1 = running solution)
+  double *r;          // CSR split form: A~ x_k (top)
+  DevState *st;
+  CallBlock *call;
+  double *H;          // LDH x LDH column-major, H(i,j) 1-based at H[(i-1) + (j-1)*LDH]
+  double *sig;        // sig[k] = ||x_k||, k = 1..
+  double *R2;         // R2[k] = ||A~ x_k||^2 (breakdown scale, R3)
+  double *tails;      // tails[k*KMAXP + c] = tail entry N+c of x_k (unnormalised)
+  double *partials;   // NDOT x grid_max
+  double *npart;      // KMAXP x grid_max   (setup: column abs sums)
+  double *scratch;    // NSCR x LDH x LDH   (controller)
+  double *coef;       // (KMAXO+1) x LDH    (GEMV coefficients)
+  kiops_trace_row *trace;
+  int grid_pass, grid_max;
+  cudaGraphConditionalHandle h_outer, h_inner, h_accept;
+};
+
+__device__ __forceinline__ const double *slot_ptr(const KParams &P, int k) {
+  // x_k for k >= 1 ; x_1 comes from the state's source pointer
+  return (k == 1) ? P.st->x1 : P.V + (size_t)(k - 1) * (size_t)P.ldN;
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Deterministic block sum of NV values per thread; result valid in thread 0.
+template <int NV>
+__device__ __forceinline__ void block_sum(double (&v)[NV], double *red /* smem NV*32 */) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+#pragma unroll
+  for (int q = 0; q < NV; q++) v[q] = warp_sum(v[q]);
+  __syncthreads();
+  if (lane == 0)
+#pragma unroll
+    for (int q = 0; q < NV; q++) red[q * 32 + wid] = v[q];
+  __syncthreads();
+  if (wid == 0) {
+#pragma unroll
+    for (int q = 0; q < NV; q++) {
+      double x = lane < nw ? red[q * 32 + lane] : 0.0;
+      v[q] = warp_sum(x);
+    }
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ void set_cond(cudaGraphConditionalHandle h, unsigned v) {
+  cudaGraphSetConditional(h, v);
+}

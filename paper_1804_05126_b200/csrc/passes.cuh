@@ -1,0 +1,445 @@
+// passes.cuh -- SURVEY 8(a) rows a1 (setup), a2-a4 (fused IOP passes) for the
+// built-in operators.  sm_100a CUDA C++, fp64, memory-bound (no tensor cores).
+//
+// One pass k (k = npass+1, 1-based) of the look-ahead ("recompute") form of Alg. 2
+// does, in ONE kernel (stencils) or two (CSR split form):
+//   1. form x_k = (A~ x_{k-1})/s_{k-1} - H(k-2,k-1) x_{k-2}/s_{k-2} - H(k-1,k-1) x_{k-1}/s_{k-1}
+//      on the tile and its halo (A~ x_{k-1} recomputed on chip from x_{k-1}), i.e.
+//      lines 4-10 of Alg. 2 for iteration k-1 with lazy normalisation (line 17 is
+//      folded into the coefficients 1/s);
+//   2. r = A~ x_k on the tile interior (Thm 1 block matvec, lines 4-6);
+//   3. block partials of S = x_k.x_k, G = x_{k-1}.x_k, E1 = x_{k-1}.r, E2 = x_k.r,
+//      R = r.r, then a deterministic last-CTA grid reduction (pass_finalize) that
+//      writes s_k = sqrt(S) = H(k,k-1) (line 11, 16), H(k-1,k) = E1/(s_{k-1}s_k)
+//      and H(k,k) = E2/s_k^2 - H(k-1,k) G/(s_{k-1}s_k) -- the MGS values of lines
+//      7-10 in exact arithmetic -- tests breakdown of iteration k-1 (R3), and forms
+//      the tail of x_{k+1} (p scalars).
+// x_k is written once (the only vector store of the pass).  HBM bytes per pass:
+// read x_{k-1}, x_{k-2}, the p vectors of B and the c coefficient arrays, write
+// x_k: the (q+1+p+c)*8N minimum of SURVEY 8(d).
+#pragma once
+#include "kiops_internal.cuh"
+
+// ---------------------------------------------------------------------------
+// a1: Eqs. 48-49, R12: ||B||_1 = max_c sum_i |u_c,i|; nu = 2^-e,
+// mu = 2^e, e = ceil(log2 ||B||_1); and the Alg. 1 l.2-8 initial state.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int ceil_log2_exact(double x) {
+  int e;
+  double f = frexp(x, &e);
+  return (f == 0.5) ? e - 1 : e;
+}
+
+__device__ void write_exact_tail(const KParams &P, double t_now, double mu, double *t1) {
+  // Eq. 47 / Alg. 1 l.13 (R13, R14): entry N+c of x_1 = mu * T_now^e / e!, e = p-1-c
+  for (int c = 0; c < P.p; c++) {
+    const int e = P.p - 1 - c;
+    double t = 1.0;
+    for (int r = 1; r <= e; r++) t = t * t_now / (double)r;
+    t1[c] = mu * t;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_setup(KParams P) {
+  const CallBlock *call = P.call;
+  const int p = P.p;
+  __shared__ double red[KMAXP * 32];
+  double v[KMAXP];
+#pragma unroll
+  for (int c = 0; c < KMAXP; c++) v[c] = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < P.N;
+       i += (long long)gridDim.x * blockDim.x) {
+#pragma unroll
+    for (int c = 0; c < KMAXP; c++)
+      if (c < p) v[c] += fabs(call->u[c + 1][i]);
+  }
+  block_sum<KMAXP>(v, red);
+  if (threadIdx.x == 0)
+    for (int c = 0; c < p; c++) P.npart[c * P.grid_max + blockIdx.x] = v[c];
+  __shared__ bool last;
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = (atomicAdd(&P.st->ticket2, 1u) == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  // column sums in fixed block order
+  double cs[KMAXP];
+#pragma unroll
+  for (int c = 0; c < KMAXP; c++) {
+    double s = 0.0;
+    if (c < p)
+      for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) s += __ldcg(&P.npart[c * P.grid_max + b]);
+    cs[c] = s;
+  }
+  block_sum<KMAXP>(cs, red);
+  if (threadIdx.x != 0) return;
+  DevState *st = P.st;
+  st->ticket2 = 0;
+  double nb = 0.0;
+  for (int c = 0; c < p; c++) nb = cs[c] > nb ? cs[c] : nb;
+  double nu = 1.0, mu = 1.0;
+  if (p > 0 && nb > 0.0) {
+    const int e = ceil_log2_exact(nb);
+    nu = ldexp(1.0, -e);
+    mu = ldexp(1.0, e);
+  }
+  st->nu = nu;
+  st->mu = mu;
+  const int n_out = call->n_out;
+  st->t_end = call->T[n_out - 1];
+  st->tau = st->t_end;                                     // Alg. 1 l.2
+  int m = P.m_init < P.m_max ? P.m_init : P.m_max;         // l.3
+  st->m = m < P.m_min ? P.m_min : m;
+  if (call->n_forced > 0) {
+    st->tau = call->forced_tau[0];
+    int fm = call->forced_m[0];
+    st->m = fm < 1 ? 1 : (fm > P.m_max ? P.m_max : fm);
+  }
+  st->t_now = 0.0;                                         // l.4
+  st->npass = 0;                                           // l.5 (j = npass - 1)
+  st->l = 0;                                               // l.6
+  st->happy = 0;
+  st->hist_valid = 0;
+  st->status = 0;
+  st->zero_start = 0;
+  st->accept = 0;
+  st->x1 = call->u[0];                                     // l.8
+  st->attempt = st->substeps = st->rejections = st->kv = st->expm_calls = st->passes = 0;
+  st->happy_count = 0;
+  st->final_m = st->m;
+  st->ticket = 0;
+  write_exact_tail(P, 0.0, mu, P.tails + 1 * KMAXP);       // t_1 at T_now = 0
+  set_cond(P.h_outer, 1u);
+  set_cond(P.h_inner, 1u);
+  set_cond(P.h_accept, 0u);
+}
+
+// ---------------------------------------------------------------------------
+// Pass prologue: per-pass scalars (identical in every CTA).
+// ---------------------------------------------------------------------------
+struct PassScalars {
+  int k;
+  const double *xprev, *xpp;  // x_{k-1}, x_{k-2} (xpp may be NULL)
+  double *xout;               // x_k destination (NULL for k = 1)
+  double a0, a1, a2;          // x_k = a0 z - a2 x_{k-2} - a1 x_{k-1},  z = (A~ x_{k-1})_top
+  double btp[KMAXP];          // nu * t_{k-1}
+  double btc[KMAXP];          // nu * t_k
+  const double *B[KMAXP];     // column c of B = u_{p-c} (Thm 1, R14)
+};
+
+__device__ __forceinline__ void load_pass_scalars(const KParams &P, PassScalars &s) {
+  const DevState *st = P.st;
+  const int k = st->npass + 1;
+  s.k = k;
+  const double nu = st->nu;
+  const double *H = P.H;
+  for (int c = 0; c < KMAXP; c++) s.B[c] = c < P.p ? P.call->u[P.p - c] : nullptr;
+  if (k == 1) {  // x_1 is the substep's start vector: no formation
+    s.xprev = st->x1;
+    s.xpp = nullptr;
+    s.xout = nullptr;
+    s.a0 = 0.0; s.a1 = -1.0; s.a2 = 0.0;
+    for (int c = 0; c < KMAXP; c++) { s.btp[c] = 0.0; s.btc[c] = c < P.p ? nu * P.tails[1 * KMAXP + c] : 0.0; }
+    return;
+  }
+  s.xprev = slot_ptr(P, k - 1);
+  s.xpp = (k >= 3) ? slot_ptr(P, k - 2) : nullptr;
+  s.xout = P.V + (size_t)(k - 1) * (size_t)P.ldN;
+  const double skm1 = P.sig[k - 1];
+  s.a0 = 1.0 / skm1;
+  s.a1 = H[(k - 2) + (size_t)(k - 2) * LDH] / skm1;                    // H(k-1,k-1)/s_{k-1}
+  s.a2 = (k >= 3) ? H[(k - 3) + (size_t)(k - 2) * LDH] / P.sig[k - 2] : 0.0;  // H(k-2,k-1)/s_{k-2}
+  for (int c = 0; c < KMAXP; c++) {
+    s.btp[c] = c < P.p ? nu * P.tails[(k - 1) * KMAXP + c] : 0.0;
+    s.btc[c] = c < P.p ? nu * P.tails[k * KMAXP + c] : 0.0;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Deterministic last-CTA finalisation of pass k (all threads of the last CTA).
+// ---------------------------------------------------------------------------
+__device__ void pass_finalize(const KParams &P, int k, int nblocks) {
+  __shared__ double red[NDOT * 32];
+  double v[NDOT];
+#pragma unroll
+  for (int q = 0; q < NDOT; q++) v[q] = 0.0;
+  for (int b = threadIdx.x; b < nblocks; b += blockDim.x)
+#pragma unroll
+    for (int q = 0; q < NDOT; q++) v[q] += __ldcg(&P.partials[q * P.grid_max + b]);
+  block_sum<NDOT>(v, red);
+  if (threadIdx.x != 0) return;
+  DevState *st = P.st;
+  st->ticket = 0;
+  const int p = P.p;
+  const double *tk = P.tails + k * KMAXP;
+  const double *tkm1 = P.tails + (k - 1) * KMAXP;
+  double Kt[KMAXP];
+  for (int c = 0; c < p; c++) Kt[c] = (c + 1 < p) ? tk[c + 1] : 0.0;  // tail of A~ x_k: K t_k (Alg. 2 l.5-6)
+  double S = v[0], G = v[1], E1 = v[2], E2 = v[3], R = v[4];
+  for (int c = 0; c < p; c++) {
+    S += tk[c] * tk[c];
+    R += Kt[c] * Kt[c];
+    E2 += tk[c] * Kt[c];
+    if (k >= 2) { G += tkm1[c] * tk[c]; E1 += tkm1[c] * Kt[c]; }
+  }
+  st->passes++;
+  st->npass = k;
+  if (!isfinite(S) || !isfinite(G) || !isfinite(E1) || !isfinite(E2) || !isfinite(R)) {
+    st->status = KIOPS_ERR_NONFINITE;  // R22
+    set_cond(P.h_inner, 0u);
+    return;
+  }
+  const double sk = sqrt(S);
+  double *H = P.H;
+#define HH(i, j) H[((i)-1) + (size_t)((j)-1) * LDH]
+  double *tn = P.tails + (k + 1) * KMAXP;  // tail of x_{k+1}
+  if (k == 1) {  // beta = ||x_1|| (Alg. 1 l.14)
+    st->beta = sk;
+    P.sig[1] = sk;
+    P.R2[1] = R;
+    if (sk == 0.0) {  // R27
+      st->zero_start = 1;
+      set_cond(P.h_inner, 0u);
+      return;
+    }
+    const double h11 = E2 / (sk * sk);
+    HH(1, 1) = h11;
+    for (int c = 0; c < p; c++) tn[c] = Kt[c] / sk - h11 * tk[c] / sk;
+    set_cond(P.h_inner, (1 < st->m + 1) ? 1u : 0u);
+    return;
+  }
+  // k >= 2 closes Alg. 2 iteration k-1
+  st->kv++;
+  const double skm1 = P.sig[k - 1];
+  const double cn = sqrt(P.R2[k - 1]) / skm1;  // ||A~ v_{k-1}|| before projection
+  const double thr = fmax(1e-12 * cn, 1e-14);  // R3
+  if (sk <= thr) {                             // Alg. 2 l.12-15
+    st->happy = 1;
+    set_cond(P.h_inner, 0u);
+    return;
+  }
+  HH(k, k - 1) = sk;  // l.16 (R2)
+  P.sig[k] = sk;
+  P.R2[k] = R;
+  const double h1 = E1 / (skm1 * sk);
+  const double h2 = E2 / (sk * sk) - h1 * G / (skm1 * sk);
+  HH(k - 1, k) = h1;
+  HH(k, k) = h2;
+  for (int c = 0; c < p; c++) tn[c] = Kt[c] / sk - h1 * tkm1[c] / skm1 - h2 * tk[c] / sk;
+  set_cond(P.h_inner, (k < st->m + 1) ? 1u : 0u);
+#undef HH
+}
+
+// write this CTA's partials, detect the last CTA, finalize.
+__device__ __forceinline__ void pass_epilogue(const KParams &P, int k, double (&v)[NDOT]) {
+  __shared__ double red[NDOT * 32];
+  __shared__ bool last;
+  block_sum<NDOT>(v, red);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int q = 0; q < NDOT; q++) P.partials[q * P.grid_max + blockIdx.x] = v[q];
+    __threadfence();
+    last = (atomicAdd(&P.st->ticket, 1u) == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (last) {
+    __threadfence();
+    pass_finalize(P, k, gridDim.x);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Stencil passes: tile + halo staged in shared memory (v1 generic tile kernel).
+// DIM = 1, 2, 3.  Tile TX x TY x TZ interior points; x_{k-1} (and kappa) staged on
+// the halo-2 region, x_k formed on the halo-1 region, r on the interior.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ long long wrapc(long long g, long long n) {
+  g %= n;
+  return g < 0 ? g + n : g;
+}
+
+template <int DIM, int TX, int TY, int TZ>
+struct TileGeo {
+  static constexpr int HX = TX + 4, HY = DIM >= 2 ? TY + 4 : 1, HZ = DIM >= 3 ? TZ + 4 : 1;
+  static constexpr int GX = TX + 2, GY = DIM >= 2 ? TY + 2 : 1, GZ = DIM >= 3 ? TZ + 2 : 1;
+  static constexpr int H2 = HX * HY * HZ, H1 = GX * GY * GZ, IN = TX * TY * TZ;
+  static constexpr int OY = DIM >= 2 ? 1 : 0, OZ = DIM >= 3 ? 1 : 0;  // halo offsets per ring
+};
+
+template <int DIM>
+__device__ __forceinline__ double stencil_at(const KParams &P, const double *s, const double *kap, int e,
+                                             int sy, int sz, double d) {
+  if (DIM == 1) {
+    return P.w[0] * s[e - 1] + P.w[1] * s[e] + P.w[2] * s[e + 1] + d * s[e];
+  } else if (DIM == 2) {
+    return P.w[0] * s[e - 1] + P.w[1] * s[e + 1] + P.w[2] * s[e - sy] + P.w[3] * s[e + sy] +
+           P.w[4] * s[e] + d * s[e];
+  } else {
+    const double xc = s[e], kc = kap[e];
+    double acc = 0.5 * (kc + kap[e - 1]) * (s[e - 1] - xc);
+    acc += 0.5 * (kc + kap[e + 1]) * (s[e + 1] - xc);
+    acc += 0.5 * (kc + kap[e - sy]) * (s[e - sy] - xc);
+    acc += 0.5 * (kc + kap[e + sy]) * (s[e + sy] - xc);
+    acc += 0.5 * (kc + kap[e - sz]) * (s[e - sz] - xc);
+    acc += 0.5 * (kc + kap[e + sz]) * (s[e + sz] - xc);
+    return acc * P.inv_h2;
+  }
+}
+
+template <int DIM, int TX, int TY, int TZ>
+__global__ void __launch_bounds__(256) k_pass_stencil(KParams P) {
+  using G = TileGeo<DIM, TX, TY, TZ>;
+  extern __shared__ double smem[];
+  double *sX1 = smem;                                  // x_{k-1} on halo-2 region
+  double *sK = sX1 + G::H2;                            // kappa on halo-2 (3D) / diag on halo-1 (1D, 2D)
+  double *sXK = sK + (DIM == 3 ? G::H2 : G::H1);       // x_k on halo-1 region
+  double *sBT = sXK + G::H1;                           // nu B t_k on the interior
+
+  __shared__ PassScalars S;
+  if (threadIdx.x == 0) load_pass_scalars(P, S);
+  __syncthreads();
+  const int p = P.p;
+  const long long nx = P.nx, ny = P.ny, nz = P.nz;
+  const long long ntx = (nx + TX - 1) / TX, nty = DIM >= 2 ? (ny + TY - 1) / TY : 1;
+  const long long b = blockIdx.x;
+  const long long ox = (b % ntx) * TX, oy = DIM >= 2 ? ((b / ntx) % nty) * TY : 0,
+                  oz = DIM >= 3 ? (b / (ntx * nty)) * TZ : 0;
+  const double *xprev = S.xprev;
+
+  // stage 1: x_{k-1} (and kappa) on the halo-2 region
+  for (int e = threadIdx.x; e < G::H2; e += blockDim.x) {
+    const int a = e % G::HX, bb = (e / G::HX) % G::HY, c = e / (G::HX * G::HY);
+    const long long gx = wrapc(ox + a - 2, nx);
+    const long long gy = DIM >= 2 ? wrapc(oy + bb - 2, ny) : 0;
+    const long long gz = DIM >= 3 ? wrapc(oz + c - 2, nz) : 0;
+    const long long g = gx + nx * (gy + ny * gz);
+    sX1[e] = xprev[g];
+    if (DIM == 3) sK[e] = P.kappa[g];
+  }
+  __syncthreads();
+
+  // stage 2: x_k on the halo-1 region (Alg. 2 l.4-10 of iteration k-1)
+  for (int e = threadIdx.x; e < G::H1; e += blockDim.x) {
+    const int a = e % G::GX, bb = (e / G::GX) % G::GY, c = e / (G::GX * G::GY);
+    const long long gx = wrapc(ox + a - 1, nx);
+    const long long gy = DIM >= 2 ? wrapc(oy + bb - 1, ny) : 0;
+    const long long gz = DIM >= 3 ? wrapc(oz + c - 1, nz) : 0;
+    const long long g = gx + nx * (gy + ny * gz);
+    const int e2 = (a + 1) + G::HX * ((bb + G::OY) + G::HY * (c + G::OZ));
+    double d = 0.0;
+    if (DIM != 3) {
+      d = P.diag ? P.diag[g] : 0.0;
+      sK[e] = d;
+    }
+    double z = stencil_at<DIM>(P, sX1, sK, e2, G::HX, G::HX * G::HY, d);
+    double bc = 0.0;
+#pragma unroll
+    for (int q = 0; q < KMAXP; q++)
+      if (q < p) {
+        const double bv = S.B[q][g];
+        z += bv * S.btp[q];
+        bc += bv * S.btc[q];
+      }
+    double xk = S.a0 * z - S.a1 * sX1[e2];
+    if (S.xpp) xk -= S.a2 * S.xpp[g];
+    sXK[e] = xk;
+    const bool inner = (a >= 1 && a <= TX) && (DIM < 2 || (bb >= 1 && bb <= TY)) && (DIM < 3 || (c >= 1 && c <= TZ));
+    if (inner) sBT[(a - 1) + TX * ((bb - G::OY) + TY * (c - G::OZ))] = bc;
+  }
+  __syncthreads();
+
+  // stage 3: r = A~ x_k on the interior, 5 partial dots, store x_k
+  double v[NDOT] = {0.0, 0.0, 0.0, 0.0, 0.0};
+  for (int e = threadIdx.x; e < G::IN; e += blockDim.x) {
+    const int a = e % TX, bb = (e / TX) % TY, c = e / (TX * TY);
+    const long long gx = ox + a, gy = oy + bb, gz = oz + c;
+    if (gx >= nx || (DIM >= 2 && gy >= ny) || (DIM >= 3 && gz >= nz)) continue;
+    const int e1 = (a + 1) + G::GX * ((bb + G::OY) + G::GY * (c + G::OZ));
+    const int e2 = (a + 2) + G::HX * ((bb + 2 * G::OY) + G::HY * (c + 2 * G::OZ));
+    const double xk = sXK[e1];
+    double d = 0.0;
+    if (DIM != 3) d = sK[e1];
+    double r;
+    if (DIM == 3) {
+      // kappa of the interior point and neighbours from the halo-2 kappa tile
+      const double *kap = sK;
+      const int sy2 = G::HX, sz2 = G::HX * G::HY, sy1 = G::GX, sz1 = G::GX * G::GY;
+      const double kc = kap[e2];
+      r = 0.5 * (kc + kap[e2 - 1]) * (sXK[e1 - 1] - xk) + 0.5 * (kc + kap[e2 + 1]) * (sXK[e1 + 1] - xk) +
+          0.5 * (kc + kap[e2 - sy2]) * (sXK[e1 - sy1] - xk) + 0.5 * (kc + kap[e2 + sy2]) * (sXK[e1 + sy1] - xk) +
+          0.5 * (kc + kap[e2 - sz2]) * (sXK[e1 - sz1] - xk) + 0.5 * (kc + kap[e2 + sz2]) * (sXK[e1 + sz1] - xk);
+      r *= P.inv_h2;
+    } else {
+      r = stencil_at<DIM>(P, sXK, nullptr, e1, G::GX, G::GX * G::GY, d);
+    }
+    r += sBT[e];
+    const double xm = sX1[e2];
+    v[0] += xk * xk;
+    v[1] += xm * xk;
+    v[2] += xm * r;
+    v[3] += xk * r;
+    v[4] += r * r;
+    if (S.xout) S.xout[gx + nx * (gy + ny * gz)] = xk;
+  }
+  pass_epilogue(P, S.k, v);
+}
+
+template <int DIM, int TX, int TY, int TZ>
+constexpr size_t stencil_smem_bytes() {
+  using G = TileGeo<DIM, TX, TY, TZ>;
+  return sizeof(double) * (size_t)(G::H2 + (DIM == 3 ? G::H2 : G::H1) + G::H1 + G::IN);
+}
+
+// ---------------------------------------------------------------------------
+// CSR split form: (a) pointwise formation of x_k from r = A~ x_{k-1}, (b) SpMV with
+// 8 lanes per row + the 5 dots.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_csr_form(KParams P) {
+  __shared__ PassScalars S;
+  if (threadIdx.x == 0) load_pass_scalars(P, S);
+  __syncthreads();
+  if (S.k == 1) return;
+  const double *r = P.r;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < P.N;
+       i += (long long)gridDim.x * blockDim.x) {
+    double xk = S.a0 * r[i] - S.a1 * S.xprev[i];
+    if (S.xpp) xk -= S.a2 * S.xpp[i];
+    S.xout[i] = xk;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_csr_spmv(KParams P) {
+  __shared__ PassScalars S;
+  if (threadIdx.x == 0) load_pass_scalars(P, S);
+  __syncthreads();
+  const int k = S.k, p = P.p;
+  const double *xk = (k == 1) ? S.xprev : S.xout;
+  const double *xm = S.xprev;
+  const int lane8 = threadIdx.x & 7;
+  double v[NDOT] = {0.0, 0.0, 0.0, 0.0, 0.0};
+  const long long groups = (long long)gridDim.x * (blockDim.x / 8);
+  for (long long row = (blockIdx.x * (long long)blockDim.x + threadIdx.x) / 8; row < P.N; row += groups) {
+    const long long b0 = P.row_ptr[row], b1 = P.row_ptr[row + 1];
+    double s = 0.0;
+    for (long long q = b0 + lane8; q < b1; q += 8) s += P.vals[q] * xk[P.col_idx[q]];
+    s += __shfl_xor_sync(0xffffffffu, s, 4);
+    s += __shfl_xor_sync(0xffffffffu, s, 2);
+    s += __shfl_xor_sync(0xffffffffu, s, 1);
+    if (lane8 == 0) {
+      double rr = s;
+#pragma unroll
+      for (int c = 0; c < KMAXP; c++)
+        if (c < p) rr += S.B[c][row] * S.btc[c];
+      const double x = xk[row], y = xm[row];
+      v[0] += x * x;
+      v[1] += y * x;
+      v[2] += y * rr;
+      v[3] += x * rr;
+      v[4] += rr * rr;
+      P.r[row] = rr;
+    }
+  }
+  pass_epilogue(P, k, v);
+}
