@@ -334,7 +334,8 @@ __global__ void __launch_bounds__(CTRL_THREADS, 1) k_ctrl(KParams P) {
 
   if (threadIdx.x == 0) {
     C.stop = 0;
-    if (st->status != 0) C.stop = 1;
+    if (st->status != 0 || st->npass < 1) C.stop = 1;
+    if (st->npass < 1 && st->status == 0) st->status = KIOPS_ERR_CUDA;
     else if (st->zero_start) C.stop = 2;
     C.t_now = st->t_now;
     const double rem0 = st->t_end - st->t_now;      // R11: never step past T_end

@@ -39,6 +39,7 @@ struct DevState {
   long long attempt, substeps, rejections, kv, expm_calls, passes, happy_count;
   unsigned int ticket;           // last-CTA counter of the grid reductions
   unsigned int ticket2;
+  unsigned long long launches;   // pass launches this call (device-side loop guard)
 };
 
 // Frozen per-ctx parameters, passed BY VALUE to every kernel (graph node params).
@@ -106,4 +107,20 @@ __device__ __forceinline__ void block_sum(double (&v)[NV], double *red /* smem N
 
 __device__ __forceinline__ void set_cond(cudaGraphConditionalHandle h, unsigned v) {
   cudaGraphSetConditional(h, v);
+}
+
+// Loop guard (block 0, thread 0 of every pass launch): the device-side WHILE loops
+// can never spin forever, even if a reduction were lost.  Returns true if tripped.
+__device__ __forceinline__ bool pass_guard(const KParams &P) {
+  if (blockIdx.x != 0 || threadIdx.x != 0) return false;
+  DevState *st = P.st;
+  const unsigned long long n = ++st->launches;
+  const unsigned long long cap = (unsigned long long)(P.max_attempts + 2) * (unsigned long long)(P.m_max + 2);
+  if (n > cap || st->npass > P.m_max) {
+    st->status = KIOPS_ERR_CUDA;
+    cudaGraphSetConditional(P.h_inner, 0u);
+    cudaGraphSetConditional(P.h_outer, 0u);
+    return true;
+  }
+  return false;
 }

@@ -110,6 +110,7 @@ __global__ void __launch_bounds__(256) k_setup(KParams P) {
   st->happy_count = 0;
   st->final_m = st->m;
   st->ticket = 0;
+  st->launches = 0;
   write_exact_tail(P, 0.0, mu, P.tails + 1 * KMAXP);       // t_1 at T_now = 0
   set_cond(P.h_outer, 1u);
   set_cond(P.h_inner, 1u);
@@ -132,7 +133,8 @@ struct PassScalars {
 __device__ __forceinline__ void load_pass_scalars(const KParams &P, PassScalars &s) {
   const DevState *st = P.st;
   const int k = st->npass + 1;
-  s.k = k;
+  s.k = (k > P.m_max + 1) ? 0 : k;  // 0 => out-of-range pass: every thread returns
+  if (s.k == 0) return;
   const double nu = st->nu;
   const double *H = P.H;
   for (int c = 0; c < KMAXP; c++) s.B[c] = c < P.p ? P.call->u[P.p - c] : nullptr;
@@ -186,6 +188,10 @@ __device__ void pass_finalize(const KParams &P, int k, int nblocks) {
   }
   st->passes++;
   st->npass = k;
+  if (st->status != 0) {
+    set_cond(P.h_inner, 0u);
+    return;
+  }
   if (!isfinite(S) || !isfinite(G) || !isfinite(E1) || !isfinite(E2) || !isfinite(R)) {
     st->status = KIOPS_ERR_NONFINITE;  // R22
     set_cond(P.h_inner, 0u);
@@ -298,8 +304,10 @@ __global__ void __launch_bounds__(256) k_pass_stencil(KParams P) {
   double *sBT = sXK + G::H1;                           // nu B t_k on the interior
 
   __shared__ PassScalars S;
+  pass_guard(P);
   if (threadIdx.x == 0) load_pass_scalars(P, S);
   __syncthreads();
+  if (S.k == 0) return;
   const int p = P.p;
   const long long nx = P.nx, ny = P.ny, nz = P.nz;
   const long long ntx = (nx + TX - 1) / TX, nty = DIM >= 2 ? (ny + TY - 1) / TY : 1;
@@ -400,7 +408,7 @@ __global__ void __launch_bounds__(256) k_csr_form(KParams P) {
   __shared__ PassScalars S;
   if (threadIdx.x == 0) load_pass_scalars(P, S);
   __syncthreads();
-  if (S.k == 1) return;
+  if (S.k <= 1) return;
   const double *r = P.r;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < P.N;
        i += (long long)gridDim.x * blockDim.x) {
@@ -412,8 +420,10 @@ __global__ void __launch_bounds__(256) k_csr_form(KParams P) {
 
 __global__ void __launch_bounds__(256) k_csr_spmv(KParams P) {
   __shared__ PassScalars S;
+  pass_guard(P);
   if (threadIdx.x == 0) load_pass_scalars(P, S);
   __syncthreads();
+  if (S.k == 0) return;
   const int k = S.k, p = P.p;
   const double *xk = (k == 1) ? S.xprev : S.xout;
   const double *xm = S.xprev;
