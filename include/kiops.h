@@ -153,9 +153,13 @@ kiops_status kiops_apply_host(kiops_ctx c, const double *const *u, const double 
 kiops_status kiops_get_trace(kiops_ctx c, void *host_buf, size_t bytes, int64_t *rows);
 
 /* TEST HOOK (not for users): force the next applies to run attempt i with
- * (tau[i], m[i]) and accept it, bypassing Alg. 4 (n = 0 clears).  tau, m: HOST,
- * n <= KIOPS_MAX_FORCED.  Used for step-level parity and the semigroup pin. */
-kiops_status kiops_set_forced_schedule(kiops_ctx c, const double *tau, const int32_t *m, int n);
+ * substep tau[i] and Krylov size m[i], bypassing Alg. 4, and accept it if
+ * accept == NULL or accept[i] != 0 (n = 0 clears).  tau, m, accept: HOST,
+ * n <= KIOPS_MAX_FORCED.  With the oracle's trace (tau, j, accept) this REPLAYS
+ * the oracle's decisions (R26: the result is unique given the decision trace);
+ * with accept == NULL it gives step-level parity and the semigroup pin. */
+kiops_status kiops_set_forced_schedule(kiops_ctx c, const double *tau, const int32_t *m,
+                                       const int32_t *accept, int n);
 
 /* TEST HOOK: copies the projected matrix H (column-major, leading dimension
  * m_max+2, H(i,j) 1-based at h[(i-1) + (j-1)*(m_max+2)]) and the norms

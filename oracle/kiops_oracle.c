@@ -494,7 +494,8 @@ int or_kiops(const or_operator *op, int p, const double *const *u, int n_out, co
       omega = T_end * eps / (tau * o->tol);
     }
     if (!isfinite(omega)) { rc = OR_ERR_NONFINITE; goto out; }
-    const int accept = forced ? 1 : (omega <= 1.4); /* P:425, delta = 1.4, R10 */
+    const int accept = forced ? (o->forced_accept ? o->forced_accept[attempt] != 0 : 1)
+                              : (omega <= 1.4); /* P:425, delta = 1.4, R10 */
     /* l.20-21: Alg. 4 */
     double tau_new = tau;
     int m_new = m;

@@ -49,9 +49,10 @@ typedef struct {
   int iop_q;                /* IOP window (2 = the paper's Alg. 2)                 */
   int task1;                /* 1 => scale output l by 1/T_l^p (Alg. 1 l.31-35)     */
   int64_t max_attempts;     /* R22 divergence guard (default 10000)                */
-  int n_forced;             /* test hook: forced (tau_i, m_i) schedule, all accepted */
+  int n_forced;             /* test hook: forced (tau_i, m_i[, accept_i]) schedule   */
   const double *forced_tau;
   const int *forced_m;
+  const int *forced_accept; /* NULL => every forced attempt accepted; else replay     */
 } or_options;
 
 typedef struct {

@@ -41,6 +41,7 @@ class _Opts(C.Structure):
         ("tol", C.c_double), ("m_init", C.c_int), ("m_min", C.c_int), ("m_max", C.c_int),
         ("iop_q", C.c_int), ("task1", C.c_int), ("max_attempts", C.c_int64),
         ("n_forced", C.c_int), ("forced_tau", _dp), ("forced_m", C.POINTER(C.c_int)),
+        ("forced_accept", C.POINTER(C.c_int)),
     ]
 
 
@@ -232,10 +233,12 @@ def kiops(op, u, T, tol=1e-7, m_init=10, m_min=10, m_max=128, iop_q=2, task1=0,
     o = _Opts(tol=tol, m_init=m_init, m_min=m_min, m_max=m_max, iop_q=iop_q, task1=task1,
               max_attempts=max_attempts)
     if forced:
-        ft = np.ascontiguousarray([t for t, _ in forced], dtype=np.float64)
-        fm = np.ascontiguousarray([m for _, m in forced], dtype=np.int32)
+        ft = np.ascontiguousarray([e[0] for e in forced], dtype=np.float64)
+        fm = np.ascontiguousarray([e[1] for e in forced], dtype=np.int32)
+        fa = np.ascontiguousarray([e[2] if len(e) > 2 else 1 for e in forced], dtype=np.int32)
         o.n_forced, o.forced_tau = len(forced), _ptr(ft)
         o.forced_m = fm.ctypes.data_as(C.POINTER(C.c_int))
+        o.forced_accept = fa.ctypes.data_as(C.POINTER(C.c_int))
     st = _Stats()
     tr = (_Trace * trace_cap)()
     tl = C.c_int64(0)

@@ -394,7 +394,7 @@ __global__ void __launch_bounds__(CTRL_THREADS, 1) k_ctrl(KParams P) {
     if (!isfinite(omega)) st->status = KIOPS_ERR_NONFINITE;
     const long long att = st->attempt;
     const bool forced = att < call->n_forced;
-    const bool accept = forced ? true : (omega <= 1.4);  // P:425 (R10)
+    const bool accept = forced ? (call->forced_acc[att] != 0) : (omega <= 1.4);  // P:425 (R10)
     double tau_new = C.tau;
     int m_new = st->m;
     if (!forced)

@@ -152,6 +152,7 @@ struct kiops_ctx_s {
   int n_forced = 0;
   double forced_tau[KIOPS_MAX_FORCED];
   int forced_m[KIOPS_MAX_FORCED];
+  int forced_acc[KIOPS_MAX_FORCED];
   long long last_attempts = 0;
   std::string err;
 };
@@ -380,7 +381,11 @@ static void fill_call(kiops_ctx c, const double *const *u, const double *T, int 
   }
   B.n_out = n_out;
   B.n_forced = c->n_forced;
-  for (int i = 0; i < c->n_forced; i++) { B.forced_tau[i] = c->forced_tau[i]; B.forced_m[i] = c->forced_m[i]; }
+  for (int i = 0; i < c->n_forced; i++) {
+    B.forced_tau[i] = c->forced_tau[i];
+    B.forced_m[i] = c->forced_m[i];
+    B.forced_acc[i] = c->forced_acc[i];
+  }
 }
 
 kiops_status kiops_apply(kiops_ctx c, const double *const *u, const double *tau_out, int n_out, double *const *w,
@@ -429,12 +434,14 @@ kiops_status kiops_get_trace(kiops_ctx c, void *host_buf, size_t bytes, int64_t 
   return KIOPS_OK;
 }
 
-kiops_status kiops_set_forced_schedule(kiops_ctx c, const double *tau, const int32_t *m, int n) {
+kiops_status kiops_set_forced_schedule(kiops_ctx c, const double *tau, const int32_t *m, const int32_t *accept,
+                                       int n) {
   if (!c || n < 0 || n > KIOPS_MAX_FORCED || (n > 0 && (!tau || !m))) return KIOPS_ERR_INVALID_ARG;
   for (int i = 0; i < n; i++) {
     if (!(tau[i] > 0.0)) return KIOPS_ERR_INVALID_ARG;
     c->forced_tau[i] = tau[i];
     c->forced_m[i] = m[i];
+    c->forced_acc[i] = accept ? (accept[i] != 0) : 1;
   }
   c->n_forced = n;
   return KIOPS_OK;

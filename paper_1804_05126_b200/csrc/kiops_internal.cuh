@@ -23,6 +23,7 @@ struct CallBlock {
   int n_forced;                  // test hook: forced schedule
   double forced_tau[KIOPS_MAX_FORCED];
   int forced_m[KIOPS_MAX_FORCED];
+  int forced_acc[KIOPS_MAX_FORCED];
 };
 
 // Controller / pass state, resident in device memory for the whole call.

@@ -429,15 +429,23 @@ __global__ void __launch_bounds__(256) k_csr_spmv(KParams P) {
   const double *xm = S.xprev;
   const int lane8 = threadIdx.x & 7;
   double v[NDOT] = {0.0, 0.0, 0.0, 0.0, 0.0};
+  // warp-uniform loop: every lane of a warp runs the same number of iterations so
+  // the 8-lane shuffles never see exited lanes (ragged N)
   const long long groups = (long long)gridDim.x * (blockDim.x / 8);
-  for (long long row = (blockIdx.x * (long long)blockDim.x + threadIdx.x) / 8; row < P.N; row += groups) {
-    const long long b0 = P.row_ptr[row], b1 = P.row_ptr[row + 1];
+  const long long g0 = (blockIdx.x * (long long)blockDim.x + threadIdx.x) / 8;
+  const long long warp_first = (blockIdx.x * (long long)blockDim.x + (threadIdx.x & ~31)) / 8;
+  for (long long it = 0; warp_first + it * groups < P.N; it++) {
+    const long long row = g0 + it * groups;
+    const bool live = row < P.N;
     double s = 0.0;
-    for (long long q = b0 + lane8; q < b1; q += 8) s += P.vals[q] * xk[P.col_idx[q]];
+    if (live) {
+      const long long b0 = P.row_ptr[row], b1 = P.row_ptr[row + 1];
+      for (long long q = b0 + lane8; q < b1; q += 8) s += P.vals[q] * xk[P.col_idx[q]];
+    }
     s += __shfl_xor_sync(0xffffffffu, s, 4);
     s += __shfl_xor_sync(0xffffffffu, s, 2);
     s += __shfl_xor_sync(0xffffffffu, s, 1);
-    if (lane8 == 0) {
+    if (live && lane8 == 0) {
       double rr = s;
 #pragma unroll
       for (int c = 0; c < KMAXP; c++)

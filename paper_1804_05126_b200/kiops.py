@@ -74,7 +74,8 @@ def lib():
                                   C.POINTER(Stats)]
         L.kiops_apply_host.argtypes = L.kiops_apply.argtypes
         L.kiops_get_trace.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.POINTER(C.c_int64)]
-        L.kiops_set_forced_schedule.argtypes = [C.c_void_p, _dp, C.POINTER(C.c_int32), C.c_int]
+        L.kiops_set_forced_schedule.argtypes = [C.c_void_p, _dp, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+                                                C.c_int]
         L.kiops_debug_basis.argtypes = [C.c_void_p, _dp, _dp, C.POINTER(C.c_int32)]
         L.kiops_destroy.argtypes = [C.c_void_p]
         L.kiops_status_string.argtypes = [C.c_int]
@@ -182,10 +183,12 @@ class Kiops:
         raise KiopsError(s, f"{what}: {msg.decode() if msg else ''}")
 
     def set_forced_schedule(self, sched):
+        """sched: list of (tau, m) (all accepted) or (tau, m, accept) (trace replay)."""
         n = len(sched)
-        tau = (C.c_double * max(1, n))(*[float(t) for t, _ in sched])
-        m = (C.c_int32 * max(1, n))(*[int(mm) for _, mm in sched])
-        s = lib().kiops_set_forced_schedule(self.ctx, tau, m, n)
+        tau = (C.c_double * max(1, n))(*[float(e[0]) for e in sched])
+        m = (C.c_int32 * max(1, n))(*[int(e[1]) for e in sched])
+        acc = (C.c_int32 * max(1, n))(*[int(e[2]) if len(e) > 2 else 1 for e in sched])
+        s = lib().kiops_set_forced_schedule(self.ctx, tau, m, acc, n)
         if s != 0:
             self._err(s, "kiops_set_forced_schedule")
 

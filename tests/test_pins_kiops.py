@@ -210,3 +210,14 @@ def test_invalid_arguments():
     assert rc == "INVALID_ARG"
     *_, rc = O.kiops(c["op"], c["u"], [0.0])
     assert rc == "INVALID_ARG"
+
+
+def test_replaying_own_trace_is_bitwise():
+    # the forced (tau, m, accept) replay hook reproduces a free run exactly (R26)
+    c = W.config4(20, 18, 16)
+    w, st, tr, rc = O.kiops(c["op"], c["u"], c["T"], tol=c["tol"])
+    sched = [(r["tau"], r["j"], r["accept"]) for r in tr]
+    w2, st2, tr2, rc2 = O.kiops(c["op"], c["u"], c["T"], tol=c["tol"], forced=sched)
+    assert rc == rc2 == "OK" and st["rejections"] > 0
+    assert all(np.array_equal(a, b) for a, b in zip(w, w2))
+    assert [(r["j"], r["accept"]) for r in tr] == [(r["j"], r["accept"]) for r in tr2]
