@@ -102,6 +102,8 @@ typedef struct {
   int32_t happy_breakdowns;
   double t_reached;       /* T_end on success                                          */
   double nu, mu;          /* Eqs. 48-49 normalisation constants used                    */
+  double pass_ms, ctrl_ms, gemv_ms; /* device-side kernel time (%globaltimer) of the fused
+                                       passes, the controller and the GEMV in this call */
 } kiops_stats;
 
 /* One row per attempt (accepted or rejected), for oracle <-> GPU trace parity. */

@@ -332,6 +332,7 @@ __global__ void __launch_bounds__(CTRL_THREADS, 1) k_ctrl(KParams P) {
   double *F = P.scratch + 9 * (size_t)LDH * LDH;   // exponential output
   double *scr = P.scratch;                          // 8 work matrices
 
+  const unsigned long long t_start = gtimer();
   if (threadIdx.x == 0) {
     C.stop = 0;
     if (st->status != 0 || st->npass < 1) C.stop = 1;
@@ -490,6 +491,7 @@ __global__ void __launch_bounds__(CTRL_THREADS, 1) k_ctrl(KParams P) {
     set_cond(P.h_outer, cont ? 1u : 0u);
     set_cond(P.h_inner, (cont && st->npass < st->m + 1) ? 1u : 0u);
     set_cond(P.h_accept, C.accept ? 1u : 0u);
+    st->ns_ctrl += gtimer() - t_start;
   }
 }
 
@@ -499,7 +501,8 @@ __global__ void __launch_bounds__(CTRL_THREADS, 1) k_ctrl(KParams P) {
 // may overwrite x_1 in place) is the last chunk.
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_gemv(KParams P) {
-  const DevState *st = P.st;
+  DevState *st = P.st;
+  if (blockIdx.x == 0 && threadIdx.x == 0) st->t_gemv0 = gtimer();
   const int j = st->gemv_j, nout = st->gemv_nout;
   const double *x1 = st->gemv_x1;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < P.N;
@@ -517,6 +520,14 @@ __global__ void __launch_bounds__(256) k_gemv(KParams P) {
 #pragma unroll
       for (int o = 0; o < GEMV_OCHUNK; o++)
         if (o0 + o < nout) st->gemv_out[o0 + o][i] = acc[o];
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(&st->gemv_ticket, 1u) == gridDim.x - 1) {
+      st->ns_gemv += gtimer() - st->t_gemv0;
+      st->gemv_ticket = 0;
     }
   }
 }

@@ -365,6 +365,9 @@ static kiops_status finish(kiops_ctx c, kiops_stats *stats) {
     stats->t_reached = S.t_now;
     stats->nu = S.nu;
     stats->mu = S.mu;
+    stats->pass_ms = S.ns_pass * 1e-6;
+    stats->ctrl_ms = S.ns_ctrl * 1e-6;
+    stats->gemv_ms = S.ns_gemv * 1e-6;
   }
   if (S.status == KIOPS_ERR_NONFINITE) { c->err = "non-finite value in the Krylov recurrence or estimate"; return KIOPS_ERR_NONFINITE; }
   if (S.status == KIOPS_ERR_NO_CONVERGENCE) { c->err = "max_attempts exceeded"; return KIOPS_ERR_NO_CONVERGENCE; }

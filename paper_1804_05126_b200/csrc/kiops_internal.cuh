@@ -41,6 +41,10 @@ struct DevState {
   unsigned int ticket;           // last-CTA counter of the grid reductions
   unsigned int ticket2;
   unsigned long long launches;   // pass launches this call (device-side loop guard)
+  // device-side kernel timing (%globaltimer, ns): graph-internal kernels cannot be
+  // bracketed by host events, so each kernel type accumulates its own duration
+  unsigned long long t_pass0, t_gemv0, ns_pass, ns_ctrl, ns_gemv;
+  unsigned int gemv_ticket;
 };
 
 // Frozen per-ctx parameters, passed BY VALUE to every kernel (graph node params).
@@ -110,11 +114,18 @@ __device__ __forceinline__ void set_cond(cudaGraphConditionalHandle h, unsigned 
   cudaGraphSetConditional(h, v);
 }
 
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 // Loop guard (block 0, thread 0 of every pass launch): the device-side WHILE loops
 // can never spin forever, even if a reduction were lost.  Returns true if tripped.
-__device__ __forceinline__ bool pass_guard(const KParams &P) {
+__device__ __forceinline__ bool pass_guard(const KParams &P, bool start_timer = true) {
   if (blockIdx.x != 0 || threadIdx.x != 0) return false;
   DevState *st = P.st;
+  if (start_timer) st->t_pass0 = gtimer();
   const unsigned long long n = ++st->launches;
   const unsigned long long cap = (unsigned long long)(P.max_attempts + 2) * (unsigned long long)(P.m_max + 2);
   if (n > cap || st->npass > P.m_max) {

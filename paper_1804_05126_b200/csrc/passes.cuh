@@ -111,6 +111,8 @@ __global__ void __launch_bounds__(256) k_setup(KParams P) {
   st->final_m = st->m;
   st->ticket = 0;
   st->launches = 0;
+  st->ns_pass = st->ns_ctrl = st->ns_gemv = 0;
+  st->gemv_ticket = 0;
   write_exact_tail(P, 0.0, mu, P.tails + 1 * KMAXP);       // t_1 at T_now = 0
   set_cond(P.h_outer, 1u);
   set_cond(P.h_inner, 1u);
@@ -188,6 +190,7 @@ __device__ void pass_finalize(const KParams &P, int k, int nblocks) {
   }
   st->passes++;
   st->npass = k;
+  st->ns_pass += gtimer() - st->t_pass0;
   if (st->status != 0) {
     set_cond(P.h_inner, 0u);
     return;
@@ -406,6 +409,7 @@ constexpr size_t stencil_smem_bytes() {
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_csr_form(KParams P) {
   __shared__ PassScalars S;
+  if (threadIdx.x == 0 && blockIdx.x == 0) P.st->t_pass0 = gtimer();
   if (threadIdx.x == 0) load_pass_scalars(P, S);
   __syncthreads();
   if (S.k <= 1) return;
@@ -420,7 +424,7 @@ __global__ void __launch_bounds__(256) k_csr_form(KParams P) {
 
 __global__ void __launch_bounds__(256) k_csr_spmv(KParams P) {
   __shared__ PassScalars S;
-  pass_guard(P);
+  pass_guard(P, false);
   if (threadIdx.x == 0) load_pass_scalars(P, S);
   __syncthreads();
   if (S.k == 0) return;
