@@ -149,6 +149,14 @@ kiops_status kiops_apply(kiops_ctx c, const double *const *u, const double *tau_
 kiops_status kiops_apply_host(kiops_ctx c, const double *const *u, const double *tau_out, int n_out,
                               double *const *w, kiops_stats *stats);
 
+/* TEST / PROFILING HOOK (not the product path): the same computation with the
+ * graph's WHILE/IF control flow run on the host -- the identical kernels are
+ * launched one by one with a device->host read of the loop conditions after each.
+ * Exists because Nsight Compute cannot profile kernel nodes of graphs that contain
+ * conditional nodes.  Same arguments and results as kiops_apply (bitwise). */
+kiops_status kiops_apply_hostloop(kiops_ctx c, const double *const *u, const double *tau_out, int n_out,
+                                  double *const *w, kiops_stats *stats);
+
 /* Copies the decision trace of the last apply (one kiops_trace_row per attempt,
  * at most KIOPS_TRACE_CAP) into host_buf (HOST, `bytes` long); *rows = rows
  * available (may exceed what fit). */

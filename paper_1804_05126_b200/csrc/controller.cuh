@@ -353,7 +353,7 @@ __global__ void __launch_bounds__(CTRL_THREADS, 1) k_ctrl(KParams P) {
   __syncthreads();
   if (C.stop == 1) {
     if (threadIdx.x == 0) {
-      set_cond(P.h_outer, 0u); set_cond(P.h_inner, 0u); set_cond(P.h_accept, 0u);
+      set_cond(P, COND_OUTER, 0u); set_cond(P, COND_INNER, 0u); set_cond(P, COND_ACCEPT, 0u);
     }
     return;
   }
@@ -368,7 +368,7 @@ __global__ void __launch_bounds__(CTRL_THREADS, 1) k_ctrl(KParams P) {
       st->t_now = st->t_end;
       st->substeps++;
       st->attempt++;
-      set_cond(P.h_outer, 0u); set_cond(P.h_inner, 0u); set_cond(P.h_accept, 1u);
+      set_cond(P, COND_OUTER, 0u); set_cond(P, COND_INNER, 0u); set_cond(P, COND_ACCEPT, 1u);
     }
     return;
   }
@@ -488,9 +488,9 @@ __global__ void __launch_bounds__(CTRL_THREADS, 1) k_ctrl(KParams P) {
     const bool more = st->status == 0 && st->t_now < st->t_end;
     bool cont = more && st->attempt < P.max_attempts;
     if (more && !cont) st->status = KIOPS_ERR_NO_CONVERGENCE;
-    set_cond(P.h_outer, cont ? 1u : 0u);
-    set_cond(P.h_inner, (cont && st->npass < st->m + 1) ? 1u : 0u);
-    set_cond(P.h_accept, C.accept ? 1u : 0u);
+    set_cond(P, COND_OUTER, cont ? 1u : 0u);
+    set_cond(P, COND_INNER, (cont && st->npass < st->m + 1) ? 1u : 0u);
+    set_cond(P, COND_ACCEPT, C.accept ? 1u : 0u);
     st->ns_ctrl += gtimer() - t_start;
   }
 }

@@ -34,11 +34,15 @@ constexpr int SM_COUNT_HINT = 148;
 #define T1D 1, 256, 1, 1
 #define T2D 2, 64, 16, 1
 #define T3D 3, 32, 8, 4
+#define M3X 64
+#define M3Y 8
+#define M3Z 32
 
 struct Layout {
   size_t V, r, staging, state, call, H, sig, R2, tails, partials, npart, scratch, coef, trace, total;
   long long ldN;
   int grid_pass, grid_setup, grid_gemv, grid_form, grid_max;
+  int block_pass;
   size_t smem_pass;
 };
 
@@ -69,6 +73,7 @@ kiops_status validate(const kiops_operator_desc *op, int p, const kiops_options 
       break;
     case KIOPS_OP_STENCIL3D7_VARKAPPA:
       if (!op->kappa) { err = "3D stencil needs kappa"; return KIOPS_ERR_INVALID_ARG; }
+      if (op->nx * op->ny > 2147483647LL) { err = "3D stencil planes must have < 2^31 points"; return KIOPS_ERR_UNSUPPORTED; }
       break;
     case KIOPS_OP_CSR:
       if (op->ny != 1 || op->nz != 1) { err = "CSR needs ny = nz = 1 (nx = rows)"; return KIOPS_ERR_INVALID_ARG; }
@@ -87,6 +92,7 @@ Layout layout(const kiops_operator_desc *op, int p, const kiops_options *o) {
   Layout L{};
   const long long N = op_n(op);
   L.ldN = (N + 31) & ~31LL;
+  L.block_pass = 256;
   const long long blocks256 = (N + 255) / 256;
   L.grid_setup = (int)std::min<long long>(blocks256, SM_COUNT_HINT * 8);
   L.grid_gemv = (int)std::min<long long>(blocks256, SM_COUNT_HINT * 8);
@@ -101,8 +107,9 @@ Layout layout(const kiops_operator_desc *op, int p, const kiops_options *o) {
       L.smem_pass = stencil_smem_bytes<T2D>();
       break;
     case KIOPS_OP_STENCIL3D7_VARKAPPA:
-      L.grid_pass = (int)(((op->nx + 31) / 32) * ((op->ny + 7) / 8) * ((op->nz + 3) / 4));
-      L.smem_pass = stencil_smem_bytes<T3D>();
+      L.grid_pass = (int)(((op->nx + M3X - 1) / M3X) * ((op->ny + M3Y - 1) / M3Y) * ((op->nz + M3Z - 1) / M3Z));
+      L.smem_pass = march3d_smem_bytes<M3X, M3Y, M3Z>();
+      L.block_pass = M3X * M3Y;
       break;
     default:
       L.grid_pass = (int)std::min<long long>((8 * N + 255) / 256, SM_COUNT_HINT * 8);
@@ -154,6 +161,7 @@ struct kiops_ctx_s {
   int forced_m[KIOPS_MAX_FORCED];
   int forced_acc[KIOPS_MAX_FORCED];
   long long last_attempts = 0;
+  void *fpass = nullptr;         // stencil pass kernel (NULL for CSR)
   std::string err;
 };
 
@@ -206,9 +214,14 @@ static kiops_status build_graph(kiops_ctx c) {
   switch (c->op.kind) {
     case KIOPS_OP_STENCIL1D3: fpass = (void *)k_pass_stencil<T1D>; break;
     case KIOPS_OP_STENCIL2D5: fpass = (void *)k_pass_stencil<T2D>; break;
-    case KIOPS_OP_STENCIL3D7_VARKAPPA: fpass = (void *)k_pass_stencil<T3D>; break;
+    case KIOPS_OP_STENCIL3D7_VARKAPPA:
+      fpass = c->p <= 2 ? (void *)k_pass_3d_march<M3X, M3Y, M3Z, 2>
+            : c->p <= 4 ? (void *)k_pass_3d_march<M3X, M3Y, M3Z, 4>
+                        : (void *)k_pass_3d_march<M3X, M3Y, M3Z, 8>;
+      break;
     default: break;
   }
+  c->fpass = fpass;
   if (fpass && c->L.smem_pass > 48 * 1024)
     CK(cudaFuncSetAttribute(fpass, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->L.smem_pass), "smem attr pass");
   CK(cudaFuncSetAttribute((void *)k_ctrl, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctrl_smem_bytes()),
@@ -223,7 +236,7 @@ static kiops_status build_graph(kiops_ctx c) {
     CK(add_kernel(b_inner, &n_a, nullptr, 0, (void *)k_csr_form, c->L.grid_form, 256, 0, &P), "node form");
     CK(add_kernel(b_inner, &n_b, &n_a, 1, (void *)k_csr_spmv, c->L.grid_pass, 256, 0, &P), "node spmv");
   } else {
-    CK(add_kernel(b_inner, &n_a, nullptr, 0, fpass, c->L.grid_pass, 256, c->L.smem_pass, &P), "node pass");
+    CK(add_kernel(b_inner, &n_a, nullptr, 0, fpass, c->L.grid_pass, c->L.block_pass, c->L.smem_pass, &P), "node pass");
   }
   CK(add_kernel(b_outer, &n_ctrl, &n_inner, 1, (void *)k_ctrl, 1, CTRL_THREADS, ctrl_smem_bytes(), &P), "node ctrl");
   CK(add_cond(b_outer, &n_if, &n_ctrl, 1, P.h_accept, cudaGraphCondTypeIf, &b_if), "node if");
@@ -422,6 +435,48 @@ kiops_status kiops_apply_host(kiops_ctx c, const double *const *u, const double 
   s = launch_and_finish(c, stats);
   if (s != KIOPS_OK) return s;
   for (int l = 0; l < n_out; l++) CK(cudaMemcpyAsync(w[l], wd[l], vb, cudaMemcpyDeviceToHost, c->stream), "D2H w");
+  return finish(c, stats);
+}
+
+static kiops_status launch_plain(kiops_ctx c, void *f, int grid, int block, size_t smem, KParams *P) {
+  void *args[] = {P};
+  CK(cudaLaunchKernel(f, dim3(grid), dim3(block), args, smem, c->stream), "cudaLaunchKernel");
+  return KIOPS_OK;
+}
+
+static kiops_status read_conds(kiops_ctx c, unsigned *cond) {
+  CK(cudaMemcpyAsync(cond, c->P.st->cond, sizeof(unsigned) * 3, cudaMemcpyDeviceToHost, c->stream), "D2H cond");
+  CK(cudaStreamSynchronize(c->stream), "sync cond");
+  return KIOPS_OK;
+}
+
+kiops_status kiops_apply_hostloop(kiops_ctx c, const double *const *u, const double *tau_out, int n_out,
+                                  double *const *w, kiops_stats *stats) {
+  kiops_status s = check_call(c, u, tau_out, n_out, w);
+  if (s != KIOPS_OK) return s;
+  fill_call(c, u, tau_out, n_out, w);
+  KParams P = c->P;
+  P.no_cond = 1;
+  unsigned *cond = (unsigned *)(c->h_state);  // scratch in pinned memory, overwritten below
+  CK(cudaMemcpyAsync(c->P.call, c->h_call, sizeof(CallBlock), cudaMemcpyHostToDevice, c->stream), "H2D call block");
+  if ((s = launch_plain(c, (void *)k_setup, c->L.grid_setup, 256, 0, &P)) != KIOPS_OK) return s;
+  if ((s = read_conds(c, cond)) != KIOPS_OK) return s;
+  while (cond[COND_OUTER]) {
+    while (cond[COND_INNER]) {
+      if (c->op.kind == KIOPS_OP_CSR) {
+        if ((s = launch_plain(c, (void *)k_csr_form, c->L.grid_form, 256, 0, &P)) != KIOPS_OK) return s;
+        if ((s = launch_plain(c, (void *)k_csr_spmv, c->L.grid_pass, 256, 0, &P)) != KIOPS_OK) return s;
+      } else {
+        if ((s = launch_plain(c, c->fpass, c->L.grid_pass, c->L.block_pass, c->L.smem_pass, &P)) != KIOPS_OK) return s;
+      }
+      if ((s = read_conds(c, cond)) != KIOPS_OK) return s;
+    }
+    if ((s = launch_plain(c, (void *)k_ctrl, 1, CTRL_THREADS, ctrl_smem_bytes(), &P)) != KIOPS_OK) return s;
+    if ((s = read_conds(c, cond)) != KIOPS_OK) return s;
+    if (cond[COND_ACCEPT])
+      if ((s = launch_plain(c, (void *)k_gemv, c->L.grid_gemv, 256, 0, &P)) != KIOPS_OK) return s;
+  }
+  CK(cudaMemcpyAsync(c->h_state, c->P.st, sizeof(DevState), cudaMemcpyDeviceToHost, c->stream), "D2H state");
   return finish(c, stats);
 }
 

@@ -45,6 +45,7 @@ struct DevState {
   // bracketed by host events, so each kernel type accumulates its own duration
   unsigned long long t_pass0, t_gemv0, ns_pass, ns_ctrl, ns_gemv;
   unsigned int gemv_ticket;
+  unsigned int cond[3];          // mirror of the graph conditionals (outer, inner, accept)
 };
 
 // Frozen per-ctx parameters, passed BY VALUE to every kernel (graph node params).
@@ -75,8 +76,10 @@ struct KParams {
   double *coef;       // (KMAXO+1) x LDH    (GEMV coefficients)
   kiops_trace_row *trace;
   int grid_pass, grid_max;
+  int no_cond;        // 1: launched outside the graph (host-loop profiling hook)
   cudaGraphConditionalHandle h_outer, h_inner, h_accept;
 };
+enum { COND_OUTER = 0, COND_INNER = 1, COND_ACCEPT = 2 };
 
 __device__ __forceinline__ const double *slot_ptr(const KParams &P, int k) {
   // x_k for k >= 1 ; x_1 comes from the state's source pointer
@@ -110,8 +113,10 @@ __device__ __forceinline__ void block_sum(double (&v)[NV], double *red /* smem N
   __syncthreads();
 }
 
-__device__ __forceinline__ void set_cond(cudaGraphConditionalHandle h, unsigned v) {
-  cudaGraphSetConditional(h, v);
+__device__ __forceinline__ void set_cond(const KParams &P, int which, unsigned v) {
+  if (!P.no_cond)
+    cudaGraphSetConditional(which == COND_OUTER ? P.h_outer : which == COND_INNER ? P.h_inner : P.h_accept, v);
+  P.st->cond[which] = v;
 }
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -130,8 +135,8 @@ __device__ __forceinline__ bool pass_guard(const KParams &P, bool start_timer = 
   const unsigned long long cap = (unsigned long long)(P.max_attempts + 2) * (unsigned long long)(P.m_max + 2);
   if (n > cap || st->npass > P.m_max) {
     st->status = KIOPS_ERR_CUDA;
-    cudaGraphSetConditional(P.h_inner, 0u);
-    cudaGraphSetConditional(P.h_outer, 0u);
+    set_cond(P, COND_INNER, 0u);
+    set_cond(P, COND_OUTER, 0u);
     return true;
   }
   return false;

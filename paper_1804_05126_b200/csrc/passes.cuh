@@ -114,9 +114,9 @@ __global__ void __launch_bounds__(256) k_setup(KParams P) {
   st->ns_pass = st->ns_ctrl = st->ns_gemv = 0;
   st->gemv_ticket = 0;
   write_exact_tail(P, 0.0, mu, P.tails + 1 * KMAXP);       // t_1 at T_now = 0
-  set_cond(P.h_outer, 1u);
-  set_cond(P.h_inner, 1u);
-  set_cond(P.h_accept, 0u);
+  set_cond(P, COND_OUTER, 1u);
+  set_cond(P, COND_INNER, 1u);
+  set_cond(P, COND_ACCEPT, 0u);
 }
 
 // ---------------------------------------------------------------------------
@@ -192,12 +192,12 @@ __device__ void pass_finalize(const KParams &P, int k, int nblocks) {
   st->npass = k;
   st->ns_pass += gtimer() - st->t_pass0;
   if (st->status != 0) {
-    set_cond(P.h_inner, 0u);
+    set_cond(P, COND_INNER, 0u);
     return;
   }
   if (!isfinite(S) || !isfinite(G) || !isfinite(E1) || !isfinite(E2) || !isfinite(R)) {
     st->status = KIOPS_ERR_NONFINITE;  // R22
-    set_cond(P.h_inner, 0u);
+    set_cond(P, COND_INNER, 0u);
     return;
   }
   const double sk = sqrt(S);
@@ -210,13 +210,13 @@ __device__ void pass_finalize(const KParams &P, int k, int nblocks) {
     P.R2[1] = R;
     if (sk == 0.0) {  // R27
       st->zero_start = 1;
-      set_cond(P.h_inner, 0u);
+      set_cond(P, COND_INNER, 0u);
       return;
     }
     const double h11 = E2 / (sk * sk);
     HH(1, 1) = h11;
     for (int c = 0; c < p; c++) tn[c] = Kt[c] / sk - h11 * tk[c] / sk;
-    set_cond(P.h_inner, (1 < st->m + 1) ? 1u : 0u);
+    set_cond(P, COND_INNER, (1 < st->m + 1) ? 1u : 0u);
     return;
   }
   // k >= 2 closes Alg. 2 iteration k-1
@@ -226,7 +226,7 @@ __device__ void pass_finalize(const KParams &P, int k, int nblocks) {
   const double thr = fmax(1e-12 * cn, 1e-14);  // R3
   if (sk <= thr) {                             // Alg. 2 l.12-15
     st->happy = 1;
-    set_cond(P.h_inner, 0u);
+    set_cond(P, COND_INNER, 0u);
     return;
   }
   HH(k, k - 1) = sk;  // l.16 (R2)
@@ -237,7 +237,7 @@ __device__ void pass_finalize(const KParams &P, int k, int nblocks) {
   HH(k - 1, k) = h1;
   HH(k, k) = h2;
   for (int c = 0; c < p; c++) tn[c] = Kt[c] / sk - h1 * tkm1[c] / skm1 - h2 * tk[c] / sk;
-  set_cond(P.h_inner, (k < st->m + 1) ? 1u : 0u);
+  set_cond(P, COND_INNER, (k < st->m + 1) ? 1u : 0u);
 #undef HH
 }
 
@@ -464,4 +464,161 @@ __global__ void __launch_bounds__(256) k_csr_spmv(KParams P) {
     }
   }
   pass_epilogue(P, k, v);
+}
+
+// ---------------------------------------------------------------------------
+// 3D variable-kappa pass, v2: 2.5D z-marching.  A CTA owns a TX x TY column of
+// the grid and a chunk of ZC z-planes; planes stream through shared-memory rings:
+//   x_{k-1}, kappa : halo-2 planes (ring 4 / 5)  -> A x_{k-1} on the halo-1 plane
+//   x_k            : halo-1 planes (ring 3)      -> r = A~ x_k on the interior
+//   nu B t_k       : interior planes (ring 2)
+// so each array is read from HBM once per pass (xy halos and the 2-plane z
+// warm-up of a chunk come from L2).  Two barriers per plane.  PM >= p bounds the
+// B terms held in registers.
+// ---------------------------------------------------------------------------
+template <int TX, int TY, int ZC, int PM>
+__global__ void __launch_bounds__(TX *TY, 2) k_pass_3d_march(KParams P) {
+  constexpr int NT = TX * TY, HX = TX + 4, HY = TY + 4, S2 = HX * HY, GX = TX + 2, GY = TY + 2, S1 = GX * GY;
+  constexpr int L2N = (S2 + NT - 1) / NT, L1N = (S1 + NT - 1) / NT;
+  extern __shared__ double smem[];
+  double *sXP = smem;             // 4 x S2
+  double *sKP = sXP + 4 * S2;     // 5 x S2
+  double *sXK = sKP + 5 * S2;     // 3 x S1
+  double *sBT = sXK + 3 * S1;     // 2 x NT
+
+  __shared__ PassScalars S;
+  pass_guard(P);
+  if (threadIdx.x == 0) load_pass_scalars(P, S);
+  __syncthreads();
+  if (S.k == 0) return;
+  const int p = P.p;
+  const long long nx = P.nx, ny = P.ny, nz = P.nz, nxy = nx * ny;
+  const long long ntx = (nx + TX - 1) / TX, nty = (ny + TY - 1) / TY;
+  const long long b = blockIdx.x;
+  const long long ox = (b % ntx) * TX, oy = ((b / ntx) % nty) * TY;
+  const long long z0 = (b / (ntx * nty)) * ZC;
+  const long long z1 = (z0 + ZC < nz) ? z0 + ZC : nz;
+  const int tid = threadIdx.x;
+  const double ih2 = P.inv_h2;
+  const double *__restrict__ xprev = S.xprev;
+  const double *__restrict__ kap = P.kappa;
+  const double *__restrict__ xpp = S.xpp;
+
+  // per-thread plane offsets (wrapped xy), computed once
+  int off2[L2N];  // in-plane offsets (nx*ny < 2^31 is validated at create)
+  int e2s[L2N];
+#pragma unroll
+  for (int q = 0; q < L2N; q++) {
+    const int e = tid + q * NT;
+    e2s[q] = e < S2 ? e : -1;
+    const int a = e % HX, bb = e / HX;
+    off2[q] = (int)(wrapc(ox + a - 2, nx) + nx * wrapc(oy + bb - 2, ny));
+  }
+  int off1[L1N];
+  int f1s[L1N], f2s[L1N], fin[L1N];
+#pragma unroll
+  for (int q = 0; q < L1N; q++) {
+    const int e = tid + q * NT;
+    f1s[q] = e < S1 ? e : -1;
+    const int a = e % GX, bb = e / GX;
+    off1[q] = (int)(wrapc(ox + a - 1, nx) + nx * wrapc(oy + bb - 1, ny));
+    f2s[q] = (a + 1) + HX * (bb + 1);
+    fin[q] = (a >= 1 && a <= TX && bb >= 1 && bb <= TY) ? (a - 1) + TX * (bb - 1) : -1;
+  }
+  const int ia = tid % TX, ib = tid / TX;
+  const int ie1 = (ia + 1) + GX * (ib + 1), ie2 = (ia + 2) + HX * (ib + 2);
+  const long long gx = ox + ia, gy = oy + ib;
+  const bool inside = gx < nx && gy < ny;
+
+  auto rz = [&](long long z) { return (int)(z - z0 + 2); };  // >= 0 for z >= z0 - 2
+  auto load_plane = [&](long long z) {
+    const long long zo = nxy * wrapc(z, nz);
+    const int r = rz(z);
+    double *dx = sXP + (r & 3) * S2;
+    double *dk = sKP + (r % 5) * S2;
+#pragma unroll
+    for (int q = 0; q < L2N; q++)
+      if (e2s[q] >= 0) {
+        dx[e2s[q]] = xprev[off2[q] + zo];
+        dk[e2s[q]] = kap[off2[q] + zo];
+      }
+  };
+
+  double v[NDOT] = {0.0, 0.0, 0.0, 0.0, 0.0};
+  load_plane(z0 - 2);
+  load_plane(z0 - 1);
+  for (long long zf = z0 - 1; zf <= z1; zf++) {
+    // formation-plane operands from HBM first (latency overlaps the plane load)
+    const long long zo = nxy * wrapc(zf, nz);
+    double bv[L1N][PM], xq[L1N];
+#pragma unroll
+    for (int q = 0; q < L1N; q++) {
+      xq[q] = 0.0;
+#pragma unroll
+      for (int c = 0; c < PM; c++) bv[q][c] = 0.0;
+      if (f1s[q] >= 0) {
+        if (xpp) xq[q] = xpp[off1[q] + zo];
+#pragma unroll
+        for (int c = 0; c < PM; c++)
+          if (c < p) bv[q][c] = S.B[c][off1[q] + zo];
+      }
+    }
+    load_plane(zf + 1);
+    __syncthreads();
+    // formation of x_k on the halo-1 plane zf
+    {
+      const int r0 = rz(zf);
+      const double *X0 = sXP + (r0 & 3) * S2, *Xm = sXP + ((r0 - 1) & 3) * S2, *Xp = sXP + ((r0 + 1) & 3) * S2;
+      const double *K0 = sKP + (r0 % 5) * S2, *Km = sKP + ((r0 + 4) % 5) * S2, *Kp = sKP + ((r0 + 1) % 5) * S2;
+      double *XK = sXK + (r0 % 3) * S1;
+      double *BT = sBT + (r0 & 1) * NT;
+#pragma unroll
+      for (int q = 0; q < L1N; q++) {
+        if (f1s[q] < 0) continue;
+        const int e = f2s[q];
+        const double xc = X0[e], kc = K0[e];
+        double ax = 0.5 * (kc + K0[e - 1]) * (X0[e - 1] - xc) + 0.5 * (kc + K0[e + 1]) * (X0[e + 1] - xc) +
+                    0.5 * (kc + K0[e - HX]) * (X0[e - HX] - xc) + 0.5 * (kc + K0[e + HX]) * (X0[e + HX] - xc) +
+                    0.5 * (kc + Km[e]) * (Xm[e] - xc) + 0.5 * (kc + Kp[e]) * (Xp[e] - xc);
+        ax *= ih2;
+        double bp = 0.0, bc = 0.0;
+#pragma unroll
+        for (int c = 0; c < PM; c++) {
+          bp += bv[q][c] * S.btp[c];
+          bc += bv[q][c] * S.btc[c];
+        }
+        const double xk = S.a0 * (ax + bp) - S.a1 * xc - S.a2 * xq[q];
+        XK[f1s[q]] = xk;
+        if (fin[q] >= 0) BT[fin[q]] = bc;
+      }
+    }
+    __syncthreads();
+    // output plane z = zf - 1: r = A~ x_k, dots, store x_k
+    const long long z = zf - 1;
+    if (z >= z0) {
+      const int r0 = rz(z);
+      const double *XK0 = sXK + (r0 % 3) * S1, *XKm = sXK + ((r0 + 2) % 3) * S1, *XKp = sXK + ((r0 + 1) % 3) * S1;
+      const double *K0 = sKP + (r0 % 5) * S2, *Km = sKP + ((r0 + 4) % 5) * S2, *Kp = sKP + ((r0 + 1) % 5) * S2;
+      const double xk = XK0[ie1], kc = K0[ie2];
+      double r = 0.5 * (kc + K0[ie2 - 1]) * (XK0[ie1 - 1] - xk) + 0.5 * (kc + K0[ie2 + 1]) * (XK0[ie1 + 1] - xk) +
+                 0.5 * (kc + K0[ie2 - HX]) * (XK0[ie1 - GX] - xk) + 0.5 * (kc + K0[ie2 + HX]) * (XK0[ie1 + GX] - xk) +
+                 0.5 * (kc + Km[ie2]) * (XKm[ie1] - xk) + 0.5 * (kc + Kp[ie2]) * (XKp[ie1] - xk);
+      r = r * ih2 + sBT[(r0 & 1) * NT + tid];
+      if (inside) {
+        const double xm = sXP[(r0 & 3) * S2 + ie2];
+        v[0] += xk * xk;
+        v[1] += xm * xk;
+        v[2] += xm * r;
+        v[3] += xk * r;
+        v[4] += r * r;
+        if (S.xout) S.xout[gx + nx * gy + nxy * z] = xk;
+      }
+    }
+  }
+  pass_epilogue(P, S.k, v);
+}
+
+template <int TX, int TY, int ZC>
+constexpr size_t march3d_smem_bytes() {
+  return sizeof(double) * (size_t)(9 * (TX + 4) * (TY + 4) + 3 * (TX + 2) * (TY + 2) + 2 * TX * TY);
 }

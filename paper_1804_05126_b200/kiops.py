@@ -51,7 +51,7 @@ class TraceRow(C.Structure):
 
 
 SYMBOLS = ["kiops_options_default", "kiops_workspace_bytes", "kiops_create", "kiops_apply",
-           "kiops_apply_host", "kiops_get_trace", "kiops_set_forced_schedule", "kiops_debug_basis",
+           "kiops_apply_host", "kiops_apply_hostloop", "kiops_get_trace", "kiops_set_forced_schedule", "kiops_debug_basis",
            "kiops_destroy", "kiops_status_string", "kiops_last_error"]
 
 _lib = None
@@ -73,6 +73,7 @@ def lib():
         L.kiops_apply.argtypes = [C.c_void_p, C.POINTER(C.c_void_p), _dp, C.c_int, C.POINTER(C.c_void_p),
                                   C.POINTER(Stats)]
         L.kiops_apply_host.argtypes = L.kiops_apply.argtypes
+        L.kiops_apply_hostloop.argtypes = L.kiops_apply.argtypes
         L.kiops_get_trace.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.POINTER(C.c_int64)]
         L.kiops_set_forced_schedule.argtypes = [C.c_void_p, _dp, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
                                                 C.c_int]
@@ -82,7 +83,7 @@ def lib():
         L.kiops_status_string.restype = C.c_char_p
         L.kiops_last_error.argtypes = [C.c_void_p]
         L.kiops_last_error.restype = C.c_char_p
-        for name in ("kiops_workspace_bytes", "kiops_create", "kiops_apply", "kiops_apply_host",
+        for name in ("kiops_workspace_bytes", "kiops_create", "kiops_apply", "kiops_apply_host", "kiops_apply_hostloop",
                      "kiops_get_trace", "kiops_set_forced_schedule", "kiops_debug_basis", "kiops_destroy"):
             getattr(L, name).restype = C.c_int
         _lib = L
@@ -192,9 +193,9 @@ class Kiops:
         if s != 0:
             self._err(s, "kiops_set_forced_schedule")
 
-    def apply(self, u, T, w=None, check=True):
+    def apply(self, u, T, w=None, check=True, hostloop=False):
         """u: p+1 CUDA float64 tensors (N,), T: output times, w: optional outputs.
-        Returns (list of output tensors, stats dict)."""
+        hostloop: profiling hook (kiops_apply_hostloop).  Returns (outputs, stats)."""
         torch = self.torch
         T = [float(t) for t in T]
         if w is None:
@@ -203,7 +204,8 @@ class Kiops:
         warr = (C.c_void_p * len(T))(*[x.data_ptr() for x in w])
         Tarr = (C.c_double * len(T))(*T)
         st = Stats()
-        s = lib().kiops_apply(self.ctx, uarr, Tarr, len(T), warr, C.byref(st))
+        fn = lib().kiops_apply_hostloop if hostloop else lib().kiops_apply
+        s = fn(self.ctx, uarr, Tarr, len(T), warr, C.byref(st))
         self.last_stats = {k: getattr(st, k) for k, _ in Stats._fields_}
         if s != 0 and check:
             self._err(s, "kiops_apply")

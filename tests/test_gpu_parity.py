@@ -244,3 +244,17 @@ def test_repeatable_bitwise():
     a = a[0].cpu().numpy()
     b, _ = k.apply(u, c["T"])
     assert np.array_equal(a, b[0].cpu().numpy())
+
+
+def test_hostloop_hook_is_bitwise_identical():
+    # the profiling hook runs the same kernels with host-side control flow
+    from paper_1804_05126_b200 import Kiops
+
+    for c in (W.config4(24, 20, 16), W.config5(20, 20, 20), W.config1()):
+        k = Kiops(c["op"], c["p"], device=DEV, tol=c["tol"])
+        u = [torch.as_tensor(x, device=DEV) for x in c["u"]]
+        a, sa = k.apply(u, c["T"])
+        a = [x.cpu().numpy() for x in a]
+        b, sb = k.apply(u, c["T"], hostloop=True)
+        assert all(np.array_equal(x, y.cpu().numpy()) for x, y in zip(a, b))
+        assert sa["krylov_vectors"] == sb["krylov_vectors"] and sa["passes"] == sb["passes"]
