@@ -108,7 +108,8 @@ Layout layout(const kiops_operator_desc *op, int p, const kiops_options *o) {
       break;
     case KIOPS_OP_STENCIL3D7_VARKAPPA:
       L.grid_pass = (int)(((op->nx + M3X - 1) / M3X) * ((op->ny + M3Y - 1) / M3Y) * ((op->nz + M3Z - 1) / M3Z));
-      L.smem_pass = march3d_smem_bytes<M3X, M3Y, M3Z>();
+      L.smem_pass = sizeof(double) * (p <= 2 ? March3<M3X, M3Y, 2>::smem_doubles
+                                     : p <= 4 ? March3<M3X, M3Y, 4>::smem_doubles : March3<M3X, M3Y, 8>::smem_doubles);
       L.block_pass = M3X * M3Y;
       break;
     default:
@@ -215,9 +216,9 @@ static kiops_status build_graph(kiops_ctx c) {
     case KIOPS_OP_STENCIL1D3: fpass = (void *)k_pass_stencil<T1D>; break;
     case KIOPS_OP_STENCIL2D5: fpass = (void *)k_pass_stencil<T2D>; break;
     case KIOPS_OP_STENCIL3D7_VARKAPPA:
-      fpass = c->p <= 2 ? (void *)k_pass_3d_march<M3X, M3Y, M3Z, 2>
-            : c->p <= 4 ? (void *)k_pass_3d_march<M3X, M3Y, M3Z, 4>
-                        : (void *)k_pass_3d_march<M3X, M3Y, M3Z, 8>;
+      fpass = c->p <= 2 ? (void *)k_pass_3d_async<M3X, M3Y, M3Z, 2>
+            : c->p <= 4 ? (void *)k_pass_3d_async<M3X, M3Y, M3Z, 4>
+                        : (void *)k_pass_3d_async<M3X, M3Y, M3Z, 8>;
       break;
     default: break;
   }

@@ -622,3 +622,183 @@ template <int TX, int TY, int ZC>
 constexpr size_t march3d_smem_bytes() {
   return sizeof(double) * (size_t)(9 * (TX + 4) * (TY + 4) + 3 * (TX + 2) * (TY + 2) + 2 * TX * TY);
 }
+
+// ---------------------------------------------------------------------------
+// 3D variable-kappa pass, v3: z-marching with asynchronous global->shared copies
+// (cp.async, LDGSTS) issued D planes ahead, so HBM latency overlaps the stencil
+// work of the current plane.  Rings (live planes after the first barrier):
+//   x_{k-1}, kappa : halo-2, D+3 / D+4 slots
+//   x_{k-2}, B     : halo-1, DF+1 slots (formation operands)
+//   x_k            : halo-1, 3 slots;  nu B t_k : interior, 2 slots
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void cp_async8(double *dst, const double *src) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+template <int TX, int TY, int PM>
+struct March3 {
+  static constexpr int NT = TX * TY, HX = TX + 4, HY = TY + 4, S2 = HX * HY, GX = TX + 2, GY = TY + 2, S1 = GX * GY;
+  static constexpr int D = PM <= 4 ? 2 : 1;       // planes in flight (both rings)
+  static constexpr int DF = D;
+  static constexpr int RX = D + 3, RK = D + 4, RF = DF + 1;
+  static constexpr int L2N = (S2 + NT - 1) / NT, L1N = (S1 + NT - 1) / NT;
+  static constexpr size_t smem_doubles = (size_t)RX * S2 + (size_t)RK * S2 + (size_t)RF * S1 * (1 + PM) +
+                                         3 * (size_t)S1 + 2 * (size_t)NT;
+};
+
+template <int TX, int TY, int ZC, int PM>
+__global__ void __launch_bounds__(TX *TY, 1) k_pass_3d_async(KParams P) {
+  using M = March3<TX, TY, PM>;
+  constexpr int NT = M::NT, HX = M::HX, S2 = M::S2, GX = M::GX, S1 = M::S1, D = M::D, DF = M::DF;
+  constexpr int RX = M::RX, RK = M::RK, RF = M::RF, L2N = M::L2N, L1N = M::L1N;
+  extern __shared__ double smem[];
+  double *sXP = smem;                 // RX x S2
+  double *sKP = sXP + RX * S2;        // RK x S2
+  double *sF = sKP + RK * S2;         // RF x (1+PM) x S1 : [slot][0] = x_{k-2}, [slot][1+c] = B_c
+  double *sXK = sF + RF * (1 + PM) * S1;  // 3 x S1
+  double *sBT = sXK + 3 * S1;         // 2 x NT
+
+  __shared__ PassScalars S;
+  pass_guard(P);
+  if (threadIdx.x == 0) load_pass_scalars(P, S);
+  __syncthreads();
+  if (S.k == 0) return;
+  const int p = P.p;
+  const long long nx = P.nx, ny = P.ny, nz = P.nz, nxy = nx * ny;
+  const long long ntx = (nx + TX - 1) / TX, nty = (ny + TY - 1) / TY;
+  const long long b = blockIdx.x;
+  const long long ox = (b % ntx) * TX, oy = ((b / ntx) % nty) * TY;
+  const long long z0 = (b / (ntx * nty)) * ZC;
+  const long long z1 = (z0 + ZC < nz) ? z0 + ZC : nz;
+  const int tid = threadIdx.x;
+  const double ih2 = P.inv_h2;
+  const bool has_pp = S.xpp != nullptr;
+
+  int off2[L2N], e2s[L2N];
+#pragma unroll
+  for (int q = 0; q < L2N; q++) {
+    const int e = tid + q * NT;
+    e2s[q] = e < S2 ? e : -1;
+    const int a = e % HX, bb = e / HX;
+    off2[q] = (int)(wrapc(ox + a - 2, nx) + nx * wrapc(oy + bb - 2, ny));
+  }
+  int off1[L1N], f1s[L1N], f2s[L1N], fin[L1N];
+#pragma unroll
+  for (int q = 0; q < L1N; q++) {
+    const int e = tid + q * NT;
+    f1s[q] = e < S1 ? e : -1;
+    const int a = e % GX, bb = e / GX;
+    off1[q] = (int)(wrapc(ox + a - 1, nx) + nx * wrapc(oy + bb - 1, ny));
+    f2s[q] = (a + 1) + HX * (bb + 1);
+    fin[q] = (a >= 1 && a <= TX && bb >= 1 && bb <= TY) ? (a - 1) + TX * (bb - 1) : -1;
+  }
+  const int ia = tid % TX, ib = tid / TX;
+  const int ie1 = (ia + 1) + GX * (ib + 1), ie2 = (ia + 2) + HX * (ib + 2);
+  const long long gx = ox + ia, gy = oy + ib;
+  const bool inside = gx < nx && gy < ny;
+
+  // async plane loaders (every thread its own elements; one commit per step)
+  auto issue_xk = [&](long long z) {  // x_{k-1} and kappa, halo-2 plane z
+    const long long zo = nxy * wrapc(z, nz);
+    const int r = (int)(z - z0 + 2);
+    const double *gxp = S.xprev + zo, *gkp = P.kappa + zo;
+    double *dx = sXP + (r % RX) * S2, *dk = sKP + (r % RK) * S2;
+#pragma unroll
+    for (int q = 0; q < L2N; q++)
+      if (e2s[q] >= 0) {
+        cp_async8(dx + e2s[q], gxp + off2[q]);
+        cp_async8(dk + e2s[q], gkp + off2[q]);
+      }
+  };
+  auto issue_f = [&](long long z) {  // x_{k-2} and B, halo-1 plane z
+    const long long zo = nxy * wrapc(z, nz);
+    const int r = (int)(z - z0 + 1);
+    double *d = sF + (r % RF) * (1 + PM) * S1;
+#pragma unroll
+    for (int q = 0; q < L1N; q++)
+      if (f1s[q] >= 0) {
+        if (has_pp) cp_async8(d + f1s[q], S.xpp + zo + off1[q]);
+#pragma unroll
+        for (int c = 0; c < PM; c++)
+          if (c < p) cp_async8(d + (1 + c) * S1 + f1s[q], S.B[c] + zo + off1[q]);
+      }
+  };
+
+  // prologue: group "init" = x/kappa planes z0-2, z0-1; then D groups ahead
+  issue_xk(z0 - 2);
+  issue_xk(z0 - 1);
+  cp_async_commit();
+  for (int i = 0; i < D; i++) {  // group i: x/kappa plane z0+i, f plane z0-1+i (if within DF)
+    issue_xk(z0 + i);
+    if (i < DF) issue_f(z0 - 1 + i);
+    cp_async_commit();
+  }
+  double v[NDOT] = {0.0, 0.0, 0.0, 0.0, 0.0};
+  for (long long zf = z0 - 1; zf <= z1; zf++) {
+    const long long i = zf - (z0 - 1);
+    cp_async_wait<D - 1>();
+    __syncthreads();  // B1: planes of group i visible; iteration i-1 finished everywhere
+    if (zf + 1 + D <= z1 + 1) issue_xk(zf + 1 + D);
+    if (i + DF <= (z1 - z0 + 1)) issue_f(zf + DF);
+    cp_async_commit();
+    {  // formation of x_k on the halo-1 plane zf
+      const int r0 = (int)(zf - z0 + 2);
+      const double *X0 = sXP + (r0 % RX) * S2, *Xm = sXP + ((r0 + RX - 1) % RX) * S2,
+                   *Xp = sXP + ((r0 + 1) % RX) * S2;
+      const double *K0 = sKP + (r0 % RK) * S2, *Km = sKP + ((r0 + RK - 1) % RK) * S2,
+                   *Kp = sKP + ((r0 + 1) % RK) * S2;
+      const double *Fs = sF + ((int)(zf - z0 + 1) % RF) * (1 + PM) * S1;
+      double *XK = sXK + (r0 % 3) * S1;
+      double *BT = sBT + (r0 & 1) * NT;
+#pragma unroll
+      for (int q = 0; q < L1N; q++) {
+        if (f1s[q] < 0) continue;
+        const int e = f2s[q], f = f1s[q];
+        const double xc = X0[e], kc = K0[e];
+        double ax = 0.5 * (kc + K0[e - 1]) * (X0[e - 1] - xc) + 0.5 * (kc + K0[e + 1]) * (X0[e + 1] - xc) +
+                    0.5 * (kc + K0[e - HX]) * (X0[e - HX] - xc) + 0.5 * (kc + K0[e + HX]) * (X0[e + HX] - xc) +
+                    0.5 * (kc + Km[e]) * (Xm[e] - xc) + 0.5 * (kc + Kp[e]) * (Xp[e] - xc);
+        double bp = 0.0, bc = 0.0;
+#pragma unroll
+        for (int c = 0; c < PM; c++)
+          if (c < p) {
+            const double bv = Fs[(1 + c) * S1 + f];
+            bp += bv * S.btp[c];
+            bc += bv * S.btc[c];
+          }
+        double xk = S.a0 * (ax * ih2 + bp) - S.a1 * xc;
+        if (has_pp) xk -= S.a2 * Fs[f];
+        XK[f] = xk;
+        if (fin[q] >= 0) BT[fin[q]] = bc;
+      }
+    }
+    __syncthreads();  // B2
+    const long long z = zf - 1;
+    if (z >= z0) {
+      const int r0 = (int)(z - z0 + 2);
+      const double *XK0 = sXK + (r0 % 3) * S1, *XKm = sXK + ((r0 + 2) % 3) * S1, *XKp = sXK + ((r0 + 1) % 3) * S1;
+      const double *K0 = sKP + (r0 % RK) * S2, *Km = sKP + ((r0 + RK - 1) % RK) * S2,
+                   *Kp = sKP + ((r0 + 1) % RK) * S2;
+      const double xk = XK0[ie1], kc = K0[ie2];
+      double r = 0.5 * (kc + K0[ie2 - 1]) * (XK0[ie1 - 1] - xk) + 0.5 * (kc + K0[ie2 + 1]) * (XK0[ie1 + 1] - xk) +
+                 0.5 * (kc + K0[ie2 - HX]) * (XK0[ie1 - GX] - xk) + 0.5 * (kc + K0[ie2 + HX]) * (XK0[ie1 + GX] - xk) +
+                 0.5 * (kc + Km[ie2]) * (XKm[ie1] - xk) + 0.5 * (kc + Kp[ie2]) * (XKp[ie1] - xk);
+      r = r * ih2 + sBT[(r0 & 1) * NT + tid];
+      if (inside) {
+        const double xm = sXP[(r0 % RX) * S2 + ie2];
+        v[0] += xk * xk;
+        v[1] += xm * xk;
+        v[2] += xm * r;
+        v[3] += xk * r;
+        v[4] += r * r;
+        if (S.xout) S.xout[gx + nx * gy + nxy * z] = xk;
+      }
+    }
+  }
+  cp_async_wait<0>();
+  pass_epilogue(P, S.k, v);
+}
