@@ -802,3 +802,160 @@ __global__ void __launch_bounds__(TX *TY, 1) k_pass_3d_async(KParams P) {
   cp_async_wait<0>();
   pass_epilogue(P, S.k, v);
 }
+
+// ---------------------------------------------------------------------------
+// 3D variable-kappa pass, v4: one thread per point of the halo-1 plane of a
+// TX x TY column tile (TX+2)(TY+2) threads), marching a chunk of ZC z-planes.
+//   * every thread forms x_k at its own halo-1 point from the x_{k-1}/kappa halo-2
+//     plane ring (stencil in shared memory) and its OWN x_{k-2} and B operands,
+//     which it prefetches with per-thread cp.async (no barrier needed for them);
+//   * interior threads then apply A~ to x_k (x_k plane ring), accumulate the five
+//     dots and store x_k.
+// Ring slots roll with counters (no modulo), all per-element index math is done
+// once.  (kappa_i + kappa_nb)(x_nb - x_i) is summed and scaled by inv_h2 / 2.
+// ---------------------------------------------------------------------------
+template <int TX, int TY, int PM>
+struct March4 {
+  static constexpr int HX = TX + 4, HY = TY + 4, S2 = HX * HY, GX = TX + 2, GY = TY + 2, S1 = GX * GY;
+  static constexpr int NT = (S1 + 31) / 32 * 32;  // threads: one per halo-1 point
+  static constexpr int D = 2;                     // planes in flight
+  static constexpr int RX = D + 3, RK = D + 4, RF = D + 1;
+  static constexpr int NF = 1 + PM;               // x_{k-2}, B_0..B_{PM-1}
+  static constexpr size_t smem_doubles = (size_t)(RX + RK) * S2 + (size_t)RF * NF * S1 + 3 * (size_t)S1 + 2 * (size_t)S1;
+};
+
+template <int TX, int TY, int ZC, int PM>
+__global__ void __launch_bounds__(March4<TX, TY, PM>::NT, 1) k_pass_3d_v4(KParams P) {
+  using M = March4<TX, TY, PM>;
+  constexpr int NT = M::NT, HX = M::HX, S2 = M::S2, GX = M::GX, S1 = M::S1, D = M::D, NF = M::NF;
+  constexpr int RX = M::RX, RK = M::RK, RF = M::RF;
+  extern __shared__ double smem[];
+  double *sXP = smem;                  // RX x S2   x_{k-1}
+  double *sKP = sXP + RX * S2;         // RK x S2   kappa
+  double *sF = sKP + RK * S2;          // RF x NF x S1 (thread-private columns)
+  double *sXK = sF + RF * NF * S1;     // 3 x S1    x_k
+  double *sBT = sXK + 3 * S1;          // 2 x S1    nu B t_k
+
+  __shared__ PassScalars S;
+  pass_guard(P);
+  if (threadIdx.x == 0) load_pass_scalars(P, S);
+  __syncthreads();
+  if (S.k == 0) return;
+  const int p = P.p;
+  const long long nx = P.nx, ny = P.ny, nz = P.nz, nxy = nx * ny;
+  const long long ntx = (nx + TX - 1) / TX, nty = (ny + TY - 1) / TY;
+  const long long b = blockIdx.x;
+  const long long ox = (b % ntx) * TX, oy = ((b / ntx) % nty) * TY;
+  const long long z0 = (b / (ntx * nty)) * ZC;
+  const long long z1 = (z0 + ZC < nz) ? z0 + ZC : nz;
+  const int nzc = (int)(z1 - z0);
+  const int t = threadIdx.x;
+  const double hh = 0.5 * P.inv_h2;
+  const bool has_pp = S.xpp != nullptr;
+  const double a0 = S.a0, a1 = S.a1, a2 = S.a2;
+  double btp[PM], btc[PM];
+  const double *Bp[PM];
+#pragma unroll
+  for (int c = 0; c < PM; c++) {
+    btp[c] = c < p ? S.btp[c] : 0.0;
+    btc[c] = c < p ? S.btc[c] : 0.0;
+    Bp[c] = c < p ? S.B[c] : nullptr;
+  }
+
+  // halo-2 elements this thread copies (e = t, t + NT)
+  const bool h2a = t < S2, h2b = t + NT < S2;
+  int o2a = 0, o2b = 0;
+  if (h2a) { const int a = t % HX, c = t / HX; o2a = (int)(wrapc(ox + a - 2, nx) + nx * wrapc(oy + c - 2, ny)); }
+  if (h2b) { const int e = t + NT, a = e % HX, c = e / HX; o2b = (int)(wrapc(ox + a - 2, nx) + nx * wrapc(oy + c - 2, ny)); }
+  // own halo-1 point
+  const bool act = t < S1;
+  const int fa = t % GX, fb = t / GX;
+  const int o1 = act ? (int)(wrapc(ox + fa - 1, nx) + nx * wrapc(oy + fb - 1, ny)) : 0;
+  const int e2 = (fa + 1) + HX * (fb + 1);  // own point in the halo-2 plane
+  const bool inner = act && fa >= 1 && fa <= TX && fb >= 1 && fb <= TY && (ox + fa - 1) < nx && (oy + fb - 1) < ny;
+  const long long gown = (ox + fa - 1) + nx * (oy + fb - 1);  // interior global in-plane index (if inner)
+
+  auto issue_x = [&](long long z, double *dx, double *dk) {
+    const long long zo = nxy * wrapc(z, nz);
+    if (h2a) { cp_async8(dx + t, S.xprev + zo + o2a); cp_async8(dk + t, P.kappa + zo + o2a); }
+    if (h2b) { cp_async8(dx + t + NT, S.xprev + zo + o2b); cp_async8(dk + t + NT, P.kappa + zo + o2b); }
+  };
+  auto issue_f = [&](long long z, double *df) {
+    if (!act) return;
+    const long long zo = nxy * wrapc(z, nz);
+    if (has_pp) cp_async8(df + t, S.xpp + zo + o1);
+#pragma unroll
+    for (int c = 0; c < PM; c++)
+      if (c < p) cp_async8(df + (1 + c) * S1 + t, Bp[c] + zo + o1);
+  };
+  // ring slot of relative plane index r (r = z - z0 + 2 for x/kappa, z - z0 + 1 for f)
+  auto sx = [&](int r) { return sXP + (r % RX) * S2; };
+  auto sk = [&](int r) { return sKP + (r % RK) * S2; };
+  auto sf = [&](int r) { return sF + (r % RF) * NF * S1; };
+
+  issue_x(z0 - 2, sx(0), sk(0));
+  issue_x(z0 - 1, sx(1), sk(1));
+  cp_async_commit();
+  for (int i = 0; i < D; i++) {
+    issue_x(z0 + i, sx(i + 2), sk(i + 2));
+    issue_f(z0 - 1 + i, sf(i));
+    cp_async_commit();
+  }
+  double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0, v4 = 0.0;
+  for (int i = 0; i <= nzc + 1; i++) {  // formation plane zf = z0 - 1 + i
+    const long long zf = z0 - 1 + i;
+    cp_async_wait<D - 1>();
+    __syncthreads();  // B1
+    if (i + 2 + D <= nzc + 3) issue_x(zf + 1 + D, sx(i + 2 + D), sk(i + 2 + D));
+    if (i + D <= nzc + 1) issue_f(zf + D, sf(i + D));
+    cp_async_commit();
+    if (act) {  // formation of x_k at the own point of plane zf
+      const double *X0 = sx(i + 1), *Xm = sx(i), *Xp = sx(i + 2);
+      const double *K0 = sk(i + 1), *Km = sk(i), *Kp = sk(i + 2);
+      const double *Fs = sf(i);
+      const double xc = X0[e2], kc = K0[e2];
+      double ax = (kc + K0[e2 - 1]) * (X0[e2 - 1] - xc);
+      ax = fma(kc + K0[e2 + 1], X0[e2 + 1] - xc, ax);
+      ax = fma(kc + K0[e2 - HX], X0[e2 - HX] - xc, ax);
+      ax = fma(kc + K0[e2 + HX], X0[e2 + HX] - xc, ax);
+      ax = fma(kc + Km[e2], Xm[e2] - xc, ax);
+      ax = fma(kc + Kp[e2], Xp[e2] - xc, ax);
+      double bp = 0.0, bc = 0.0;
+#pragma unroll
+      for (int c = 0; c < PM; c++)
+        if (c < p) {
+          const double bv = Fs[(1 + c) * S1 + t];
+          bp = fma(bv, btp[c], bp);
+          bc = fma(bv, btc[c], bc);
+        }
+      double xk = a0 * fma(ax, hh, bp) - a1 * xc;
+      if (has_pp) xk -= a2 * Fs[t];
+      sXK[(i % 3) * S1 + t] = xk;
+      sBT[(i & 1) * S1 + t] = bc;
+    }
+    __syncthreads();  // B2
+    if (i >= 2 && inner) {  // output plane z = zf - 1
+      const long long z = zf - 1;
+      const double *XK0 = sXK + ((i + 2) % 3) * S1, *XKm = sXK + ((i + 1) % 3) * S1, *XKp = sXK + (i % 3) * S1;
+      const double *K0 = sk(i), *Km = sk(i - 1), *Kp = sk(i + 1);
+      const double xk = XK0[t], kc = K0[e2];
+      double r = (kc + K0[e2 - 1]) * (XK0[t - 1] - xk);
+      r = fma(kc + K0[e2 + 1], XK0[t + 1] - xk, r);
+      r = fma(kc + K0[e2 - HX], XK0[t - GX] - xk, r);
+      r = fma(kc + K0[e2 + HX], XK0[t + GX] - xk, r);
+      r = fma(kc + Km[e2], XKm[t] - xk, r);
+      r = fma(kc + Kp[e2], XKp[t] - xk, r);
+      r = fma(r, hh, sBT[((i + 1) & 1) * S1 + t]);
+      const double xm = sx(i)[e2];
+      v0 = fma(xk, xk, v0);
+      v1 = fma(xm, xk, v1);
+      v2 = fma(xm, r, v2);
+      v3 = fma(xk, r, v3);
+      v4 = fma(r, r, v4);
+      if (S.xout) S.xout[gown + nxy * z] = xk;
+    }
+  }
+  cp_async_wait<0>();
+  double v[NDOT] = {v0, v1, v2, v3, v4};
+  pass_epilogue(P, S.k, v);
+}
