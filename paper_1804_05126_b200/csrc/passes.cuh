@@ -875,44 +875,57 @@ __global__ void __launch_bounds__(March4<TX, TY, PM>::NT, 1) k_pass_3d_v4(KParam
   const bool inner = act && fa >= 1 && fa <= TX && fb >= 1 && fb <= TY && (ox + fa - 1) < nx && (oy + fb - 1) < ny;
   const long long gown = (ox + fa - 1) + nx * (oy + fb - 1);  // interior global in-plane index (if inner)
 
-  auto issue_x = [&](long long z, double *dx, double *dk) {
-    const long long zo = nxy * wrapc(z, nz);
-    if (h2a) { cp_async8(dx + t, S.xprev + zo + o2a); cp_async8(dk + t, P.kappa + zo + o2a); }
-    if (h2b) { cp_async8(dx + t + NT, S.xprev + zo + o2b); cp_async8(dk + t + NT, P.kappa + zo + o2b); }
+  // element byte offsets (per thread) and plane pointers (uniform, rolled per plane)
+  const double *gX = S.xprev, *gK = P.kappa, *gPP = S.xpp;
+  auto issue_x = [&](long long zo, double *dx, double *dk) {
+    const double *px = gX + zo, *pk = gK + zo;
+    if (h2a) { cp_async8(dx + t, px + o2a); cp_async8(dk + t, pk + o2a); }
+    if (h2b) { cp_async8(dx + t + NT, px + o2b); cp_async8(dk + t + NT, pk + o2b); }
   };
-  auto issue_f = [&](long long z, double *df) {
+  auto issue_f = [&](long long zo, double *df) {
     if (!act) return;
-    const long long zo = nxy * wrapc(z, nz);
-    if (has_pp) cp_async8(df + t, S.xpp + zo + o1);
+    if (has_pp) cp_async8(df + t, gPP + zo + o1);
 #pragma unroll
     for (int c = 0; c < PM; c++)
       if (c < p) cp_async8(df + (1 + c) * S1 + t, Bp[c] + zo + o1);
   };
-  // ring slot of relative plane index r (r = z - z0 + 2 for x/kappa, z - z0 + 1 for f)
-  auto sx = [&](int r) { return sXP + (r % RX) * S2; };
-  auto sk = [&](int r) { return sKP + (r % RK) * S2; };
-  auto sf = [&](int r) { return sF + (r % RF) * NF * S1; };
+  auto inc = [](int s, int R) { return s + 1 == R ? 0 : s + 1; };
+  auto znext = [&](long long z) { return z + 1 == nz ? 0 : z + 1; };  // wrapped plane index
 
-  issue_x(z0 - 2, sx(0), sk(0));
-  issue_x(z0 - 1, sx(1), sk(1));
+  // prologue: x/kappa planes r = 0 .. D+1 (z0-2 .. z0+D-1), f planes r = 0 .. D-1
+  long long zx = wrapc(z0 - 2, nz), zfp = wrapc(z0 - 1, nz);
+  issue_x(zx * nxy, sXP + 0 * S2, sKP + 0 * S2);
+  zx = znext(zx);
+  issue_x(zx * nxy, sXP + 1 * S2, sKP + 1 * S2);
+  zx = znext(zx);
   cp_async_commit();
-  for (int i = 0; i < D; i++) {
-    issue_x(z0 + i, sx(i + 2), sk(i + 2));
-    issue_f(z0 - 1 + i, sf(i));
+  for (int q = 0; q < D; q++) {
+    issue_x(zx * nxy, sXP + (q + 2) * S2, sKP + (q + 2) * S2);
+    zx = znext(zx);
+    issue_f(zfp * nxy, sF + q * NF * S1);
+    zfp = znext(zfp);
     cp_async_commit();
   }
+  // rolling slots: x ring slot of r = i (xs), kappa ring slot of r = i-1 (ks), f slot of r = i
+  int xs = 0, ks = RK - 1, fs = 0, xi = (D + 2) % RX, ki = (D + 2) % RK, fi = D % RF;
+  int k0 = 0, km = 2, kp = 1;  // x_k ring slots of planes zf-1 (i-1), zf-2 (i-2), zf (i) after rotation
   double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0, v4 = 0.0;
-  for (int i = 0; i <= nzc + 1; i++) {  // formation plane zf = z0 - 1 + i
-    const long long zf = z0 - 1 + i;
+  long long zout = z0;  // output plane (valid from i = 2)
+  for (int i = 0; i <= nzc + 1; i++) {
     cp_async_wait<D - 1>();
     __syncthreads();  // B1
-    if (i + 2 + D <= nzc + 3) issue_x(zf + 1 + D, sx(i + 2 + D), sk(i + 2 + D));
-    if (i + D <= nzc + 1) issue_f(zf + D, sf(i + D));
+    if (i + 2 + D <= nzc + 3) issue_x(zx * nxy, sXP + xi * S2, sKP + ki * S2);
+    if (i + D <= nzc + 1) issue_f(zfp * nxy, sF + fi * NF * S1);
     cp_async_commit();
+    zx = znext(zx);
+    zfp = znext(zfp);
+    const int xs1 = inc(xs, RX), xs2 = inc(xs1, RX);
+    const int ks0 = inc(ks, RK), ks1 = inc(ks0, RK), ks2 = inc(ks1, RK);
+    // x_k ring: this iteration writes slot kp (plane zf); output reads k0 (zf-1), km (zf-2), kp (zf)
     if (act) {  // formation of x_k at the own point of plane zf
-      const double *X0 = sx(i + 1), *Xm = sx(i), *Xp = sx(i + 2);
-      const double *K0 = sk(i + 1), *Km = sk(i), *Kp = sk(i + 2);
-      const double *Fs = sf(i);
+      const double *X0 = sXP + xs1 * S2, *Xm = sXP + xs * S2, *Xp = sXP + xs2 * S2;
+      const double *K0 = sKP + ks1 * S2, *Km = sKP + ks0 * S2, *Kp = sKP + ks2 * S2;
+      const double *Fs = sF + fs * NF * S1;
       const double xc = X0[e2], kc = K0[e2];
       double ax = (kc + K0[e2 - 1]) * (X0[e2 - 1] - xc);
       ax = fma(kc + K0[e2 + 1], X0[e2 + 1] - xc, ax);
@@ -930,14 +943,13 @@ __global__ void __launch_bounds__(March4<TX, TY, PM>::NT, 1) k_pass_3d_v4(KParam
         }
       double xk = a0 * fma(ax, hh, bp) - a1 * xc;
       if (has_pp) xk -= a2 * Fs[t];
-      sXK[(i % 3) * S1 + t] = xk;
+      sXK[kp * S1 + t] = xk;
       sBT[(i & 1) * S1 + t] = bc;
     }
     __syncthreads();  // B2
-    if (i >= 2 && inner) {  // output plane z = zf - 1
-      const long long z = zf - 1;
-      const double *XK0 = sXK + ((i + 2) % 3) * S1, *XKm = sXK + ((i + 1) % 3) * S1, *XKp = sXK + (i % 3) * S1;
-      const double *K0 = sk(i), *Km = sk(i - 1), *Kp = sk(i + 1);
+    if (i >= 2 && inner) {  // output plane zout = zf - 1
+      const double *XK0 = sXK + k0 * S1, *XKm = sXK + km * S1, *XKp = sXK + kp * S1;
+      const double *K0 = sKP + ks0 * S2, *Km = sKP + ks * S2, *Kp = sKP + ks1 * S2;
       const double xk = XK0[t], kc = K0[e2];
       double r = (kc + K0[e2 - 1]) * (XK0[t - 1] - xk);
       r = fma(kc + K0[e2 + 1], XK0[t + 1] - xk, r);
@@ -946,14 +958,26 @@ __global__ void __launch_bounds__(March4<TX, TY, PM>::NT, 1) k_pass_3d_v4(KParam
       r = fma(kc + Km[e2], XKm[t] - xk, r);
       r = fma(kc + Kp[e2], XKp[t] - xk, r);
       r = fma(r, hh, sBT[((i + 1) & 1) * S1 + t]);
-      const double xm = sx(i)[e2];
+      const double xm = sXP[xs * S2 + e2];
       v0 = fma(xk, xk, v0);
       v1 = fma(xm, xk, v1);
       v2 = fma(xm, r, v2);
       v3 = fma(xk, r, v3);
       v4 = fma(r, r, v4);
-      if (S.xout) S.xout[gown + nxy * z] = xk;
+      if (S.xout) S.xout[gown + nxy * zout] = xk;
     }
+    if (i >= 2) zout++;
+    // roll every ring by one plane
+    xs = xs1;
+    ks = ks0;
+    fs = inc(fs, RF);
+    xi = inc(xi, RX);
+    ki = inc(ki, RK);
+    fi = inc(fi, RF);
+    const int tk = km;
+    km = k0;
+    k0 = kp;
+    kp = tk;
   }
   cp_async_wait<0>();
   double v[NDOT] = {v0, v1, v2, v3, v4};
