@@ -804,37 +804,40 @@ __global__ void __launch_bounds__(TX *TY, 1) k_pass_3d_async(KParams P) {
 }
 
 // ---------------------------------------------------------------------------
-// 3D variable-kappa pass, v4: one thread per point of the halo-1 plane of a
-// TX x TY column tile (TX+2)(TY+2) threads), marching a chunk of ZC z-planes.
-//   * every thread forms x_k at its own halo-1 point from the x_{k-1}/kappa halo-2
-//     plane ring (stencil in shared memory) and its OWN x_{k-2} and B operands,
-//     which it prefetches with per-thread cp.async (no barrier needed for them);
-//   * interior threads then apply A~ to x_k (x_k plane ring), accumulate the five
-//     dots and store x_k.
-// Ring slots roll with counters (no modulo), all per-element index math is done
-// once.  (kappa_i + kappa_nb)(x_nb - x_i) is summed and scaled by inv_h2 / 2.
+// 3D variable-kappa pass (v6): one thread per point of the halo-1 plane of a
+// TX x TY column tile, marching a chunk of ZC z-planes.
+//  * x_{k-1} and kappa halo-2 planes stream into shared-memory rings with cp.async
+//    (LDGSTS), D planes ahead; each thread also prefetches its OWN x_{k-2} and B
+//    operands (thread-private ring, no barrier needed for them);
+//  * every thread forms x_k at its own halo-1 point (A~ x_{k-1}: in-plane
+//    neighbours from shared memory, z-neighbours of its own column from
+//    registers), publishes it to a 2-plane x_k ring, and -- if interior -- applies
+//    A~ to x_k of the PREVIOUS plane (in-plane neighbours from the ring, own column
+//    and the previous plane's kappa neighbours from registers), accumulates the
+//    five dots and stores x_k: one barrier per plane, ~(11 + p) + 4 shared loads
+//    per point.
+// (kappa_i + kappa_nb)(x_nb - x_i) is summed and scaled by inv_h2 / 2.
 // ---------------------------------------------------------------------------
 template <int TX, int TY, int PM>
 struct March4 {
   static constexpr int HX = TX + 4, HY = TY + 4, S2 = HX * HY, GX = TX + 2, GY = TY + 2, S1 = GX * GY;
   static constexpr int NT = (S1 + 31) / 32 * 32;  // threads: one per halo-1 point
   static constexpr int D = 2;                     // planes in flight
-  static constexpr int RX = D + 3, RK = D + 4, RF = D + 1;
+  static constexpr int RX = D + 2, RF = D + 1;    // x_{k-1}/kappa ring, operand ring
   static constexpr int NF = 1 + PM;               // x_{k-2}, B_0..B_{PM-1}
-  static constexpr size_t smem_doubles = (size_t)(RX + RK) * S2 + (size_t)RF * NF * S1 + 3 * (size_t)S1 + 2 * (size_t)S1;
+  static constexpr size_t smem_doubles = (size_t)2 * RX * S2 + (size_t)RF * NF * S1 + 2 * (size_t)S1;
 };
 
 template <int TX, int TY, int ZC, int PM>
 __global__ void __launch_bounds__(March4<TX, TY, PM>::NT, 1) k_pass_3d_v4(KParams P) {
   using M = March4<TX, TY, PM>;
   constexpr int NT = M::NT, HX = M::HX, S2 = M::S2, GX = M::GX, S1 = M::S1, D = M::D, NF = M::NF;
-  constexpr int RX = M::RX, RK = M::RK, RF = M::RF;
+  constexpr int RX = M::RX, RF = M::RF;
   extern __shared__ double smem[];
   double *sXP = smem;                  // RX x S2   x_{k-1}
-  double *sKP = sXP + RX * S2;         // RK x S2   kappa
-  double *sF = sKP + RK * S2;          // RF x NF x S1 (thread-private columns)
-  double *sXK = sF + RF * NF * S1;     // 3 x S1    x_k
-  double *sBT = sXK + 3 * S1;          // 2 x S1    nu B t_k
+  double *sKP = sXP + RX * S2;         // RX x S2   kappa
+  double *sF = sKP + RX * S2;          // RF x NF x S1 (thread-private columns)
+  double *sXK = sF + RF * NF * S1;     // 2 x S1    x_k
 
   __shared__ PassScalars S;
   pass_guard(P);
@@ -871,11 +874,10 @@ __global__ void __launch_bounds__(March4<TX, TY, PM>::NT, 1) k_pass_3d_v4(KParam
   const bool act = t < S1;
   const int fa = t % GX, fb = t / GX;
   const int o1 = act ? (int)(wrapc(ox + fa - 1, nx) + nx * wrapc(oy + fb - 1, ny)) : 0;
-  const int e2 = (fa + 1) + HX * (fb + 1);  // own point in the halo-2 plane
+  const int e2 = act ? (fa + 1) + HX * (fb + 1) : HX + 1;  // own point in the halo-2 plane
   const bool inner = act && fa >= 1 && fa <= TX && fb >= 1 && fb <= TY && (ox + fa - 1) < nx && (oy + fb - 1) < ny;
   const long long gown = (ox + fa - 1) + nx * (oy + fb - 1);  // interior global in-plane index (if inner)
 
-  // element byte offsets (per thread) and plane pointers (uniform, rolled per plane)
   const double *gX = S.xprev, *gK = P.kappa, *gPP = S.xpp;
   auto issue_x = [&](long long zo, double *dx, double *dk) {
     const double *px = gX + zo, *pk = gK + zo;
@@ -892,12 +894,12 @@ __global__ void __launch_bounds__(March4<TX, TY, PM>::NT, 1) k_pass_3d_v4(KParam
   auto inc = [](int s, int R) { return s + 1 == R ? 0 : s + 1; };
   auto znext = [&](long long z) { return z + 1 == nz ? 0 : z + 1; };  // wrapped plane index
 
-  // prologue: x/kappa planes r = 0 .. D+1 (z0-2 .. z0+D-1), f planes r = 0 .. D-1
+  // prologue: x/kappa planes r = 0 .. D+1 (z0-2 .. z0+D-1) in slots 0..D+1, f planes r = 0..D-1
   long long zx = wrapc(z0 - 2, nz), zfp = wrapc(z0 - 1, nz);
-  issue_x(zx * nxy, sXP + 0 * S2, sKP + 0 * S2);
-  zx = znext(zx);
-  issue_x(zx * nxy, sXP + 1 * S2, sKP + 1 * S2);
-  zx = znext(zx);
+  for (int q = 0; q < 2; q++) {
+    issue_x(zx * nxy, sXP + q * S2, sKP + q * S2);
+    zx = znext(zx);
+  }
   cp_async_commit();
   for (int q = 0; q < D; q++) {
     issue_x(zx * nxy, sXP + (q + 2) * S2, sKP + (q + 2) * S2);
@@ -906,78 +908,77 @@ __global__ void __launch_bounds__(March4<TX, TY, PM>::NT, 1) k_pass_3d_v4(KParam
     zfp = znext(zfp);
     cp_async_commit();
   }
-  // rolling slots: x ring slot of r = i (xs), kappa ring slot of r = i-1 (ks), f slot of r = i
-  int xs = 0, ks = RK - 1, fs = 0, xi = (D + 2) % RX, ki = (D + 2) % RK, fi = D % RF;
-  int k0 = 0, km = 2, kp = 1;  // x_k ring slots of planes zf-1 (i-1), zf-2 (i-2), zf (i) after rotation
+  // own-column registers.  Plane r = z - z0 + 2 (x/kappa); formation plane zf = z0 - 1 + i
+  cp_async_wait<D - 1>();  // groups init, 0 landed: planes r = 0..2
+  __syncthreads();
+  double xo_m = sXP[0 * S2 + e2], xo_0 = sXP[1 * S2 + e2];       // x_{k-1}(zf-1), x_{k-1}(zf) for i = 0
+  double ko_mm = 0.0, ko_m = sKP[0 * S2 + e2], ko_0 = sKP[1 * S2 + e2];
+  double kW = 0.0, kE = 0.0, kS = 0.0, kN = 0.0;                   // kappa neighbours of the previous plane
+  double xk_m = 0.0, xk_0 = 0.0, bt_0 = 0.0;                       // x_k(zf-2), x_k(zf-1), nu B t_k(zf-1)
   double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0, v4 = 0.0;
-  long long zout = z0;  // output plane (valid from i = 2)
+  int xs = 1, xi = (D + 2) % RX, fs = 0, fi = D % RF;  // x ring slot of r = i+1 (center), issue slots
+  long long zout = z0;
   for (int i = 0; i <= nzc + 1; i++) {
     cp_async_wait<D - 1>();
-    __syncthreads();  // B1
-    if (i + 2 + D <= nzc + 3) issue_x(zx * nxy, sXP + xi * S2, sKP + ki * S2);
+    __syncthreads();  // the one barrier per plane (at i = 0 it also orders the register
+                      // initialisation above before slot 0 is refilled)
+    if (i + 2 + D <= nzc + 3) issue_x(zx * nxy, sXP + xi * S2, sKP + xi * S2);
     if (i + D <= nzc + 1) issue_f(zfp * nxy, sF + fi * NF * S1);
     cp_async_commit();
     zx = znext(zx);
     zfp = znext(zfp);
-    const int xs1 = inc(xs, RX), xs2 = inc(xs1, RX);
-    const int ks0 = inc(ks, RK), ks1 = inc(ks0, RK), ks2 = inc(ks1, RK);
-    // x_k ring: this iteration writes slot kp (plane zf); output reads k0 (zf-1), km (zf-2), kp (zf)
-    if (act) {  // formation of x_k at the own point of plane zf
-      const double *X0 = sXP + xs1 * S2, *Xm = sXP + xs * S2, *Xp = sXP + xs2 * S2;
-      const double *K0 = sKP + ks1 * S2, *Km = sKP + ks0 * S2, *Kp = sKP + ks2 * S2;
-      const double *Fs = sF + fs * NF * S1;
-      const double xc = X0[e2], kc = K0[e2];
-      double ax = (kc + K0[e2 - 1]) * (X0[e2 - 1] - xc);
-      ax = fma(kc + K0[e2 + 1], X0[e2 + 1] - xc, ax);
-      ax = fma(kc + K0[e2 - HX], X0[e2 - HX] - xc, ax);
-      ax = fma(kc + K0[e2 + HX], X0[e2 + HX] - xc, ax);
-      ax = fma(kc + Km[e2], Xm[e2] - xc, ax);
-      ax = fma(kc + Kp[e2], Xp[e2] - xc, ax);
-      double bp = 0.0, bc = 0.0;
+    const int xsp = inc(xs, RX);
+    const double *X0 = sXP + xs * S2, *K0 = sKP + xs * S2;
+    // formation of x_k at the own point of plane zf (Alg. 2 l.4-10 of iteration k-1)
+    const double xo_p = sXP[xsp * S2 + e2], ko_p = sKP[xsp * S2 + e2];
+    const double nW = K0[e2 - 1], nE = K0[e2 + 1], nS = K0[e2 - HX], nN = K0[e2 + HX];
+    double ax = (ko_0 + nW) * (X0[e2 - 1] - xo_0);
+    double ay = (ko_0 + nE) * (X0[e2 + 1] - xo_0);
+    ax = fma(ko_0 + nS, X0[e2 - HX] - xo_0, ax);
+    ay = fma(ko_0 + nN, X0[e2 + HX] - xo_0, ay);
+    ax = fma(ko_0 + ko_m, xo_m - xo_0, ax);
+    ay = fma(ko_0 + ko_p, xo_p - xo_0, ay);
+    const double *Fs = sF + fs * NF * S1;
+    double bp = 0.0, bc = 0.0;
 #pragma unroll
-      for (int c = 0; c < PM; c++)
-        if (c < p) {
-          const double bv = Fs[(1 + c) * S1 + t];
-          bp = fma(bv, btp[c], bp);
-          bc = fma(bv, btc[c], bc);
-        }
-      double xk = a0 * fma(ax, hh, bp) - a1 * xc;
-      if (has_pp) xk -= a2 * Fs[t];
-      sXK[kp * S1 + t] = xk;
-      sBT[(i & 1) * S1 + t] = bc;
-    }
-    __syncthreads();  // B2
-    if (i >= 2 && inner) {  // output plane zout = zf - 1
-      const double *XK0 = sXK + k0 * S1, *XKm = sXK + km * S1, *XKp = sXK + kp * S1;
-      const double *K0 = sKP + ks0 * S2, *Km = sKP + ks * S2, *Kp = sKP + ks1 * S2;
-      const double xk = XK0[t], kc = K0[e2];
-      double r = (kc + K0[e2 - 1]) * (XK0[t - 1] - xk);
-      r = fma(kc + K0[e2 + 1], XK0[t + 1] - xk, r);
-      r = fma(kc + K0[e2 - HX], XK0[t - GX] - xk, r);
-      r = fma(kc + K0[e2 + HX], XK0[t + GX] - xk, r);
-      r = fma(kc + Km[e2], XKm[t] - xk, r);
-      r = fma(kc + Kp[e2], XKp[t] - xk, r);
-      r = fma(r, hh, sBT[((i + 1) & 1) * S1 + t]);
-      const double xm = sXP[xs * S2 + e2];
-      v0 = fma(xk, xk, v0);
-      v1 = fma(xm, xk, v1);
+    for (int c = 0; c < PM; c++)
+      if (c < p) {
+        const double bv = Fs[(1 + c) * S1 + t];
+        bp = fma(bv, btp[c], bp);
+        bc = fma(bv, btc[c], bc);
+      }
+    double xk_p = a0 * fma(ax + ay, hh, bp) - a1 * xo_0;
+    if (has_pp) xk_p -= a2 * Fs[t];
+    double *XKn = sXK + (i & 1) * S1;
+    if (act) XKn[t] = xk_p;
+    // output plane zout = zf - 1 (x_k of that plane was published one barrier ago)
+    if (i >= 2 && inner) {
+      const double *XK0 = sXK + ((i + 1) & 1) * S1;
+      double rx = (ko_m + kW) * (XK0[t - 1] - xk_0);
+      double ry = (ko_m + kE) * (XK0[t + 1] - xk_0);
+      rx = fma(ko_m + kS, XK0[t - GX] - xk_0, rx);
+      ry = fma(ko_m + kN, XK0[t + GX] - xk_0, ry);
+      rx = fma(ko_m + ko_mm, xk_m - xk_0, rx);
+      ry = fma(ko_m + ko_0, xk_p - xk_0, ry);
+      const double r = fma(rx + ry, hh, bt_0);
+      const double xm = xo_m;
+      v0 = fma(xk_0, xk_0, v0);
+      v1 = fma(xm, xk_0, v1);
       v2 = fma(xm, r, v2);
-      v3 = fma(xk, r, v3);
+      v3 = fma(xk_0, r, v3);
       v4 = fma(r, r, v4);
-      if (S.xout) S.xout[gown + nxy * zout] = xk;
+      if (S.xout) S.xout[gown + nxy * zout] = xk_0;
     }
     if (i >= 2) zout++;
-    // roll every ring by one plane
-    xs = xs1;
-    ks = ks0;
-    fs = inc(fs, RF);
+    // roll own-column registers and ring slots by one plane
+    xo_m = xo_0; xo_0 = xo_p;
+    ko_mm = ko_m; ko_m = ko_0; ko_0 = ko_p;
+    kW = nW; kE = nE; kS = nS; kN = nN;
+    xk_m = xk_0; xk_0 = xk_p; bt_0 = bc;
+    xs = xsp;
     xi = inc(xi, RX);
-    ki = inc(ki, RK);
+    fs = inc(fs, RF);
     fi = inc(fi, RF);
-    const int tk = km;
-    km = k0;
-    k0 = kp;
-    kp = tk;
   }
   cp_async_wait<0>();
   double v[NDOT] = {v0, v1, v2, v3, v4};

@@ -43,3 +43,7 @@ tot = sum(int(x[hs[col]] or 0) for x in data)
 print("stall samples", tot, "sass lines", len(data))
 for row in sorted(data, key=lambda x: -int(x[hs[col]] or 0))[:top]:
     print(f"{row[hs[col]]:>6s} {row[hs['Instructions Executed']]:>10s}  {row[hs['Source']][:100]}")
+# stall reasons, totals over the kernel
+names = [n for n in s[1] if n.startswith("stall_") and "Not Issued" not in n]
+tot_r = {n: sum(int(x[hs[n]] or 0) for x in data) for n in names}
+print("stall reasons:", ", ".join(f"{k[6:]}={v}" for k, v in sorted(tot_r.items(), key=lambda x: -x[1]) if v))
