@@ -18,6 +18,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -35,7 +36,7 @@ constexpr int SM_COUNT_HINT = 148;
 #define T2D 2, 64, 16, 1
 #define T3D 3, 32, 8, 4
 #define M3X 32
-#define M3Y 16
+#define M3Y 8
 #define M3Z 32
 
 struct Layout {
@@ -108,9 +109,8 @@ Layout layout(const kiops_operator_desc *op, int p, const kiops_options *o) {
       break;
     case KIOPS_OP_STENCIL3D7_VARKAPPA:
       L.grid_pass = (int)(((op->nx + M3X - 1) / M3X) * ((op->ny + M3Y - 1) / M3Y) * ((op->nz + M3Z - 1) / M3Z));
-      L.smem_pass = sizeof(double) * (p <= 2 ? March4<M3X, M3Y, 2>::smem_doubles
-                                     : p <= 4 ? March4<M3X, M3Y, 4>::smem_doubles : March4<M3X, M3Y, 8>::smem_doubles);
-      L.block_pass = March4<M3X, M3Y, 2>::NT;
+      L.smem_pass = sizeof(double) * March7<M3X, M3Y, 2>::smem_doubles;
+      L.block_pass = March7<M3X, M3Y, 2>::NT;
       break;
     default:
       L.grid_pass = (int)std::min<long long>((8 * N + 255) / 256, SM_COUNT_HINT * 8);
@@ -216,9 +216,14 @@ static kiops_status build_graph(kiops_ctx c) {
     case KIOPS_OP_STENCIL1D3: fpass = (void *)k_pass_stencil<T1D>; break;
     case KIOPS_OP_STENCIL2D5: fpass = (void *)k_pass_stencil<T2D>; break;
     case KIOPS_OP_STENCIL3D7_VARKAPPA:
-      fpass = c->p <= 2 ? (void *)k_pass_3d_v4<M3X, M3Y, M3Z, 2>
-            : c->p <= 4 ? (void *)k_pass_3d_v4<M3X, M3Y, M3Z, 4>
-                        : (void *)k_pass_3d_v4<M3X, M3Y, M3Z, 8>;
+      if (getenv("KIOPS_3D_MINB2"))  // experiment switch: 2 CTAs/SM (register-capped)
+        fpass = c->p <= 2 ? (void *)k_pass_3d_v7<M3X, M3Y, M3Z, 2, 2>
+              : c->p <= 4 ? (void *)k_pass_3d_v7<M3X, M3Y, M3Z, 4, 2>
+                          : (void *)k_pass_3d_v7<M3X, M3Y, M3Z, 8, 2>;
+      else
+        fpass = c->p <= 2 ? (void *)k_pass_3d_v7<M3X, M3Y, M3Z, 2, 1>
+              : c->p <= 4 ? (void *)k_pass_3d_v7<M3X, M3Y, M3Z, 4, 1>
+                          : (void *)k_pass_3d_v7<M3X, M3Y, M3Z, 8, 1>;
       break;
     default: break;
   }

@@ -984,3 +984,168 @@ __global__ void __launch_bounds__(March4<TX, TY, PM>::NT, 1) k_pass_3d_v4(KParam
   double v[NDOT] = {v0, v1, v2, v3, v4};
   pass_epilogue(P, S.k, v);
 }
+
+// ---------------------------------------------------------------------------
+// 3D variable-kappa pass (v7, the one in use): as v6, with
+//  * 32 x 8 column tiles: (TX+2)(TY+2) = 340 threads, two CTAs per SM;
+//  * own x_{k-2} / B operands prefetched two planes ahead into registers
+//    (double buffer, loop unrolled by two so buffers never move);
+//  * the six face sums kappa_i + kappa_nb of the formation at (x, y, z) are kept
+//    and reused by the output stencil at the same point one plane later;
+//  * per-thread global pointers precomputed; plane offsets roll incrementally.
+// ---------------------------------------------------------------------------
+template <int TX, int TY, int PM>
+struct March7 {
+  static constexpr int HX = TX + 4, HY = TY + 4, S2 = HX * HY, GX = TX + 2, GY = TY + 2, S1 = GX * GY;
+  static constexpr int NT = (S1 + 31) / 32 * 32;
+  static constexpr int D = 2, RX = 4;
+  static constexpr size_t smem_doubles = (size_t)2 * RX * S2 + 2 * (size_t)S1;
+};
+
+template <int PM>
+struct Ops {
+  double pp;
+  double b[PM];
+};
+
+template <int TX, int TY, int ZC, int PM, int MINB>
+__global__ void __launch_bounds__(March7<TX, TY, PM>::NT, MINB) k_pass_3d_v7(KParams P) {
+  using M = March7<TX, TY, PM>;
+  constexpr int NT = M::NT, HX = M::HX, S2 = M::S2, GX = M::GX, S1 = M::S1, D = M::D, RX = M::RX;
+  static_assert(RX == 4, "ring slots use & 3");
+  extern __shared__ double smem[];
+  double *sX = smem;            // 4 x S2   x_{k-1}
+  double *sK = sX + RX * S2;    // 4 x S2   kappa
+  double *sXK = sK + RX * S2;   // 2 x S1   x_k
+
+  __shared__ PassScalars S;
+  pass_guard(P);
+  if (threadIdx.x == 0) load_pass_scalars(P, S);
+  __syncthreads();
+  if (S.k == 0) return;
+  const int p = P.p;
+  const long long nx = P.nx, ny = P.ny, nz = P.nz, nxy = nx * ny;
+  const long long ntx = (nx + TX - 1) / TX, nty = (ny + TY - 1) / TY;
+  const long long bidx = blockIdx.x;
+  const long long ox = (bidx % ntx) * TX, oy = ((bidx / ntx) % nty) * TY;
+  const long long z0 = (bidx / (ntx * nty)) * ZC;
+  const long long z1 = (z0 + ZC < nz) ? z0 + ZC : nz;
+  const int nzc = (int)(z1 - z0);
+  const int t = threadIdx.x;
+  const double hh = 0.5 * P.inv_h2;
+  const double a0 = S.a0, a1 = S.a1, a2 = S.a2;
+  double btp[PM], btc[PM];
+#pragma unroll
+  for (int c = 0; c < PM; c++) {
+    btp[c] = c < p ? S.btp[c] : 0.0;
+    btc[c] = c < p ? S.btc[c] : 0.0;
+  }
+  // halo-2 copy elements (t, t + NT): 32-bit in-plane offsets (nx*ny < 2^31 validated)
+  const bool h2a = t < S2, h2b = t + NT < S2;
+  int o2a = 0, o2b = 0;
+  if (h2a) { const int a = t % HX, c = t / HX; o2a = (int)(wrapc(ox + a - 2, nx) + nx * wrapc(oy + c - 2, ny)); }
+  if (h2b) { const int e = t + NT, a = e % HX, c = e / HX; o2b = (int)(wrapc(ox + a - 2, nx) + nx * wrapc(oy + c - 2, ny)); }
+  // own halo-1 point
+  const bool act = t < S1;
+  const int fa = t % GX, fb = t / GX;
+  const int o1 = act ? (int)(wrapc(ox + fa - 1, nx) + nx * wrapc(oy + fb - 1, ny)) : 0;
+  const int e2 = act ? (fa + 1) + HX * (fb + 1) : HX + 1;
+  const bool inner = act && fa >= 1 && fa <= TX && fb >= 1 && fb <= TY && (ox + fa - 1) < nx && (oy + fb - 1) < ny;
+  const bool has_pp = S.xpp != nullptr;
+  const int oo = (int)((ox + fa - 1) + nx * (oy + fb - 1));
+
+  auto znext = [&](long long zo) { const long long n = zo + nxy; return n == nz * nxy ? 0 : n; };
+  long long zoX = wrapc(z0 - 2, nz) * nxy;  // element offset of the next x/kappa plane to copy
+  auto issue_x = [&](int slot) {
+    double *dx = sX + slot * S2, *dk = sK + slot * S2;
+    const double *gx = S.xprev + zoX, *gk = P.kappa + zoX;
+    if (h2a) { cp_async8(dx + t, gx + o2a); cp_async8(dk + t, gk + o2a); }
+    if (h2b) { cp_async8(dx + t + NT, gx + o2b); cp_async8(dk + t + NT, gk + o2b); }
+    zoX = znext(zoX);
+  };
+  long long zoF = wrapc(z0 - 1, nz) * nxy;  // element offset of the next operand plane
+  auto load_ops = [&](Ops<PM> &o) {
+    o.pp = 0.0;
+    if (act) {
+      if (has_pp) o.pp = __ldg(S.xpp + zoF + o1);
+#pragma unroll
+      for (int c = 0; c < PM; c++) o.b[c] = c < p ? __ldg(S.B[c] + zoF + o1) : 0.0;
+    }
+    zoF = znext(zoF);
+  };
+
+  issue_x(0);
+  issue_x(1);
+  cp_async_commit();
+  issue_x(2);
+  cp_async_commit();
+  issue_x(3);
+  cp_async_commit();
+  Ops<PM> opA, opB;
+  load_ops(opA);  // plane i = 0
+  load_ops(opB);  // plane i = 1
+  cp_async_wait<D - 1>();
+  __syncthreads();
+  double xo_m = sX[0 * S2 + e2], xo_0 = sX[1 * S2 + e2];
+  double ko_m = sK[0 * S2 + e2], ko_0 = sK[1 * S2 + e2];
+  double gW = 0.0, gE = 0.0, gS = 0.0, gN = 0.0, gD = 0.0, gU = 0.0;  // face sums at (x, y, zout)
+  double xk_m = 0.0, xk_0 = 0.0, bt_0 = 0.0;
+  double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0, v4 = 0.0;
+  long long zo_out = z0 * nxy;
+
+  auto body = [&](const int i, Ops<PM> &op) {
+    cp_async_wait<D - 1>();
+    __syncthreads();  // the one barrier per plane
+    if (i + 2 + D <= nzc + 3) issue_x((i + 2 + D) & 3);
+    cp_async_commit();
+    const double *X0 = sX + ((i + 1) & 3) * S2, *K0 = sK + ((i + 1) & 3) * S2;
+    const double xo_p = sX[((i + 2) & 3) * S2 + e2], ko_p = sK[((i + 2) & 3) * S2 + e2];
+    // formation (Alg. 2 l.4-10 of iteration k-1) at the own point of plane zf
+    const double fW = ko_0 + K0[e2 - 1], fE = ko_0 + K0[e2 + 1], fS = ko_0 + K0[e2 - HX],
+                 fN = ko_0 + K0[e2 + HX], fD = ko_0 + ko_m, fU = ko_0 + ko_p;
+    double ax = fW * (X0[e2 - 1] - xo_0);
+    double ay = fE * (X0[e2 + 1] - xo_0);
+    ax = fma(fS, X0[e2 - HX] - xo_0, ax);
+    ay = fma(fN, X0[e2 + HX] - xo_0, ay);
+    ax = fma(fD, xo_m - xo_0, ax);
+    ay = fma(fU, xo_p - xo_0, ay);
+    double bp = 0.0, bc = 0.0;
+#pragma unroll
+    for (int c = 0; c < PM; c++) {
+      bp = fma(op.b[c], btp[c], bp);
+      bc = fma(op.b[c], btc[c], bc);
+    }
+    const double xk_p = a0 * fma(ax + ay, hh, bp) - a1 * xo_0 - a2 * op.pp;
+    if (i + 2 <= nzc + 1) load_ops(op);  // operands of plane i + 2 (same buffer)
+    if (act) sXK[(i & 1) * S1 + t] = xk_p;
+    // output plane zf - 1: x_k of that plane was published before this barrier
+    if (i >= 2 && inner) {
+      const double *XK0 = sXK + ((i + 1) & 1) * S1;
+      double rx = gW * (XK0[t - 1] - xk_0);
+      double ry = gE * (XK0[t + 1] - xk_0);
+      rx = fma(gS, XK0[t - GX] - xk_0, rx);
+      ry = fma(gN, XK0[t + GX] - xk_0, ry);
+      rx = fma(gD, xk_m - xk_0, rx);
+      ry = fma(gU, xk_p - xk_0, ry);
+      const double r = fma(rx + ry, hh, bt_0);
+      v0 = fma(xk_0, xk_0, v0);
+      v1 = fma(xo_m, xk_0, v1);
+      v2 = fma(xo_m, r, v2);
+      v3 = fma(xk_0, r, v3);
+      v4 = fma(r, r, v4);
+      if (S.xout) S.xout[zo_out + oo] = xk_0;
+    }
+    if (i >= 2) zo_out += nxy;
+    xo_m = xo_0; xo_0 = xo_p;
+    ko_m = ko_0; ko_0 = ko_p;
+    gW = fW; gE = fE; gS = fS; gN = fN; gD = fD; gU = fU;
+    xk_m = xk_0; xk_0 = xk_p; bt_0 = bc;
+  };
+  for (int i = 0; i <= nzc + 1; i += 2) {
+    body(i, opA);
+    if (i + 1 <= nzc + 1) body(i + 1, opB);
+  }
+  cp_async_wait<0>();
+  double v[NDOT] = {v0, v1, v2, v3, v4};
+  pass_epilogue(P, S.k, v);
+}
