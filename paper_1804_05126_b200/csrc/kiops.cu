@@ -109,8 +109,8 @@ Layout layout(const kiops_operator_desc *op, int p, const kiops_options *o) {
       break;
     case KIOPS_OP_STENCIL3D7_VARKAPPA:
       L.grid_pass = (int)(((op->nx + M3X - 1) / M3X) * ((op->ny + M3Y - 1) / M3Y) * ((op->nz + M3Z - 1) / M3Z));
-      L.smem_pass = sizeof(double) * March7<M3X, M3Y, 2>::smem_doubles;
-      L.block_pass = March7<M3X, M3Y, 2>::NT;
+      L.smem_pass = sizeof(double) * Lazy3<M3X, M3Y>::smem_doubles;
+      L.block_pass = Lazy3<M3X, M3Y>::NT;
       break;
     default:
       L.grid_pass = (int)std::min<long long>((8 * N + 255) / 256, SM_COUNT_HINT * 8);
@@ -120,7 +120,7 @@ Layout layout(const kiops_operator_desc *op, int p, const kiops_options *o) {
   size_t off = 0;
   const size_t vec = (size_t)L.ldN * sizeof(double);
   L.V = off; off += al((size_t)(o->m_max + 1) * vec);
-  L.r = off; off += (op->kind == KIOPS_OP_CSR) ? al(vec) : 0;
+  L.r = off; off += (op->kind == KIOPS_OP_CSR || op->kind == KIOPS_OP_STENCIL3D7_VARKAPPA) ? 2 * al(vec) : 0;
   L.staging = off; off += o->host_staging ? al((size_t)(p + 1 + o->max_outputs) * vec) : 0;
   L.state = off; off += al(sizeof(DevState));
   L.call = off; off += al(sizeof(CallBlock));
@@ -216,14 +216,9 @@ static kiops_status build_graph(kiops_ctx c) {
     case KIOPS_OP_STENCIL1D3: fpass = (void *)k_pass_stencil<T1D>; break;
     case KIOPS_OP_STENCIL2D5: fpass = (void *)k_pass_stencil<T2D>; break;
     case KIOPS_OP_STENCIL3D7_VARKAPPA:
-      if (getenv("KIOPS_3D_MINB2"))  // experiment switch: 2 CTAs/SM (register-capped)
-        fpass = c->p <= 2 ? (void *)k_pass_3d_v7<M3X, M3Y, M3Z, 2, 2>
-              : c->p <= 4 ? (void *)k_pass_3d_v7<M3X, M3Y, M3Z, 4, 2>
-                          : (void *)k_pass_3d_v7<M3X, M3Y, M3Z, 8, 2>;
-      else
-        fpass = c->p <= 2 ? (void *)k_pass_3d_v7<M3X, M3Y, M3Z, 2, 1>
-              : c->p <= 4 ? (void *)k_pass_3d_v7<M3X, M3Y, M3Z, 4, 1>
-                          : (void *)k_pass_3d_v7<M3X, M3Y, M3Z, 8, 1>;
+      fpass = c->p <= 2 ? (void *)k_pass_3d_lazy<M3X, M3Y, M3Z, 2, 2>
+            : c->p <= 4 ? (void *)k_pass_3d_lazy<M3X, M3Y, M3Z, 4, 2>
+                        : (void *)k_pass_3d_lazy<M3X, M3Y, M3Z, 8, 2>;
       break;
     default: break;
   }

@@ -1149,3 +1149,132 @@ __global__ void __launch_bounds__(March7<TX, TY, PM>::NT, MINB) k_pass_3d_v7(KPa
   double v[NDOT] = {v0, v1, v2, v3, v4};
   pass_epilogue(P, S.k, v);
 }
+
+// ---------------------------------------------------------------------------
+// 3D variable-kappa pass, LAZY form (SURVEY 8(a) a3 "lazy normalisation"):
+// pass k forms x_k POINTWISE from the stored r_{k-1} = A~ x_{k-1} (ping-pong r
+// buffers), x_{k-1} and x_{k-2}, then applies A~ once to x_k:
+//     x_k = r_{k-1}/s_{k-1} - H(k-2,k-1) x_{k-2}/s_{k-2} - H(k-1,k-1) x_{k-1}/s_{k-1}
+//     r_k = A x_k + nu B t_k                                  (stored for pass k+1)
+// HBM per pass: read r_{k-1}, x_{k-1}, x_{k-2}, kappa, B; write x_k, r_k
+// ((q+3+p+c) 8N, two vectors above the minimum) with ONE stencil level and a small
+// per-thread state.  One thread per halo-1 point of a TX x TY column tile marches a
+// chunk of ZC planes; x_k and kappa planes go through 2-plane shared rings,
+// z-neighbours stay in registers, operands are prefetched one plane ahead.
+// ---------------------------------------------------------------------------
+template <int TX, int TY>
+struct Lazy3 {
+  static constexpr int GX = TX + 2, GY = TY + 2, S1 = GX * GY;
+  static constexpr int NT = (S1 + 31) / 32 * 32;
+  static constexpr size_t smem_doubles = 4 * (size_t)S1;
+};
+
+template <int PM>
+struct LOps {
+  double r, xm, xpp, kap, bt;
+};
+
+template <int TX, int TY, int ZC, int PM, int MINB>
+__global__ void __launch_bounds__(Lazy3<TX, TY>::NT, MINB) k_pass_3d_lazy(KParams P) {
+  using M = Lazy3<TX, TY>;
+  constexpr int NT = M::NT, GX = M::GX, S1 = M::S1;
+  extern __shared__ double smem[];
+  double *sXK = smem;          // 2 x S1  x_k planes
+  double *sKP = smem + 2 * S1; // 2 x S1  kappa planes
+
+  __shared__ PassScalars S;
+  pass_guard(P);
+  if (threadIdx.x == 0) load_pass_scalars(P, S);
+  __syncthreads();
+  if (S.k == 0) return;
+  const int p = P.p, k = S.k;
+  const long long nx = P.nx, ny = P.ny, nz = P.nz, nxy = nx * ny;
+  const long long ntx = (nx + TX - 1) / TX, nty = (ny + TY - 1) / TY;
+  const long long bidx = blockIdx.x;
+  const long long ox = (bidx % ntx) * TX, oy = ((bidx / ntx) % nty) * TY;
+  const long long z0 = (bidx / (ntx * nty)) * ZC;
+  const long long z1 = (z0 + ZC < nz) ? z0 + ZC : nz;
+  const int nzc = (int)(z1 - z0);
+  const int t = threadIdx.x;
+  const double hh = 0.5 * P.inv_h2;
+  const double a0 = S.a0, a1 = S.a1, a2 = S.a2;
+  const bool act = t < S1;
+  const int fa = t % GX, fb = t / GX;
+  const int o1 = act ? (int)(wrapc(ox + fa - 1, nx) + nx * wrapc(oy + fb - 1, ny)) : 0;
+  const bool inner = act && fa >= 1 && fa <= TX && fb >= 1 && fb <= TY && (ox + fa - 1) < nx && (oy + fb - 1) < ny;
+  const bool use_r = k >= 2, use_pp = S.xpp != nullptr;
+  const double *rin = P.r + (size_t)((k - 1) & 1) * (size_t)P.ldN;  // r_{k-1}
+  double *rout = P.r + (size_t)(k & 1) * (size_t)P.ldN;             // r_k
+  const double *xprev = S.xprev, *xpp = S.xpp, *kap = P.kappa;
+  double btc[PM];
+  const double *Bc[PM];
+#pragma unroll
+  for (int c = 0; c < PM; c++) {
+    btc[c] = c < p ? S.btc[c] : 0.0;
+    Bc[c] = c < p ? S.B[c] : nullptr;
+  }
+  auto znext = [&](long long zo) { const long long n = zo + nxy; return n == nz * nxy ? 0 : n; };
+  long long zoL = wrapc(z0 - 1, nz) * nxy;  // next plane to load
+  auto load = [&](LOps<PM> &o) {
+    o.r = o.xm = o.xpp = o.kap = o.bt = 0.0;
+    if (act) {
+      const long long g = zoL + o1;
+      if (use_r) o.r = __ldg(rin + g);
+      o.xm = __ldg(xprev + g);
+      if (use_pp) o.xpp = __ldg(xpp + g);
+      o.kap = __ldg(kap + g);
+      if (inner) {
+        double s = 0.0;
+#pragma unroll
+        for (int c = 0; c < PM; c++)
+          if (c < p) s = fma(__ldg(Bc[c] + g), btc[c], s);
+        o.bt = s;
+      }
+    }
+    zoL = znext(zoL);
+  };
+  // plane zf = z0 - 1 + i ; x_k formed for planes z0-1 .. z1 (own column), output z0 .. z1-1
+  LOps<PM> cur, nxt;
+  load(cur);
+  double xk_m = 0.0, xk_0 = 0.0, k_m = 0.0, k_0 = 0.0, xm_0 = 0.0, bt_0 = 0.0;
+  double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0, v4 = 0.0;
+  long long zo_out = z0 * nxy;
+  const int oo = (int)((ox + fa - 1) + nx * (oy + fb - 1));
+  for (int i = 0; i <= nzc + 1; i++) {
+    if (i + 1 <= nzc + 1) load(nxt);
+    // formation of x_k at the own point of plane zf = z0 - 1 + i (pointwise)
+    const double xk_p = use_r ? a0 * cur.r - a1 * cur.xm - a2 * cur.xpp : cur.xm;
+    __syncthreads();  // every thread finished the output that read slot (i & 1)
+    if (act) {
+      sXK[(i & 1) * S1 + t] = xk_p;
+      sKP[(i & 1) * S1 + t] = cur.kap;
+    }
+    // output plane z = zf - 1 (its in-plane x_k / kappa were published last iteration)
+    if (i >= 2 && inner) {
+      const double *X0 = sXK + ((i + 1) & 1) * S1, *K0 = sKP + ((i + 1) & 1) * S1;
+      const double kc = k_0, xc = xk_0;
+      double rx = (kc + K0[t - 1]) * (X0[t - 1] - xc);
+      double ry = (kc + K0[t + 1]) * (X0[t + 1] - xc);
+      rx = fma(kc + K0[t - GX], X0[t - GX] - xc, rx);
+      ry = fma(kc + K0[t + GX], X0[t + GX] - xc, ry);
+      rx = fma(kc + k_m, xk_m - xc, rx);
+      ry = fma(kc + cur.kap, xk_p - xc, ry);
+      const double r = fma(rx + ry, hh, bt_0);
+      v0 = fma(xc, xc, v0);
+      v1 = fma(xm_0, xc, v1);
+      v2 = fma(xm_0, r, v2);
+      v3 = fma(xc, r, v3);
+      v4 = fma(r, r, v4);
+      if (S.xout) S.xout[zo_out + oo] = xc;
+      rout[zo_out + oo] = r;
+    }
+    if (i >= 2) zo_out += nxy;
+    xk_m = xk_0; xk_0 = xk_p;
+    k_m = k_0; k_0 = cur.kap;
+    xm_0 = cur.xm;
+    bt_0 = cur.bt;
+    cur = nxt;
+  }
+  double v[NDOT] = {v0, v1, v2, v3, v4};
+  pass_epilogue(P, k, v);
+}
