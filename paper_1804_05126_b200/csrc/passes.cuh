@@ -1162,25 +1162,23 @@ __global__ void __launch_bounds__(March7<TX, TY, PM>::NT, MINB) k_pass_3d_v7(KPa
 // chunk of ZC planes; x_k and kappa planes go through 2-plane shared rings,
 // z-neighbours stay in registers, operands are prefetched one plane ahead.
 // ---------------------------------------------------------------------------
-template <int TX, int TY>
+template <int TX, int TY, int PM>
 struct Lazy3 {
   static constexpr int GX = TX + 2, GY = TY + 2, S1 = GX * GY;
   static constexpr int NT = (S1 + 31) / 32 * 32;
-  static constexpr size_t smem_doubles = 4 * (size_t)S1;
-};
-
-template <int PM>
-struct LOps {
-  double r, xm, xpp, kap, bt;
+  static constexpr int D = 2, RD = D + 1;          // operand planes in flight, private ring depth
+  static constexpr int NOP = 4 + PM;               // r, x_{k-1}, x_{k-2}, kappa, B_0..B_{PM-1}
+  static constexpr size_t smem_doubles = 4 * (size_t)NT + (size_t)RD * NOP * NT;
 };
 
 template <int TX, int TY, int ZC, int PM, int MINB>
-__global__ void __launch_bounds__(Lazy3<TX, TY>::NT, MINB) k_pass_3d_lazy(KParams P) {
-  using M = Lazy3<TX, TY>;
-  constexpr int NT = M::NT, GX = M::GX, S1 = M::S1;
+__global__ void __launch_bounds__(Lazy3<TX, TY, PM>::NT, MINB) k_pass_3d_lazy(KParams P) {
+  using M = Lazy3<TX, TY, PM>;
+  constexpr int NT = M::NT, GX = M::GX, S1 = M::S1, D = M::D, RD = M::RD, NOP = M::NOP;
   extern __shared__ double smem[];
-  double *sXK = smem;          // 2 x S1  x_k planes
-  double *sKP = smem + 2 * S1; // 2 x S1  kappa planes
+  double *sXK = smem;            // 2 x NT  x_k planes (shared)
+  double *sKP = smem + 2 * NT;   // 2 x NT  kappa planes (shared)
+  double *sOp = smem + 4 * NT;   // RD x NOP x NT  thread-private operand ring (cp.async)
 
   __shared__ PassScalars S;
   pass_guard(P);
@@ -1196,85 +1194,83 @@ __global__ void __launch_bounds__(Lazy3<TX, TY>::NT, MINB) k_pass_3d_lazy(KParam
   const long long z1 = (z0 + ZC < nz) ? z0 + ZC : nz;
   const int nzc = (int)(z1 - z0);
   const int t = threadIdx.x;
-  const double hh = 0.5 * P.inv_h2;
-  const double a0 = S.a0, a1 = S.a1, a2 = S.a2;
   const bool act = t < S1;
   const int fa = t % GX, fb = t / GX;
   const int o1 = act ? (int)(wrapc(ox + fa - 1, nx) + nx * wrapc(oy + fb - 1, ny)) : 0;
   const bool inner = act && fa >= 1 && fa <= TX && fb >= 1 && fb <= TY && (ox + fa - 1) < nx && (oy + fb - 1) < ny;
   const bool use_r = k >= 2, use_pp = S.xpp != nullptr;
-  const double *rin = P.r + (size_t)((k - 1) & 1) * (size_t)P.ldN;  // r_{k-1}
-  double *rout = P.r + (size_t)(k & 1) * (size_t)P.ldN;             // r_k
-  const double *xprev = S.xprev, *xpp = S.xpp, *kap = P.kappa;
-  double btc[PM];
-  const double *Bc[PM];
-#pragma unroll
-  for (int c = 0; c < PM; c++) {
-    btc[c] = c < p ? S.btc[c] : 0.0;
-    Bc[c] = c < p ? S.B[c] : nullptr;
-  }
+  const int oo = (int)((ox + fa - 1) + nx * (oy + fb - 1));
+
   auto znext = [&](long long zo) { const long long n = zo + nxy; return n == nz * nxy ? 0 : n; };
-  long long zoL = wrapc(z0 - 1, nz) * nxy;  // next plane to load
-  auto load = [&](LOps<PM> &o) {
-    o.r = o.xm = o.xpp = o.kap = o.bt = 0.0;
+  long long zoL = wrapc(z0 - 1, nz) * nxy;  // next operand plane to copy
+  auto issue = [&](int slot) {
     if (act) {
+      double *d = sOp + slot * NOP * NT + t;
       const long long g = zoL + o1;
-      if (use_r) o.r = __ldg(rin + g);
-      o.xm = __ldg(xprev + g);
-      if (use_pp) o.xpp = __ldg(xpp + g);
-      o.kap = __ldg(kap + g);
-      if (inner) {
-        double s = 0.0;
+      if (use_r) cp_async8(d, P.r + (size_t)((k - 1) & 1) * (size_t)P.ldN + g);
+      cp_async8(d + NT, S.xprev + g);
+      if (use_pp) cp_async8(d + 2 * NT, S.xpp + g);
+      cp_async8(d + 3 * NT, P.kappa + g);
+      if (inner)
 #pragma unroll
         for (int c = 0; c < PM; c++)
-          if (c < p) s = fma(__ldg(Bc[c] + g), btc[c], s);
-        o.bt = s;
-      }
+          if (c < p) cp_async8(d + (4 + c) * NT, S.B[c] + g);
     }
     zoL = znext(zoL);
   };
   // plane zf = z0 - 1 + i ; x_k formed for planes z0-1 .. z1 (own column), output z0 .. z1-1
-  LOps<PM> cur, nxt;
-  load(cur);
+  for (int q = 0; q < D; q++) {
+    issue(q);
+    cp_async_commit();
+  }
   double xk_m = 0.0, xk_0 = 0.0, k_m = 0.0, k_0 = 0.0, xm_0 = 0.0, bt_0 = 0.0;
   double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0, v4 = 0.0;
   long long zo_out = z0 * nxy;
-  const int oo = (int)((ox + fa - 1) + nx * (oy + fb - 1));
+  int rs = 0, ri = D;  // private ring: slot read this plane, slot issued this plane
   for (int i = 0; i <= nzc + 1; i++) {
-    if (i + 1 <= nzc + 1) load(nxt);
-    // formation of x_k at the own point of plane zf = z0 - 1 + i (pointwise)
-    const double xk_p = use_r ? a0 * cur.r - a1 * cur.xm - a2 * cur.xpp : cur.xm;
+    if (i + D <= nzc + 1) issue(ri);
+    cp_async_commit();
+    cp_async_wait<D>();  // this thread's copies of plane i have landed
+    const double *o = sOp + rs * NOP * NT + t;
+    const double xm = o[NT], kc_p = o[3 * NT];
+    double xk_p = xm;
+    if (use_r) xk_p = S.a0 * o[0] - S.a1 * xm - (use_pp ? S.a2 * o[2 * NT] : 0.0);
+    double bt = 0.0;
+    if (inner)
+#pragma unroll
+      for (int c = 0; c < PM; c++)
+        if (c < p) bt = fma(o[(4 + c) * NT], S.btc[c], bt);
     __syncthreads();  // every thread finished the output that read slot (i & 1)
-    if (act) {
-      sXK[(i & 1) * S1 + t] = xk_p;
-      sKP[(i & 1) * S1 + t] = cur.kap;
-    }
+    sXK[(i & 1) * NT + t] = xk_p;
+    sKP[(i & 1) * NT + t] = kc_p;
     // output plane z = zf - 1 (its in-plane x_k / kappa were published last iteration)
     if (i >= 2 && inner) {
-      const double *X0 = sXK + ((i + 1) & 1) * S1, *K0 = sKP + ((i + 1) & 1) * S1;
+      const double *X0 = sXK + ((i + 1) & 1) * NT, *K0 = sKP + ((i + 1) & 1) * NT;
       const double kc = k_0, xc = xk_0;
       double rx = (kc + K0[t - 1]) * (X0[t - 1] - xc);
       double ry = (kc + K0[t + 1]) * (X0[t + 1] - xc);
       rx = fma(kc + K0[t - GX], X0[t - GX] - xc, rx);
       ry = fma(kc + K0[t + GX], X0[t + GX] - xc, ry);
       rx = fma(kc + k_m, xk_m - xc, rx);
-      ry = fma(kc + cur.kap, xk_p - xc, ry);
-      const double r = fma(rx + ry, hh, bt_0);
+      ry = fma(kc + kc_p, xk_p - xc, ry);
+      const double r = fma(rx + ry, 0.5 * P.inv_h2, bt_0);
       v0 = fma(xc, xc, v0);
       v1 = fma(xm_0, xc, v1);
       v2 = fma(xm_0, r, v2);
       v3 = fma(xc, r, v3);
       v4 = fma(r, r, v4);
       if (S.xout) S.xout[zo_out + oo] = xc;
-      rout[zo_out + oo] = r;
+      P.r[(size_t)(k & 1) * (size_t)P.ldN + zo_out + oo] = r;
     }
     if (i >= 2) zo_out += nxy;
     xk_m = xk_0; xk_0 = xk_p;
-    k_m = k_0; k_0 = cur.kap;
-    xm_0 = cur.xm;
-    bt_0 = cur.bt;
-    cur = nxt;
+    k_m = k_0; k_0 = kc_p;
+    xm_0 = xm;
+    bt_0 = bt;
+    rs = rs + 1 == RD ? 0 : rs + 1;
+    ri = ri + 1 == RD ? 0 : ri + 1;
   }
+  cp_async_wait<0>();
   double v[NDOT] = {v0, v1, v2, v3, v4};
   pass_epilogue(P, k, v);
 }
