@@ -109,9 +109,14 @@ Layout layout(const kiops_operator_desc *op, int p, const kiops_options *o) {
       break;
     case KIOPS_OP_STENCIL3D7_VARKAPPA:
       L.grid_pass = (int)(((op->nx + M3X - 1) / M3X) * ((op->ny + M3Y - 1) / M3Y) * ((op->nz + M3Z - 1) / M3Z));
-      L.smem_pass = sizeof(double) * (p <= 2 ? Lazy3<M3X, M3Y, 2>::smem_doubles
-                                     : p <= 4 ? Lazy3<M3X, M3Y, 4>::smem_doubles : Lazy3<M3X, M3Y, 8>::smem_doubles);
-      L.block_pass = Lazy3<M3X, M3Y, 2>::NT;
+      if (op->nx % 2 == 0 && op->nx >= 2 && p <= 4) {  // pair kernel (16-byte aligned rows)
+        L.smem_pass = sizeof(double) * (p <= 2 ? LazyP<M3X, M3Y, 2>::smem_doubles : LazyP<M3X, M3Y, 4>::smem_doubles);
+        L.block_pass = LazyP<M3X, M3Y, 2>::NT;
+      } else {
+        L.smem_pass = sizeof(double) * (p <= 2 ? Lazy3<M3X, M3Y, 2>::smem_doubles
+                                       : p <= 4 ? Lazy3<M3X, M3Y, 4>::smem_doubles : Lazy3<M3X, M3Y, 8>::smem_doubles);
+        L.block_pass = Lazy3<M3X, M3Y, 2>::NT;
+      }
       break;
     default:
       L.grid_pass = (int)std::min<long long>((8 * N + 255) / 256, SM_COUNT_HINT * 8);
@@ -217,9 +222,12 @@ static kiops_status build_graph(kiops_ctx c) {
     case KIOPS_OP_STENCIL1D3: fpass = (void *)k_pass_stencil<T1D>; break;
     case KIOPS_OP_STENCIL2D5: fpass = (void *)k_pass_stencil<T2D>; break;
     case KIOPS_OP_STENCIL3D7_VARKAPPA:
-      fpass = c->p <= 2 ? (void *)k_pass_3d_lazy<M3X, M3Y, M3Z, 2, 3>
-            : c->p <= 4 ? (void *)k_pass_3d_lazy<M3X, M3Y, M3Z, 4, 3>
-                        : (void *)k_pass_3d_lazy<M3X, M3Y, M3Z, 8, 2>;
+      if (c->op.nx % 2 == 0 && c->op.nx >= 2 && c->p <= 4)
+        fpass = c->p <= 2 ? (void *)k_pass_3d_lazyp<M3X, M3Y, M3Z, 2, 3> : (void *)k_pass_3d_lazyp<M3X, M3Y, M3Z, 4, 2>;
+      else
+        fpass = c->p <= 2 ? (void *)k_pass_3d_lazy<M3X, M3Y, M3Z, 2, 3>
+              : c->p <= 4 ? (void *)k_pass_3d_lazy<M3X, M3Y, M3Z, 4, 3>
+                          : (void *)k_pass_3d_lazy<M3X, M3Y, M3Z, 8, 2>;
       break;
     default: break;
   }

@@ -1274,3 +1274,165 @@ __global__ void __launch_bounds__(Lazy3<TX, TY, PM>::NT, MINB) k_pass_3d_lazy(KP
   double v[NDOT] = {v0, v1, v2, v3, v4};
   pass_epilogue(P, k, v);
 }
+
+// ---------------------------------------------------------------------------
+// 3D variable-kappa LAZY pass, pair version (in use for even nx): every thread
+// owns TWO x-adjacent points (a 16-byte aligned pair) of the halo-1 plane of a
+// TX x TY column tile, so every cp.async, shared load/store and global store
+// moves 16 bytes and the x-neighbour inside the pair comes from registers.
+// Pairs span x in [ox-2, ox+TX+2) (one unused point each side keeps alignment).
+// Same arithmetic and dots as k_pass_3d_lazy.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void cp_async16(void *dst, const void *src) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(src) : "memory");
+}
+
+template <int TX, int TY, int PM>
+struct LazyP {
+  static constexpr int PX = TX / 2 + 2, GY = TY + 2, NPAIR = PX * GY;  // pairs per plane
+  static constexpr int NT = (NPAIR + 31) / 32 * 32;
+  static constexpr int D = 2, RD = D + 1, NOP = 4 + PM;
+  static constexpr size_t smem_doubles = 4 * (size_t)NPAIR * 2 + (size_t)RD * NOP * NT * 2;
+};
+
+template <int TX, int TY, int ZC, int PM, int MINB>
+__global__ void __launch_bounds__(LazyP<TX, TY, PM>::NT, MINB) k_pass_3d_lazyp(KParams P) {
+  using M = LazyP<TX, TY, PM>;
+  constexpr int NT = M::NT, PX = M::PX, NPAIR = M::NPAIR, D = M::D, RD = M::RD, NOP = M::NOP;
+  extern __shared__ double2 smem2[];
+  double2 *sXK = smem2;                // 2 x NPAIR   x_k pairs (shared plane ring)
+  double2 *sKP = smem2 + 2 * NPAIR;    // 2 x NPAIR   kappa pairs
+  double2 *sOp = smem2 + 4 * NPAIR;    // RD x NOP x NT  thread-private operand ring
+
+  __shared__ PassScalars S;
+  pass_guard(P);
+  if (threadIdx.x == 0) load_pass_scalars(P, S);
+  __syncthreads();
+  if (S.k == 0) return;
+  const int p = P.p, k = S.k;
+  const long long nx = P.nx, ny = P.ny, nz = P.nz, nxy = nx * ny;
+  const long long ntx = (nx + TX - 1) / TX, nty = (ny + TY - 1) / TY;
+  const long long bidx = blockIdx.x;
+  const long long ox = (bidx % ntx) * TX, oy = ((bidx / ntx) % nty) * TY;
+  const long long z0 = (bidx / (ntx * nty)) * ZC;
+  const long long z1 = (z0 + ZC < nz) ? z0 + ZC : nz;
+  const int nzc = (int)(z1 - z0);
+  const int t = threadIdx.x;
+  const bool act = t < NPAIR;
+  const int px = t % PX, py = t / PX;
+  // pair start x = ox - 2 + 2 px (even); wrapped global in-plane offset of the pair
+  const int o1 = act ? (int)(wrapc(ox - 2 + 2 * px, nx) + nx * wrapc(oy - 1 + py, ny)) : 0;
+  const bool rowin = py >= 1 && py <= TY && (oy - 1 + py) < ny;
+  const bool pin = act && rowin && px >= 1 && px <= TX / 2 && (ox - 2 + 2 * px) < nx;  // both points interior
+  const bool use_r = k >= 2, use_pp = S.xpp != nullptr;
+  const int oo = (int)((ox - 2 + 2 * px) + nx * (oy - 1 + py));
+  const double *rin = P.r + (size_t)((k - 1) & 1) * (size_t)P.ldN;
+  double *rout = P.r + (size_t)(k & 1) * (size_t)P.ldN;
+  const double *xprev = S.xprev, *xpp = S.xpp, *kap = P.kappa;
+  double *xout = S.xout;
+  const double a0 = S.a0, a1 = S.a1, a2 = S.a2, hh = 0.5 * P.inv_h2;
+  const double *Bc[PM];
+  double btc[PM];
+#pragma unroll
+  for (int c = 0; c < PM; c++) {
+    Bc[c] = c < p ? S.B[c] : nullptr;
+    btc[c] = c < p ? S.btc[c] : 0.0;
+  }
+
+  auto znext = [&](long long zo) { const long long n = zo + nxy; return n == nz * nxy ? 0 : n; };
+  long long zoL = wrapc(z0 - 1, nz) * nxy;
+  auto issue = [&](int slot) {
+    if (act) {
+      double2 *d = sOp + slot * NOP * NT + t;
+      const long long g = zoL + o1;
+      if (use_r) cp_async16(d, rin + g);
+      cp_async16(d + NT, xprev + g);
+      if (use_pp) cp_async16(d + 2 * NT, xpp + g);
+      cp_async16(d + 3 * NT, kap + g);
+      if (pin)
+#pragma unroll
+        for (int c = 0; c < PM; c++)
+          if (c < p) cp_async16(d + (4 + c) * NT, Bc[c] + g);
+    }
+    zoL = znext(zoL);
+  };
+  for (int q = 0; q < D; q++) {
+    issue(q);
+    cp_async_commit();
+  }
+  double2 xk_m = {0.0, 0.0}, xk_0 = {0.0, 0.0}, k_m = {0.0, 0.0}, k_0 = {0.0, 0.0}, xm_0 = {0.0, 0.0},
+          bt_0 = {0.0, 0.0};
+  double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0, v4 = 0.0;
+  long long zo_out = z0 * nxy;
+  int rs = 0, ri = D;
+  for (int i = 0; i <= nzc + 1; i++) {
+    if (i + D <= nzc + 1) issue(ri);
+    cp_async_commit();
+    cp_async_wait<D>();
+    const double2 *o = sOp + rs * NOP * NT + t;
+    const double2 xm = o[NT], kc_p = o[3 * NT];
+    double2 xk_p = xm;
+    if (use_r) {
+      const double2 rr = o[0];
+      xk_p.x = a0 * rr.x - a1 * xm.x;
+      xk_p.y = a0 * rr.y - a1 * xm.y;
+      if (use_pp) {
+        const double2 pp = o[2 * NT];
+        xk_p.x -= a2 * pp.x;
+        xk_p.y -= a2 * pp.y;
+      }
+    }
+    double2 bt = {0.0, 0.0};
+    if (pin)
+#pragma unroll
+      for (int c = 0; c < PM; c++)
+        if (c < p) {
+          const double2 b = o[(4 + c) * NT];
+          bt.x = fma(b.x, btc[c], bt.x);
+          bt.y = fma(b.y, btc[c], bt.y);
+        }
+    __syncthreads();  // the output that read slot (i & 1) has finished everywhere
+    if (act) {
+      sXK[(i & 1) * NPAIR + t] = xk_p;
+      sKP[(i & 1) * NPAIR + t] = kc_p;
+    }
+    if (i >= 2 && pin) {  // output plane z = zf - 1 for both points of the pair
+      const double2 *X0 = sXK + ((i + 1) & 1) * NPAIR, *K0 = sKP + ((i + 1) & 1) * NPAIR;
+      const double xl = X0[t - 1].y, xr = X0[t + 1].x, kl = K0[t - 1].y, kr = K0[t + 1].x;
+      const double2 xs = X0[t - PX], xn = X0[t + PX], ks = K0[t - PX], kn = K0[t + PX];
+      const double2 xc = xk_0, kc = k_0;
+      // point a (x), point b (x + 1)
+      double ra = (kc.x + kl) * (xl - xc.x);
+      double rb = (kc.y + kr) * (xr - xc.y);
+      ra = fma(kc.x + kc.y, xc.y - xc.x, ra);
+      rb = fma(kc.y + kc.x, xc.x - xc.y, rb);
+      ra = fma(kc.x + ks.x, xs.x - xc.x, ra);
+      rb = fma(kc.y + ks.y, xs.y - xc.y, rb);
+      ra = fma(kc.x + kn.x, xn.x - xc.x, ra);
+      rb = fma(kc.y + kn.y, xn.y - xc.y, rb);
+      ra = fma(kc.x + k_m.x, xk_m.x - xc.x, ra);
+      rb = fma(kc.y + k_m.y, xk_m.y - xc.y, rb);
+      ra = fma(kc.x + kc_p.x, xk_p.x - xc.x, ra);
+      rb = fma(kc.y + kc_p.y, xk_p.y - xc.y, rb);
+      const double r_a = fma(ra, hh, bt_0.x), r_b = fma(rb, hh, bt_0.y);
+      v0 = fma(xc.x, xc.x, fma(xc.y, xc.y, v0));
+      v1 = fma(xm_0.x, xc.x, fma(xm_0.y, xc.y, v1));
+      v2 = fma(xm_0.x, r_a, fma(xm_0.y, r_b, v2));
+      v3 = fma(xc.x, r_a, fma(xc.y, r_b, v3));
+      v4 = fma(r_a, r_a, fma(r_b, r_b, v4));
+      if (xout) *reinterpret_cast<double2 *>(xout + zo_out + oo) = xc;
+      *reinterpret_cast<double2 *>(rout + zo_out + oo) = make_double2(r_a, r_b);
+    }
+    if (i >= 2) zo_out += nxy;
+    xk_m = xk_0; xk_0 = xk_p;
+    k_m = k_0; k_0 = kc_p;
+    xm_0 = xm;
+    bt_0 = bt;
+    rs = rs + 1 == RD ? 0 : rs + 1;
+    ri = ri + 1 == RD ? 0 : ri + 1;
+  }
+  cp_async_wait<0>();
+  double v[NDOT] = {v0, v1, v2, v3, v4};
+  pass_epilogue(P, k, v);
+}
