@@ -109,8 +109,9 @@ Layout layout(const kiops_operator_desc *op, int p, const kiops_options *o) {
       break;
     case KIOPS_OP_STENCIL3D7_VARKAPPA:
       L.grid_pass = (int)(((op->nx + M3X - 1) / M3X) * ((op->ny + M3Y - 1) / M3Y) * ((op->nz + M3Z - 1) / M3Z));
-      if (op->nx % 2 == 0 && op->nx >= 2 && p <= 4) {  // pair kernel (16-byte aligned rows)
-        L.smem_pass = sizeof(double) * (p <= 2 ? LazyP<M3X, M3Y, 2>::smem_doubles : LazyP<M3X, M3Y, 4>::smem_doubles);
+      if (op->nx % 2 == 0 && op->nx >= 2 && p >= 1 && p <= 4) {  // pair kernel (16-byte aligned rows), exact p
+        L.smem_pass = sizeof(double) * (p == 1 ? LazyP<M3X, M3Y, 1>::smem_doubles : p == 2 ? LazyP<M3X, M3Y, 2>::smem_doubles
+                                       : p == 3 ? LazyP<M3X, M3Y, 3>::smem_doubles : LazyP<M3X, M3Y, 4>::smem_doubles);
         L.block_pass = LazyP<M3X, M3Y, 2>::NT;
       } else {
         L.smem_pass = sizeof(double) * (p <= 2 ? Lazy3<M3X, M3Y, 2>::smem_doubles
@@ -222,8 +223,11 @@ static kiops_status build_graph(kiops_ctx c) {
     case KIOPS_OP_STENCIL1D3: fpass = (void *)k_pass_stencil<T1D>; break;
     case KIOPS_OP_STENCIL2D5: fpass = (void *)k_pass_stencil<T2D>; break;
     case KIOPS_OP_STENCIL3D7_VARKAPPA:
-      if (c->op.nx % 2 == 0 && c->op.nx >= 2 && c->p <= 4)
-        fpass = c->p <= 2 ? (void *)k_pass_3d_lazyp<M3X, M3Y, M3Z, 2, 3> : (void *)k_pass_3d_lazyp<M3X, M3Y, M3Z, 4, 2>;
+      if (c->op.nx % 2 == 0 && c->op.nx >= 2 && c->p >= 1 && c->p <= 4)
+        fpass = c->p == 1 ? (void *)k_pass_3d_lazyp<M3X, M3Y, M3Z, 1, 3>
+              : c->p == 2 ? (void *)k_pass_3d_lazyp<M3X, M3Y, M3Z, 2, 3>
+              : c->p == 3 ? (void *)k_pass_3d_lazyp<M3X, M3Y, M3Z, 3, 3>
+                          : (void *)k_pass_3d_lazyp<M3X, M3Y, M3Z, 4, 2>;
       else
         fpass = c->p <= 2 ? (void *)k_pass_3d_lazy<M3X, M3Y, M3Z, 2, 3>
               : c->p <= 4 ? (void *)k_pass_3d_lazy<M3X, M3Y, M3Z, 4, 3>

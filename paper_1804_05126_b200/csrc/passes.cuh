@@ -1310,7 +1310,7 @@ __global__ void __launch_bounds__(LazyP<TX, TY, PM>::NT, MINB) k_pass_3d_lazyp(K
   if (threadIdx.x == 0) load_pass_scalars(P, S);
   __syncthreads();
   if (S.k == 0) return;
-  const int p = P.p, k = S.k;
+  const int k = S.k;  // PM == p exactly (template)
   const long long nx = P.nx, ny = P.ny, nz = P.nz, nxy = nx * ny;
   const long long ntx = (nx + TX - 1) / TX, nty = (ny + TY - 1) / TY;
   const long long bidx = blockIdx.x;
@@ -1327,6 +1327,9 @@ __global__ void __launch_bounds__(LazyP<TX, TY, PM>::NT, MINB) k_pass_3d_lazyp(K
   const bool pin = act && rowin && px >= 1 && px <= TX / 2 && (ox - 2 + 2 * px) < nx;  // both points interior
   const bool use_r = k >= 2, use_pp = S.xpp != nullptr;
   const int oo = (int)((ox - 2 + 2 * px) + nx * (oy - 1 + py));
+  // neighbour pair indices, clamped inside the plane for halo pairs (their results are masked)
+  const int tl = px > 0 ? t - 1 : t, tr = px < PX - 1 ? t + 1 : t;
+  const int ts = py > 0 ? t - PX : t, tn = py < M::GY - 1 ? t + PX : t;
   const double *rin = P.r + (size_t)((k - 1) & 1) * (size_t)P.ldN;
   double *rout = P.r + (size_t)(k & 1) * (size_t)P.ldN;
   const double *xprev = S.xprev, *xpp = S.xpp, *kap = P.kappa;
@@ -1336,8 +1339,8 @@ __global__ void __launch_bounds__(LazyP<TX, TY, PM>::NT, MINB) k_pass_3d_lazyp(K
   double btc[PM];
 #pragma unroll
   for (int c = 0; c < PM; c++) {
-    Bc[c] = c < p ? S.B[c] : nullptr;
-    btc[c] = c < p ? S.btc[c] : 0.0;
+    Bc[c] = S.B[c];
+    btc[c] = S.btc[c];
   }
 
   auto znext = [&](long long zo) { const long long n = zo + nxy; return n == nz * nxy ? 0 : n; };
@@ -1350,10 +1353,8 @@ __global__ void __launch_bounds__(LazyP<TX, TY, PM>::NT, MINB) k_pass_3d_lazyp(K
       cp_async16(d + NT, xprev + g);
       if (use_pp) cp_async16(d + 2 * NT, xpp + g);
       cp_async16(d + 3 * NT, kap + g);
-      if (pin)
 #pragma unroll
-        for (int c = 0; c < PM; c++)
-          if (c < p) cp_async16(d + (4 + c) * NT, Bc[c] + g);
+      for (int c = 0; c < PM; c++) cp_async16(d + (4 + c) * NT, Bc[c] + g);
     }
     zoL = znext(zoL);
   };
@@ -1384,23 +1385,22 @@ __global__ void __launch_bounds__(LazyP<TX, TY, PM>::NT, MINB) k_pass_3d_lazyp(K
       }
     }
     double2 bt = {0.0, 0.0};
-    if (pin)
 #pragma unroll
-      for (int c = 0; c < PM; c++)
-        if (c < p) {
-          const double2 b = o[(4 + c) * NT];
-          bt.x = fma(b.x, btc[c], bt.x);
-          bt.y = fma(b.y, btc[c], bt.y);
-        }
+    for (int c = 0; c < PM; c++) {
+      const double2 b = o[(4 + c) * NT];
+      bt.x = fma(b.x, btc[c], bt.x);
+      bt.y = fma(b.y, btc[c], bt.y);
+    }
     __syncthreads();  // the output that read slot (i & 1) has finished everywhere
     if (act) {
       sXK[(i & 1) * NPAIR + t] = xk_p;
       sKP[(i & 1) * NPAIR + t] = kc_p;
     }
-    if (i >= 2 && pin) {  // output plane z = zf - 1 for both points of the pair
+    if (i >= 2) {  // output plane z = zf - 1 for both points of the pair (branch-free;
+                   // halo pairs compute with clamped neighbours and are masked)
       const double2 *X0 = sXK + ((i + 1) & 1) * NPAIR, *K0 = sKP + ((i + 1) & 1) * NPAIR;
-      const double xl = X0[t - 1].y, xr = X0[t + 1].x, kl = K0[t - 1].y, kr = K0[t + 1].x;
-      const double2 xs = X0[t - PX], xn = X0[t + PX], ks = K0[t - PX], kn = K0[t + PX];
+      const double xl = X0[tl].y, xr = X0[tr].x, kl = K0[tl].y, kr = K0[tr].x;
+      const double2 xs = X0[ts], xn = X0[tn], ks = K0[ts], kn = K0[tn];
       const double2 xc = xk_0, kc = k_0;
       // point a (x), point b (x + 1)
       double ra = (kc.x + kl) * (xl - xc.x);
@@ -1416,13 +1416,17 @@ __global__ void __launch_bounds__(LazyP<TX, TY, PM>::NT, MINB) k_pass_3d_lazyp(K
       ra = fma(kc.x + kc_p.x, xk_p.x - xc.x, ra);
       rb = fma(kc.y + kc_p.y, xk_p.y - xc.y, rb);
       const double r_a = fma(ra, hh, bt_0.x), r_b = fma(rb, hh, bt_0.y);
-      v0 = fma(xc.x, xc.x, fma(xc.y, xc.y, v0));
-      v1 = fma(xm_0.x, xc.x, fma(xm_0.y, xc.y, v1));
-      v2 = fma(xm_0.x, r_a, fma(xm_0.y, r_b, v2));
-      v3 = fma(xc.x, r_a, fma(xc.y, r_b, v3));
-      v4 = fma(r_a, r_a, fma(r_b, r_b, v4));
-      if (xout) *reinterpret_cast<double2 *>(xout + zo_out + oo) = xc;
-      *reinterpret_cast<double2 *>(rout + zo_out + oo) = make_double2(r_a, r_b);
+      const double w = pin ? 1.0 : 0.0;
+      const double wxa = w * xc.x, wxb = w * xc.y, wra = w * r_a, wrb = w * r_b;
+      v0 = fma(wxa, xc.x, fma(wxb, xc.y, v0));
+      v1 = fma(xm_0.x, wxa, fma(xm_0.y, wxb, v1));
+      v2 = fma(xm_0.x, wra, fma(xm_0.y, wrb, v2));
+      v3 = fma(wxa, r_a, fma(wxb, r_b, v3));
+      v4 = fma(wra, r_a, fma(wrb, r_b, v4));
+      if (pin) {
+        if (xout) *reinterpret_cast<double2 *>(xout + zo_out + oo) = xc;
+        *reinterpret_cast<double2 *>(rout + zo_out + oo) = make_double2(r_a, r_b);
+      }
     }
     if (i >= 2) zo_out += nxy;
     xk_m = xk_0; xk_0 = xk_p;
