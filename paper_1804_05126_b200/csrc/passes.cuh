@@ -1328,8 +1328,9 @@ __global__ void __launch_bounds__(LazyP<TX, TY, PM>::NT, MINB) k_pass_3d_lazyp(K
   const bool use_r = k >= 2, use_pp = S.xpp != nullptr;
   const int oo = (int)((ox - 2 + 2 * px) + nx * (oy - 1 + py));
   // neighbour pair indices, clamped inside the plane for halo pairs (their results are masked)
-  const int tl = px > 0 ? t - 1 : t, tr = px < PX - 1 ? t + 1 : t;
-  const int ts = py > 0 ? t - PX : t, tn = py < M::GY - 1 ? t + PX : t;
+  const int tc = act ? t : 0;
+  const int tl = act && px > 0 ? t - 1 : tc, tr = act && px < PX - 1 ? t + 1 : tc;
+  const int ts = act && py > 0 ? t - PX : tc, tn = act && py < M::GY - 1 ? t + PX : tc;
   const double *rin = P.r + (size_t)((k - 1) & 1) * (size_t)P.ldN;
   double *rout = P.r + (size_t)(k & 1) * (size_t)P.ldN;
   const double *xprev = S.xprev, *xpp = S.xpp, *kap = P.kappa;
@@ -1416,8 +1417,8 @@ __global__ void __launch_bounds__(LazyP<TX, TY, PM>::NT, MINB) k_pass_3d_lazyp(K
       ra = fma(kc.x + kc_p.x, xk_p.x - xc.x, ra);
       rb = fma(kc.y + kc_p.y, xk_p.y - xc.y, rb);
       const double r_a = fma(ra, hh, bt_0.x), r_b = fma(rb, hh, bt_0.y);
-      const double w = pin ? 1.0 : 0.0;
-      const double wxa = w * xc.x, wxb = w * xc.y, wra = w * r_a, wrb = w * r_b;
+      // selects (not products) so garbage in masked halo lanes can never leak (0 * NaN)
+      const double wxa = pin ? xc.x : 0.0, wxb = pin ? xc.y : 0.0, wra = pin ? r_a : 0.0, wrb = pin ? r_b : 0.0;
       v0 = fma(wxa, xc.x, fma(wxb, xc.y, v0));
       v1 = fma(xm_0.x, wxa, fma(xm_0.y, wxb, v1));
       v2 = fma(xm_0.x, wra, fma(xm_0.y, wrb, v2));
