@@ -1359,6 +1359,8 @@ __global__ void __launch_bounds__(LazyP<TX, TY, PM>::NT, MINB) k_pass_3d_lazyp(K
     }
     zoL = znext(zoL);
   };
+  if (!act)  // idle lanes compute on zeros (their results are masked; keep them finite)
+    for (int q = 0; q < RD * NOP; q++) sOp[q * NT + t] = make_double2(0.0, 0.0);
   for (int q = 0; q < D; q++) {
     issue(q);
     cp_async_commit();
