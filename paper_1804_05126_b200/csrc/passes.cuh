@@ -1327,10 +1327,6 @@ __global__ void __launch_bounds__(LazyP<TX, TY, PM>::NT, MINB) k_pass_3d_lazyp(K
   const bool pin = act && rowin && px >= 1 && px <= TX / 2 && (ox - 2 + 2 * px) < nx;  // both points interior
   const bool use_r = k >= 2, use_pp = S.xpp != nullptr;
   const int oo = (int)((ox - 2 + 2 * px) + nx * (oy - 1 + py));
-  // neighbour pair indices, clamped inside the plane for halo pairs (their results are masked)
-  const int tc = act ? t : 0;
-  const int tl = act && px > 0 ? t - 1 : tc, tr = act && px < PX - 1 ? t + 1 : tc;
-  const int ts = act && py > 0 ? t - PX : tc, tn = act && py < M::GY - 1 ? t + PX : tc;
   const double *rin = P.r + (size_t)((k - 1) & 1) * (size_t)P.ldN;
   double *rout = P.r + (size_t)(k & 1) * (size_t)P.ldN;
   const double *xprev = S.xprev, *xpp = S.xpp, *kap = P.kappa;
@@ -1359,8 +1355,6 @@ __global__ void __launch_bounds__(LazyP<TX, TY, PM>::NT, MINB) k_pass_3d_lazyp(K
     }
     zoL = znext(zoL);
   };
-  if (!act)  // idle lanes compute on zeros (their results are masked; keep them finite)
-    for (int q = 0; q < RD * NOP; q++) sOp[q * NT + t] = make_double2(0.0, 0.0);
   for (int q = 0; q < D; q++) {
     issue(q);
     cp_async_commit();
@@ -1399,11 +1393,10 @@ __global__ void __launch_bounds__(LazyP<TX, TY, PM>::NT, MINB) k_pass_3d_lazyp(K
       sXK[(i & 1) * NPAIR + t] = xk_p;
       sKP[(i & 1) * NPAIR + t] = kc_p;
     }
-    if (i >= 2) {  // output plane z = zf - 1 for both points of the pair (branch-free;
-                   // halo pairs compute with clamped neighbours and are masked)
+    if (i >= 2 && pin) {  // output plane z = zf - 1 for both points of the pair
       const double2 *X0 = sXK + ((i + 1) & 1) * NPAIR, *K0 = sKP + ((i + 1) & 1) * NPAIR;
-      const double xl = X0[tl].y, xr = X0[tr].x, kl = K0[tl].y, kr = K0[tr].x;
-      const double2 xs = X0[ts], xn = X0[tn], ks = K0[ts], kn = K0[tn];
+      const double xl = X0[t - 1].y, xr = X0[t + 1].x, kl = K0[t - 1].y, kr = K0[t + 1].x;
+      const double2 xs = X0[t - PX], xn = X0[t + PX], ks = K0[t - PX], kn = K0[t + PX];
       const double2 xc = xk_0, kc = k_0;
       // point a (x), point b (x + 1)
       double ra = (kc.x + kl) * (xl - xc.x);
@@ -1419,17 +1412,13 @@ __global__ void __launch_bounds__(LazyP<TX, TY, PM>::NT, MINB) k_pass_3d_lazyp(K
       ra = fma(kc.x + kc_p.x, xk_p.x - xc.x, ra);
       rb = fma(kc.y + kc_p.y, xk_p.y - xc.y, rb);
       const double r_a = fma(ra, hh, bt_0.x), r_b = fma(rb, hh, bt_0.y);
-      // selects (not products) so garbage in masked halo lanes can never leak (0 * NaN)
-      const double wxa = pin ? xc.x : 0.0, wxb = pin ? xc.y : 0.0, wra = pin ? r_a : 0.0, wrb = pin ? r_b : 0.0;
-      v0 = fma(wxa, xc.x, fma(wxb, xc.y, v0));
-      v1 = fma(xm_0.x, wxa, fma(xm_0.y, wxb, v1));
-      v2 = fma(xm_0.x, wra, fma(xm_0.y, wrb, v2));
-      v3 = fma(wxa, r_a, fma(wxb, r_b, v3));
-      v4 = fma(wra, r_a, fma(wrb, r_b, v4));
-      if (pin) {
-        if (xout) *reinterpret_cast<double2 *>(xout + zo_out + oo) = xc;
-        *reinterpret_cast<double2 *>(rout + zo_out + oo) = make_double2(r_a, r_b);
-      }
+      v0 = fma(xc.x, xc.x, fma(xc.y, xc.y, v0));
+      v1 = fma(xm_0.x, xc.x, fma(xm_0.y, xc.y, v1));
+      v2 = fma(xm_0.x, r_a, fma(xm_0.y, r_b, v2));
+      v3 = fma(xc.x, r_a, fma(xc.y, r_b, v3));
+      v4 = fma(r_a, r_a, fma(r_b, r_b, v4));
+      if (xout) *reinterpret_cast<double2 *>(xout + zo_out + oo) = xc;
+      *reinterpret_cast<double2 *>(rout + zo_out + oo) = make_double2(r_a, r_b);
     }
     if (i >= 2) zo_out += nxy;
     xk_m = xk_0; xk_0 = xk_p;
