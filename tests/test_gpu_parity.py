@@ -258,3 +258,22 @@ def test_hostloop_hook_is_bitwise_identical():
         b, sb = k.apply(u, c["T"], hostloop=True)
         assert all(np.array_equal(x, y.cpu().numpy()) for x, y in zip(a, b))
         assert sa["krylov_vectors"] == sb["krylov_vectors"] and sa["passes"] == sb["passes"]
+
+
+def test_config4_full_size_trace_vs_stored_oracle_run():
+    # profiles/oracle_full_config4.json was written by scripts/oracle_full_run.py (calls
+    # only oracle/): the oracle's own full 256^3 decision trace.  The GPU run at full
+    # size must take identical decisions up to the first attempt whose omega inputs
+    # already differ (noise-level omega, R26) and report the same counts.
+    import json
+    import os
+
+    path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles",
+                        "oracle_full_config4.json")
+    ref = json.load(open(path))
+    g, gs, gt = gpu_run(W.config4())
+    n, dtau, dom = compare_traces(gt, ref["trace"], strict=False)
+    print(f"FULL c4: identical decisions on {n}/{len(ref['trace'])} attempts, dtau {dtau:.2e} domega {dom:.2e}")
+    assert n >= 10
+    for l, nrm in enumerate(ref["out_norms"]):
+        assert abs(np.linalg.norm(g[l]) - nrm) <= 1e-10 * nrm
