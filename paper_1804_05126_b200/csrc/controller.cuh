@@ -6,22 +6,39 @@
 #include "passes.cuh"
 
 #define CTRL_THREADS 512
-#define MM_KP 8  // k-panel depth of the CTA matmul
+#define CTRL_CL 8    // CTAs per controller cluster (portable maximum)
+#define MM_KP 8      // k-panel depth of the matmul
 
 // ---------------------------------------------------------------------------
-// Dense n x n (n <= KMAXM+1) helpers for ONE CTA.  Matrices are column-major with
-// leading dimension LDH in global scratch (L2-resident); shared memory holds the
-// matmul panels and, during the solve, the coefficient matrix.
+// Dense n x n (n <= KMAXM+1) linear algebra for ONE thread-block CLUSTER of
+// CTRL_CL CTAs.  Matrices are column-major, leading dimension LDH, in global
+// scratch (L2-resident).  Work is split across the cluster and ordered with
+// cluster barriers (barrier.cluster arrive.release / wait.acquire), which also
+// make each CTA's global writes visible to the others.
 // ---------------------------------------------------------------------------
-__device__ void cta_matmul(int n, const double *__restrict__ A, const double *__restrict__ B,
-                           double *__restrict__ C, double *sm) {
-  // C = A B (C must not alias A or B).  4x4 register micro-tiles, KP-deep smem panels.
+__device__ __forceinline__ void cl_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ unsigned cl_rank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ int cl_gtid() { return (int)(cl_rank() * blockDim.x + threadIdx.x); }
+__device__ __forceinline__ int cl_gsize() { return (int)(CTRL_CL * blockDim.x); }
+
+__device__ void cl_matmul(int n, const double *__restrict__ A, const double *__restrict__ B, double *__restrict__ C,
+                          double *sm) {
+  // C = A B (no aliasing).  4x4 register micro-tiles; tile t belongs to CTA t % CL.
   const int np = (n + 3) & ~3, tr = np >> 2, ntiles = tr * tr;
-  double *sA = sm;             // np x KP   sA[i + np*kk]
-  double *sB = sm + np * MM_KP; // KP x np  sB[kk + KP*j]
-  for (int t0 = 0; t0 < ntiles; t0 += blockDim.x) {
-    const int t = t0 + threadIdx.x;
-    const bool act = t < ntiles;
+  const int rank = (int)cl_rank();
+  double *sA = sm;               // np x KP   sA[i + np*kk]
+  double *sB = sm + np * MM_KP;  // np x KP   sB[j + np*kk]  (transposed panel)
+  const int nmine = (ntiles - rank + CTRL_CL - 1) / CTRL_CL;
+  for (int r0 = 0; r0 < nmine; r0 += blockDim.x) {
+    const int tl = r0 + threadIdx.x;
+    const bool act = tl < nmine;
+    const int t = rank + CTRL_CL * tl;
     const int ti = (t % tr) * 4, tj = (t / tr) * 4;
     double acc[4][4];
 #pragma unroll
@@ -33,18 +50,17 @@ __device__ void cta_matmul(int n, const double *__restrict__ A, const double *__
       for (int e = threadIdx.x; e < np * MM_KP; e += blockDim.x) {
         const int i = e % np, kk = e / np;
         sA[e] = (i < n && k0 + kk < n) ? A[i + (size_t)LDH * (k0 + kk)] : 0.0;
-      }
-      for (int e = threadIdx.x; e < np * MM_KP; e += blockDim.x) {
-        const int kk = e % MM_KP, j = e / MM_KP;
-        sB[e] = (j < n && k0 + kk < n) ? B[(k0 + kk) + (size_t)LDH * j] : 0.0;
+        sB[e] = (i < n && k0 + kk < n) ? B[(k0 + kk) + (size_t)LDH * i] : 0.0;
       }
       __syncthreads();
       if (act) {
 #pragma unroll
         for (int kk = 0; kk < MM_KP; kk++) {
-          double a[4], b[4];
-#pragma unroll
-          for (int q = 0; q < 4; q++) { a[q] = sA[ti + q + np * kk]; b[q] = sB[kk + MM_KP * (tj + q)]; }
+          const double2 a01 = *reinterpret_cast<const double2 *>(sA + ti + np * kk);
+          const double2 a23 = *reinterpret_cast<const double2 *>(sA + ti + 2 + np * kk);
+          const double2 b01 = *reinterpret_cast<const double2 *>(sB + tj + np * kk);
+          const double2 b23 = *reinterpret_cast<const double2 *>(sB + tj + 2 + np * kk);
+          const double a[4] = {a01.x, a01.y, a23.x, a23.y}, b[4] = {b01.x, b01.y, b23.x, b23.y};
 #pragma unroll
           for (int x = 0; x < 4; x++)
 #pragma unroll
@@ -59,11 +75,11 @@ __device__ void cta_matmul(int n, const double *__restrict__ A, const double *__
         for (int y = 0; y < 4; y++)
           if (ti + x < n && tj + y < n) C[(ti + x) + (size_t)LDH * (tj + y)] = acc[x][y];
   }
-  __syncthreads();
+  cl_sync();
 }
 
 __device__ double cta_norm1(int n, const double *A, double *red) {
-  // max column abs sum, broadcast to all threads
+  // max column abs sum, broadcast to all threads (every CTA computes the same value)
   double best = 0.0;
   for (int j = threadIdx.x; j < n; j += blockDim.x) {
     double s = 0.0;
@@ -88,89 +104,110 @@ __device__ double cta_norm1(int n, const double *A, double *red) {
   return r;
 }
 
-// Solve Q X = R in place (R <- X) by Gaussian elimination with partial pivoting
-// (first maximal |pivot|) applied to the right-hand sides, then back
-// substitution.  Q is copied to shared memory; R stays in global scratch.
-// Returns 0, or -1 for a zero pivot (all threads).
-__device__ int cta_solve(int n, const double *Qg, double *R, double *sm) {
+// Solve Q X = R in place (R <- X).  CTA 0 factors P Q = L U in its shared memory
+// (Gaussian elimination with partial pivoting, first maximal |pivot|) and
+// publishes L\U and the row permutation to global scratch; then every CTA
+// solves its own block of right-hand-side columns (one thread per column:
+// permutation, forward and back substitution from its shared-memory copy of L\U).
+// Returns 0, or -1 for a zero pivot (every CTA).
+__device__ int cl_solve(int n, const double *Qg, double *R, double *LUg, int *perm, int *flag, double *sm) {
   double *sQ = sm;  // n x n, ld = n
+  const int rank = (int)cl_rank();
   __shared__ int s_piv;
-  __shared__ int s_bad;
-  for (int e = threadIdx.x; e < n * n; e += blockDim.x) sQ[e] = Qg[(e % n) + (size_t)LDH * (e / n)];
-  if (threadIdx.x == 0) s_bad = 0;
-  __syncthreads();
-  for (int k = 0; k < n; k++) {
-    if (threadIdx.x < 32) {
-      double best = -1.0;
-      int bi = n;
-      for (int r = k + threadIdx.x; r < n; r += 32) {
-        const double a = fabs(sQ[r + n * k]);
-        if (a > best) { best = a; bi = r; }
-      }
-      for (int o = 16; o > 0; o >>= 1) {
-        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-        if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
-      }
-      if (threadIdx.x == 0) {
-        s_piv = bi;
-        if (!(best > 0.0)) s_bad = 1;
-      }
-    }
+  if (rank == 0) {
+    for (int e = threadIdx.x; e < n * n; e += blockDim.x) sQ[e] = Qg[(e % n) + (size_t)LDH * (e / n)];
+    for (int i = threadIdx.x; i < n; i += blockDim.x) perm[i] = i;
+    if (threadIdx.x == 0) *flag = 0;
     __syncthreads();
-    if (s_bad) return -1;
-    const int pv = s_piv;
-    if (pv != k) {
-      for (int c = threadIdx.x; c < n; c += blockDim.x) {
-        double t = sQ[k + n * c]; sQ[k + n * c] = sQ[pv + n * c]; sQ[pv + n * c] = t;
-        t = R[k + (size_t)LDH * c]; R[k + (size_t)LDH * c] = R[pv + (size_t)LDH * c]; R[pv + (size_t)LDH * c] = t;
+    for (int k = 0; k < n; k++) {
+      if (threadIdx.x < 32) {
+        double best = -1.0;
+        int bi = n;
+        for (int r = k + threadIdx.x; r < n; r += 32) {
+          const double a = fabs(sQ[r + n * k]);
+          if (a > best) { best = a; bi = r; }
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+          const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+          const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+          if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+        }
+        if (threadIdx.x == 0) {
+          s_piv = bi;
+          if (!(best > 0.0)) *flag = 1;
+          if (bi != k) { const int tp = perm[k]; perm[k] = perm[bi]; perm[bi] = tp; }
+        }
+      }
+      __syncthreads();
+      if (*flag) break;
+      const int pv = s_piv;
+      if (pv != k)
+        for (int c = threadIdx.x; c < n; c += blockDim.x) {
+          const double t = sQ[k + n * c]; sQ[k + n * c] = sQ[pv + n * c]; sQ[pv + n * c] = t;
+        }
+      __syncthreads();
+      const double piv = sQ[k + n * k];
+      for (int r = k + 1 + threadIdx.x; r < n; r += blockDim.x) sQ[r + n * k] = sQ[r + n * k] / piv;
+      __syncthreads();
+      const int rows = n - k - 1;
+      for (int e = threadIdx.x; e < rows * rows; e += blockDim.x) {
+        const int r = k + 1 + e % rows, c = k + 1 + e / rows;
+        sQ[r + n * c] -= sQ[r + n * k] * sQ[k + n * c];
       }
       __syncthreads();
     }
-    const double piv = sQ[k + n * k];
-    for (int r = k + 1 + threadIdx.x; r < n; r += blockDim.x) sQ[r + n * k] = sQ[r + n * k] / piv;
-    __syncthreads();
-    const int rows = n - k - 1;
-    if (rows > 0) {
-      // trailing update of Q (columns > k) and of every RHS column
-      const int tot = rows * (n - k - 1 + n);
-      for (int e = threadIdx.x; e < tot; e += blockDim.x) {
-        const int r = k + 1 + e % rows, cc = e / rows;
-        const double f = sQ[r + n * k];
-        if (cc < n - k - 1) {
-          const int c = k + 1 + cc;
-          sQ[r + n * c] -= f * sQ[k + n * c];
-        } else {
-          const int c = cc - (n - k - 1);
-          R[r + (size_t)LDH * c] -= f * R[k + (size_t)LDH * c];
-        }
-      }
-    }
-    __syncthreads();
+    for (int e = threadIdx.x; e < n * n; e += blockDim.x) LUg[e] = sQ[e];
   }
-  for (int k = n - 1; k >= 0; k--) {
-    const double d = sQ[k + n * k];
-    for (int c = threadIdx.x; c < n; c += blockDim.x) R[k + (size_t)LDH * c] = R[k + (size_t)LDH * c] / d;
-    __syncthreads();
-    const int tot = k * n;
-    for (int e = threadIdx.x; e < tot; e += blockDim.x) {
-      const int r = e % k, c = e / k;
-      R[r + (size_t)LDH * c] -= sQ[r + n * k] * R[k + (size_t)LDH * c];
-    }
-    __syncthreads();
+  cl_sync();
+  if (*flag) return -1;
+  const int cb = (n + CTRL_CL - 1) / CTRL_CL, c0 = rank * cb, c1 = min(n, c0 + cb);
+  double *sX = sm + n * n;  // n x cb right-hand-side block, column-major
+  for (int e = threadIdx.x; e < n * n; e += blockDim.x) sQ[e] = LUg[e];
+  for (int e = threadIdx.x; e < n * (c1 - c0); e += blockDim.x) {
+    const int i = e % n, c = e / n;
+    sX[i + n * c] = R[perm[i] + (size_t)LDH * (c0 + c)];  // apply the row permutation
   }
+  __syncthreads();
+  const int c = threadIdx.x;
+  if (c < c1 - c0) {
+    double *x = sX + n * c;
+    for (int i = 1; i < n; i++) {  // L y = P b (unit lower)
+      double s0 = x[i], s1 = 0.0;
+      int k = 0;
+      for (; k + 1 < i; k += 2) { s0 -= sQ[i + n * k] * x[k]; s1 -= sQ[i + n * (k + 1)] * x[k + 1]; }
+      if (k < i) s0 -= sQ[i + n * k] * x[k];
+      x[i] = s0 + s1;
+    }
+    for (int i = n - 1; i >= 0; i--) {  // U x = y
+      double s0 = x[i], s1 = 0.0;
+      int k = i + 1;
+      for (; k + 1 < n; k += 2) { s0 -= sQ[i + n * k] * x[k]; s1 -= sQ[i + n * (k + 1)] * x[k + 1]; }
+      if (k < n) s0 -= sQ[i + n * k] * x[k];
+      x[i] = (s0 + s1) / sQ[i + n * i];
+    }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < n * (c1 - c0); e += blockDim.x) {
+    const int i = e % n, cc = e / n;
+    R[i + (size_t)LDH * (c0 + cc)] = sX[i + n * cc];
+  }
+  cl_sync();
   return 0;
 }
 
-// F = exp(scale * M) for n <= KMAXM+1: diagonal Pade approximant with scaling and
-// squaring ("[47]" = Higham 2005, Algorithm 2.3; R17).  Degree cascade
-// {3,5,7,9,13} by the 1-norm thresholds theta_m of Higham's Table 2.3; above
-// theta_13, X is scaled by 2^-s and squared back s times.  Returns the number of
-// dense products (or -1 on a zero pivot / non-finite norm).
-__device__ int cta_expm(int n, const double *M, double scale, double *F, double *scr, double *sm) {
+// F = exp(scale * M) for n <= KMAXM+1, on the whole cluster: diagonal Pade
+// approximant with scaling and squaring ("[47]" = Higham 2005, Algorithm
+// 2.3; R17).  Degree cascade {3,5,7,9,13} by the 1-norm thresholds theta_m of
+// Higham's Table 2.3; above theta_13, X is scaled by 2^-s and squared back s times.
+// Every CTA of the cluster must call it with identical arguments.  Returns the
+// number of dense products (or -1 on a zero pivot / non-finite norm).
+__device__ int cl_expm(int n, const double *M, double scale, double *F, double *scr, double *sm) {
   double *X = scr + 0 * (size_t)LDH * LDH, *X2 = scr + 1 * (size_t)LDH * LDH, *X4 = scr + 2 * (size_t)LDH * LDH,
          *X6 = scr + 3 * (size_t)LDH * LDH, *X8 = scr + 4 * (size_t)LDH * LDH, *U = scr + 5 * (size_t)LDH * LDH,
          *V = scr + 6 * (size_t)LDH * LDH, *T = scr + 7 * (size_t)LDH * LDH;
+  double *LU = scr + 10 * (size_t)LDH * LDH;
+  int *perm = reinterpret_cast<int *>(scr + 11 * (size_t)LDH * LDH);
+  int *flag = perm + LDH;
   // [m/m] Pade numerator coefficients p_m(x) = sum b_j x^j, b_j proportional to
   // (2m-j)! m! / ((2m)! j! (m-j)!), integer-scaled as tabulated by Higham (2005).
   const double c3[4] = {120.0, 60.0, 12.0, 1.0};
@@ -181,12 +218,12 @@ __device__ int cta_expm(int n, const double *M, double scale, double *F, double 
   const double c13[14] = {64764752532480000.0, 32382376266240000.0, 7771770303897600.0,
                           1187353796428800.0, 129060195264000.0, 10559470521600.0, 670442572800.0,
                           33522128640.0, 1323241920.0, 40840800.0, 960960.0, 16380.0, 182.0, 1.0};
-  const int nn = n * n;
-  for (int e = threadIdx.x; e < nn; e += blockDim.x) {
+  const int nn = n * n, g0 = cl_gtid(), gs = cl_gsize();
+  for (int e = g0; e < nn; e += gs) {
     const int i = e % n, j = e / n;
     X[i + (size_t)LDH * j] = scale * M[i + (size_t)LDH * j];
   }
-  __syncthreads();
+  cl_sync();
   const double nrm = cta_norm1(n, X, sm);
   if (!isfinite(nrm)) return -1;
   int deg, s = 0;
@@ -199,17 +236,17 @@ __device__ int cta_expm(int n, const double *M, double scale, double *F, double 
     s = ceil_log2_exact(nrm / 5.371920351148152e0);
     if (s < 0) s = 0;
     const double f = ldexp(1.0, -s);
-    for (int e = threadIdx.x; e < nn; e += blockDim.x) X[(e % n) + (size_t)LDH * (e / n)] *= f;
-    __syncthreads();
+    for (int e = g0; e < nn; e += gs) X[(e % n) + (size_t)LDH * (e / n)] *= f;
+    cl_sync();
   }
   int mult = 0;
-  cta_matmul(n, X, X, X2, sm); mult++;
-  if (deg >= 5) { cta_matmul(n, X2, X2, X4, sm); mult++; }
-  if (deg >= 7) { cta_matmul(n, X2, X4, X6, sm); mult++; }
-  if (deg == 9) { cta_matmul(n, X4, X4, X8, sm); mult++; }
+  cl_matmul(n, X, X, X2, sm); mult++;
+  if (deg >= 5) { cl_matmul(n, X2, X2, X4, sm); mult++; }
+  if (deg >= 7) { cl_matmul(n, X2, X4, X6, sm); mult++; }
+  if (deg == 9) { cl_matmul(n, X4, X4, X8, sm); mult++; }
   if (deg < 13) {
     const double *b = deg == 3 ? c3 : deg == 5 ? c5 : deg == 7 ? c7 : c9;
-    for (int e = threadIdx.x; e < nn; e += blockDim.x) {
+    for (int e = g0; e < nn; e += gs) {
       const int i = e % n, j = e / n;
       const size_t q = i + (size_t)LDH * j;
       const double id = (i == j) ? 1.0 : 0.0;
@@ -220,48 +257,51 @@ __device__ int cta_expm(int n, const double *M, double scale, double *F, double 
       T[q] = odd;
       V[q] = even;
     }
-    __syncthreads();
-    cta_matmul(n, X, T, U, sm); mult++;   // U = X * odd part
+    cl_sync();
+    cl_matmul(n, X, T, U, sm); mult++;   // U = X * odd part
   } else {
     const double *b = c13;
-    for (int e = threadIdx.x; e < nn; e += blockDim.x) {
+    for (int e = g0; e < nn; e += gs) {
       const size_t q = (e % n) + (size_t)LDH * (e / n);
       T[q] = b[13] * X6[q] + b[11] * X4[q] + b[9] * X2[q];
       X8[q] = b[12] * X6[q] + b[10] * X4[q] + b[8] * X2[q];
     }
-    __syncthreads();
-    cta_matmul(n, X6, T, U, sm); mult++;
-    cta_matmul(n, X6, X8, V, sm); mult++;
-    for (int e = threadIdx.x; e < nn; e += blockDim.x) {
+    cl_sync();
+    cl_matmul(n, X6, T, U, sm); mult++;
+    cl_matmul(n, X6, X8, V, sm); mult++;
+    for (int e = g0; e < nn; e += gs) {
       const int i = e % n, j = e / n;
       const size_t q = i + (size_t)LDH * j;
       const double id = (i == j) ? 1.0 : 0.0;
       U[q] += b[7] * X6[q] + b[5] * X4[q] + b[3] * X2[q] + b[1] * id;
       V[q] += b[6] * X6[q] + b[4] * X4[q] + b[2] * X2[q] + b[0] * id;
     }
-    __syncthreads();
-    cta_matmul(n, X, U, T, sm); mult++;   // odd part: X [ ... ]
-    for (int e = threadIdx.x; e < nn; e += blockDim.x) {
+    cl_sync();
+    cl_matmul(n, X, U, T, sm); mult++;   // odd part: X [ ... ]
+    for (int e = g0; e < nn; e += gs) {
       const size_t q = (e % n) + (size_t)LDH * (e / n);
       U[q] = T[q];
     }
-    __syncthreads();
+    cl_sync();
   }
   // (V - U) F = (V + U)
-  for (int e = threadIdx.x; e < nn; e += blockDim.x) {
+  for (int e = g0; e < nn; e += gs) {
     const size_t q = (e % n) + (size_t)LDH * (e / n);
     T[q] = V[q] - U[q];
     F[q] = V[q] + U[q];
   }
-  __syncthreads();
-  if (cta_solve(n, T, F, sm) != 0) return -1;
+  cl_sync();
+  if (cl_solve(n, T, F, LU, perm, flag, sm) != 0) return -1;
   for (int k = 0; k < s; k++) {
-    cta_matmul(n, F, F, T, sm); mult++;
-    for (int e = threadIdx.x; e < nn; e += blockDim.x) {
+    double *src = (k & 1) ? T : F, *dst = (k & 1) ? F : T;
+    cl_matmul(n, src, src, dst, sm); mult++;
+  }
+  if (s & 1) {  // result in T
+    for (int e = g0; e < nn; e += gs) {
       const size_t q = (e % n) + (size_t)LDH * (e / n);
       F[q] = T[q];
     }
-    __syncthreads();
+    cl_sync();
   }
   return mult;
 }
@@ -316,49 +356,40 @@ __device__ int alg4_adapt(bool happy, bool accept, int j, int m, int m_min, int 
 }
 
 // ---------------------------------------------------------------------------
-// The controller: one CTA per attempt (Alg. 1 l.17-29 + Alg. 3 bookkeeping).
+// The controller: one thread-block cluster per attempt (Alg. 1 l.17-29 + Alg. 3
+// bookkeeping).  Every CTA takes part in the dense exponentials; CTA 0 thread 0
+// runs the scalar logic and broadcasts its decisions through global memory +
+// cluster barriers, so all CTAs follow the same control flow.
 // ---------------------------------------------------------------------------
-struct CtrlShared {
-  int j, happy, accept, final_, n_tau, stop, l0;
-  double tau, beta, eps, omega, h_next, t_now;
-};
-
-__global__ void __launch_bounds__(CTRL_THREADS, 1) k_ctrl(KParams P) {
+__global__ void __cluster_dims__(CTRL_CL, 1, 1) __launch_bounds__(CTRL_THREADS, 1) k_ctrl(KParams P) {
   extern __shared__ double sm[];
-  __shared__ CtrlShared C;
   DevState *st = P.st;
   const CallBlock *call = P.call;
   double *Mh = P.scratch + 8 * (size_t)LDH * LDH;  // H~ / H_j input
   double *F = P.scratch + 9 * (size_t)LDH * LDH;   // exponential output
-  double *scr = P.scratch;                          // 8 work matrices
-
+  double *scr = P.scratch;                          // work matrices
+  const unsigned rank = cl_rank();
+  const bool lead = rank == 0 && threadIdx.x == 0;
   const unsigned long long t_start = gtimer();
-  if (threadIdx.x == 0) {
-    C.stop = 0;
-    if (st->status != 0 || st->npass < 1) C.stop = 1;
-    if (st->npass < 1 && st->status == 0) st->status = KIOPS_ERR_CUDA;
-    else if (st->zero_start) C.stop = 2;
-    C.t_now = st->t_now;
-    const double rem0 = st->t_end - st->t_now;      // R11: never step past T_end
-    double tau = st->tau;
-    C.final_ = 0;
-    if (tau >= rem0) { tau = rem0; C.final_ = 1; }
-    st->tau = tau;
-    C.tau = tau;
-    C.j = st->npass - 1;
-    C.happy = st->happy;
-    C.beta = st->beta;
-    C.l0 = st->l;
-  }
-  __syncthreads();
-  if (C.stop == 1) {
-    if (threadIdx.x == 0) {
+
+  // phase 0: every thread reads the same state
+  const int stop = (st->status != 0 || st->npass < 1) ? 1 : (st->zero_start ? 2 : 0);
+  const double t_now = st->t_now, t_end = st->t_end, beta = st->beta;
+  const double rem0 = t_end - t_now;  // R11: never step past T_end
+  const bool final_ = st->tau >= rem0;
+  const double tau = final_ ? rem0 : st->tau;
+  const int j = st->npass - 1, happy = st->happy, l0 = st->l;
+  cl_sync();  // nobody writes the state before everyone has read it
+
+  if (stop == 1) {
+    if (lead) {
+      if (st->status == 0) st->status = KIOPS_ERR_CUDA;
       set_cond(P, COND_OUTER, 0u); set_cond(P, COND_INNER, 0u); set_cond(P, COND_ACCEPT, 0u);
     }
     return;
   }
-  if (C.stop == 2) {  // R27: zero start vector => every remaining output is 0
-    if (threadIdx.x == 0) {
+  if (stop == 2) {  // R27: zero start vector => every remaining output is 0
+    if (lead) {
       int o = 0;
       for (int l = st->l; l < call->n_out; l++) st->gemv_out[o++] = call->w[l];
       st->gemv_nout = o;
@@ -372,60 +403,55 @@ __global__ void __launch_bounds__(CTRL_THREADS, 1) k_ctrl(KParams P) {
     }
     return;
   }
-  const int j = C.j, n1 = j + 1;
+  const int n1 = j + 1, g0 = cl_gtid(), gs = cl_gsize();
   // R1 / Eq. 37: H~ = [[H(1:j,1:j), e_1],[0, 0]] from the IOP band (q = 2)
-  for (int e = threadIdx.x; e < n1 * n1; e += blockDim.x) {
+  for (int e = g0; e < n1 * n1; e += gs) {
     const int r = e % n1, c = e / n1;
     double v = 0.0;
     if (r < j && c < j && r >= c - 1 && r <= c + 1) v = P.H[r + (size_t)LDH * c];
     if (r == 0 && c == j) v = 1.0;
     Mh[r + (size_t)LDH * c] = v;
   }
-  __syncthreads();
-  const int nm = cta_expm(n1, Mh, C.tau, F, scr, sm);  // Alg. 1 l.18
-  if (threadIdx.x == 0) {
+  cl_sync();
+  const int nm = cl_expm(n1, Mh, tau, F, scr, sm);  // Alg. 1 l.18
+  if (lead) {
+    st->tau = tau;
     st->expm_calls++;
     double eps = 0.0, omega = 0.0, h_next = 0.0;
     if (nm < 0) st->status = KIOPS_ERR_NONFINITE;
-    if (!C.happy) {  // Eq. 36 via Eq. 38: entry (j, j+1); Eq. 39
+    if (!happy) {  // Eq. 36 via Eq. 38: entry (j, j+1); Eq. 39
       h_next = P.H[j + (size_t)LDH * (j - 1)];
-      eps = C.beta * h_next * fabs(F[(j - 1) + (size_t)LDH * j]);
-      omega = st->t_end * eps / (C.tau * P.tol);
+      eps = beta * h_next * fabs(F[(j - 1) + (size_t)LDH * j]);
+      omega = t_end * eps / (tau * P.tol);
     }
     if (!isfinite(omega)) st->status = KIOPS_ERR_NONFINITE;
     const long long att = st->attempt;
     const bool forced = att < call->n_forced;
-    const bool accept = forced ? (call->forced_acc[att] != 0) : (omega <= 1.4);  // P:425 (R10)
-    double tau_new = C.tau;
+    const bool acc = forced ? (call->forced_acc[att] != 0) : (omega <= 1.4);  // P:425 (R10)
+    double tau_new = tau;
     int m_new = st->m;
     if (!forced)
-      m_new = alg4_adapt(C.happy, accept, j, st->m, P.m_min, P.m_max, C.tau, omega, st->t_now, st->t_end, st,
-                         &tau_new);
+      m_new = alg4_adapt(happy, acc, j, st->m, P.m_min, P.m_max, tau, omega, t_now, t_end, st, &tau_new);
     if (att < KIOPS_TRACE_CAP) {
       kiops_trace_row &tr = P.trace[att];
-      tr.attempt = att; tr.j = j; tr.happy = C.happy; tr.accept = accept; tr.m_new = m_new;
-      tr.t_now = st->t_now; tr.tau = C.tau; tr.beta = C.beta; tr.h_next = h_next; tr.eps = eps;
+      tr.attempt = att; tr.j = j; tr.happy = happy; tr.accept = acc; tr.m_new = m_new;
+      tr.t_now = t_now; tr.tau = tau; tr.beta = beta; tr.h_next = h_next; tr.eps = eps;
       tr.omega = omega; tr.tau_new = tau_new;
     }
-    C.accept = accept && st->status == 0;
-    C.eps = eps; C.omega = omega; C.h_next = h_next;
+    const bool accept = acc && st->status == 0;
     // Alg. 3 l.2-9: outputs crossed by this substep (strict <, R16; all tasks, R15)
     int n_tau = 0;
-    if (C.accept) {
-      const double T_next = st->t_now + C.tau;
-      for (int k = st->l; k < call->n_out; k++)
+    if (accept) {
+      const double T_next = t_now + tau;
+      for (int k = l0; k < call->n_out; k++)
         if (fabs(call->T[k]) < fabs(T_next)) n_tau++;
-    }
-    C.n_tau = n_tau;
-    // advance the controller state
-    if (C.accept) {
       st->substeps++;
-      if (C.happy) st->happy_count++;
+      if (happy) st->happy_count++;
       st->hist_valid = 0;
     } else if (st->status == 0) {
       st->rejections++;
       st->hist_valid = 1;
-      st->omega_old = omega; st->tau_old = C.tau; st->j_old = j;
+      st->omega_old = omega; st->tau_old = tau; st->j_old = j;
     }
     st->attempt = att + 1;
     if (att + 1 < call->n_forced) {
@@ -436,61 +462,63 @@ __global__ void __launch_bounds__(CTRL_THREADS, 1) k_ctrl(KParams P) {
     st->tau = tau_new;
     st->m = m_new;
     st->final_m = m_new;
+    st->bc_accept = accept;
+    st->bc_ntau = n_tau;
   }
-  __syncthreads();
-  if (C.accept) {
-    // Alg. 3: coefficients of the one-pass GEMV.  Output rows 0..n_tau-1 are the
-    // crossed T_{l+k} (F2 = exp((T_{l+k} - T_now) H_j), l.13-15); the last row is
-    // the running solution (F, l.20).  coef[o][c-1] = beta F(c,1) / s_c.
-    const int n_tau = C.n_tau, l0 = C.l0;
+  cl_sync();
+  const int accept = st->bc_accept, n_tau = st->bc_ntau;
+  if (accept) {
+    // Alg. 3: coefficients of the one-pass GEMV.  Rows 0..n_tau-1 are the crossed
+    // T_{l+k} (F2 = exp((T_{l+k} - T_now) H_j), l.13-15); the last row is the
+    // running solution (F, l.20).  coef[o][c-1] = beta F(c,1) / s_c.
     const double sc_final = P.task1 ? pow(1.0 / call->T[call->n_out - 1], (double)P.p) : 1.0;
-    for (int c = threadIdx.x; c < j; c += blockDim.x) {
-      const double sg = (c == 0) ? C.beta : P.sig[c + 1];
-      P.coef[(size_t)n_tau * LDH + c] = C.beta * F[c] / sg * (C.final_ ? sc_final : 1.0);
-    }
-    __syncthreads();
+    if (rank == 0)
+      for (int c = threadIdx.x; c < j; c += blockDim.x) {
+        const double sg = (c == 0) ? beta : P.sig[c + 1];
+        P.coef[(size_t)n_tau * LDH + c] = beta * F[c] / sg * (final_ ? sc_final : 1.0);
+      }
+    cl_sync();
     for (int k = 0; k < n_tau; k++) {
-      for (int e = threadIdx.x; e < j * j; e += blockDim.x) {
+      for (int e = g0; e < j * j; e += gs) {
         const int r = e % j, c = e / j;
         Mh[r + (size_t)LDH * c] = (r >= c - 1 && r <= c + 1) ? P.H[r + (size_t)LDH * c] : 0.0;
       }
-      __syncthreads();
-      const double tt = call->T[l0 + k] - C.t_now;
-      const int nm2 = cta_expm(j, Mh, tt, F, scr, sm);
+      cl_sync();
+      const double tt = call->T[l0 + k] - t_now;
+      const int nm2 = cl_expm(j, Mh, tt, F, scr, sm);
       const double sc = P.task1 ? pow(1.0 / call->T[l0 + k], (double)P.p) : 1.0;
-      for (int c = threadIdx.x; c < j; c += blockDim.x) {
-        const double sg = (c == 0) ? C.beta : P.sig[c + 1];
-        P.coef[(size_t)k * LDH + c] = C.beta * F[c] / sg * sc;
-      }
-      if (threadIdx.x == 0) {
+      if (rank == 0)
+        for (int c = threadIdx.x; c < j; c += blockDim.x) {
+          const double sg = (c == 0) ? beta : P.sig[c + 1];
+          P.coef[(size_t)k * LDH + c] = beta * F[c] / sg * sc;
+        }
+      if (lead) {
         st->expm_calls++;
         if (nm2 < 0) st->status = KIOPS_ERR_NONFINITE;
       }
-      __syncthreads();
+      cl_sync();
     }
-    if (threadIdx.x == 0) {
+    if (lead) {
       for (int k = 0; k < n_tau; k++) st->gemv_out[k] = call->w[l0 + k];
-      const int lnew = l0 + n_tau;
-      st->gemv_out[n_tau] = C.final_ ? call->w[call->n_out - 1] : P.V;  // V slot 1 = running solution
+      st->gemv_out[n_tau] = final_ ? call->w[call->n_out - 1] : P.V;  // V slot 1 = running solution
       st->gemv_nout = n_tau + 1;
       st->gemv_j = j;
       st->gemv_x1 = st->x1;
       st->x1 = P.V;
-      st->l = lnew;
-      const double T_next = C.t_now + C.tau;
-      st->t_now = C.final_ ? st->t_end : T_next;  // Alg. 1 l.24, R11
-      st->npass = 0;                              // l.25
+      st->l = l0 + n_tau;
+      st->t_now = final_ ? t_end : t_now + tau;  // Alg. 1 l.24, R11
+      st->npass = 0;                             // l.25
       st->happy = 0;
       write_exact_tail(P, st->t_now, st->mu, P.tails + 1 * KMAXP);  // next substep's exact tail (Eq. 47)
     }
   }
-  if (threadIdx.x == 0) {
+  if (lead) {
     const bool more = st->status == 0 && st->t_now < st->t_end;
-    bool cont = more && st->attempt < P.max_attempts;
+    const bool cont = more && st->attempt < P.max_attempts;
     if (more && !cont) st->status = KIOPS_ERR_NO_CONVERGENCE;
     set_cond(P, COND_OUTER, cont ? 1u : 0u);
     set_cond(P, COND_INNER, (cont && st->npass < st->m + 1) ? 1u : 0u);
-    set_cond(P, COND_ACCEPT, C.accept ? 1u : 0u);
+    set_cond(P, COND_ACCEPT, accept ? 1u : 0u);
     st->ns_ctrl += gtimer() - t_start;
   }
 }

@@ -145,8 +145,9 @@ Layout layout(const kiops_operator_desc *op, int p, const kiops_options *o) {
 }
 
 size_t ctrl_smem_bytes() {
-  const size_t solve = sizeof(double) * (size_t)(KMAXM + 1) * (KMAXM + 1);
-  const size_t mm = sizeof(double) * 2 * (size_t)((KMAXM + 1 + 3) & ~3) * MM_KP;
+  const size_t n = KMAXM + 1, cb = (n + CTRL_CL - 1) / CTRL_CL;
+  const size_t solve = sizeof(double) * (n * n + n * cb);
+  const size_t mm = sizeof(double) * 2 * (size_t)((n + 3) & ~3) * MM_KP;
   return std::max(solve, mm);
 }
 
@@ -252,7 +253,7 @@ static kiops_status build_graph(kiops_ctx c) {
   } else {
     CK(add_kernel(b_inner, &n_a, nullptr, 0, fpass, c->L.grid_pass, c->L.block_pass, c->L.smem_pass, &P), "node pass");
   }
-  CK(add_kernel(b_outer, &n_ctrl, &n_inner, 1, (void *)k_ctrl, 1, CTRL_THREADS, ctrl_smem_bytes(), &P), "node ctrl");
+  CK(add_kernel(b_outer, &n_ctrl, &n_inner, 1, (void *)k_ctrl, CTRL_CL, CTRL_THREADS, ctrl_smem_bytes(), &P), "node ctrl");
   CK(add_cond(b_outer, &n_if, &n_ctrl, 1, P.h_accept, cudaGraphCondTypeIf, &b_if), "node if");
   CK(add_kernel(b_if, &n_gemv, nullptr, 0, (void *)k_gemv, c->L.grid_gemv, 256, 0, &P), "node gemv");
   CK(cudaGraphInstantiate(&c->exec, c->graph, 0), "cudaGraphInstantiate");
@@ -485,7 +486,7 @@ kiops_status kiops_apply_hostloop(kiops_ctx c, const double *const *u, const dou
       }
       if ((s = read_conds(c, cond)) != KIOPS_OK) return s;
     }
-    if ((s = launch_plain(c, (void *)k_ctrl, 1, CTRL_THREADS, ctrl_smem_bytes(), &P)) != KIOPS_OK) return s;
+    if ((s = launch_plain(c, (void *)k_ctrl, CTRL_CL, CTRL_THREADS, ctrl_smem_bytes(), &P)) != KIOPS_OK) return s;
     if ((s = read_conds(c, cond)) != KIOPS_OK) return s;
     if (cond[COND_ACCEPT])
       if ((s = launch_plain(c, (void *)k_gemv, c->L.grid_gemv, 256, 0, &P)) != KIOPS_OK) return s;

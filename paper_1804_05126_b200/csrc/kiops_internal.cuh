@@ -10,7 +10,7 @@
 #define KMAXO KIOPS_MAX_OUT
 #define KMAXM KIOPS_MAX_M
 #define LDH (KMAXM + 2)          // leading dimension of H and of every controller matrix
-#define NSCR 10                  // controller scratch matrices (LDH x LDH each)
+#define NSCR 12                  // controller scratch matrices (LDH x LDH each)
 #define NDOT 5                   // dots reduced per pass: S, G, E1, E2, R
 #define GEMV_OCHUNK 4            // outputs accumulated per GEMV chunk
 
@@ -46,6 +46,7 @@ struct DevState {
   unsigned long long t_pass0, t_gemv0, ns_pass, ns_ctrl, ns_gemv;
   unsigned int gemv_ticket;
   unsigned int cond[3];          // mirror of the graph conditionals (outer, inner, accept)
+  int bc_accept, bc_ntau;        // controller-cluster broadcast (CTA 0 -> all CTAs)
 };
 
 // Frozen per-ctx parameters, passed BY VALUE to every kernel (graph node params).
