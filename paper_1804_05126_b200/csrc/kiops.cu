@@ -35,6 +35,7 @@ constexpr int SM_COUNT_HINT = 148;
 #define T1D 1, 256, 1, 1
 #define T2D 2, 64, 16, 1
 #define T3D 3, 32, 8, 4
+#define L2YC 8
 #define M3X 32
 #define M3Y 8
 #define M3Z 32
@@ -100,12 +101,18 @@ Layout layout(const kiops_operator_desc *op, int p, const kiops_options *o) {
   L.grid_form = L.grid_gemv;
   switch (op->kind) {
     case KIOPS_OP_STENCIL1D3:
-      L.grid_pass = (int)((op->nx + 255) / 256);
-      L.smem_pass = stencil_smem_bytes<T1D>();
-      break;
     case KIOPS_OP_STENCIL2D5:
-      L.grid_pass = (int)(((op->nx + 63) / 64) * ((op->ny + 15) / 16));
-      L.smem_pass = stencil_smem_bytes<T2D>();
+      if (op->nx % 2 == 0 && p <= 4) {  // warp-strip lazy kernel (16-byte pairs)
+        const long long strips = (op->nx + 59) / 60 * ((op->ny + L2YC - 1) / L2YC);
+        L.grid_pass = (int)((strips + 7) / 8);
+        L.smem_pass = 0;
+      } else if (op->kind == KIOPS_OP_STENCIL1D3) {
+        L.grid_pass = (int)((op->nx + 255) / 256);
+        L.smem_pass = stencil_smem_bytes<T1D>();
+      } else {
+        L.grid_pass = (int)(((op->nx + 63) / 64) * ((op->ny + 15) / 16));
+        L.smem_pass = stencil_smem_bytes<T2D>();
+      }
       break;
     case KIOPS_OP_STENCIL3D7_VARKAPPA:
       L.grid_pass = (int)(((op->nx + M3X - 1) / M3X) * ((op->ny + M3Y - 1) / M3Y) * ((op->nz + M3Z - 1) / M3Z));
@@ -127,7 +134,7 @@ Layout layout(const kiops_operator_desc *op, int p, const kiops_options *o) {
   size_t off = 0;
   const size_t vec = (size_t)L.ldN * sizeof(double);
   L.V = off; off += al((size_t)(o->m_max + 1) * vec);
-  L.r = off; off += (op->kind == KIOPS_OP_CSR || op->kind == KIOPS_OP_STENCIL3D7_VARKAPPA) ? 2 * al(vec) : 0;
+  L.r = off; off += 2 * al(vec);  // r_k ping-pong (lazy passes; CSR uses the first)
   L.staging = off; off += o->host_staging ? al((size_t)(p + 1 + o->max_outputs) * vec) : 0;
   L.state = off; off += al(sizeof(DevState));
   L.call = off; off += al(sizeof(CallBlock));
@@ -220,9 +227,17 @@ static kiops_status build_graph(kiops_ctx c) {
   CK(cudaGraphConditionalHandleCreate(&P.h_accept, c->graph, 0, cudaGraphCondAssignDefault), "handle accept");
 
   void *fpass = nullptr;
+  const bool lazy2d = c->op.nx % 2 == 0 && c->p <= 4;
   switch (c->op.kind) {
-    case KIOPS_OP_STENCIL1D3: fpass = (void *)k_pass_stencil<T1D>; break;
-    case KIOPS_OP_STENCIL2D5: fpass = (void *)k_pass_stencil<T2D>; break;
+    case KIOPS_OP_STENCIL1D3:
+    case KIOPS_OP_STENCIL2D5:
+      if (lazy2d)
+        fpass = c->p == 0 ? (void *)k_pass_2d_lazy<L2YC, 0> : c->p == 1 ? (void *)k_pass_2d_lazy<L2YC, 1>
+              : c->p == 2 ? (void *)k_pass_2d_lazy<L2YC, 2> : c->p == 3 ? (void *)k_pass_2d_lazy<L2YC, 3>
+                          : (void *)k_pass_2d_lazy<L2YC, 4>;
+      else
+        fpass = c->op.kind == KIOPS_OP_STENCIL1D3 ? (void *)k_pass_stencil<T1D> : (void *)k_pass_stencil<T2D>;
+      break;
     case KIOPS_OP_STENCIL3D7_VARKAPPA:
       if (c->op.nx % 2 == 0 && c->op.nx >= 2 && c->p >= 1 && c->p <= 4)
         fpass = c->p == 1 ? (void *)k_pass_3d_lazyp<M3X, M3Y, M3Z, 1, 3>
@@ -307,6 +322,10 @@ kiops_status kiops_create(const kiops_operator_desc *op, int p, const kiops_opti
   P.N = op_n(op);
   P.ldN = L.ldN;
   for (int i = 0; i < 5; i++) P.w[i] = op->w[i];
+  if (op->kind == KIOPS_OP_STENCIL1D3 && op->nx % 2 == 0 && p <= 4) {
+    // the 1D operator runs on the 2D warp-strip kernel (ny = 1): {W, E, S, N, C} = {W, E, 0, 0, C}
+    P.w[0] = op->w[0]; P.w[1] = op->w[2]; P.w[2] = 0.0; P.w[3] = 0.0; P.w[4] = op->w[1];
+  }
   P.diag = op->diag;
   P.kappa = op->kappa;
   P.inv_h2 = op->inv_h2;

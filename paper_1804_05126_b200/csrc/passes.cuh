@@ -1432,3 +1432,110 @@ __global__ void __launch_bounds__(LazyP<TX, TY, PM>::NT, MINB) k_pass_3d_lazyp(K
   double v[NDOT] = {v0, v1, v2, v3, v4};
   pass_epilogue(P, k, v);
 }
+
+// ---------------------------------------------------------------------------
+// 2D / 1D 5-point (+ diagonal) LAZY pass (in use for even nx): one WARP owns a
+// strip of 30 interior x-pairs (+1 halo pair each side) and marches YC rows in y.
+// Lane l holds the 16-byte aligned pair x = x0 - 2 + 2l, x0 + 1 - 2 + 2l.
+//   x_k  = a0 r_{k-1} - a1 x_{k-1} - a2 x_{k-2}   (pointwise, every lane)
+//   r_k  = W x_k(x-1) + E x_k(x+1) + S x_k(y-1) + N x_k(y+1) + (C + d) x_k + nu B t_k
+// x-neighbours come from warp shuffles, y-neighbours from registers: no shared
+// memory, no barriers.  Operands are prefetched one row ahead in registers.
+// 1D uses the same kernel with ny = 1 and S = N = 0.
+// ---------------------------------------------------------------------------
+template <int PM>
+struct Row2 {
+  double2 r, xm, pp, d, b[PM > 0 ? PM : 1];
+};
+
+template <int YC, int PM>
+__global__ void __launch_bounds__(256, 2) k_pass_2d_lazy(KParams P) {
+  constexpr int IP = 30;  // interior pairs per warp strip
+  __shared__ PassScalars S;
+  pass_guard(P);
+  if (threadIdx.x == 0) load_pass_scalars(P, S);
+  __syncthreads();
+  if (S.k == 0) return;
+  const int k = S.k;
+  const long long nx = P.nx, ny = P.ny;
+  const long long nsx = (nx + 2 * IP - 1) / (2 * IP), ncy = (ny + YC - 1) / YC;
+  const int lane = threadIdx.x & 31;
+  const long long w = (blockIdx.x * (long long)blockDim.x + threadIdx.x) / 32;
+  const bool wact = w < nsx * ncy;
+  const long long sx = wact ? w % nsx : 0, cy = wact ? w / nsx : 0;
+  const long long x0 = sx * 2 * IP, y0 = cy * YC;
+  const long long y1 = (y0 + YC < ny) ? y0 + YC : ny;
+  const long long px = x0 - 2 + 2 * lane;                 // first point of the own pair
+  const long long pxw = wrapc(px, nx);
+  const bool pin = wact && lane >= 1 && lane <= IP && px < nx;
+  const bool use_r = k >= 2, use_pp = S.xpp != nullptr, use_d = P.diag != nullptr;
+  const double *rin = P.r + (size_t)((k - 1) & 1) * (size_t)P.ldN;
+  double *rout = P.r + (size_t)(k & 1) * (size_t)P.ldN;
+  const double a0 = S.a0, a1 = S.a1, a2 = S.a2;
+  const double Ww = P.w[0], Ew = P.w[1], Sw = P.w[2], Nw = P.w[3], Cw = P.w[4];
+  double btc[PM > 0 ? PM : 1];
+  const double *Bc[PM > 0 ? PM : 1];
+#pragma unroll
+  for (int c = 0; c < PM; c++) { btc[c] = S.btc[c]; Bc[c] = S.B[c]; }
+
+  auto load = [&](long long y, Row2<PM> &o) {
+    const long long g = pxw + nx * wrapc(y, ny);
+    const double2 z2 = make_double2(0.0, 0.0);
+    o.r = z2; o.pp = z2; o.d = z2;
+    if (use_r) o.r = __ldg(reinterpret_cast<const double2 *>(rin + g));
+    o.xm = __ldg(reinterpret_cast<const double2 *>(S.xprev + g));
+    if (use_pp) o.pp = __ldg(reinterpret_cast<const double2 *>(S.xpp + g));
+    if (use_d) o.d = __ldg(reinterpret_cast<const double2 *>(P.diag + g));
+#pragma unroll
+    for (int c = 0; c < PM; c++) o.b[c] = pin ? __ldg(reinterpret_cast<const double2 *>(Bc[c] + g)) : z2;
+  };
+  auto form = [&](const Row2<PM> &o) {
+    if (!use_r) return o.xm;
+    double2 x;
+    x.x = a0 * o.r.x - a1 * o.xm.x - a2 * o.pp.x;
+    x.y = a0 * o.r.y - a1 * o.xm.y - a2 * o.pp.y;
+    return x;
+  };
+  double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0, v4 = 0.0;
+  if (wact) {
+    Row2<PM> cur, nxt;
+    load(y0 - 1, cur);
+    load(y0, nxt);
+    double2 xk_m = form(cur);                 // x_k(y - 1)
+    load(y0 + 1, cur);                        // row y0 + 1 (N neighbour of row y0)
+    Row2<PM> row0 = nxt;                      // operands of row y (output row)
+    double2 xk_0 = form(row0);                // x_k(y)
+    for (long long y = y0; y < y1; y++) {
+      Row2<PM> ahead;
+      if (y + 2 <= y1) load(y + 2, ahead);     // prefetch row y + 2
+      const double2 xk_p = form(cur);          // x_k(y + 1)
+      // x-neighbours of row y: left of point a is lane-1's point b, right of b is lane+1's a
+      const double xl = __shfl_up_sync(0xffffffffu, xk_0.y, 1);
+      const double xr = __shfl_down_sync(0xffffffffu, xk_0.x, 1);
+      double ra = Ww * xl + Ew * xk_0.y + Sw * xk_m.x + Nw * xk_p.x + (Cw + row0.d.x) * xk_0.x;
+      double rb = Ww * xk_0.x + Ew * xr + Sw * xk_m.y + Nw * xk_p.y + (Cw + row0.d.y) * xk_0.y;
+#pragma unroll
+      for (int c = 0; c < PM; c++) {
+        ra = fma(row0.b[c].x, btc[c], ra);
+        rb = fma(row0.b[c].y, btc[c], rb);
+      }
+      if (pin) {
+        const double2 xm = row0.xm;
+        v0 = fma(xk_0.x, xk_0.x, fma(xk_0.y, xk_0.y, v0));
+        v1 = fma(xm.x, xk_0.x, fma(xm.y, xk_0.y, v1));
+        v2 = fma(xm.x, ra, fma(xm.y, rb, v2));
+        v3 = fma(xk_0.x, ra, fma(xk_0.y, rb, v3));
+        v4 = fma(ra, ra, fma(rb, rb, v4));
+        const long long g = px + nx * y;
+        if (S.xout) *reinterpret_cast<double2 *>(S.xout + g) = xk_0;
+        *reinterpret_cast<double2 *>(rout + g) = make_double2(ra, rb);
+      }
+      xk_m = xk_0;
+      xk_0 = xk_p;
+      row0 = cur;
+      cur = ahead;
+    }
+  }
+  double v[NDOT] = {v0, v1, v2, v3, v4};
+  pass_epilogue(P, k, v);
+}
