@@ -7,7 +7,7 @@
 
 #define CTRL_THREADS 512
 #define CTRL_CL 8    // CTAs per controller cluster (portable maximum)
-#define MM_KP 8      // k-panel depth of the matmul
+#define MM_KP 32     // k-panel depth of the matmul (fewer barriers per product)
 
 // ---------------------------------------------------------------------------
 // Dense n x n (n <= KMAXM+1) linear algebra for ONE thread-block CLUSTER of
@@ -54,7 +54,7 @@ __device__ void cl_matmul(int n, const double *__restrict__ A, const double *__r
       }
       __syncthreads();
       if (act) {
-#pragma unroll
+#pragma unroll 8
         for (int kk = 0; kk < MM_KP; kk++) {
           const double2 a01 = *reinterpret_cast<const double2 *>(sA + ti + np * kk);
           const double2 a23 = *reinterpret_cast<const double2 *>(sA + ti + 2 + np * kk);
@@ -533,21 +533,77 @@ __global__ void __launch_bounds__(256) k_gemv(KParams P) {
   if (blockIdx.x == 0 && threadIdx.x == 0) st->t_gemv0 = gtimer();
   const int j = st->gemv_j, nout = st->gemv_nout;
   const double *x1 = st->gemv_x1;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < P.N;
-       i += (long long)gridDim.x * blockDim.x) {
-    for (int o0 = 0; o0 < nout; o0 += GEMV_OCHUNK) {
-      double acc[GEMV_OCHUNK];
+  const long long N = P.N;
+  __shared__ double sc[GEMV_OCHUNK * LDH];
+  __shared__ double *outp[GEMV_OCHUNK];
+  // 16-byte path when every stream is 16-byte aligned (V slots always are)
+  bool vec = ((uintptr_t)x1 & 15) == 0;
+  for (int o = 0; o < nout; o++) vec = vec && (((uintptr_t)st->gemv_out[o] & 15) == 0);
+  const long long npair = vec ? N / 2 : 0;
+  const long long gt = blockIdx.x * (long long)blockDim.x + threadIdx.x, gsz = (long long)gridDim.x * blockDim.x;
+  for (int o0 = 0; o0 < nout; o0 += GEMV_OCHUNK) {
+    const int no = min(GEMV_OCHUNK, nout - o0);
+    __syncthreads();
+    for (int e = threadIdx.x; e < no * j; e += blockDim.x) sc[(e / j) * LDH + e % j] = P.coef[(size_t)(o0 + e / j) * LDH + e % j];
+    if (threadIdx.x < no) outp[threadIdx.x] = st->gemv_out[o0 + threadIdx.x];
+    __syncthreads();
+    for (long long q = gt; q < npair; q += gsz) {
+      double2 acc[GEMV_OCHUNK];
 #pragma unroll
-      for (int o = 0; o < GEMV_OCHUNK; o++) acc[o] = 0.0;
-      for (int c = 0; c < j; c++) {
-        const double x = (c == 0) ? x1[i] : P.V[(size_t)c * P.ldN + i];
+      for (int o = 0; o < GEMV_OCHUNK; o++) acc[o] = make_double2(0.0, 0.0);
+      if (j > 0) {
+        const double2 x = __ldg(reinterpret_cast<const double2 *>(x1) + q);
+#pragma unroll
+        for (int o = 0; o < GEMV_OCHUNK; o++) {
+          acc[o].x = fma(sc[o * LDH], x.x, acc[o].x);
+          acc[o].y = fma(sc[o * LDH], x.y, acc[o].y);
+        }
+      }
+      const double2 *vp = reinterpret_cast<const double2 *>(P.V + P.ldN) + q;  // slot 2
+      const long long ld2 = P.ldN / 2;
+      int c = 1;
+      for (; c + 3 < j; c += 4) {
+        const double2 xa = __ldg(vp), xb = __ldg(vp + ld2), xc = __ldg(vp + 2 * ld2), xd = __ldg(vp + 3 * ld2);
+        vp += 4 * ld2;
+#pragma unroll
+        for (int o = 0; o < GEMV_OCHUNK; o++) {
+          if (o < no) {
+            const double *cf = sc + o * LDH + c;
+            acc[o].x = fma(cf[0], xa.x, acc[o].x); acc[o].y = fma(cf[0], xa.y, acc[o].y);
+            acc[o].x = fma(cf[1], xb.x, acc[o].x); acc[o].y = fma(cf[1], xb.y, acc[o].y);
+            acc[o].x = fma(cf[2], xc.x, acc[o].x); acc[o].y = fma(cf[2], xc.y, acc[o].y);
+            acc[o].x = fma(cf[3], xd.x, acc[o].x); acc[o].y = fma(cf[3], xd.y, acc[o].y);
+          }
+        }
+      }
+      for (; c < j; c++) {
+        const double2 xa = __ldg(vp);
+        vp += ld2;
 #pragma unroll
         for (int o = 0; o < GEMV_OCHUNK; o++)
-          if (o0 + o < nout) acc[o] = fma(P.coef[(size_t)(o0 + o) * LDH + c], x, acc[o]);
+          if (o < no) {
+            acc[o].x = fma(sc[o * LDH + c], xa.x, acc[o].x);
+            acc[o].y = fma(sc[o * LDH + c], xa.y, acc[o].y);
+          }
       }
 #pragma unroll
       for (int o = 0; o < GEMV_OCHUNK; o++)
-        if (o0 + o < nout) st->gemv_out[o0 + o][i] = acc[o];
+        if (o < no) reinterpret_cast<double2 *>(outp[o])[q] = acc[o];
+    }
+    // scalar path: odd tail element or unaligned streams
+    for (long long i = 2 * npair + gt; i < N; i += gsz) {
+      double acc[GEMV_OCHUNK];
+#pragma unroll
+      for (int o = 0; o < GEMV_OCHUNK; o++) acc[o] = 0.0;
+      for (int cc = 0; cc < j; cc++) {
+        const double x = (cc == 0) ? x1[i] : P.V[(size_t)cc * P.ldN + i];
+#pragma unroll
+        for (int o = 0; o < GEMV_OCHUNK; o++)
+          if (o < no) acc[o] = fma(sc[o * LDH + cc], x, acc[o]);
+      }
+#pragma unroll
+      for (int o = 0; o < GEMV_OCHUNK; o++)
+        if (o < no) outp[o][i] = acc[o];
     }
   }
   __syncthreads();

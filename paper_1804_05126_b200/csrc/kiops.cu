@@ -97,7 +97,7 @@ Layout layout(const kiops_operator_desc *op, int p, const kiops_options *o) {
   L.block_pass = 256;
   const long long blocks256 = (N + 255) / 256;
   L.grid_setup = (int)std::min<long long>(blocks256, SM_COUNT_HINT * 8);
-  L.grid_gemv = (int)std::min<long long>(blocks256, SM_COUNT_HINT * 8);
+  L.grid_gemv = (int)std::min<long long>((N / 2 + 255) / 256 + 1, SM_COUNT_HINT * 8);
   L.grid_form = L.grid_gemv;
   switch (op->kind) {
     case KIOPS_OP_STENCIL1D3:
