@@ -1350,8 +1350,9 @@ __global__ void __launch_bounds__(LazyP<TX, TY, PM>::NT, MINB) k_pass_3d_lazyp(K
       cp_async16(d + NT, xprev + g);
       if (use_pp) cp_async16(d + 2 * NT, xpp + g);
       cp_async16(d + 3 * NT, kap + g);
+      if (pin)
 #pragma unroll
-      for (int c = 0; c < PM; c++) cp_async16(d + (4 + c) * NT, Bc[c] + g);
+        for (int c = 0; c < PM; c++) cp_async16(d + (4 + c) * NT, Bc[c] + g);
     }
     zoL = znext(zoL);
   };
@@ -1382,12 +1383,13 @@ __global__ void __launch_bounds__(LazyP<TX, TY, PM>::NT, MINB) k_pass_3d_lazyp(K
       }
     }
     double2 bt = {0.0, 0.0};
+    if (pin)
 #pragma unroll
-    for (int c = 0; c < PM; c++) {
-      const double2 b = o[(4 + c) * NT];
-      bt.x = fma(b.x, btc[c], bt.x);
-      bt.y = fma(b.y, btc[c], bt.y);
-    }
+      for (int c = 0; c < PM; c++) {
+        const double2 b = o[(4 + c) * NT];
+        bt.x = fma(b.x, btc[c], bt.x);
+        bt.y = fma(b.y, btc[c], bt.y);
+      }
     __syncthreads();  // the output that read slot (i & 1) has finished everywhere
     if (act) {
       sXK[(i & 1) * NPAIR + t] = xk_p;
