@@ -176,6 +176,8 @@ def main():
     ap.add_argument("--impl", default="kiops", choices=["kiops", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--hostloop", action="store_true",
+                    help="profiling only: same kernels, host-driven loop (ncu cannot see kernels in conditional graphs)")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
@@ -203,7 +205,7 @@ def main():
     stream = k.stream
     w = [torch.empty(cfg["N"], dtype=torch.float64, device=dev) for _ in cfg["T"]]
     for _ in range(max(3, args.warmup)):
-        k.apply(u, cfg["T"], w)
+        k.apply(u, cfg["T"], w, hostloop=args.hostloop)
     torch.cuda.synchronize()
 
     clk = ClockSampler(os.path.join(ROOT, f"gpurun_out/clocks_rank{rank}.csv"
@@ -219,7 +221,7 @@ def main():
         ev1 = torch.cuda.Event(enable_timing=True)
         ev0.record(stream)
         for _ in range(args.steps):
-            _, st = k.apply(u, cfg["T"], w)
+            _, st = k.apply(u, cfg["T"], w, hostloop=args.hostloop)
             for key in totals:
                 totals[key] += st[key]
         ev1.record(stream)
@@ -273,6 +275,7 @@ def main():
         "config": {"workload": cfg["name"], "N": cfg["N"], "p": cfg["p"], "T": [float(t) for t in cfg["T"]],
                    "tol": cfg["tol"], "m_max": cfg["m_max"], "iop_q": cfg["iop_q"],
                    "parallelism": f"replicas{world}" if world > 1 else "single",
+                   "control_flow": "host loop (profiling)" if args.hostloop else "device graph (WHILE/IF conditional nodes)",
                    "l2": "inputs larger than L2 (vector 134 MB, basis 17 GB); no flush needed",
                    "per_call": {"krylov_vectors": per_step["krylov_vectors"], "passes": per_step["passes"],
                                 "substeps": per_step["substeps"], "rejections": per_step["rejections"],
