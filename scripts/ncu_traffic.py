@@ -1,0 +1,25 @@
+"""Extract per-launch DRAM traffic of the fused pass from a full ncu report into
+profiles/ncu_traffic_config<k>.json (read by bench.py's roofline.traffic).
+usage: ncu_traffic.py report.ncu-rep config_index [kernel_regex]"""
+import csv
+import io
+import json
+import re
+import subprocess
+import sys
+
+rep, idx = sys.argv[1], int(sys.argv[2])
+pat = re.compile(sys.argv[3] if len(sys.argv) > 3 else "k_pass|k_csr")
+out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+r = list(csv.reader(io.StringIO(out)))
+h = r[0]
+ki, rd, wr, du = (h.index(x) for x in ("Kernel Name", "dram__bytes_read.sum", "dram__bytes_write.sum",
+                                        "gpu__time_duration.sum"))
+units = r[1]
+mult = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+rows = [x for x in r[2:] if pat.search(x[ki])]
+tr = [float(x[rd]) * mult[units[rd]] + float(x[wr]) * mult[units[wr]] for x in rows]
+res = {"report": rep.split("/")[-1], "kernel": rows[0][ki][:80], "launches": len(rows),
+       "bytes_per_launch": sum(tr) / len(tr), "duration_us": [float(x[du]) for x in rows]}
+json.dump(res, open(f"profiles/ncu_traffic_config{idx}.json", "w"), indent=1)
+print(res)
