@@ -56,13 +56,26 @@ def oracle_counts(idx):
 
 
 def cpu_sample(cfg, idx, n_kv=6):
-    """Oracle as it stands, bounded sample of the same workload: Alg. 2 for n_kv
-    Krylov vectors at full size from the real start vector, plus one Pade
-    exponential of a 129^2 H~ from the oracle's own Alg. 2 on the same-weights 48^3
-    grid; scaled to one call by the oracle's own full-size counts."""
+    """Oracle as it stands on the host cores (1 thread).  If one full oracle call of
+    this workload takes < 20 s (profiles/oracle_full_config<k>.json), time the full
+    call (median of up to 3).  Otherwise a bounded sample of the same workload:
+    Alg. 2 for n_kv Krylov vectors at full size from the real start vector, plus one
+    Pade exponential of a 129^2 H~ from the oracle's own Alg. 2 on the same-weights
+    48^3 grid, scaled to one call by the oracle's own full-size counts."""
     from oracle import oracle as O
     from workloads import configs as W
 
+    st, wall = oracle_counts(idx)
+    if st is not None and wall is not None and wall < 20.0:
+        ts = []
+        for _ in range(3 if wall < 2.0 else 1):
+            t0 = time.perf_counter()
+            O.kiops(cfg["op"], cfg["u"], cfg["T"], tol=cfg["tol"], m_init=cfg["m_init"], m_min=cfg["m_min"],
+                    m_max=cfg["m_max"], iop_q=cfg["iop_q"])
+            ts.append(time.perf_counter() - t0)
+        v = float(np.median(ts)) * 1e3
+        return {"value": v, "unit": "ms/call", "cores": 1, "kind": "oracle",
+                "sample": f"full oracle call (Alg. 1-4, 1 thread), median of {len(ts)}"}
     p, N = cfg["p"], cfg["N"]
     nu, mu = O.normalisation(cfg["u"])
     v0 = np.r_[cfg["u"][0], np.zeros(max(p - 1, 0)), [mu] if p else []]
@@ -133,6 +146,17 @@ class ClockSampler:
                     reasons.add(nm)
         return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": float(rows[0][2]), "reasons": sorted(reasons),
                 "samples": len(rows)}
+
+
+def max_over_ranks(x, dist=None, device="cpu"):
+    """max of a per-rank float over all ranks (identity without a process group)"""
+    if dist is None or not dist.is_available() or not dist.is_initialized():
+        return float(x)
+    import torch
+
+    t = torch.tensor([float(x)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
 
 
 def bytes_per_pass(cfg):
@@ -228,11 +252,7 @@ def main():
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
-    ms_total = ev0.elapsed_time(ev1)
-    if world > 1:
-        t = torch.tensor([ms_total], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_total = float(t.item())
+    ms_total = max_over_ranks(ev0.elapsed_time(ev1), dist if world > 1 else None, dev)
     ms_step = ms_total / args.steps
 
     # end to end: host buffers through kiops_apply_host, copies inside the timed region
@@ -247,11 +267,7 @@ def main():
         k.apply_host(hu, cfg["T"], hw)
     e1.record(stream)
     torch.cuda.synchronize()
-    e2e_ms = e0.elapsed_time(e1) / args.e2e_steps
-    if world > 1:
-        t = torch.tensor([e2e_ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_ms = float(t.item())
+    e2e_ms = max_over_ranks(e0.elapsed_time(e1) / args.e2e_steps, dist if world > 1 else None, dev)
 
     bpp = bytes_per_pass(cfg)
     passes = totals["passes"] / args.steps

@@ -40,6 +40,13 @@ constexpr int SM_COUNT_HINT = 148;
 #define M3Y 8
 #define M3Z 32
 
+// prefetch depth of the 3D pair pass (planes in flight); KIOPS_3D_DEPTH=3 selects the
+// deeper variant (2 CTAs/SM) for experiments, default 2 (3 CTAs/SM)
+static int lazyp_depth() {
+  const char *e = getenv("KIOPS_3D_DEPTH");
+  return (e && e[0] == '3') ? 3 : 2;
+}
+
 struct Layout {
   size_t V, r, staging, state, call, H, sig, R2, tails, partials, npart, scratch, coef, trace, total;
   long long ldN;
@@ -117,8 +124,11 @@ Layout layout(const kiops_operator_desc *op, int p, const kiops_options *o) {
     case KIOPS_OP_STENCIL3D7_VARKAPPA:
       L.grid_pass = (int)(((op->nx + M3X - 1) / M3X) * ((op->ny + M3Y - 1) / M3Y) * ((op->nz + M3Z - 1) / M3Z));
       if (op->nx % 2 == 0 && op->nx >= 2 && p >= 1 && p <= 4) {  // pair kernel (16-byte aligned rows), exact p
-        L.smem_pass = sizeof(double) * (p == 1 ? LazyP<M3X, M3Y, 1>::smem_doubles : p == 2 ? LazyP<M3X, M3Y, 2>::smem_doubles
-                                       : p == 3 ? LazyP<M3X, M3Y, 3>::smem_doubles : LazyP<M3X, M3Y, 4>::smem_doubles);
+        const int dd = lazyp_depth();
+        L.smem_pass = sizeof(double) * (dd == 3 ? (p == 1 ? LazyP<M3X, M3Y, 1, 3>::smem_doubles : p == 2 ? LazyP<M3X, M3Y, 2, 3>::smem_doubles
+                                                 : p == 3 ? LazyP<M3X, M3Y, 3, 3>::smem_doubles : LazyP<M3X, M3Y, 4, 3>::smem_doubles)
+                                              : (p == 1 ? LazyP<M3X, M3Y, 1, 2>::smem_doubles : p == 2 ? LazyP<M3X, M3Y, 2, 2>::smem_doubles
+                                                 : p == 3 ? LazyP<M3X, M3Y, 3, 2>::smem_doubles : LazyP<M3X, M3Y, 4, 2>::smem_doubles));
         L.block_pass = LazyP<M3X, M3Y, 2>::NT;
       } else {
         L.smem_pass = sizeof(double) * (p <= 2 ? Lazy3<M3X, M3Y, 2>::smem_doubles
@@ -240,10 +250,15 @@ static kiops_status build_graph(kiops_ctx c) {
       break;
     case KIOPS_OP_STENCIL3D7_VARKAPPA:
       if (c->op.nx % 2 == 0 && c->op.nx >= 2 && c->p >= 1 && c->p <= 4)
-        fpass = c->p == 1 ? (void *)k_pass_3d_lazyp<M3X, M3Y, M3Z, 1, 3>
-              : c->p == 2 ? (void *)k_pass_3d_lazyp<M3X, M3Y, M3Z, 2, 3>
-              : c->p == 3 ? (void *)k_pass_3d_lazyp<M3X, M3Y, M3Z, 3, 3>
-                          : (void *)k_pass_3d_lazyp<M3X, M3Y, M3Z, 4, 2>;
+        fpass = lazyp_depth() == 3
+                    ? (c->p == 1 ? (void *)k_pass_3d_lazyp<M3X, M3Y, M3Z, 1, 2, 3>
+                       : c->p == 2 ? (void *)k_pass_3d_lazyp<M3X, M3Y, M3Z, 2, 2, 3>
+                       : c->p == 3 ? (void *)k_pass_3d_lazyp<M3X, M3Y, M3Z, 3, 2, 3>
+                                   : (void *)k_pass_3d_lazyp<M3X, M3Y, M3Z, 4, 2, 3>)
+                    : (c->p == 1 ? (void *)k_pass_3d_lazyp<M3X, M3Y, M3Z, 1, 3, 2>
+                       : c->p == 2 ? (void *)k_pass_3d_lazyp<M3X, M3Y, M3Z, 2, 3, 2>
+                       : c->p == 3 ? (void *)k_pass_3d_lazyp<M3X, M3Y, M3Z, 3, 3, 2>
+                                   : (void *)k_pass_3d_lazyp<M3X, M3Y, M3Z, 4, 2, 2>);
       else
         fpass = c->p <= 2 ? (void *)k_pass_3d_lazy<M3X, M3Y, M3Z, 2, 3>
               : c->p <= 4 ? (void *)k_pass_3d_lazy<M3X, M3Y, M3Z, 4, 3>
@@ -252,7 +267,7 @@ static kiops_status build_graph(kiops_ctx c) {
     default: break;
   }
   c->fpass = fpass;
-  if (fpass && c->L.smem_pass > 48 * 1024)
+  if (fpass && c->L.smem_pass > 0)
     CK(cudaFuncSetAttribute(fpass, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->L.smem_pass), "smem attr pass");
   CK(cudaFuncSetAttribute((void *)k_ctrl, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctrl_smem_bytes()),
      "smem attr ctrl");

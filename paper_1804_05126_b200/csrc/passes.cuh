@@ -1288,17 +1288,17 @@ __device__ __forceinline__ void cp_async16(void *dst, const void *src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(src) : "memory");
 }
 
-template <int TX, int TY, int PM>
+template <int TX, int TY, int PM, int DD = 2>
 struct LazyP {
   static constexpr int PX = TX / 2 + 2, GY = TY + 2, NPAIR = PX * GY;  // pairs per plane
   static constexpr int NT = (NPAIR + 31) / 32 * 32;
-  static constexpr int D = 2, RD = D + 1, NOP = 4 + PM;
+  static constexpr int D = DD, RD = D + 1, NOP = 4 + PM;
   static constexpr size_t smem_doubles = 4 * (size_t)NPAIR * 2 + (size_t)RD * NOP * NT * 2;
 };
 
-template <int TX, int TY, int ZC, int PM, int MINB>
-__global__ void __launch_bounds__(LazyP<TX, TY, PM>::NT, MINB) k_pass_3d_lazyp(KParams P) {
-  using M = LazyP<TX, TY, PM>;
+template <int TX, int TY, int ZC, int PM, int MINB, int DD = 2>
+__global__ void __launch_bounds__(LazyP<TX, TY, PM, DD>::NT, MINB) k_pass_3d_lazyp(KParams P) {
+  using M = LazyP<TX, TY, PM, DD>;
   constexpr int NT = M::NT, PX = M::PX, NPAIR = M::NPAIR, D = M::D, RD = M::RD, NOP = M::NOP;
   extern __shared__ double2 smem2[];
   double2 *sXK = smem2;                // 2 x NPAIR   x_k pairs (shared plane ring)
