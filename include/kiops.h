@@ -117,15 +117,19 @@ typedef struct {
 void kiops_options_default(kiops_options *o);
 
 /* Bytes of DEVICE workspace kiops_create needs for this operator, p and options.
- * Returns KIOPS_ERR_INVALID_ARG / KIOPS_ERR_UNSUPPORTED like kiops_create would. */
+ * Returns KIOPS_ERR_INVALID_ARG / KIOPS_ERR_UNSUPPORTED like kiops_create would.
+ * CSR: the workspace also holds a SELL-32 copy of the matrix (slices of 32 rows
+ * padded to their longest row), so this call reads op->row_ptr from the device
+ * once (KIOPS_ERR_CUDA if it cannot); row_ptr must not change before create. */
 kiops_status kiops_workspace_bytes(const kiops_operator_desc *op, int p, const kiops_options *o,
                                    size_t *bytes);
 
 /* Creates a context: validates op, p and o (R21), carves the caller-owned DEVICE
  * workspace (>= kiops_workspace_bytes, 256-byte aligned; the library never calls
- * cudaMalloc for it) and instantiates the CUDA graph on `cuda_stream` (a
- * cudaStream_t; NULL = legacy default stream).  The ctx keeps op's arrays
- * borrowed.  On error *out is NULL. */
+ * cudaMalloc for it), builds the SELL-32 copy for CSR operators (the CSR arrays
+ * are not read again by kiops_apply), and instantiates the CUDA graph on
+ * `cuda_stream` (a cudaStream_t; NULL = legacy default stream).  The ctx keeps
+ * op's arrays borrowed.  Synchronises the stream.  On error *out is NULL. */
 kiops_status kiops_create(const kiops_operator_desc *op, int p, const kiops_options *o,
                           void *cuda_stream, void *workspace, size_t workspace_bytes,
                           kiops_ctx *out);

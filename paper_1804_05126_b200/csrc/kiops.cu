@@ -22,6 +22,7 @@
 #include <cstring>
 #include <new>
 #include <string>
+#include <vector>
 
 #include "controller.cuh"
 #include "kiops_internal.cuh"
@@ -48,7 +49,9 @@ static int lazyp_depth() {
 }
 
 struct Layout {
-  size_t V, r, staging, state, call, H, sig, R2, tails, partials, npart, scratch, coef, trace, total;
+  size_t V, r, staging, state, call, H, sig, R2, tails, partials, npart, scratch, coef, trace, sell_off, sell_col,
+      sell_val, total;
+  long long sell_entries;
   long long ldN;
   int grid_pass, grid_setup, grid_gemv, grid_form, grid_max;
   int block_pass;
@@ -97,6 +100,25 @@ kiops_status validate(const kiops_operator_desc *op, int p, const kiops_options 
   return KIOPS_OK;
 }
 
+// SELL-32 slice offsets from the (device) CSR row pointer; host computation, done at
+// workspace sizing / create time only (not on the apply path).
+static std::vector<long long> sell_offsets(const kiops_operator_desc *op) {
+  const long long N = op_n(op), ns = (N + 31) / 32;
+  std::vector<long long> rp(N + 1), off(ns + 1, 0);
+  if (cudaMemcpy(rp.data(), op->row_ptr, sizeof(long long) * (N + 1), cudaMemcpyDeviceToHost) != cudaSuccess)
+    return {};
+  for (long long s = 0; s < ns; s++) {
+    long long mx = 0;
+    for (long long r = 32 * s; r < std::min(N, 32 * s + 32); r++) mx = std::max(mx, rp[r + 1] - rp[r]);
+    off[s + 1] = off[s] + 32 * mx;
+  }
+  return off;
+}
+static long long sell_size(const kiops_operator_desc *op) {
+  std::vector<long long> off = sell_offsets(op);
+  return off.empty() ? -1 : off.back();
+}
+
 Layout layout(const kiops_operator_desc *op, int p, const kiops_options *o) {
   Layout L{};
   const long long N = op_n(op);
@@ -136,8 +158,8 @@ Layout layout(const kiops_operator_desc *op, int p, const kiops_options *o) {
         L.block_pass = Lazy3<M3X, M3Y, 2>::NT;
       }
       break;
-    default:
-      L.grid_pass = (int)std::min<long long>((8 * N + 255) / 256, SM_COUNT_HINT * 8);
+    default:  // CSR (SELL-32): thread per row, 8 CTAs of 256 per SM
+      L.grid_pass = (int)std::min<long long>((N + 255) / 256, SM_COUNT_HINT * 8);
       L.smem_pass = 0;
   }
   L.grid_max = std::max(L.grid_pass, L.grid_setup);
@@ -157,6 +179,14 @@ Layout layout(const kiops_operator_desc *op, int p, const kiops_options *o) {
   L.scratch = off; off += al(sizeof(double) * NSCR * (size_t)LDH * LDH);
   L.coef = off; off += al(sizeof(double) * (KMAXO + 1) * (size_t)LDH);
   L.trace = off; off += al(sizeof(kiops_trace_row) * (size_t)KIOPS_TRACE_CAP);
+  L.sell_entries = 0;
+  if (op->kind == KIOPS_OP_CSR) {  // SELL-32 copy: exact size from the row lengths
+    const long long ns = (N + 31) / 32;
+    L.sell_entries = sell_size(op);
+    L.sell_off = off; off += al(sizeof(long long) * (size_t)(ns + 1));
+    L.sell_col = off; off += al(sizeof(int) * (size_t)L.sell_entries);
+    L.sell_val = off; off += al(sizeof(double) * (size_t)L.sell_entries);
+  }
   L.total = off;
   return L;
 }
@@ -279,7 +309,7 @@ static kiops_status build_graph(kiops_ctx c) {
   CK(add_cond(b_outer, &n_inner, nullptr, 0, P.h_inner, cudaGraphCondTypeWhile, &b_inner), "node inner");
   if (c->op.kind == KIOPS_OP_CSR) {
     CK(add_kernel(b_inner, &n_a, nullptr, 0, (void *)k_csr_form, c->L.grid_form, 256, 0, &P), "node form");
-    CK(add_kernel(b_inner, &n_b, &n_a, 1, (void *)k_csr_spmv, c->L.grid_pass, 256, 0, &P), "node spmv");
+    CK(add_kernel(b_inner, &n_b, &n_a, 1, (void *)k_sell_spmv, c->L.grid_pass, 256, 0, &P), "node spmv");
   } else {
     CK(add_kernel(b_inner, &n_a, nullptr, 0, fpass, c->L.grid_pass, c->L.block_pass, c->L.smem_pass, &P), "node pass");
   }
@@ -310,7 +340,9 @@ kiops_status kiops_workspace_bytes(const kiops_operator_desc *op, int p, const k
   kiops_status s = validate(op, p, o, err);
   if (s != KIOPS_OK) return s;
   if (!bytes) return KIOPS_ERR_INVALID_ARG;
-  *bytes = layout(op, p, o).total;
+  const Layout L = layout(op, p, o);
+  if (op->kind == KIOPS_OP_CSR && L.sell_entries < 0) return KIOPS_ERR_CUDA;  // row_ptr not readable
+  *bytes = L.total;
   return KIOPS_OK;
 }
 
@@ -366,6 +398,11 @@ kiops_status kiops_create(const kiops_operator_desc *op, int p, const kiops_opti
   P.scratch = (double *)(w + L.scratch);
   P.coef = (double *)(w + L.coef);
   P.trace = (kiops_trace_row *)(w + L.trace);
+  if (op->kind == KIOPS_OP_CSR) {
+    P.sell_off = (const long long *)(w + L.sell_off);
+    P.sell_col = (const int *)(w + L.sell_col);
+    P.sell_val = (const double *)(w + L.sell_val);
+  }
   P.grid_pass = L.grid_pass;
   P.grid_max = L.grid_max;
   kiops_status st = KIOPS_OK;
@@ -378,6 +415,22 @@ kiops_status kiops_create(const kiops_operator_desc *op, int p, const kiops_opti
     if (e == cudaSuccess) e = cudaMemsetAsync(P.H, 0, sizeof(double) * LDH * LDH, c->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
     if (e != cudaSuccess) st = cuda_fail(c, e, "workspace init");
+  }
+  if (st == KIOPS_OK && op->kind == KIOPS_OP_CSR) {  // build the SELL-32 copy once
+    std::vector<long long> off = sell_offsets(op);
+    if (off.empty() || off.back() != L.sell_entries) {
+      c->err = "SELL sizing failed (row_ptr changed between kiops_workspace_bytes and kiops_create?)";
+      st = KIOPS_ERR_WORKSPACE;
+    } else {
+      e = cudaMemcpy((void *)P.sell_off, off.data(), sizeof(long long) * off.size(), cudaMemcpyHostToDevice);
+      if (e == cudaSuccess) {
+        k_sell_build<<<SM_COUNT_HINT * 8, 256, 0, c->stream>>>(P.N, P.row_ptr, P.col_idx, P.vals, P.sell_off,
+                                                               (int *)P.sell_col, (double *)P.sell_val);
+        e = cudaGetLastError();
+      }
+      if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+      if (e != cudaSuccess) st = cuda_fail(c, e, "SELL build");
+    }
   }
   if (st == KIOPS_OK) st = build_graph(c);
   if (st != KIOPS_OK) {
@@ -514,7 +567,7 @@ kiops_status kiops_apply_hostloop(kiops_ctx c, const double *const *u, const dou
     while (cond[COND_INNER]) {
       if (c->op.kind == KIOPS_OP_CSR) {
         if ((s = launch_plain(c, (void *)k_csr_form, c->L.grid_form, 256, 0, &P)) != KIOPS_OK) return s;
-        if ((s = launch_plain(c, (void *)k_csr_spmv, c->L.grid_pass, 256, 0, &P)) != KIOPS_OK) return s;
+        if ((s = launch_plain(c, (void *)k_sell_spmv, c->L.grid_pass, 256, 0, &P)) != KIOPS_OK) return s;
       } else {
         if ((s = launch_plain(c, c->fpass, c->L.grid_pass, c->L.block_pass, c->L.smem_pass, &P)) != KIOPS_OK) return s;
       }

@@ -59,6 +59,9 @@ struct KParams {
   const long long *row_ptr;
   const int *col_idx;
   const double *vals;
+  const long long *sell_off;   // CSR as SELL-32 (built at create): slice offsets (in entries)
+  const int *sell_col;
+  const double *sell_val;
   int p;
   double tol;
   int m_init, m_min, m_max, task1;

@@ -423,33 +423,48 @@ __global__ void __launch_bounds__(256) k_csr_form(KParams P) {
 }
 
 __global__ void __launch_bounds__(256) k_csr_spmv(KParams P) {
+  // 16 lanes per row, two entries per lane issued together (a 27-point row is one
+  // round of loads + one round of gathers); warp-uniform row loop (two rows per warp)
   __shared__ PassScalars S;
   pass_guard(P, false);
   if (threadIdx.x == 0) load_pass_scalars(P, S);
   __syncthreads();
   if (S.k == 0) return;
   const int k = S.k, p = P.p;
-  const double *xk = (k == 1) ? S.xprev : S.xout;
-  const double *xm = S.xprev;
-  const int lane8 = threadIdx.x & 7;
+  const double *__restrict__ xk = (k == 1) ? S.xprev : S.xout;
+  const double *__restrict__ xm = S.xprev;
+  const double *__restrict__ vals = P.vals;
+  const int *__restrict__ cols = P.col_idx;
+  const long long *__restrict__ rp = P.row_ptr;
+  const int l16 = threadIdx.x & 15;
+  const unsigned half = (threadIdx.x & 16) ? 0xffff0000u : 0x0000ffffu;
   double v[NDOT] = {0.0, 0.0, 0.0, 0.0, 0.0};
-  // warp-uniform loop: every lane of a warp runs the same number of iterations so
-  // the 8-lane shuffles never see exited lanes (ragged N)
-  const long long groups = (long long)gridDim.x * (blockDim.x / 8);
-  const long long g0 = (blockIdx.x * (long long)blockDim.x + threadIdx.x) / 8;
-  const long long warp_first = (blockIdx.x * (long long)blockDim.x + (threadIdx.x & ~31)) / 8;
+  const long long groups = (long long)gridDim.x * (blockDim.x / 16);
+  const long long g0 = (blockIdx.x * (long long)blockDim.x + threadIdx.x) / 16;
+  const long long warp_first = (blockIdx.x * (long long)blockDim.x + (threadIdx.x & ~31)) / 16;
   for (long long it = 0; warp_first + it * groups < P.N; it++) {
     const long long row = g0 + it * groups;
     const bool live = row < P.N;
     double s = 0.0;
     if (live) {
-      const long long b0 = P.row_ptr[row], b1 = P.row_ptr[row + 1];
-      for (long long q = b0 + lane8; q < b1; q += 8) s += P.vals[q] * xk[P.col_idx[q]];
+      const long long b0 = __ldg(rp + row), b1 = __ldg(rp + row + 1);
+      for (long long q = b0 + l16; q < b1; q += 32) {
+        const bool two = q + 16 < b1;
+        const double va = __ldg(vals + q);
+        const int ca = __ldg(cols + q);
+        const double vb = two ? __ldg(vals + q + 16) : 0.0;
+        const int cb = two ? __ldg(cols + q + 16) : ca;
+        const double xa = xk[ca], xb = xk[cb];
+        s = fma(va, xa, s);
+        s = fma(vb, xb, s);
+      }
     }
+    s += __shfl_xor_sync(0xffffffffu, s, 8);
     s += __shfl_xor_sync(0xffffffffu, s, 4);
     s += __shfl_xor_sync(0xffffffffu, s, 2);
     s += __shfl_xor_sync(0xffffffffu, s, 1);
-    if (live && lane8 == 0) {
+    (void)half;
+    if (live && l16 == 0) {
       double rr = s;
 #pragma unroll
       for (int c = 0; c < KMAXP; c++)
@@ -1539,5 +1554,70 @@ __global__ void __launch_bounds__(256, 2) k_pass_2d_lazy(KParams P) {
     }
   }
   double v[NDOT] = {v0, v1, v2, v3, v4};
+  pass_epilogue(P, k, v);
+}
+
+// ---------------------------------------------------------------------------
+// CSR operators run on a SELL-32 copy built at kiops_create:
+// slice s = rows 32s..32s+31, padded to the slice's longest row, entry (k, lane)
+// at off[s] + 32k + lane (pad: value 0, column = the row itself).  A warp = a slice:
+// every value/column load is 256/128 contiguous bytes and the k-loop carries no
+// dependency, so the gathers of x_k stream with full memory-level parallelism.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_sell_build(long long N, const long long *__restrict__ rp,
+                                                   const int *__restrict__ cols, const double *__restrict__ vals,
+                                                   const long long *__restrict__ soff, int *__restrict__ scol,
+                                                   double *__restrict__ sval) {
+  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < (N + 31) / 32 * 32;
+       r += (long long)gridDim.x * blockDim.x) {
+    const long long sl = r / 32, lane = r % 32, o0 = soff[sl], len = (soff[sl + 1] - o0) / 32;
+    const long long b0 = r < N ? rp[r] : 0, n = r < N ? rp[r + 1] - b0 : 0;
+    const int self = (int)(r < N ? r : 0);
+    for (long long k = 0; k < len; k++) {
+      const long long d = o0 + 32 * k + lane;
+      scol[d] = k < n ? cols[b0 + k] : self;
+      sval[d] = k < n ? vals[b0 + k] : 0.0;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) k_sell_spmv(KParams P) {
+  __shared__ PassScalars S;
+  pass_guard(P, false);
+  if (threadIdx.x == 0) load_pass_scalars(P, S);
+  __syncthreads();
+  if (S.k == 0) return;
+  const int k = S.k, p = P.p;
+  const double *__restrict__ xk = (k == 1) ? S.xprev : S.xout;
+  const double *__restrict__ xm = S.xprev;
+  const double *__restrict__ sval = P.sell_val;
+  const int *__restrict__ scol = P.sell_col;
+  const long long *__restrict__ soff = P.sell_off;
+  double v[NDOT] = {0.0, 0.0, 0.0, 0.0, 0.0};
+  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < P.N; r += (long long)gridDim.x * blockDim.x) {
+    const long long sl = r >> 5, o0 = soff[sl] + (r & 31), len = (soff[sl + 1] - soff[sl]) >> 5;
+    double a0 = 0.0, a1 = 0.0;
+    long long q = o0;
+    int kk = 0;
+#pragma unroll 4
+    for (; kk + 1 < len; kk += 2, q += 64) {
+      const double va = __ldg(sval + q), vb = __ldg(sval + q + 32);
+      const int ca = __ldg(scol + q), cb = __ldg(scol + q + 32);
+      a0 = fma(va, __ldg(xk + ca), a0);
+      a1 = fma(vb, __ldg(xk + cb), a1);
+    }
+    if (kk < len) a0 = fma(__ldg(sval + q), __ldg(xk + __ldg(scol + q)), a0);
+    double rr = a0 + a1;
+#pragma unroll
+    for (int c = 0; c < KMAXP; c++)
+      if (c < p) rr += S.B[c][r] * S.btc[c];
+    const double x = xk[r], y = xm[r];
+    v[0] += x * x;
+    v[1] += y * x;
+    v[2] += y * rr;
+    v[3] += x * rr;
+    v[4] += rr * rr;
+    P.r[r] = rr;
+  }
   pass_epilogue(P, k, v);
 }
