@@ -195,19 +195,143 @@ __device__ int cl_solve(int n, const double *Qg, double *R, double *LUg, int *pe
   return 0;
 }
 
-// F = exp(scale * M) for n <= KMAXM+1, on the whole cluster: diagonal Pade
-// approximant with scaling and squaring ("[47]" = Higham 2005, Algorithm
-// 2.3; R17).  Degree cascade {3,5,7,9,13} by the 1-norm thresholds theta_m of
-// Higham's Table 2.3; above theta_13, X is scaled by 2^-s and squared back s times.
-// Every CTA of the cluster must call it with identical arguments.  Returns the
-// number of dense products (or -1 on a zero pivot / non-finite norm).
-__device__ int cl_expm(int n, const double *M, double scale, double *F, double *scr, double *sm) {
-  double *X = scr + 0 * (size_t)LDH * LDH, *X2 = scr + 1 * (size_t)LDH * LDH, *X4 = scr + 2 * (size_t)LDH * LDH,
-         *X6 = scr + 3 * (size_t)LDH * LDH, *X8 = scr + 4 * (size_t)LDH * LDH, *U = scr + 5 * (size_t)LDH * LDH,
-         *V = scr + 6 * (size_t)LDH * LDH, *T = scr + 7 * (size_t)LDH * LDH;
-  double *LU = scr + 10 * (size_t)LDH * LDH;
-  int *perm = reinterpret_cast<int *>(scr + 11 * (size_t)LDH * LDH);
-  int *flag = perm + LDH;
+// ---------------------------------------------------------------------------
+// Storage / synchronisation policies for the Pade exponential:
+//  * ClusterBk: matrices in global scratch (ld = LDH), work split over the cluster;
+//  * SmemBk:    n <= SMALL_N, every matrix in ONE CTA's shared memory (ld = n),
+//               __syncthreads only (used by CTA 0 alone for the small projected
+//               matrices of configs 1-3, where cluster barriers would dominate).
+// ---------------------------------------------------------------------------
+#define SMALL_N 48
+
+struct ClusterBk {
+  double *scr, *sm;
+  __device__ int ld() const { return LDH; }
+  __device__ double *mat(int i) const { return scr + (size_t)i * LDH * LDH; }
+  __device__ int gid() const { return cl_gtid(); }
+  __device__ int gsz() const { return cl_gsize(); }
+  __device__ void sync() const { cl_sync(); }
+  __device__ void matmul(int n, const double *A, const double *B, double *C) const { cl_matmul(n, A, B, C, sm); }
+  __device__ double norm1(int n, const double *A) const { return cta_norm1(n, A, sm); }
+  __device__ int solve(int n, const double *Q, double *R) const {
+    return cl_solve(n, Q, R, scr + 10 * (size_t)LDH * LDH, reinterpret_cast<int *>(scr + 11 * (size_t)LDH * LDH),
+                    reinterpret_cast<int *>(scr + 11 * (size_t)LDH * LDH) + LDH, sm);
+  }
+};
+
+struct SmemBk {
+  double *base;   // 10 matrices of n x n (ld = n) + a reduction scratch
+  int n_;
+  __device__ int ld() const { return n_; }
+  __device__ double *mat(int i) const { return base + (size_t)i * n_ * n_; }
+  __device__ int gid() const { return threadIdx.x; }
+  __device__ int gsz() const { return blockDim.x; }
+  __device__ void sync() const { __syncthreads(); }
+  __device__ void matmul(int n, const double *A, const double *B, double *C) const {
+    for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+      const int i = e % n, j = e / n;
+      double s0 = 0.0, s1 = 0.0;
+      int k = 0;
+      for (; k + 1 < n; k += 2) {
+        s0 = fma(A[i + n * k], B[k + n * j], s0);
+        s1 = fma(A[i + n * (k + 1)], B[k + 1 + n * j], s1);
+      }
+      if (k < n) s0 = fma(A[i + n * k], B[k + n * j], s0);
+      C[e] = s0 + s1;
+    }
+    __syncthreads();
+  }
+  __device__ double norm1(int n, const double *A) const {
+    double *red = base + 10 * (size_t)n_ * n_;
+    double best = 0.0;
+    for (int j = threadIdx.x; j < n; j += blockDim.x) {
+      double s = 0.0;
+      for (int i = 0; i < n; i++) s += fabs(A[i + n * j]);
+      best = (s > best || s != s) ? s : best;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      const double x = __shfl_xor_sync(0xffffffffu, best, o);
+      best = (x > best || x != x) ? x : best;
+    }
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = best;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double bb = 0.0;
+      for (int w = 0; w < (int)((blockDim.x + 31) >> 5); w++) bb = (red[w] > bb || red[w] != red[w]) ? red[w] : bb;
+      red[32] = bb;
+    }
+    __syncthreads();
+    const double r = red[32];
+    __syncthreads();
+    return r;
+  }
+  // Q X = R in place (R <- X), Gaussian elimination with partial pivoting applied to
+  // the right-hand sides, then back substitution; Q is destroyed.
+  __device__ int solve(int n, double *Q, double *R) const {
+    __shared__ int s_piv, s_bad;
+    if (threadIdx.x == 0) s_bad = 0;
+    __syncthreads();
+    for (int k = 0; k < n; k++) {
+      if (threadIdx.x < 32) {
+        double best = -1.0;
+        int bi = n;
+        for (int r = k + threadIdx.x; r < n; r += 32) {
+          const double a = fabs(Q[r + n * k]);
+          if (a > best) { best = a; bi = r; }
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+          const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+          const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+          if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+        }
+        if (threadIdx.x == 0) { s_piv = bi; if (!(best > 0.0)) s_bad = 1; }
+      }
+      __syncthreads();
+      if (s_bad) return -1;
+      const int pv = s_piv;
+      if (pv != k) {
+        for (int c = threadIdx.x; c < n; c += blockDim.x) {
+          double t = Q[k + n * c]; Q[k + n * c] = Q[pv + n * c]; Q[pv + n * c] = t;
+          t = R[k + n * c]; R[k + n * c] = R[pv + n * c]; R[pv + n * c] = t;
+        }
+        __syncthreads();
+      }
+      const int rows = n - k - 1;
+      const double piv = Q[k + n * k];
+      for (int e = threadIdx.x; e < rows * (rows + n); e += blockDim.x) {
+        const int r = k + 1 + e % rows, cc = e / rows;
+        const double f = Q[r + n * k] / piv;
+        if (cc < rows) Q[r + n * (k + 1 + cc)] -= f * Q[k + n * (k + 1 + cc)];
+        else R[r + n * (cc - rows)] -= f * R[k + n * (cc - rows)];
+      }
+      __syncthreads();
+    }
+    for (int k = n - 1; k >= 0; k--) {
+      const double d = Q[k + n * k];
+      for (int c = threadIdx.x; c < n; c += blockDim.x) R[k + n * c] = R[k + n * c] / d;
+      __syncthreads();
+      for (int e = threadIdx.x; e < k * n; e += blockDim.x) {
+        const int r = e % k, c = e / k;
+        R[r + n * c] -= Q[r + n * k] * R[k + n * c];
+      }
+      __syncthreads();
+    }
+    return 0;
+  }
+};
+
+// F = exp(scale * M) for n <= KMAXM+1: diagonal Pade approximant with scaling and
+// squaring ("[47]" = Higham 2005, Algorithm 2.3; R17).  Degree cascade
+// {3,5,7,9,13} by the 1-norm thresholds theta_m of Higham's Table 2.3; above
+// theta_13, X is scaled by 2^-s and squared back s times.  M and F use the
+// policy's leading dimension.  Every participant must call it with identical
+// arguments.  Returns the number of dense products (or -1 on a zero pivot /
+// non-finite norm).
+template <class Bk>
+__device__ int pade_expm(const Bk &bk, int n, const double *M, double scale, double *F) {
+  const int ld = bk.ld();
+  double *X = bk.mat(0), *X2 = bk.mat(1), *X4 = bk.mat(2), *X6 = bk.mat(3), *X8 = bk.mat(4), *U = bk.mat(5),
+         *V = bk.mat(6), *T = bk.mat(7);
   // [m/m] Pade numerator coefficients p_m(x) = sum b_j x^j, b_j proportional to
   // (2m-j)! m! / ((2m)! j! (m-j)!), integer-scaled as tabulated by Higham (2005).
   const double c3[4] = {120.0, 60.0, 12.0, 1.0};
@@ -218,13 +342,13 @@ __device__ int cl_expm(int n, const double *M, double scale, double *F, double *
   const double c13[14] = {64764752532480000.0, 32382376266240000.0, 7771770303897600.0,
                           1187353796428800.0, 129060195264000.0, 10559470521600.0, 670442572800.0,
                           33522128640.0, 1323241920.0, 40840800.0, 960960.0, 16380.0, 182.0, 1.0};
-  const int nn = n * n, g0 = cl_gtid(), gs = cl_gsize();
+  const int nn = n * n, g0 = bk.gid(), gs = bk.gsz();
   for (int e = g0; e < nn; e += gs) {
     const int i = e % n, j = e / n;
-    X[i + (size_t)LDH * j] = scale * M[i + (size_t)LDH * j];
+    X[i + (size_t)ld * j] = scale * M[i + (size_t)ld * j];
   }
-  cl_sync();
-  const double nrm = cta_norm1(n, X, sm);
+  bk.sync();
+  const double nrm = bk.norm1(n, X);
   if (!isfinite(nrm)) return -1;
   int deg, s = 0;
   if (nrm <= 1.495585217958292e-2) deg = 3;
@@ -236,19 +360,19 @@ __device__ int cl_expm(int n, const double *M, double scale, double *F, double *
     s = ceil_log2_exact(nrm / 5.371920351148152e0);
     if (s < 0) s = 0;
     const double f = ldexp(1.0, -s);
-    for (int e = g0; e < nn; e += gs) X[(e % n) + (size_t)LDH * (e / n)] *= f;
-    cl_sync();
+    for (int e = g0; e < nn; e += gs) X[(e % n) + (size_t)ld * (e / n)] *= f;
+    bk.sync();
   }
   int mult = 0;
-  cl_matmul(n, X, X, X2, sm); mult++;
-  if (deg >= 5) { cl_matmul(n, X2, X2, X4, sm); mult++; }
-  if (deg >= 7) { cl_matmul(n, X2, X4, X6, sm); mult++; }
-  if (deg == 9) { cl_matmul(n, X4, X4, X8, sm); mult++; }
+  bk.matmul(n, X, X, X2); mult++;
+  if (deg >= 5) { bk.matmul(n, X2, X2, X4); mult++; }
+  if (deg >= 7) { bk.matmul(n, X2, X4, X6); mult++; }
+  if (deg == 9) { bk.matmul(n, X4, X4, X8); mult++; }
   if (deg < 13) {
     const double *b = deg == 3 ? c3 : deg == 5 ? c5 : deg == 7 ? c7 : c9;
     for (int e = g0; e < nn; e += gs) {
       const int i = e % n, j = e / n;
-      const size_t q = i + (size_t)LDH * j;
+      const size_t q = i + (size_t)ld * j;
       const double id = (i == j) ? 1.0 : 0.0;
       double odd = b[1] * id + b[3] * X2[q], even = b[0] * id + b[2] * X2[q];
       if (deg >= 5) { odd += b[5] * X4[q]; even += b[4] * X4[q]; }
@@ -257,53 +381,73 @@ __device__ int cl_expm(int n, const double *M, double scale, double *F, double *
       T[q] = odd;
       V[q] = even;
     }
-    cl_sync();
-    cl_matmul(n, X, T, U, sm); mult++;   // U = X * odd part
+    bk.sync();
+    bk.matmul(n, X, T, U); mult++;   // U = X * odd part
   } else {
     const double *b = c13;
     for (int e = g0; e < nn; e += gs) {
-      const size_t q = (e % n) + (size_t)LDH * (e / n);
+      const size_t q = (e % n) + (size_t)ld * (e / n);
       T[q] = b[13] * X6[q] + b[11] * X4[q] + b[9] * X2[q];
       X8[q] = b[12] * X6[q] + b[10] * X4[q] + b[8] * X2[q];
     }
-    cl_sync();
-    cl_matmul(n, X6, T, U, sm); mult++;
-    cl_matmul(n, X6, X8, V, sm); mult++;
+    bk.sync();
+    bk.matmul(n, X6, T, U); mult++;
+    bk.matmul(n, X6, X8, V); mult++;
     for (int e = g0; e < nn; e += gs) {
       const int i = e % n, j = e / n;
-      const size_t q = i + (size_t)LDH * j;
+      const size_t q = i + (size_t)ld * j;
       const double id = (i == j) ? 1.0 : 0.0;
       U[q] += b[7] * X6[q] + b[5] * X4[q] + b[3] * X2[q] + b[1] * id;
       V[q] += b[6] * X6[q] + b[4] * X4[q] + b[2] * X2[q] + b[0] * id;
     }
-    cl_sync();
-    cl_matmul(n, X, U, T, sm); mult++;   // odd part: X [ ... ]
+    bk.sync();
+    bk.matmul(n, X, U, T); mult++;   // odd part: X [ ... ]
     for (int e = g0; e < nn; e += gs) {
-      const size_t q = (e % n) + (size_t)LDH * (e / n);
+      const size_t q = (e % n) + (size_t)ld * (e / n);
       U[q] = T[q];
     }
-    cl_sync();
+    bk.sync();
   }
   // (V - U) F = (V + U)
   for (int e = g0; e < nn; e += gs) {
-    const size_t q = (e % n) + (size_t)LDH * (e / n);
+    const size_t q = (e % n) + (size_t)ld * (e / n);
     T[q] = V[q] - U[q];
     F[q] = V[q] + U[q];
   }
-  cl_sync();
-  if (cl_solve(n, T, F, LU, perm, flag, sm) != 0) return -1;
+  bk.sync();
+  if (bk.solve(n, T, F) != 0) return -1;
   for (int k = 0; k < s; k++) {
     double *src = (k & 1) ? T : F, *dst = (k & 1) ? F : T;
-    cl_matmul(n, src, src, dst, sm); mult++;
+    bk.matmul(n, src, src, dst); mult++;
   }
   if (s & 1) {  // result in T
     for (int e = g0; e < nn; e += gs) {
-      const size_t q = (e % n) + (size_t)LDH * (e / n);
+      const size_t q = (e % n) + (size_t)ld * (e / n);
       F[q] = T[q];
     }
-    cl_sync();
+    bk.sync();
   }
   return mult;
+}
+
+// F (global, ld LDH) = exp(scale M), M global (ld LDH).  n > SMALL_N: the whole
+// cluster; otherwise CTA 0 alone in shared memory (the others wait at the barrier).
+__device__ int cl_expm(int n, const double *M, double scale, double *F, double *scr, double *sm) {
+  if (n > SMALL_N) {
+    ClusterBk bk{scr, sm};
+    return pade_expm(bk, n, M, scale, F);
+  }
+  if (cl_rank() == 0) {
+    SmemBk bk{sm, n};
+    double *Ms = bk.mat(8), *Fs = bk.mat(9);
+    for (int e = threadIdx.x; e < n * n; e += blockDim.x) Ms[e] = M[(e % n) + (size_t)LDH * (e / n)];
+    __syncthreads();
+    const int r = pade_expm(bk, n, Ms, scale, Fs);
+    for (int e = threadIdx.x; e < n * n; e += blockDim.x) F[(e % n) + (size_t)LDH * (e / n)] = Fs[e];
+    if (threadIdx.x == 0) reinterpret_cast<int *>(scr + 11 * (size_t)LDH * LDH)[LDH + 1] = r;
+  }
+  cl_sync();
+  return reinterpret_cast<int *>(scr + 11 * (size_t)LDH * LDH)[LDH + 1];
 }
 
 // ---------------------------------------------------------------------------

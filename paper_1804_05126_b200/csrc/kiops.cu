@@ -48,6 +48,17 @@ static int lazyp_depth() {
   return (e && e[0] == '3') ? 3 : 2;
 }
 
+// 2D warp-strip variant (experiment switch KIOPS_2D_VARIANT): 0 = YC 8 / 2 CTAs per SM
+// (default), 1 = YC 4 / 2, 2 = YC 4 / 3, 3 = YC 16 / 2
+static int l2_variant() {
+  const char *e = getenv("KIOPS_2D_VARIANT");
+  return e ? atoi(e) : 0;
+}
+static int l2_yc() {
+  const int v = l2_variant();
+  return (v == 1 || v == 2) ? 4 : v == 3 ? 16 : 8;
+}
+
 struct Layout {
   size_t V, r, staging, state, call, H, sig, R2, tails, partials, npart, scratch, coef, trace, sell_off, sell_col,
       sell_val, total;
@@ -132,7 +143,8 @@ Layout layout(const kiops_operator_desc *op, int p, const kiops_options *o) {
     case KIOPS_OP_STENCIL1D3:
     case KIOPS_OP_STENCIL2D5:
       if (op->nx % 2 == 0 && p <= 4) {  // warp-strip lazy kernel (16-byte pairs)
-        const long long strips = (op->nx + 59) / 60 * ((op->ny + L2YC - 1) / L2YC);
+        const int yc = l2_yc();
+        const long long strips = (op->nx + 59) / 60 * ((op->ny + yc - 1) / yc);
         L.grid_pass = (int)((strips + 7) / 8);
         L.smem_pass = 0;
       } else if (op->kind == KIOPS_OP_STENCIL1D3) {
@@ -195,7 +207,8 @@ size_t ctrl_smem_bytes() {
   const size_t n = KMAXM + 1, cb = (n + CTRL_CL - 1) / CTRL_CL;
   const size_t solve = sizeof(double) * (n * n + n * cb);
   const size_t mm = sizeof(double) * 2 * (size_t)((n + 3) & ~3) * MM_KP;
-  return std::max(solve, mm);
+  const size_t small = sizeof(double) * (10 * (size_t)SMALL_N * SMALL_N + 64);  // single-CTA path
+  return std::max(std::max(solve, mm), small);
 }
 
 }  // namespace
@@ -271,10 +284,14 @@ static kiops_status build_graph(kiops_ctx c) {
   switch (c->op.kind) {
     case KIOPS_OP_STENCIL1D3:
     case KIOPS_OP_STENCIL2D5:
-      if (lazy2d)
-        fpass = c->p == 0 ? (void *)k_pass_2d_lazy<L2YC, 0> : c->p == 1 ? (void *)k_pass_2d_lazy<L2YC, 1>
-              : c->p == 2 ? (void *)k_pass_2d_lazy<L2YC, 2> : c->p == 3 ? (void *)k_pass_2d_lazy<L2YC, 3>
-                          : (void *)k_pass_2d_lazy<L2YC, 4>;
+      if (lazy2d) {
+        const int v = l2_variant();
+#define K2(YC, MB) (c->p == 0 ? (void *)k_pass_2d_lazy<YC, 0, MB> : c->p == 1 ? (void *)k_pass_2d_lazy<YC, 1, MB> \
+                  : c->p == 2 ? (void *)k_pass_2d_lazy<YC, 2, MB> : c->p == 3 ? (void *)k_pass_2d_lazy<YC, 3, MB> \
+                              : (void *)k_pass_2d_lazy<YC, 4, MB>)
+        fpass = v == 1 ? K2(4, 2) : v == 2 ? K2(4, 3) : v == 3 ? K2(16, 2) : K2(8, 2);
+#undef K2
+      }
       else
         fpass = c->op.kind == KIOPS_OP_STENCIL1D3 ? (void *)k_pass_stencil<T1D> : (void *)k_pass_stencil<T2D>;
       break;

@@ -1380,6 +1380,7 @@ __global__ void __launch_bounds__(LazyP<TX, TY, PM, DD>::NT, MINB) k_pass_3d_laz
   double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0, v4 = 0.0;
   long long zo_out = z0 * nxy;
   int rs = 0, ri = D;
+#pragma unroll 6
   for (int i = 0; i <= nzc + 1; i++) {
     if (i + D <= nzc + 1) issue(ri);
     cp_async_commit();
@@ -1465,8 +1466,8 @@ struct Row2 {
   double2 r, xm, pp, d, b[PM > 0 ? PM : 1];
 };
 
-template <int YC, int PM>
-__global__ void __launch_bounds__(256, 2) k_pass_2d_lazy(KParams P) {
+template <int YC, int PM, int MINB = 2>
+__global__ void __launch_bounds__(256, MINB) k_pass_2d_lazy(KParams P) {
   constexpr int IP = 30;  // interior pairs per warp strip
   __shared__ PassScalars S;
   pass_guard(P);
