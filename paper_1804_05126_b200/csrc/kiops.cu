@@ -37,27 +37,11 @@ constexpr int SM_COUNT_HINT = 148;
 #define T2D 2, 64, 16, 1
 #define T3D 3, 32, 8, 4
 #define L2YC 8
-#define M3X 32
+#define M3X 32   // one-point-per-thread 3D pass (odd nx / p > 4)
 #define M3Y 8
-#define M3Z 32
-
-// prefetch depth of the 3D pair pass (planes in flight); KIOPS_3D_DEPTH=3 selects the
-// deeper variant (2 CTAs/SM) for experiments, default 2 (3 CTAs/SM)
-static int lazyp_depth() {
-  const char *e = getenv("KIOPS_3D_DEPTH");
-  return (e && e[0] == '3') ? 3 : 2;
-}
-
-// 2D warp-strip variant (experiment switch KIOPS_2D_VARIANT): 0 = YC 8 / 2 CTAs per SM
-// (default), 1 = YC 4 / 2, 2 = YC 4 / 3, 3 = YC 16 / 2
-static int l2_variant() {
-  const char *e = getenv("KIOPS_2D_VARIANT");
-  return e ? atoi(e) : 0;
-}
-static int l2_yc() {
-  const int v = l2_variant();
-  return (v == 1 || v == 2) ? 4 : v == 3 ? 16 : 8;
-}
+#define M3Z 32   // z-planes per CTA chunk
+#define P3X 64   // pair 3D pass tile (measured best of 32x8, 32x16, 64x8, 64x16, 128x8)
+#define P3Y 8
 
 struct Layout {
   size_t V, r, staging, state, call, H, sig, R2, tails, partials, npart, scratch, coef, trace, sell_off, sell_col,
@@ -143,7 +127,7 @@ Layout layout(const kiops_operator_desc *op, int p, const kiops_options *o) {
     case KIOPS_OP_STENCIL1D3:
     case KIOPS_OP_STENCIL2D5:
       if (op->nx % 2 == 0 && p <= 4) {  // warp-strip lazy kernel (16-byte pairs)
-        const int yc = l2_yc();
+        const int yc = L2YC;
         const long long strips = (op->nx + 59) / 60 * ((op->ny + yc - 1) / yc);
         L.grid_pass = (int)((strips + 7) / 8);
         L.smem_pass = 0;
@@ -156,15 +140,13 @@ Layout layout(const kiops_operator_desc *op, int p, const kiops_options *o) {
       }
       break;
     case KIOPS_OP_STENCIL3D7_VARKAPPA:
-      L.grid_pass = (int)(((op->nx + M3X - 1) / M3X) * ((op->ny + M3Y - 1) / M3Y) * ((op->nz + M3Z - 1) / M3Z));
-      if (op->nx % 2 == 0 && op->nx >= 2 && p >= 1 && p <= 4) {  // pair kernel (16-byte aligned rows), exact p
-        const int dd = lazyp_depth();
-        L.smem_pass = sizeof(double) * (dd == 3 ? (p == 1 ? LazyP<M3X, M3Y, 1, 3>::smem_doubles : p == 2 ? LazyP<M3X, M3Y, 2, 3>::smem_doubles
-                                                 : p == 3 ? LazyP<M3X, M3Y, 3, 3>::smem_doubles : LazyP<M3X, M3Y, 4, 3>::smem_doubles)
-                                              : (p == 1 ? LazyP<M3X, M3Y, 1, 2>::smem_doubles : p == 2 ? LazyP<M3X, M3Y, 2, 2>::smem_doubles
-                                                 : p == 3 ? LazyP<M3X, M3Y, 3, 2>::smem_doubles : LazyP<M3X, M3Y, 4, 2>::smem_doubles));
-        L.block_pass = LazyP<M3X, M3Y, 2>::NT;
+      if (op->nx % 2 == 0 && op->nx >= 2 && p >= 1 && p <= 4) {  // pair kernel (16-byte rows), exact p
+        L.grid_pass = (int)(((op->nx + P3X - 1) / P3X) * ((op->ny + P3Y - 1) / P3Y) * ((op->nz + M3Z - 1) / M3Z));
+        L.smem_pass = sizeof(double) * (p == 1 ? LazyP<P3X, P3Y, 1, 1>::smem_doubles : p == 2 ? LazyP<P3X, P3Y, 2, 1>::smem_doubles
+                                       : p == 3 ? LazyP<P3X, P3Y, 3, 1>::smem_doubles : LazyP<P3X, P3Y, 4, 1>::smem_doubles);
+        L.block_pass = LazyP<P3X, P3Y, 2, 1>::NT;
       } else {
+        L.grid_pass = (int)(((op->nx + M3X - 1) / M3X) * ((op->ny + M3Y - 1) / M3Y) * ((op->nz + M3Z - 1) / M3Z));
         L.smem_pass = sizeof(double) * (p <= 2 ? Lazy3<M3X, M3Y, 2>::smem_doubles
                                        : p <= 4 ? Lazy3<M3X, M3Y, 4>::smem_doubles : Lazy3<M3X, M3Y, 8>::smem_doubles);
         L.block_pass = Lazy3<M3X, M3Y, 2>::NT;
@@ -284,28 +266,19 @@ static kiops_status build_graph(kiops_ctx c) {
   switch (c->op.kind) {
     case KIOPS_OP_STENCIL1D3:
     case KIOPS_OP_STENCIL2D5:
-      if (lazy2d) {
-        const int v = l2_variant();
-#define K2(YC, MB) (c->p == 0 ? (void *)k_pass_2d_lazy<YC, 0, MB> : c->p == 1 ? (void *)k_pass_2d_lazy<YC, 1, MB> \
-                  : c->p == 2 ? (void *)k_pass_2d_lazy<YC, 2, MB> : c->p == 3 ? (void *)k_pass_2d_lazy<YC, 3, MB> \
-                              : (void *)k_pass_2d_lazy<YC, 4, MB>)
-        fpass = v == 1 ? K2(4, 2) : v == 2 ? K2(4, 3) : v == 3 ? K2(16, 2) : K2(8, 2);
-#undef K2
-      }
+      if (lazy2d)  // strip height 8, 2 CTAs/SM: measured best of YC 4/8/16 and 2-3 CTAs/SM
+        fpass = c->p == 0 ? (void *)k_pass_2d_lazy<L2YC, 0, 2> : c->p == 1 ? (void *)k_pass_2d_lazy<L2YC, 1, 2>
+              : c->p == 2 ? (void *)k_pass_2d_lazy<L2YC, 2, 2> : c->p == 3 ? (void *)k_pass_2d_lazy<L2YC, 3, 2>
+                          : (void *)k_pass_2d_lazy<L2YC, 4, 2>;
       else
         fpass = c->op.kind == KIOPS_OP_STENCIL1D3 ? (void *)k_pass_stencil<T1D> : (void *)k_pass_stencil<T2D>;
       break;
     case KIOPS_OP_STENCIL3D7_VARKAPPA:
       if (c->op.nx % 2 == 0 && c->op.nx >= 2 && c->p >= 1 && c->p <= 4)
-        fpass = lazyp_depth() == 3
-                    ? (c->p == 1 ? (void *)k_pass_3d_lazyp<M3X, M3Y, M3Z, 1, 2, 3>
-                       : c->p == 2 ? (void *)k_pass_3d_lazyp<M3X, M3Y, M3Z, 2, 2, 3>
-                       : c->p == 3 ? (void *)k_pass_3d_lazyp<M3X, M3Y, M3Z, 3, 2, 3>
-                                   : (void *)k_pass_3d_lazyp<M3X, M3Y, M3Z, 4, 2, 3>)
-                    : (c->p == 1 ? (void *)k_pass_3d_lazyp<M3X, M3Y, M3Z, 1, 3, 2>
-                       : c->p == 2 ? (void *)k_pass_3d_lazyp<M3X, M3Y, M3Z, 2, 3, 2>
-                       : c->p == 3 ? (void *)k_pass_3d_lazyp<M3X, M3Y, M3Z, 3, 3, 2>
-                                   : (void *)k_pass_3d_lazyp<M3X, M3Y, M3Z, 4, 2, 2>);
+        fpass = c->p == 1 ? (void *)k_pass_3d_lazyp<P3X, P3Y, M3Z, 1, 2, 1>
+              : c->p == 2 ? (void *)k_pass_3d_lazyp<P3X, P3Y, M3Z, 2, 2, 1>
+              : c->p == 3 ? (void *)k_pass_3d_lazyp<P3X, P3Y, M3Z, 3, 2, 1>
+                          : (void *)k_pass_3d_lazyp<P3X, P3Y, M3Z, 4, 2, 1>;
       else
         fpass = c->p <= 2 ? (void *)k_pass_3d_lazy<M3X, M3Y, M3Z, 2, 3>
               : c->p <= 4 ? (void *)k_pass_3d_lazy<M3X, M3Y, M3Z, 4, 3>
