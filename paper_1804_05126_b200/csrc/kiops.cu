@@ -7,7 +7,7 @@
 //   k_setup                                  a1 (Eqs. 48-49), Alg. 1 l.2-8
 //   WHILE (outer)                            Alg. 1 l.9   T_now < T_end
 //     WHILE (inner)                          Alg. 2 l.2   j < m and not happy
-//       k_pass_*  (CSR: k_csr_form, k_csr_spmv)      a2-a4
+//       k_pass_*  (CSR: k_csr_form, k_sell_spmv)     a2-a4
 //     k_ctrl                                 a5-a7, Alg. 3 bookkeeping (one CTA)
 //     IF (accept)
 //       k_gemv                               a8, Alg. 3 l.15, l.20

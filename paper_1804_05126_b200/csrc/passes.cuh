@@ -1,22 +1,22 @@
 // passes.cuh -- SURVEY 8(a) rows a1 (setup), a2-a4 (fused IOP passes) for the
 // built-in operators.  sm_100a CUDA C++, fp64, memory-bound (no tensor cores).
 //
-// One pass k (k = npass+1, 1-based) of the look-ahead ("recompute") form of Alg. 2
-// does, in ONE kernel (stencils) or two (CSR split form):
-//   1. form x_k = (A~ x_{k-1})/s_{k-1} - H(k-2,k-1) x_{k-2}/s_{k-2} - H(k-1,k-1) x_{k-1}/s_{k-1}
-//      on the tile and its halo (A~ x_{k-1} recomputed on chip from x_{k-1}), i.e.
-//      lines 4-10 of Alg. 2 for iteration k-1 with lazy normalisation (line 17 is
-//      folded into the coefficients 1/s);
-//   2. r = A~ x_k on the tile interior (Thm 1 block matvec, lines 4-6);
-//   3. block partials of S = x_k.x_k, G = x_{k-1}.x_k, E1 = x_{k-1}.r, E2 = x_k.r,
-//      R = r.r, then a deterministic last-CTA grid reduction (pass_finalize) that
-//      writes s_k = sqrt(S) = H(k,k-1) (line 11, 16), H(k-1,k) = E1/(s_{k-1}s_k)
-//      and H(k,k) = E2/s_k^2 - H(k-1,k) G/(s_{k-1}s_k) -- the MGS values of lines
-//      7-10 in exact arithmetic -- tests breakdown of iteration k-1 (R3), and forms
-//      the tail of x_{k+1} (p scalars).
-// x_k is written once (the only vector store of the pass).  HBM bytes per pass:
-// read x_{k-1}, x_{k-2}, the p vectors of B and the c coefficient arrays, write
-// x_k: the (q+1+p+c)*8N minimum of SURVEY 8(d).
+// Every pass k (k = npass+1, 1-based) completes Alg. 2 iteration k-1 and
+// starts iteration k:
+//   1. form x_k = (A~ x_{k-1})_top/s_{k-1} - H(k-2,k-1) x_{k-2}/s_{k-2}
+//                 - H(k-1,k-1) x_{k-1}/s_{k-1}                     (l.7-10; l.17 folded)
+//   2. r_k = A x_k + nu B t_k  (Thm 1 block matvec, l.4-6)
+//   3. block partials of S = x_k.x_k, G = x_{k-1}.x_k, E1 = x_{k-1}.r_k, E2 = x_k.r_k,
+//      R = r_k.r_k, then a deterministic last-CTA grid reduction (pass_finalize)
+//      writing s_k = sqrt(S) = H(k,k-1) (l.11, l.16), H(k-1,k) = E1/(s_{k-1}s_k),
+//      H(k,k) = E2/s_k^2 - H(k-1,k) G/(s_{k-1}s_k) -- the MGS values of l.7-10 in
+//      exact arithmetic -- the breakdown test of iteration k-1 (R3), and the tail
+//      of x_{k+1} (p scalars).
+// The kernels in use are LAZY: (A~ x_{k-1})_top = r_{k-1} is read from the previous
+// pass's output (ping-pong buffers), so step 1 is pointwise and one stencil level
+// is applied per pass; HBM per pass = (q+3+p+c) 8N (SURVEY 8(d) "design" bytes).
+// k_pass_stencil (generic tile kernel for odd nx) instead recomputes A~ x_{k-1} on
+// chip from a halo-2 tile ("look-ahead" form, (q+1+p+c) 8N).
 #pragma once
 #include "kiops_internal.cuh"
 
@@ -422,230 +422,7 @@ __global__ void __launch_bounds__(256) k_csr_form(KParams P) {
   }
 }
 
-__global__ void __launch_bounds__(256) k_csr_spmv(KParams P) {
-  // 16 lanes per row, two entries per lane issued together (a 27-point row is one
-  // round of loads + one round of gathers); warp-uniform row loop (two rows per warp)
-  __shared__ PassScalars S;
-  pass_guard(P, false);
-  if (threadIdx.x == 0) load_pass_scalars(P, S);
-  __syncthreads();
-  if (S.k == 0) return;
-  const int k = S.k, p = P.p;
-  const double *__restrict__ xk = (k == 1) ? S.xprev : S.xout;
-  const double *__restrict__ xm = S.xprev;
-  const double *__restrict__ vals = P.vals;
-  const int *__restrict__ cols = P.col_idx;
-  const long long *__restrict__ rp = P.row_ptr;
-  const int l16 = threadIdx.x & 15;
-  const unsigned half = (threadIdx.x & 16) ? 0xffff0000u : 0x0000ffffu;
-  double v[NDOT] = {0.0, 0.0, 0.0, 0.0, 0.0};
-  const long long groups = (long long)gridDim.x * (blockDim.x / 16);
-  const long long g0 = (blockIdx.x * (long long)blockDim.x + threadIdx.x) / 16;
-  const long long warp_first = (blockIdx.x * (long long)blockDim.x + (threadIdx.x & ~31)) / 16;
-  for (long long it = 0; warp_first + it * groups < P.N; it++) {
-    const long long row = g0 + it * groups;
-    const bool live = row < P.N;
-    double s = 0.0;
-    if (live) {
-      const long long b0 = __ldg(rp + row), b1 = __ldg(rp + row + 1);
-      for (long long q = b0 + l16; q < b1; q += 32) {
-        const bool two = q + 16 < b1;
-        const double va = __ldg(vals + q);
-        const int ca = __ldg(cols + q);
-        const double vb = two ? __ldg(vals + q + 16) : 0.0;
-        const int cb = two ? __ldg(cols + q + 16) : ca;
-        const double xa = xk[ca], xb = xk[cb];
-        s = fma(va, xa, s);
-        s = fma(vb, xb, s);
-      }
-    }
-    s += __shfl_xor_sync(0xffffffffu, s, 8);
-    s += __shfl_xor_sync(0xffffffffu, s, 4);
-    s += __shfl_xor_sync(0xffffffffu, s, 2);
-    s += __shfl_xor_sync(0xffffffffu, s, 1);
-    (void)half;
-    if (live && l16 == 0) {
-      double rr = s;
-#pragma unroll
-      for (int c = 0; c < KMAXP; c++)
-        if (c < p) rr += S.B[c][row] * S.btc[c];
-      const double x = xk[row], y = xm[row];
-      v[0] += x * x;
-      v[1] += y * x;
-      v[2] += y * rr;
-      v[3] += x * rr;
-      v[4] += rr * rr;
-      P.r[row] = rr;
-    }
-  }
-  pass_epilogue(P, k, v);
-}
 
-// ---------------------------------------------------------------------------
-// 3D variable-kappa pass, v2: 2.5D z-marching.  A CTA owns a TX x TY column of
-// the grid and a chunk of ZC z-planes; planes stream through shared-memory rings:
-//   x_{k-1}, kappa : halo-2 planes (ring 4 / 5)  -> A x_{k-1} on the halo-1 plane
-//   x_k            : halo-1 planes (ring 3)      -> r = A~ x_k on the interior
-//   nu B t_k       : interior planes (ring 2)
-// so each array is read from HBM once per pass (xy halos and the 2-plane z
-// warm-up of a chunk come from L2).  Two barriers per plane.  PM >= p bounds the
-// B terms held in registers.
-// ---------------------------------------------------------------------------
-template <int TX, int TY, int ZC, int PM>
-__global__ void __launch_bounds__(TX *TY, 2) k_pass_3d_march(KParams P) {
-  constexpr int NT = TX * TY, HX = TX + 4, HY = TY + 4, S2 = HX * HY, GX = TX + 2, GY = TY + 2, S1 = GX * GY;
-  constexpr int L2N = (S2 + NT - 1) / NT, L1N = (S1 + NT - 1) / NT;
-  extern __shared__ double smem[];
-  double *sXP = smem;             // 4 x S2
-  double *sKP = sXP + 4 * S2;     // 5 x S2
-  double *sXK = sKP + 5 * S2;     // 3 x S1
-  double *sBT = sXK + 3 * S1;     // 2 x NT
-
-  __shared__ PassScalars S;
-  pass_guard(P);
-  if (threadIdx.x == 0) load_pass_scalars(P, S);
-  __syncthreads();
-  if (S.k == 0) return;
-  const int p = P.p;
-  const long long nx = P.nx, ny = P.ny, nz = P.nz, nxy = nx * ny;
-  const long long ntx = (nx + TX - 1) / TX, nty = (ny + TY - 1) / TY;
-  const long long b = blockIdx.x;
-  const long long ox = (b % ntx) * TX, oy = ((b / ntx) % nty) * TY;
-  const long long z0 = (b / (ntx * nty)) * ZC;
-  const long long z1 = (z0 + ZC < nz) ? z0 + ZC : nz;
-  const int tid = threadIdx.x;
-  const double ih2 = P.inv_h2;
-  const double *__restrict__ xprev = S.xprev;
-  const double *__restrict__ kap = P.kappa;
-  const double *__restrict__ xpp = S.xpp;
-
-  // per-thread plane offsets (wrapped xy), computed once
-  int off2[L2N];  // in-plane offsets (nx*ny < 2^31 is validated at create)
-  int e2s[L2N];
-#pragma unroll
-  for (int q = 0; q < L2N; q++) {
-    const int e = tid + q * NT;
-    e2s[q] = e < S2 ? e : -1;
-    const int a = e % HX, bb = e / HX;
-    off2[q] = (int)(wrapc(ox + a - 2, nx) + nx * wrapc(oy + bb - 2, ny));
-  }
-  int off1[L1N];
-  int f1s[L1N], f2s[L1N], fin[L1N];
-#pragma unroll
-  for (int q = 0; q < L1N; q++) {
-    const int e = tid + q * NT;
-    f1s[q] = e < S1 ? e : -1;
-    const int a = e % GX, bb = e / GX;
-    off1[q] = (int)(wrapc(ox + a - 1, nx) + nx * wrapc(oy + bb - 1, ny));
-    f2s[q] = (a + 1) + HX * (bb + 1);
-    fin[q] = (a >= 1 && a <= TX && bb >= 1 && bb <= TY) ? (a - 1) + TX * (bb - 1) : -1;
-  }
-  const int ia = tid % TX, ib = tid / TX;
-  const int ie1 = (ia + 1) + GX * (ib + 1), ie2 = (ia + 2) + HX * (ib + 2);
-  const long long gx = ox + ia, gy = oy + ib;
-  const bool inside = gx < nx && gy < ny;
-
-  auto rz = [&](long long z) { return (int)(z - z0 + 2); };  // >= 0 for z >= z0 - 2
-  auto load_plane = [&](long long z) {
-    const long long zo = nxy * wrapc(z, nz);
-    const int r = rz(z);
-    double *dx = sXP + (r & 3) * S2;
-    double *dk = sKP + (r % 5) * S2;
-#pragma unroll
-    for (int q = 0; q < L2N; q++)
-      if (e2s[q] >= 0) {
-        dx[e2s[q]] = xprev[off2[q] + zo];
-        dk[e2s[q]] = kap[off2[q] + zo];
-      }
-  };
-
-  double v[NDOT] = {0.0, 0.0, 0.0, 0.0, 0.0};
-  load_plane(z0 - 2);
-  load_plane(z0 - 1);
-  for (long long zf = z0 - 1; zf <= z1; zf++) {
-    // formation-plane operands from HBM first (latency overlaps the plane load)
-    const long long zo = nxy * wrapc(zf, nz);
-    double bv[L1N][PM], xq[L1N];
-#pragma unroll
-    for (int q = 0; q < L1N; q++) {
-      xq[q] = 0.0;
-#pragma unroll
-      for (int c = 0; c < PM; c++) bv[q][c] = 0.0;
-      if (f1s[q] >= 0) {
-        if (xpp) xq[q] = xpp[off1[q] + zo];
-#pragma unroll
-        for (int c = 0; c < PM; c++)
-          if (c < p) bv[q][c] = S.B[c][off1[q] + zo];
-      }
-    }
-    load_plane(zf + 1);
-    __syncthreads();
-    // formation of x_k on the halo-1 plane zf
-    {
-      const int r0 = rz(zf);
-      const double *X0 = sXP + (r0 & 3) * S2, *Xm = sXP + ((r0 - 1) & 3) * S2, *Xp = sXP + ((r0 + 1) & 3) * S2;
-      const double *K0 = sKP + (r0 % 5) * S2, *Km = sKP + ((r0 + 4) % 5) * S2, *Kp = sKP + ((r0 + 1) % 5) * S2;
-      double *XK = sXK + (r0 % 3) * S1;
-      double *BT = sBT + (r0 & 1) * NT;
-#pragma unroll
-      for (int q = 0; q < L1N; q++) {
-        if (f1s[q] < 0) continue;
-        const int e = f2s[q];
-        const double xc = X0[e], kc = K0[e];
-        double ax = 0.5 * (kc + K0[e - 1]) * (X0[e - 1] - xc) + 0.5 * (kc + K0[e + 1]) * (X0[e + 1] - xc) +
-                    0.5 * (kc + K0[e - HX]) * (X0[e - HX] - xc) + 0.5 * (kc + K0[e + HX]) * (X0[e + HX] - xc) +
-                    0.5 * (kc + Km[e]) * (Xm[e] - xc) + 0.5 * (kc + Kp[e]) * (Xp[e] - xc);
-        ax *= ih2;
-        double bp = 0.0, bc = 0.0;
-#pragma unroll
-        for (int c = 0; c < PM; c++) {
-          bp += bv[q][c] * S.btp[c];
-          bc += bv[q][c] * S.btc[c];
-        }
-        const double xk = S.a0 * (ax + bp) - S.a1 * xc - S.a2 * xq[q];
-        XK[f1s[q]] = xk;
-        if (fin[q] >= 0) BT[fin[q]] = bc;
-      }
-    }
-    __syncthreads();
-    // output plane z = zf - 1: r = A~ x_k, dots, store x_k
-    const long long z = zf - 1;
-    if (z >= z0) {
-      const int r0 = rz(z);
-      const double *XK0 = sXK + (r0 % 3) * S1, *XKm = sXK + ((r0 + 2) % 3) * S1, *XKp = sXK + ((r0 + 1) % 3) * S1;
-      const double *K0 = sKP + (r0 % 5) * S2, *Km = sKP + ((r0 + 4) % 5) * S2, *Kp = sKP + ((r0 + 1) % 5) * S2;
-      const double xk = XK0[ie1], kc = K0[ie2];
-      double r = 0.5 * (kc + K0[ie2 - 1]) * (XK0[ie1 - 1] - xk) + 0.5 * (kc + K0[ie2 + 1]) * (XK0[ie1 + 1] - xk) +
-                 0.5 * (kc + K0[ie2 - HX]) * (XK0[ie1 - GX] - xk) + 0.5 * (kc + K0[ie2 + HX]) * (XK0[ie1 + GX] - xk) +
-                 0.5 * (kc + Km[ie2]) * (XKm[ie1] - xk) + 0.5 * (kc + Kp[ie2]) * (XKp[ie1] - xk);
-      r = r * ih2 + sBT[(r0 & 1) * NT + tid];
-      if (inside) {
-        const double xm = sXP[(r0 & 3) * S2 + ie2];
-        v[0] += xk * xk;
-        v[1] += xm * xk;
-        v[2] += xm * r;
-        v[3] += xk * r;
-        v[4] += r * r;
-        if (S.xout) S.xout[gx + nx * gy + nxy * z] = xk;
-      }
-    }
-  }
-  pass_epilogue(P, S.k, v);
-}
-
-template <int TX, int TY, int ZC>
-constexpr size_t march3d_smem_bytes() {
-  return sizeof(double) * (size_t)(9 * (TX + 4) * (TY + 4) + 3 * (TX + 2) * (TY + 2) + 2 * TX * TY);
-}
-
-// ---------------------------------------------------------------------------
-// 3D variable-kappa pass, v3: z-marching with asynchronous global->shared copies
-// (cp.async, LDGSTS) issued D planes ahead, so HBM latency overlaps the stencil
-// work of the current plane.  Rings (live planes after the first barrier):
-//   x_{k-1}, kappa : halo-2, D+3 / D+4 slots
-//   x_{k-2}, B     : halo-1, DF+1 slots (formation operands)
-//   x_k            : halo-1, 3 slots;  nu B t_k : interior, 2 slots
-// ---------------------------------------------------------------------------
 __device__ __forceinline__ void cp_async8(double *dst, const double *src) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(dst);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(src) : "memory");
@@ -653,517 +430,6 @@ __device__ __forceinline__ void cp_async8(double *dst, const double *src) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
-
-template <int TX, int TY, int PM>
-struct March3 {
-  static constexpr int NT = TX * TY, HX = TX + 4, HY = TY + 4, S2 = HX * HY, GX = TX + 2, GY = TY + 2, S1 = GX * GY;
-  static constexpr int D = PM <= 4 ? 2 : 1;       // planes in flight (both rings)
-  static constexpr int DF = D;
-  static constexpr int RX = D + 3, RK = D + 4, RF = DF + 1;
-  static constexpr int L2N = (S2 + NT - 1) / NT, L1N = (S1 + NT - 1) / NT;
-  static constexpr size_t smem_doubles = (size_t)RX * S2 + (size_t)RK * S2 + (size_t)RF * S1 * (1 + PM) +
-                                         3 * (size_t)S1 + 2 * (size_t)NT;
-};
-
-template <int TX, int TY, int ZC, int PM>
-__global__ void __launch_bounds__(TX *TY, 1) k_pass_3d_async(KParams P) {
-  using M = March3<TX, TY, PM>;
-  constexpr int NT = M::NT, HX = M::HX, S2 = M::S2, GX = M::GX, S1 = M::S1, D = M::D, DF = M::DF;
-  constexpr int RX = M::RX, RK = M::RK, RF = M::RF, L2N = M::L2N, L1N = M::L1N;
-  extern __shared__ double smem[];
-  double *sXP = smem;                 // RX x S2
-  double *sKP = sXP + RX * S2;        // RK x S2
-  double *sF = sKP + RK * S2;         // RF x (1+PM) x S1 : [slot][0] = x_{k-2}, [slot][1+c] = B_c
-  double *sXK = sF + RF * (1 + PM) * S1;  // 3 x S1
-  double *sBT = sXK + 3 * S1;         // 2 x NT
-
-  __shared__ PassScalars S;
-  pass_guard(P);
-  if (threadIdx.x == 0) load_pass_scalars(P, S);
-  __syncthreads();
-  if (S.k == 0) return;
-  const int p = P.p;
-  const long long nx = P.nx, ny = P.ny, nz = P.nz, nxy = nx * ny;
-  const long long ntx = (nx + TX - 1) / TX, nty = (ny + TY - 1) / TY;
-  const long long b = blockIdx.x;
-  const long long ox = (b % ntx) * TX, oy = ((b / ntx) % nty) * TY;
-  const long long z0 = (b / (ntx * nty)) * ZC;
-  const long long z1 = (z0 + ZC < nz) ? z0 + ZC : nz;
-  const int tid = threadIdx.x;
-  const double ih2 = P.inv_h2;
-  const bool has_pp = S.xpp != nullptr;
-
-  int off2[L2N], e2s[L2N];
-#pragma unroll
-  for (int q = 0; q < L2N; q++) {
-    const int e = tid + q * NT;
-    e2s[q] = e < S2 ? e : -1;
-    const int a = e % HX, bb = e / HX;
-    off2[q] = (int)(wrapc(ox + a - 2, nx) + nx * wrapc(oy + bb - 2, ny));
-  }
-  int off1[L1N], f1s[L1N], f2s[L1N], fin[L1N];
-#pragma unroll
-  for (int q = 0; q < L1N; q++) {
-    const int e = tid + q * NT;
-    f1s[q] = e < S1 ? e : -1;
-    const int a = e % GX, bb = e / GX;
-    off1[q] = (int)(wrapc(ox + a - 1, nx) + nx * wrapc(oy + bb - 1, ny));
-    f2s[q] = (a + 1) + HX * (bb + 1);
-    fin[q] = (a >= 1 && a <= TX && bb >= 1 && bb <= TY) ? (a - 1) + TX * (bb - 1) : -1;
-  }
-  const int ia = tid % TX, ib = tid / TX;
-  const int ie1 = (ia + 1) + GX * (ib + 1), ie2 = (ia + 2) + HX * (ib + 2);
-  const long long gx = ox + ia, gy = oy + ib;
-  const bool inside = gx < nx && gy < ny;
-
-  // async plane loaders (every thread its own elements; one commit per step)
-  auto issue_xk = [&](long long z) {  // x_{k-1} and kappa, halo-2 plane z
-    const long long zo = nxy * wrapc(z, nz);
-    const int r = (int)(z - z0 + 2);
-    const double *gxp = S.xprev + zo, *gkp = P.kappa + zo;
-    double *dx = sXP + (r % RX) * S2, *dk = sKP + (r % RK) * S2;
-#pragma unroll
-    for (int q = 0; q < L2N; q++)
-      if (e2s[q] >= 0) {
-        cp_async8(dx + e2s[q], gxp + off2[q]);
-        cp_async8(dk + e2s[q], gkp + off2[q]);
-      }
-  };
-  auto issue_f = [&](long long z) {  // x_{k-2} and B, halo-1 plane z
-    const long long zo = nxy * wrapc(z, nz);
-    const int r = (int)(z - z0 + 1);
-    double *d = sF + (r % RF) * (1 + PM) * S1;
-#pragma unroll
-    for (int q = 0; q < L1N; q++)
-      if (f1s[q] >= 0) {
-        if (has_pp) cp_async8(d + f1s[q], S.xpp + zo + off1[q]);
-#pragma unroll
-        for (int c = 0; c < PM; c++)
-          if (c < p) cp_async8(d + (1 + c) * S1 + f1s[q], S.B[c] + zo + off1[q]);
-      }
-  };
-
-  // prologue: group "init" = x/kappa planes z0-2, z0-1; then D groups ahead
-  issue_xk(z0 - 2);
-  issue_xk(z0 - 1);
-  cp_async_commit();
-  for (int i = 0; i < D; i++) {  // group i: x/kappa plane z0+i, f plane z0-1+i (if within DF)
-    issue_xk(z0 + i);
-    if (i < DF) issue_f(z0 - 1 + i);
-    cp_async_commit();
-  }
-  double v[NDOT] = {0.0, 0.0, 0.0, 0.0, 0.0};
-  for (long long zf = z0 - 1; zf <= z1; zf++) {
-    const long long i = zf - (z0 - 1);
-    cp_async_wait<D - 1>();
-    __syncthreads();  // B1: planes of group i visible; iteration i-1 finished everywhere
-    if (zf + 1 + D <= z1 + 1) issue_xk(zf + 1 + D);
-    if (i + DF <= (z1 - z0 + 1)) issue_f(zf + DF);
-    cp_async_commit();
-    {  // formation of x_k on the halo-1 plane zf
-      const int r0 = (int)(zf - z0 + 2);
-      const double *X0 = sXP + (r0 % RX) * S2, *Xm = sXP + ((r0 + RX - 1) % RX) * S2,
-                   *Xp = sXP + ((r0 + 1) % RX) * S2;
-      const double *K0 = sKP + (r0 % RK) * S2, *Km = sKP + ((r0 + RK - 1) % RK) * S2,
-                   *Kp = sKP + ((r0 + 1) % RK) * S2;
-      const double *Fs = sF + ((int)(zf - z0 + 1) % RF) * (1 + PM) * S1;
-      double *XK = sXK + (r0 % 3) * S1;
-      double *BT = sBT + (r0 & 1) * NT;
-#pragma unroll
-      for (int q = 0; q < L1N; q++) {
-        if (f1s[q] < 0) continue;
-        const int e = f2s[q], f = f1s[q];
-        const double xc = X0[e], kc = K0[e];
-        double ax = 0.5 * (kc + K0[e - 1]) * (X0[e - 1] - xc) + 0.5 * (kc + K0[e + 1]) * (X0[e + 1] - xc) +
-                    0.5 * (kc + K0[e - HX]) * (X0[e - HX] - xc) + 0.5 * (kc + K0[e + HX]) * (X0[e + HX] - xc) +
-                    0.5 * (kc + Km[e]) * (Xm[e] - xc) + 0.5 * (kc + Kp[e]) * (Xp[e] - xc);
-        double bp = 0.0, bc = 0.0;
-#pragma unroll
-        for (int c = 0; c < PM; c++)
-          if (c < p) {
-            const double bv = Fs[(1 + c) * S1 + f];
-            bp += bv * S.btp[c];
-            bc += bv * S.btc[c];
-          }
-        double xk = S.a0 * (ax * ih2 + bp) - S.a1 * xc;
-        if (has_pp) xk -= S.a2 * Fs[f];
-        XK[f] = xk;
-        if (fin[q] >= 0) BT[fin[q]] = bc;
-      }
-    }
-    __syncthreads();  // B2
-    const long long z = zf - 1;
-    if (z >= z0) {
-      const int r0 = (int)(z - z0 + 2);
-      const double *XK0 = sXK + (r0 % 3) * S1, *XKm = sXK + ((r0 + 2) % 3) * S1, *XKp = sXK + ((r0 + 1) % 3) * S1;
-      const double *K0 = sKP + (r0 % RK) * S2, *Km = sKP + ((r0 + RK - 1) % RK) * S2,
-                   *Kp = sKP + ((r0 + 1) % RK) * S2;
-      const double xk = XK0[ie1], kc = K0[ie2];
-      double r = 0.5 * (kc + K0[ie2 - 1]) * (XK0[ie1 - 1] - xk) + 0.5 * (kc + K0[ie2 + 1]) * (XK0[ie1 + 1] - xk) +
-                 0.5 * (kc + K0[ie2 - HX]) * (XK0[ie1 - GX] - xk) + 0.5 * (kc + K0[ie2 + HX]) * (XK0[ie1 + GX] - xk) +
-                 0.5 * (kc + Km[ie2]) * (XKm[ie1] - xk) + 0.5 * (kc + Kp[ie2]) * (XKp[ie1] - xk);
-      r = r * ih2 + sBT[(r0 & 1) * NT + tid];
-      if (inside) {
-        const double xm = sXP[(r0 % RX) * S2 + ie2];
-        v[0] += xk * xk;
-        v[1] += xm * xk;
-        v[2] += xm * r;
-        v[3] += xk * r;
-        v[4] += r * r;
-        if (S.xout) S.xout[gx + nx * gy + nxy * z] = xk;
-      }
-    }
-  }
-  cp_async_wait<0>();
-  pass_epilogue(P, S.k, v);
-}
-
-// ---------------------------------------------------------------------------
-// 3D variable-kappa pass (v6): one thread per point of the halo-1 plane of a
-// TX x TY column tile, marching a chunk of ZC z-planes.
-//  * x_{k-1} and kappa halo-2 planes stream into shared-memory rings with cp.async
-//    (LDGSTS), D planes ahead; each thread also prefetches its OWN x_{k-2} and B
-//    operands (thread-private ring, no barrier needed for them);
-//  * every thread forms x_k at its own halo-1 point (A~ x_{k-1}: in-plane
-//    neighbours from shared memory, z-neighbours of its own column from
-//    registers), publishes it to a 2-plane x_k ring, and -- if interior -- applies
-//    A~ to x_k of the PREVIOUS plane (in-plane neighbours from the ring, own column
-//    and the previous plane's kappa neighbours from registers), accumulates the
-//    five dots and stores x_k: one barrier per plane, ~(11 + p) + 4 shared loads
-//    per point.
-// (kappa_i + kappa_nb)(x_nb - x_i) is summed and scaled by inv_h2 / 2.
-// ---------------------------------------------------------------------------
-template <int TX, int TY, int PM>
-struct March4 {
-  static constexpr int HX = TX + 4, HY = TY + 4, S2 = HX * HY, GX = TX + 2, GY = TY + 2, S1 = GX * GY;
-  static constexpr int NT = (S1 + 31) / 32 * 32;  // threads: one per halo-1 point
-  static constexpr int D = 2;                     // planes in flight
-  static constexpr int RX = D + 2, RF = D + 1;    // x_{k-1}/kappa ring, operand ring
-  static constexpr int NF = 1 + PM;               // x_{k-2}, B_0..B_{PM-1}
-  static constexpr size_t smem_doubles = (size_t)2 * RX * S2 + (size_t)RF * NF * S1 + 2 * (size_t)S1;
-};
-
-template <int TX, int TY, int ZC, int PM>
-__global__ void __launch_bounds__(March4<TX, TY, PM>::NT, 1) k_pass_3d_v4(KParams P) {
-  using M = March4<TX, TY, PM>;
-  constexpr int NT = M::NT, HX = M::HX, S2 = M::S2, GX = M::GX, S1 = M::S1, D = M::D, NF = M::NF;
-  constexpr int RX = M::RX, RF = M::RF;
-  extern __shared__ double smem[];
-  double *sXP = smem;                  // RX x S2   x_{k-1}
-  double *sKP = sXP + RX * S2;         // RX x S2   kappa
-  double *sF = sKP + RX * S2;          // RF x NF x S1 (thread-private columns)
-  double *sXK = sF + RF * NF * S1;     // 2 x S1    x_k
-
-  __shared__ PassScalars S;
-  pass_guard(P);
-  if (threadIdx.x == 0) load_pass_scalars(P, S);
-  __syncthreads();
-  if (S.k == 0) return;
-  const int p = P.p;
-  const long long nx = P.nx, ny = P.ny, nz = P.nz, nxy = nx * ny;
-  const long long ntx = (nx + TX - 1) / TX, nty = (ny + TY - 1) / TY;
-  const long long b = blockIdx.x;
-  const long long ox = (b % ntx) * TX, oy = ((b / ntx) % nty) * TY;
-  const long long z0 = (b / (ntx * nty)) * ZC;
-  const long long z1 = (z0 + ZC < nz) ? z0 + ZC : nz;
-  const int nzc = (int)(z1 - z0);
-  const int t = threadIdx.x;
-  const double hh = 0.5 * P.inv_h2;
-  const bool has_pp = S.xpp != nullptr;
-  const double a0 = S.a0, a1 = S.a1, a2 = S.a2;
-  double btp[PM], btc[PM];
-  const double *Bp[PM];
-#pragma unroll
-  for (int c = 0; c < PM; c++) {
-    btp[c] = c < p ? S.btp[c] : 0.0;
-    btc[c] = c < p ? S.btc[c] : 0.0;
-    Bp[c] = c < p ? S.B[c] : nullptr;
-  }
-
-  // halo-2 elements this thread copies (e = t, t + NT)
-  const bool h2a = t < S2, h2b = t + NT < S2;
-  int o2a = 0, o2b = 0;
-  if (h2a) { const int a = t % HX, c = t / HX; o2a = (int)(wrapc(ox + a - 2, nx) + nx * wrapc(oy + c - 2, ny)); }
-  if (h2b) { const int e = t + NT, a = e % HX, c = e / HX; o2b = (int)(wrapc(ox + a - 2, nx) + nx * wrapc(oy + c - 2, ny)); }
-  // own halo-1 point
-  const bool act = t < S1;
-  const int fa = t % GX, fb = t / GX;
-  const int o1 = act ? (int)(wrapc(ox + fa - 1, nx) + nx * wrapc(oy + fb - 1, ny)) : 0;
-  const int e2 = act ? (fa + 1) + HX * (fb + 1) : HX + 1;  // own point in the halo-2 plane
-  const bool inner = act && fa >= 1 && fa <= TX && fb >= 1 && fb <= TY && (ox + fa - 1) < nx && (oy + fb - 1) < ny;
-  const long long gown = (ox + fa - 1) + nx * (oy + fb - 1);  // interior global in-plane index (if inner)
-
-  const double *gX = S.xprev, *gK = P.kappa, *gPP = S.xpp;
-  auto issue_x = [&](long long zo, double *dx, double *dk) {
-    const double *px = gX + zo, *pk = gK + zo;
-    if (h2a) { cp_async8(dx + t, px + o2a); cp_async8(dk + t, pk + o2a); }
-    if (h2b) { cp_async8(dx + t + NT, px + o2b); cp_async8(dk + t + NT, pk + o2b); }
-  };
-  auto issue_f = [&](long long zo, double *df) {
-    if (!act) return;
-    if (has_pp) cp_async8(df + t, gPP + zo + o1);
-#pragma unroll
-    for (int c = 0; c < PM; c++)
-      if (c < p) cp_async8(df + (1 + c) * S1 + t, Bp[c] + zo + o1);
-  };
-  auto inc = [](int s, int R) { return s + 1 == R ? 0 : s + 1; };
-  auto znext = [&](long long z) { return z + 1 == nz ? 0 : z + 1; };  // wrapped plane index
-
-  // prologue: x/kappa planes r = 0 .. D+1 (z0-2 .. z0+D-1) in slots 0..D+1, f planes r = 0..D-1
-  long long zx = wrapc(z0 - 2, nz), zfp = wrapc(z0 - 1, nz);
-  for (int q = 0; q < 2; q++) {
-    issue_x(zx * nxy, sXP + q * S2, sKP + q * S2);
-    zx = znext(zx);
-  }
-  cp_async_commit();
-  for (int q = 0; q < D; q++) {
-    issue_x(zx * nxy, sXP + (q + 2) * S2, sKP + (q + 2) * S2);
-    zx = znext(zx);
-    issue_f(zfp * nxy, sF + q * NF * S1);
-    zfp = znext(zfp);
-    cp_async_commit();
-  }
-  // own-column registers.  Plane r = z - z0 + 2 (x/kappa); formation plane zf = z0 - 1 + i
-  cp_async_wait<D - 1>();  // groups init, 0 landed: planes r = 0..2
-  __syncthreads();
-  double xo_m = sXP[0 * S2 + e2], xo_0 = sXP[1 * S2 + e2];       // x_{k-1}(zf-1), x_{k-1}(zf) for i = 0
-  double ko_mm = 0.0, ko_m = sKP[0 * S2 + e2], ko_0 = sKP[1 * S2 + e2];
-  double kW = 0.0, kE = 0.0, kS = 0.0, kN = 0.0;                   // kappa neighbours of the previous plane
-  double xk_m = 0.0, xk_0 = 0.0, bt_0 = 0.0;                       // x_k(zf-2), x_k(zf-1), nu B t_k(zf-1)
-  double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0, v4 = 0.0;
-  int xs = 1, xi = (D + 2) % RX, fs = 0, fi = D % RF;  // x ring slot of r = i+1 (center), issue slots
-  long long zout = z0;
-  for (int i = 0; i <= nzc + 1; i++) {
-    cp_async_wait<D - 1>();
-    __syncthreads();  // the one barrier per plane (at i = 0 it also orders the register
-                      // initialisation above before slot 0 is refilled)
-    if (i + 2 + D <= nzc + 3) issue_x(zx * nxy, sXP + xi * S2, sKP + xi * S2);
-    if (i + D <= nzc + 1) issue_f(zfp * nxy, sF + fi * NF * S1);
-    cp_async_commit();
-    zx = znext(zx);
-    zfp = znext(zfp);
-    const int xsp = inc(xs, RX);
-    const double *X0 = sXP + xs * S2, *K0 = sKP + xs * S2;
-    // formation of x_k at the own point of plane zf (Alg. 2 l.4-10 of iteration k-1)
-    const double xo_p = sXP[xsp * S2 + e2], ko_p = sKP[xsp * S2 + e2];
-    const double nW = K0[e2 - 1], nE = K0[e2 + 1], nS = K0[e2 - HX], nN = K0[e2 + HX];
-    double ax = (ko_0 + nW) * (X0[e2 - 1] - xo_0);
-    double ay = (ko_0 + nE) * (X0[e2 + 1] - xo_0);
-    ax = fma(ko_0 + nS, X0[e2 - HX] - xo_0, ax);
-    ay = fma(ko_0 + nN, X0[e2 + HX] - xo_0, ay);
-    ax = fma(ko_0 + ko_m, xo_m - xo_0, ax);
-    ay = fma(ko_0 + ko_p, xo_p - xo_0, ay);
-    const double *Fs = sF + fs * NF * S1;
-    double bp = 0.0, bc = 0.0;
-#pragma unroll
-    for (int c = 0; c < PM; c++)
-      if (c < p) {
-        const double bv = Fs[(1 + c) * S1 + t];
-        bp = fma(bv, btp[c], bp);
-        bc = fma(bv, btc[c], bc);
-      }
-    double xk_p = a0 * fma(ax + ay, hh, bp) - a1 * xo_0;
-    if (has_pp) xk_p -= a2 * Fs[t];
-    double *XKn = sXK + (i & 1) * S1;
-    if (act) XKn[t] = xk_p;
-    // output plane zout = zf - 1 (x_k of that plane was published one barrier ago)
-    if (i >= 2 && inner) {
-      const double *XK0 = sXK + ((i + 1) & 1) * S1;
-      double rx = (ko_m + kW) * (XK0[t - 1] - xk_0);
-      double ry = (ko_m + kE) * (XK0[t + 1] - xk_0);
-      rx = fma(ko_m + kS, XK0[t - GX] - xk_0, rx);
-      ry = fma(ko_m + kN, XK0[t + GX] - xk_0, ry);
-      rx = fma(ko_m + ko_mm, xk_m - xk_0, rx);
-      ry = fma(ko_m + ko_0, xk_p - xk_0, ry);
-      const double r = fma(rx + ry, hh, bt_0);
-      const double xm = xo_m;
-      v0 = fma(xk_0, xk_0, v0);
-      v1 = fma(xm, xk_0, v1);
-      v2 = fma(xm, r, v2);
-      v3 = fma(xk_0, r, v3);
-      v4 = fma(r, r, v4);
-      if (S.xout) S.xout[gown + nxy * zout] = xk_0;
-    }
-    if (i >= 2) zout++;
-    // roll own-column registers and ring slots by one plane
-    xo_m = xo_0; xo_0 = xo_p;
-    ko_mm = ko_m; ko_m = ko_0; ko_0 = ko_p;
-    kW = nW; kE = nE; kS = nS; kN = nN;
-    xk_m = xk_0; xk_0 = xk_p; bt_0 = bc;
-    xs = xsp;
-    xi = inc(xi, RX);
-    fs = inc(fs, RF);
-    fi = inc(fi, RF);
-  }
-  cp_async_wait<0>();
-  double v[NDOT] = {v0, v1, v2, v3, v4};
-  pass_epilogue(P, S.k, v);
-}
-
-// ---------------------------------------------------------------------------
-// 3D variable-kappa pass (v7, the one in use): as v6, with
-//  * 32 x 8 column tiles: (TX+2)(TY+2) = 340 threads, two CTAs per SM;
-//  * own x_{k-2} / B operands prefetched two planes ahead into registers
-//    (double buffer, loop unrolled by two so buffers never move);
-//  * the six face sums kappa_i + kappa_nb of the formation at (x, y, z) are kept
-//    and reused by the output stencil at the same point one plane later;
-//  * per-thread global pointers precomputed; plane offsets roll incrementally.
-// ---------------------------------------------------------------------------
-template <int TX, int TY, int PM>
-struct March7 {
-  static constexpr int HX = TX + 4, HY = TY + 4, S2 = HX * HY, GX = TX + 2, GY = TY + 2, S1 = GX * GY;
-  static constexpr int NT = (S1 + 31) / 32 * 32;
-  static constexpr int D = 2, RX = 4;
-  static constexpr size_t smem_doubles = (size_t)2 * RX * S2 + 2 * (size_t)S1;
-};
-
-template <int PM>
-struct Ops {
-  double pp;
-  double b[PM];
-};
-
-template <int TX, int TY, int ZC, int PM, int MINB>
-__global__ void __launch_bounds__(March7<TX, TY, PM>::NT, MINB) k_pass_3d_v7(KParams P) {
-  using M = March7<TX, TY, PM>;
-  constexpr int NT = M::NT, HX = M::HX, S2 = M::S2, GX = M::GX, S1 = M::S1, D = M::D, RX = M::RX;
-  static_assert(RX == 4, "ring slots use & 3");
-  extern __shared__ double smem[];
-  double *sX = smem;            // 4 x S2   x_{k-1}
-  double *sK = sX + RX * S2;    // 4 x S2   kappa
-  double *sXK = sK + RX * S2;   // 2 x S1   x_k
-
-  __shared__ PassScalars S;
-  pass_guard(P);
-  if (threadIdx.x == 0) load_pass_scalars(P, S);
-  __syncthreads();
-  if (S.k == 0) return;
-  const int p = P.p;
-  const long long nx = P.nx, ny = P.ny, nz = P.nz, nxy = nx * ny;
-  const long long ntx = (nx + TX - 1) / TX, nty = (ny + TY - 1) / TY;
-  const long long bidx = blockIdx.x;
-  const long long ox = (bidx % ntx) * TX, oy = ((bidx / ntx) % nty) * TY;
-  const long long z0 = (bidx / (ntx * nty)) * ZC;
-  const long long z1 = (z0 + ZC < nz) ? z0 + ZC : nz;
-  const int nzc = (int)(z1 - z0);
-  const int t = threadIdx.x;
-  const double hh = 0.5 * P.inv_h2;
-  const double a0 = S.a0, a1 = S.a1, a2 = S.a2;
-  double btp[PM], btc[PM];
-#pragma unroll
-  for (int c = 0; c < PM; c++) {
-    btp[c] = c < p ? S.btp[c] : 0.0;
-    btc[c] = c < p ? S.btc[c] : 0.0;
-  }
-  // halo-2 copy elements (t, t + NT): 32-bit in-plane offsets (nx*ny < 2^31 validated)
-  const bool h2a = t < S2, h2b = t + NT < S2;
-  int o2a = 0, o2b = 0;
-  if (h2a) { const int a = t % HX, c = t / HX; o2a = (int)(wrapc(ox + a - 2, nx) + nx * wrapc(oy + c - 2, ny)); }
-  if (h2b) { const int e = t + NT, a = e % HX, c = e / HX; o2b = (int)(wrapc(ox + a - 2, nx) + nx * wrapc(oy + c - 2, ny)); }
-  // own halo-1 point
-  const bool act = t < S1;
-  const int fa = t % GX, fb = t / GX;
-  const int o1 = act ? (int)(wrapc(ox + fa - 1, nx) + nx * wrapc(oy + fb - 1, ny)) : 0;
-  const int e2 = act ? (fa + 1) + HX * (fb + 1) : HX + 1;
-  const bool inner = act && fa >= 1 && fa <= TX && fb >= 1 && fb <= TY && (ox + fa - 1) < nx && (oy + fb - 1) < ny;
-  const bool has_pp = S.xpp != nullptr;
-  const int oo = (int)((ox + fa - 1) + nx * (oy + fb - 1));
-
-  auto znext = [&](long long zo) { const long long n = zo + nxy; return n == nz * nxy ? 0 : n; };
-  long long zoX = wrapc(z0 - 2, nz) * nxy;  // element offset of the next x/kappa plane to copy
-  auto issue_x = [&](int slot) {
-    double *dx = sX + slot * S2, *dk = sK + slot * S2;
-    const double *gx = S.xprev + zoX, *gk = P.kappa + zoX;
-    if (h2a) { cp_async8(dx + t, gx + o2a); cp_async8(dk + t, gk + o2a); }
-    if (h2b) { cp_async8(dx + t + NT, gx + o2b); cp_async8(dk + t + NT, gk + o2b); }
-    zoX = znext(zoX);
-  };
-  long long zoF = wrapc(z0 - 1, nz) * nxy;  // element offset of the next operand plane
-  auto load_ops = [&](Ops<PM> &o) {
-    o.pp = 0.0;
-    if (act) {
-      if (has_pp) o.pp = __ldg(S.xpp + zoF + o1);
-#pragma unroll
-      for (int c = 0; c < PM; c++) o.b[c] = c < p ? __ldg(S.B[c] + zoF + o1) : 0.0;
-    }
-    zoF = znext(zoF);
-  };
-
-  issue_x(0);
-  issue_x(1);
-  cp_async_commit();
-  issue_x(2);
-  cp_async_commit();
-  issue_x(3);
-  cp_async_commit();
-  Ops<PM> opA, opB;
-  load_ops(opA);  // plane i = 0
-  load_ops(opB);  // plane i = 1
-  cp_async_wait<D - 1>();
-  __syncthreads();
-  double xo_m = sX[0 * S2 + e2], xo_0 = sX[1 * S2 + e2];
-  double ko_m = sK[0 * S2 + e2], ko_0 = sK[1 * S2 + e2];
-  double gW = 0.0, gE = 0.0, gS = 0.0, gN = 0.0, gD = 0.0, gU = 0.0;  // face sums at (x, y, zout)
-  double xk_m = 0.0, xk_0 = 0.0, bt_0 = 0.0;
-  double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0, v4 = 0.0;
-  long long zo_out = z0 * nxy;
-
-  auto body = [&](const int i, Ops<PM> &op) {
-    cp_async_wait<D - 1>();
-    __syncthreads();  // the one barrier per plane
-    if (i + 2 + D <= nzc + 3) issue_x((i + 2 + D) & 3);
-    cp_async_commit();
-    const double *X0 = sX + ((i + 1) & 3) * S2, *K0 = sK + ((i + 1) & 3) * S2;
-    const double xo_p = sX[((i + 2) & 3) * S2 + e2], ko_p = sK[((i + 2) & 3) * S2 + e2];
-    // formation (Alg. 2 l.4-10 of iteration k-1) at the own point of plane zf
-    const double fW = ko_0 + K0[e2 - 1], fE = ko_0 + K0[e2 + 1], fS = ko_0 + K0[e2 - HX],
-                 fN = ko_0 + K0[e2 + HX], fD = ko_0 + ko_m, fU = ko_0 + ko_p;
-    double ax = fW * (X0[e2 - 1] - xo_0);
-    double ay = fE * (X0[e2 + 1] - xo_0);
-    ax = fma(fS, X0[e2 - HX] - xo_0, ax);
-    ay = fma(fN, X0[e2 + HX] - xo_0, ay);
-    ax = fma(fD, xo_m - xo_0, ax);
-    ay = fma(fU, xo_p - xo_0, ay);
-    double bp = 0.0, bc = 0.0;
-#pragma unroll
-    for (int c = 0; c < PM; c++) {
-      bp = fma(op.b[c], btp[c], bp);
-      bc = fma(op.b[c], btc[c], bc);
-    }
-    const double xk_p = a0 * fma(ax + ay, hh, bp) - a1 * xo_0 - a2 * op.pp;
-    if (i + 2 <= nzc + 1) load_ops(op);  // operands of plane i + 2 (same buffer)
-    if (act) sXK[(i & 1) * S1 + t] = xk_p;
-    // output plane zf - 1: x_k of that plane was published before this barrier
-    if (i >= 2 && inner) {
-      const double *XK0 = sXK + ((i + 1) & 1) * S1;
-      double rx = gW * (XK0[t - 1] - xk_0);
-      double ry = gE * (XK0[t + 1] - xk_0);
-      rx = fma(gS, XK0[t - GX] - xk_0, rx);
-      ry = fma(gN, XK0[t + GX] - xk_0, ry);
-      rx = fma(gD, xk_m - xk_0, rx);
-      ry = fma(gU, xk_p - xk_0, ry);
-      const double r = fma(rx + ry, hh, bt_0);
-      v0 = fma(xk_0, xk_0, v0);
-      v1 = fma(xo_m, xk_0, v1);
-      v2 = fma(xo_m, r, v2);
-      v3 = fma(xk_0, r, v3);
-      v4 = fma(r, r, v4);
-      if (S.xout) S.xout[zo_out + oo] = xk_0;
-    }
-    if (i >= 2) zo_out += nxy;
-    xo_m = xo_0; xo_0 = xo_p;
-    ko_m = ko_0; ko_0 = ko_p;
-    gW = fW; gE = fE; gS = fS; gN = fN; gD = fD; gU = fU;
-    xk_m = xk_0; xk_0 = xk_p; bt_0 = bc;
-  };
-  for (int i = 0; i <= nzc + 1; i += 2) {
-    body(i, opA);
-    if (i + 1 <= nzc + 1) body(i + 1, opB);
-  }
-  cp_async_wait<0>();
-  double v[NDOT] = {v0, v1, v2, v3, v4};
-  pass_epilogue(P, S.k, v);
-}
 
 // ---------------------------------------------------------------------------
 // 3D variable-kappa pass, LAZY form (SURVEY 8(a) a3 "lazy normalisation"):
