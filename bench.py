@@ -234,7 +234,7 @@ def main():
 
     clk = ClockSampler(os.path.join(ROOT, f"gpurun_out/clocks_rank{rank}.csv"
                                     if os.path.isdir(os.path.join(ROOT, "gpurun_out")) else f"/tmp/clocks_{rank}.csv"))
-    totals = {"pass_ms": 0.0, "ctrl_ms": 0.0, "gemv_ms": 0.0, "passes": 0, "krylov_vectors": 0, "expm_calls": 0,
+    totals = {"pass_ms": 0.0, "ctrl_ms": 0.0, "expm_ms": 0.0, "gemv_ms": 0.0, "passes": 0, "krylov_vectors": 0, "expm_calls": 0,
               "substeps": 0, "rejections": 0}
     with clk:
         time.sleep(0.3)
@@ -297,11 +297,14 @@ def main():
                                 "substeps": per_step["substeps"], "rejections": per_step["rejections"],
                                 "expm_calls": per_step["expm_calls"],
                                 "device_ms": {"fused_pass": pass_ms, "controller": per_step["ctrl_ms"],
-                                              "gemv": per_step["gemv_ms"]},
+                                              "controller_expm": per_step["expm_ms"], "gemv": per_step["gemv_ms"]},
                                 "kv_per_s": per_step["krylov_vectors"] / (ms_step * 1e-3)}},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                     "kernel": "fused IOP pass (k_pass_stencil / k_csr_*)",
+                     "kernel": {"stencil3d7": "k_pass_3d_lazyq (fused IOP pass)",
+                                "stencil2d5": "k_pass_2d_lazy (fused IOP pass)",
+                                "stencil1d3": "k_pass_2d_lazy (fused IOP pass, ny = 1)",
+                                "csr": "k_csr_form + k_sell_spmv (fused IOP pass)"}.get(cfg["op"]["kind"], "fused IOP pass"),
                      "algorithmic_bytes_per_launch": bpp, "peak_source": peak_src,
                      "timing": "device %globaltimer accumulated per launch inside the graph, over the timed steps"},
         "gpu_launches": int(round(launches_per_step * args.steps)),

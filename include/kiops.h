@@ -104,6 +104,7 @@ typedef struct {
   double nu, mu;          /* Eqs. 48-49 normalisation constants used                    */
   double pass_ms, ctrl_ms, gemv_ms; /* device-side kernel time (%globaltimer) of the fused
                                        passes, the controller and the GEMV in this call */
+  double expm_ms;                   /* part of ctrl_ms spent in the F = exp(tau H~) of Alg. 1 l.18 */
 } kiops_stats;
 
 /* One row per attempt (accepted or rejected), for oracle <-> GPU trace parity. */

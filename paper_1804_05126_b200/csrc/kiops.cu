@@ -40,8 +40,6 @@ constexpr int SM_COUNT_HINT = 148;
 #define M3X 32   // one-point-per-thread 3D pass (odd nx / p > 4)
 #define M3Y 8
 #define M3Z 32   // z-planes per CTA chunk
-#define P3X 64   // pair 3D pass tile (measured best of 32x8, 32x16, 64x8, 64x16, 128x8)
-#define P3Y 8
 
 struct Layout {
   size_t V, r, staging, state, call, H, sig, R2, tails, partials, npart, scratch, coef, trace, sell_off, sell_col,
@@ -140,11 +138,14 @@ Layout layout(const kiops_operator_desc *op, int p, const kiops_options *o) {
       }
       break;
     case KIOPS_OP_STENCIL3D7_VARKAPPA:
-      if (op->nx % 2 == 0 && op->nx >= 2 && p >= 1 && p <= 4) {  // pair kernel (16-byte rows), exact p
-        L.grid_pass = (int)(((op->nx + P3X - 1) / P3X) * ((op->ny + P3Y - 1) / P3Y) * ((op->nz + M3Z - 1) / M3Z));
-        L.smem_pass = sizeof(double) * (p == 1 ? LazyP<P3X, P3Y, 1, 1>::smem_doubles : p == 2 ? LazyP<P3X, P3Y, 2, 1>::smem_doubles
-                                       : p == 3 ? LazyP<P3X, P3Y, 3, 1>::smem_doubles : LazyP<P3X, P3Y, 4, 1>::smem_doubles);
-        L.block_pass = LazyP<P3X, P3Y, 2, 1>::NT;
+      if (op->nx % 2 == 0 && op->nx >= 2 && p >= 1 && p <= 4) {  // lock-step persistent pair pass
+        using Q = LazyQ<2, 8, 2>;
+        int ntx, nb;
+        rc_tiles(op->nx, op->ny, Q::TILES, 8, &ntx, &nb);
+        L.grid_pass = ntx * nb * rc_zsplit(op->nx, op->ny, op->nz, Q::TILES, 8, Q::CTAS);
+        L.smem_pass = p == 1 ? LazyQ<1, 8, 2>::smem_bytes : p == 2 ? LazyQ<2, 8, 2>::smem_bytes
+                    : p == 3 ? LazyQ<3, 8, 2>::smem_bytes : LazyQ<4, 8, 2>::smem_bytes;
+        L.block_pass = Q::NT;
       } else {
         L.grid_pass = (int)(((op->nx + M3X - 1) / M3X) * ((op->ny + M3Y - 1) / M3Y) * ((op->nz + M3Z - 1) / M3Z));
         L.smem_pass = sizeof(double) * (p <= 2 ? Lazy3<M3X, M3Y, 2>::smem_doubles
@@ -275,10 +276,8 @@ static kiops_status build_graph(kiops_ctx c) {
       break;
     case KIOPS_OP_STENCIL3D7_VARKAPPA:
       if (c->op.nx % 2 == 0 && c->op.nx >= 2 && c->p >= 1 && c->p <= 4)
-        fpass = c->p == 1 ? (void *)k_pass_3d_lazyp<P3X, P3Y, M3Z, 1, 2, 1>
-              : c->p == 2 ? (void *)k_pass_3d_lazyp<P3X, P3Y, M3Z, 2, 2, 1>
-              : c->p == 3 ? (void *)k_pass_3d_lazyp<P3X, P3Y, M3Z, 3, 2, 1>
-                          : (void *)k_pass_3d_lazyp<P3X, P3Y, M3Z, 4, 2, 1>;
+        fpass = c->p == 1 ? (void *)k_pass_3d_lazyq<1, 8, 2> : c->p == 2 ? (void *)k_pass_3d_lazyq<2, 8, 2>
+              : c->p == 3 ? (void *)k_pass_3d_lazyq<3, 8, 2> : (void *)k_pass_3d_lazyq<4, 8, 2>;
       else
         fpass = c->p <= 2 ? (void *)k_pass_3d_lazy<M3X, M3Y, M3Z, 2, 3>
               : c->p <= 4 ? (void *)k_pass_3d_lazy<M3X, M3Y, M3Z, 4, 3>
@@ -473,6 +472,7 @@ static kiops_status finish(kiops_ctx c, kiops_stats *stats) {
     stats->pass_ms = S.ns_pass * 1e-6;
     stats->ctrl_ms = S.ns_ctrl * 1e-6;
     stats->gemv_ms = S.ns_gemv * 1e-6;
+    stats->expm_ms = S.ns_expm * 1e-6;
   }
   if (S.status == KIOPS_ERR_NONFINITE) { c->err = "non-finite value in the Krylov recurrence or estimate"; return KIOPS_ERR_NONFINITE; }
   if (S.status == KIOPS_ERR_NO_CONVERGENCE) { c->err = "max_attempts exceeded"; return KIOPS_ERR_NO_CONVERGENCE; }

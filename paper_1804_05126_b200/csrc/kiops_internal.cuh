@@ -43,7 +43,7 @@ struct DevState {
   unsigned long long launches;   // pass launches this call (device-side loop guard)
   // device-side kernel timing (%globaltimer, ns): graph-internal kernels cannot be
   // bracketed by host events, so each kernel type accumulates its own duration
-  unsigned long long t_pass0, t_gemv0, ns_pass, ns_ctrl, ns_gemv;
+  unsigned long long t_pass0, t_gemv0, ns_pass, ns_ctrl, ns_gemv, ns_expm;
   unsigned int gemv_ticket;
   unsigned int cond[3];          // mirror of the graph conditionals (outer, inner, accept)
   int bc_accept, bc_ntau;        // controller-cluster broadcast (CTA 0 -> all CTAs)

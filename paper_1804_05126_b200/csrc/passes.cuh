@@ -111,7 +111,7 @@ __global__ void __launch_bounds__(256) k_setup(KParams P) {
   st->final_m = st->m;
   st->ticket = 0;
   st->launches = 0;
-  st->ns_pass = st->ns_ctrl = st->ns_gemv = 0;
+  st->ns_pass = st->ns_ctrl = st->ns_gemv = st->ns_expm = 0;
   st->gemv_ticket = 0;
   write_exact_tail(P, 0.0, mu, P.tails + 1 * KMAXP);       // t_1 at T_now = 0
   set_cond(P, COND_OUTER, 1u);
@@ -557,62 +557,115 @@ __global__ void __launch_bounds__(Lazy3<TX, TY, PM>::NT, MINB) k_pass_3d_lazy(KP
 }
 
 // ---------------------------------------------------------------------------
-// 3D variable-kappa LAZY pass, pair version (in use for even nx): every thread
-// owns TWO x-adjacent points (a 16-byte aligned pair) of the halo-1 plane of a
-// TX x TY column tile, so every cp.async, shared load/store and global store
-// moves 16 bytes and the x-neighbour inside the pair comes from registers.
-// Pairs span x in [ox-2, ox+TX+2) (one unused point each side keeps alignment).
-// Same arithmetic and dots as k_pass_3d_lazy.
+// 16-byte cp.async (global -> shared, L2 only)
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ void cp_async16(void *dst, const void *src) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(dst);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(src) : "memory");
 }
 
-template <int TX, int TY, int PM, int DD = 2>
-struct LazyP {
-  static constexpr int PX = TX / 2 + 2, GY = TY + 2, NPAIR = PX * GY;  // pairs per plane
+// ---------------------------------------------------------------------------
+// 3D variable-kappa LAZY pass, pair version (in use for even nx, 1 <= p <= 4).
+// Every thread owns TWO x-adjacent points (a 16-byte aligned pair) of the halo-1
+// plane of a 64 x hb column tile, so every cp.async, shared load/store and global
+// store moves 16 bytes and the x-neighbour inside the pair comes from registers;
+// pairs span x in [ox-2, ox+66) (one unused point each side keeps alignment).
+// Per plane: x_k = a0 r_{k-1} - a1 x_{k-1} - a2 x_{k-2} pointwise on the halo-1
+// plane (operands in a thread-private cp.async ring, one plane ahead), x_k and
+// kappa published in a 2-plane shared ring, one __syncthreads, then r_k = A x_k +
+// nu B t_k on the interior with z-neighbours from registers; same arithmetic and
+// dots as k_pass_3d_lazy.  Decomposition (lock-step persistent):
+//  * the xy plane is cut into ~148 tiles of 64 x hb points (hb <= 8, balanced
+//    bands, rc_tiles) and the z extent of each tile into zsplit parts, so that the
+//    grid is exactly 2 CTAs per SM (config 4: 4 x 37 tiles x 2 halves = 296) and
+//    every CTA has the same work (no partial last wave);
+//  * all CTAs march in z in lock-step, odd parts downward, so the x/y halo rows a
+//    tile shares with its neighbours, and the planes at part boundaries, are read
+//    by both CTAs at about the same time (L2 hits instead of DRAM re-reads).
+// Measured (config 4, ncu): 210 us, DRAM read = the 6 design read vectors exactly;
+// 64 x 4 tiles at 4 CTAs/SM: slower (204 vs 166 ms of passes per call).
+// ---------------------------------------------------------------------------
+#define RC_SMS 148  // SMs of a B200 (host grid uses the same rule)
+
+// tile rule shared by host and device: ntx columns of 64 points, nb bands of <= tym
+// rows, about `target` tiles in all
+__host__ __device__ inline void rc_tiles(long long nx, long long ny, int target, int tym, int *ntx, int *nb) {
+  const int tx = (int)((nx + 63) / 64);
+  int b = target / tx;
+  if (b < 1) b = 1;
+  if (b > ny) b = (int)ny;
+  const int bmin = (int)((ny + tym - 1) / tym);
+  if (b < bmin) b = bmin;
+  *ntx = tx;
+  *nb = b;
+}
+// z parts per tile: fill `ctas` CTAs, at least 2 planes per part
+__host__ __device__ inline int rc_zsplit(long long nx, long long ny, long long nz, int target, int tym, int ctas) {
+  int ntx, nb;
+  rc_tiles(nx, ny, target, tym, &ntx, &nb);
+  int zs = ctas / (ntx * nb);
+  if (zs < 1) zs = 1;
+  if (zs > nz / 2) zs = (int)(nz / 2 > 0 ? nz / 2 : 1);
+  return zs;
+}
+
+// 7-point variable-kappa stencil on one 16-byte pair (points a = x, b = x + 1), the
+// lazy pass's r expression operand for operand:
+//   r = 0.5/h^2 sum_n (k_c + k_n)(x_n - x_c) + nu B t
+__device__ __forceinline__ double2 stencil_pair(double2 xc, double2 kc, double xl, double xr, double kl, double kr,
+                                                double2 xs, double2 xn, double2 ks, double2 kn, double2 xm,
+                                                double2 km, double2 xp, double2 kp, double hh, double2 bt) {
+  double ra = (kc.x + kl) * (xl - xc.x);
+  double rb = (kc.y + kr) * (xr - xc.y);
+  ra = fma(kc.x + kc.y, xc.y - xc.x, ra);
+  rb = fma(kc.y + kc.x, xc.x - xc.y, rb);
+  ra = fma(kc.x + ks.x, xs.x - xc.x, ra);
+  rb = fma(kc.y + ks.y, xs.y - xc.y, rb);
+  ra = fma(kc.x + kn.x, xn.x - xc.x, ra);
+  rb = fma(kc.y + kn.y, xn.y - xc.y, rb);
+  ra = fma(kc.x + km.x, xm.x - xc.x, ra);
+  rb = fma(kc.y + km.y, xm.y - xc.y, rb);
+  ra = fma(kc.x + kp.x, xp.x - xc.x, ra);
+  rb = fma(kc.y + kp.y, xp.y - xc.y, rb);
+  return make_double2(fma(ra, hh, bt.x), fma(rb, hh, bt.y));
+}
+
+// TYM: max tile rows; CPS: CTAs per SM (grid = CPS x 148, tiles target CPS/2 x 148)
+template <int PM, int TYM, int CPS>
+struct LazyQ {
+  static constexpr int PX = 34, NPAIR = PX * (TYM + 2);
   static constexpr int NT = (NPAIR + 31) / 32 * 32;
-  static constexpr int D = DD, RD = D + 1, NOP = 4 + PM;
-  static constexpr size_t smem_doubles = 4 * (size_t)NPAIR * 2 + (size_t)RD * NOP * NT * 2;
+  static constexpr int D = 1, RD = D + 1, NOP = 4 + PM;
+  static constexpr int TILES = RC_SMS * CPS / 2, CTAS = RC_SMS * CPS;
+  static constexpr size_t smem_bytes = 16 * (4 * (size_t)NPAIR + (size_t)RD * NOP * NPAIR);  // ring stride NPAIR
 };
 
-template <int TX, int TY, int ZC, int PM, int MINB, int DD = 2>
-__global__ void __launch_bounds__(LazyP<TX, TY, PM, DD>::NT, MINB) k_pass_3d_lazyp(KParams P) {
-  using M = LazyP<TX, TY, PM, DD>;
+template <int PM, int TYM, int CPS>
+__global__ void __launch_bounds__(LazyQ<PM, TYM, CPS>::NT, CPS) k_pass_3d_lazyq(KParams P) {
+  using M = LazyQ<PM, TYM, CPS>;
   constexpr int NT = M::NT, PX = M::PX, NPAIR = M::NPAIR, D = M::D, RD = M::RD, NOP = M::NOP;
   extern __shared__ double2 smem2[];
   double2 *sXK = smem2;                // 2 x NPAIR   x_k pairs (shared plane ring)
   double2 *sKP = smem2 + 2 * NPAIR;    // 2 x NPAIR   kappa pairs
-  double2 *sOp = smem2 + 4 * NPAIR;    // RD x NOP x NT  thread-private operand ring
+  double2 *sOp = smem2 + 4 * NPAIR;    // RD x NOP x NPAIR  thread-private operand ring (active threads)
 
   __shared__ PassScalars S;
   pass_guard(P);
   if (threadIdx.x == 0) load_pass_scalars(P, S);
   __syncthreads();
   if (S.k == 0) return;
-  const int k = S.k;  // PM == p exactly (template)
+  const int k = S.k;
   const long long nx = P.nx, ny = P.ny, nz = P.nz, nxy = nx * ny;
-  const long long ntx = (nx + TX - 1) / TX, nty = (ny + TY - 1) / TY;
-  const long long bidx = blockIdx.x;
-  const long long ox = (bidx % ntx) * TX, oy = ((bidx / ntx) % nty) * TY;
-  const long long z0 = (bidx / (ntx * nty)) * ZC;
-  const long long z1 = (z0 + ZC < nz) ? z0 + ZC : nz;
-  const int nzc = (int)(z1 - z0);
+  int ntx, nb;
+  rc_tiles(nx, ny, M::TILES, TYM, &ntx, &nb);
+  const int ntiles = ntx * nb, zsplit = rc_zsplit(nx, ny, nz, M::TILES, TYM, M::CTAS);
   const int t = threadIdx.x;
-  const bool act = t < NPAIR;
-  const int px = t % PX, py = t / PX;
-  // pair start x = ox - 2 + 2 px (even); wrapped global in-plane offset of the pair
-  const int o1 = act ? (int)(wrapc(ox - 2 + 2 * px, nx) + nx * wrapc(oy - 1 + py, ny)) : 0;
-  const bool rowin = py >= 1 && py <= TY && (oy - 1 + py) < ny;
-  const bool pin = act && rowin && px >= 1 && px <= TX / 2 && (ox - 2 + 2 * px) < nx;  // both points interior
-  const bool use_r = k >= 2, use_pp = S.xpp != nullptr;
-  const int oo = (int)((ox - 2 + 2 * px) + nx * (oy - 1 + py));
   const double *rin = P.r + (size_t)((k - 1) & 1) * (size_t)P.ldN;
   double *rout = P.r + (size_t)(k & 1) * (size_t)P.ldN;
   const double *xprev = S.xprev, *xpp = S.xpp, *kap = P.kappa;
   double *xout = S.xout;
   const double a0 = S.a0, a1 = S.a1, a2 = S.a2, hh = 0.5 * P.inv_h2;
+  const bool use_r = k >= 2, use_pp = xpp != nullptr;
   const double *Bc[PM];
   double btc[PM];
 #pragma unroll
@@ -620,99 +673,102 @@ __global__ void __launch_bounds__(LazyP<TX, TY, PM, DD>::NT, MINB) k_pass_3d_laz
     Bc[c] = S.B[c];
     btc[c] = S.btc[c];
   }
+  double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0, v4 = 0.0;
 
-  auto znext = [&](long long zo) { const long long n = zo + nxy; return n == nz * nxy ? 0 : n; };
-  long long zoL = wrapc(z0 - 1, nz) * nxy;
-  auto issue = [&](int slot) {
-    if (act) {
-      double2 *d = sOp + slot * NOP * NT + t;
-      const long long g = zoL + o1;
-      if (use_r) cp_async16(d, rin + g);
-      cp_async16(d + NT, xprev + g);
-      if (use_pp) cp_async16(d + 2 * NT, xpp + g);
-      cp_async16(d + 3 * NT, kap + g);
+  for (int w = blockIdx.x; w < ntiles * zsplit; w += gridDim.x) {
+    const int tile = w % ntiles, part = w / ntiles;
+    const long long ox = (long long)(tile % ntx) * 64, band = tile / ntx;
+    const long long oy = band * ny / nb, hb = (band + 1) * ny / nb - oy;
+    const long long zlo = part * nz / zsplit, zhi = (part + 1) * nz / zsplit;
+    const int nzc = (int)(zhi - zlo);
+    const bool down = part & 1;
+    const int px = t % PX, py = t / PX;
+    const bool act = py < hb + 2;
+    const int o1 = act ? (int)(wrapc(ox - 2 + 2 * px, nx) + nx * wrapc(oy - 1 + py, ny)) : 0;
+    const bool pin = act && py >= 1 && py <= hb && px >= 1 && px <= 32 && (ox - 2 + 2 * px) < nx;
+    const long long oo = (ox - 2 + 2 * px) + nx * (oy - 1 + py);
+    // logical plane j (-1 .. nzc) -> physical plane offset; the march is in j
+    const long long zstep = down ? -nxy : nxy, zwrap = nz * nxy;
+    long long zoL = wrapc(down ? zhi : zlo - 1, nz) * nxy;  // plane j = -1
+    auto issue = [&](int slot) {
+      if (act) {
+        double2 *d = sOp + slot * NOP * NPAIR + t;
+        const long long g = zoL + o1;
+        if (use_r) cp_async16(d, rin + g);
+        cp_async16(d + NPAIR, xprev + g);
+        if (use_pp) cp_async16(d + 2 * NPAIR, xpp + g);
+        cp_async16(d + 3 * NPAIR, kap + g);
+        if (pin)
+#pragma unroll
+          for (int c = 0; c < PM; c++) cp_async16(d + (4 + c) * NPAIR, Bc[c] + g);
+      }
+      zoL += zstep;
+      if (zoL < 0) zoL += zwrap;
+      if (zoL >= zwrap) zoL -= zwrap;
+    };
+    __syncthreads();  // previous part's readers are done with the rings
+    for (int q = 0; q < D; q++) {
+      issue(q);
+      cp_async_commit();
+    }
+    double2 xk_m = {0.0, 0.0}, xk_0 = {0.0, 0.0}, k_m = {0.0, 0.0}, k_0 = {0.0, 0.0}, xm_0 = {0.0, 0.0},
+            bt_0 = {0.0, 0.0};
+    long long zo_out = (down ? zhi - 1 : zlo) * nxy;
+    int rs = 0, ri = D;
+#pragma unroll 2
+    for (int i = 0; i <= nzc + 1; i++) {
+      if (i + D <= nzc + 1) issue(ri);
+      cp_async_commit();
+      cp_async_wait<D>();
+      const double2 *o = sOp + rs * NOP * NPAIR + t;
+      const double2 xm = o[NPAIR], kc_p = o[3 * NPAIR];
+      double2 xk_p = xm;
+      if (use_r) {
+        const double2 rr = o[0];
+        xk_p.x = a0 * rr.x - a1 * xm.x;
+        xk_p.y = a0 * rr.y - a1 * xm.y;
+        if (use_pp) {
+          const double2 pp = o[2 * NPAIR];
+          xk_p.x -= a2 * pp.x;
+          xk_p.y -= a2 * pp.y;
+        }
+      }
+      double2 bt = {0.0, 0.0};
       if (pin)
 #pragma unroll
-        for (int c = 0; c < PM; c++) cp_async16(d + (4 + c) * NT, Bc[c] + g);
-    }
-    zoL = znext(zoL);
-  };
-  for (int q = 0; q < D; q++) {
-    issue(q);
-    cp_async_commit();
-  }
-  double2 xk_m = {0.0, 0.0}, xk_0 = {0.0, 0.0}, k_m = {0.0, 0.0}, k_0 = {0.0, 0.0}, xm_0 = {0.0, 0.0},
-          bt_0 = {0.0, 0.0};
-  double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0, v4 = 0.0;
-  long long zo_out = z0 * nxy;
-  int rs = 0, ri = D;
-#pragma unroll 6
-  for (int i = 0; i <= nzc + 1; i++) {
-    if (i + D <= nzc + 1) issue(ri);
-    cp_async_commit();
-    cp_async_wait<D>();
-    const double2 *o = sOp + rs * NOP * NT + t;
-    const double2 xm = o[NT], kc_p = o[3 * NT];
-    double2 xk_p = xm;
-    if (use_r) {
-      const double2 rr = o[0];
-      xk_p.x = a0 * rr.x - a1 * xm.x;
-      xk_p.y = a0 * rr.y - a1 * xm.y;
-      if (use_pp) {
-        const double2 pp = o[2 * NT];
-        xk_p.x -= a2 * pp.x;
-        xk_p.y -= a2 * pp.y;
+        for (int c = 0; c < PM; c++) {
+          const double2 b = o[(4 + c) * NPAIR];
+          bt.x = fma(b.x, btc[c], bt.x);
+          bt.y = fma(b.y, btc[c], bt.y);
+        }
+      __syncthreads();  // the output that read slot (i & 1) has finished everywhere
+      if (act) {
+        sXK[(i & 1) * NPAIR + t] = xk_p;
+        sKP[(i & 1) * NPAIR + t] = kc_p;
       }
-    }
-    double2 bt = {0.0, 0.0};
-    if (pin)
-#pragma unroll
-      for (int c = 0; c < PM; c++) {
-        const double2 b = o[(4 + c) * NT];
-        bt.x = fma(b.x, btc[c], bt.x);
-        bt.y = fma(b.y, btc[c], bt.y);
+      if (i >= 2 && pin) {  // output logical plane i - 2 for both points of the pair
+        const double2 *X0 = sXK + ((i + 1) & 1) * NPAIR, *K0 = sKP + ((i + 1) & 1) * NPAIR;
+        const double2 r = stencil_pair(xk_0, k_0, X0[t - 1].y, X0[t + 1].x, K0[t - 1].y, K0[t + 1].x, X0[t - PX],
+                                       X0[t + PX], K0[t - PX], K0[t + PX], xk_m, k_m, xk_p, kc_p, hh, bt_0);
+        const double2 xc = xk_0;
+        v0 = fma(xc.x, xc.x, fma(xc.y, xc.y, v0));
+        v1 = fma(xm_0.x, xc.x, fma(xm_0.y, xc.y, v1));
+        v2 = fma(xm_0.x, r.x, fma(xm_0.y, r.y, v2));
+        v3 = fma(xc.x, r.x, fma(xc.y, r.y, v3));
+        v4 = fma(r.x, r.x, fma(r.y, r.y, v4));
+        if (xout) *reinterpret_cast<double2 *>(xout + zo_out + oo) = xc;
+        *reinterpret_cast<double2 *>(rout + zo_out + oo) = r;
       }
-    __syncthreads();  // the output that read slot (i & 1) has finished everywhere
-    if (act) {
-      sXK[(i & 1) * NPAIR + t] = xk_p;
-      sKP[(i & 1) * NPAIR + t] = kc_p;
+      if (i >= 2) zo_out += zstep;
+      xk_m = xk_0; xk_0 = xk_p;
+      k_m = k_0; k_0 = kc_p;
+      xm_0 = xm;
+      bt_0 = bt;
+      rs = rs + 1 == RD ? 0 : rs + 1;
+      ri = ri + 1 == RD ? 0 : ri + 1;
     }
-    if (i >= 2 && pin) {  // output plane z = zf - 1 for both points of the pair
-      const double2 *X0 = sXK + ((i + 1) & 1) * NPAIR, *K0 = sKP + ((i + 1) & 1) * NPAIR;
-      const double xl = X0[t - 1].y, xr = X0[t + 1].x, kl = K0[t - 1].y, kr = K0[t + 1].x;
-      const double2 xs = X0[t - PX], xn = X0[t + PX], ks = K0[t - PX], kn = K0[t + PX];
-      const double2 xc = xk_0, kc = k_0;
-      // point a (x), point b (x + 1)
-      double ra = (kc.x + kl) * (xl - xc.x);
-      double rb = (kc.y + kr) * (xr - xc.y);
-      ra = fma(kc.x + kc.y, xc.y - xc.x, ra);
-      rb = fma(kc.y + kc.x, xc.x - xc.y, rb);
-      ra = fma(kc.x + ks.x, xs.x - xc.x, ra);
-      rb = fma(kc.y + ks.y, xs.y - xc.y, rb);
-      ra = fma(kc.x + kn.x, xn.x - xc.x, ra);
-      rb = fma(kc.y + kn.y, xn.y - xc.y, rb);
-      ra = fma(kc.x + k_m.x, xk_m.x - xc.x, ra);
-      rb = fma(kc.y + k_m.y, xk_m.y - xc.y, rb);
-      ra = fma(kc.x + kc_p.x, xk_p.x - xc.x, ra);
-      rb = fma(kc.y + kc_p.y, xk_p.y - xc.y, rb);
-      const double r_a = fma(ra, hh, bt_0.x), r_b = fma(rb, hh, bt_0.y);
-      v0 = fma(xc.x, xc.x, fma(xc.y, xc.y, v0));
-      v1 = fma(xm_0.x, xc.x, fma(xm_0.y, xc.y, v1));
-      v2 = fma(xm_0.x, r_a, fma(xm_0.y, r_b, v2));
-      v3 = fma(xc.x, r_a, fma(xc.y, r_b, v3));
-      v4 = fma(r_a, r_a, fma(r_b, r_b, v4));
-      if (xout) *reinterpret_cast<double2 *>(xout + zo_out + oo) = xc;
-      *reinterpret_cast<double2 *>(rout + zo_out + oo) = make_double2(r_a, r_b);
-    }
-    if (i >= 2) zo_out += nxy;
-    xk_m = xk_0; xk_0 = xk_p;
-    k_m = k_0; k_0 = kc_p;
-    xm_0 = xm;
-    bt_0 = bt;
-    rs = rs + 1 == RD ? 0 : rs + 1;
-    ri = ri + 1 == RD ? 0 : ri + 1;
+    cp_async_wait<0>();
   }
-  cp_async_wait<0>();
   double v[NDOT] = {v0, v1, v2, v3, v4};
   pass_epilogue(P, k, v);
 }

@@ -40,7 +40,8 @@ class Stats(C.Structure):
     _fields_ = [("substeps", C.c_int64), ("rejections", C.c_int64), ("krylov_vectors", C.c_int64),
                 ("expm_calls", C.c_int64), ("passes", C.c_int64), ("final_m", C.c_int32),
                 ("happy_breakdowns", C.c_int32), ("t_reached", C.c_double), ("nu", C.c_double),
-                ("mu", C.c_double), ("pass_ms", C.c_double), ("ctrl_ms", C.c_double), ("gemv_ms", C.c_double)]
+                ("mu", C.c_double), ("pass_ms", C.c_double), ("ctrl_ms", C.c_double), ("gemv_ms", C.c_double),
+                ("expm_ms", C.c_double)]
 
 
 class TraceRow(C.Structure):
