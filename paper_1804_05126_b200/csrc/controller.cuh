@@ -198,7 +198,7 @@ __device__ int cl_solve(int n, const double *Qg, double *R, double *LUg, int *pe
 // ---------------------------------------------------------------------------
 // Storage / synchronisation policies for the Pade exponential:
 //  * ClusterBk: matrices in global scratch (ld = LDH), work split over the cluster;
-//  * SmemBk:    n <= SMALL_N, every matrix in ONE CTA's shared memory (ld = n),
+//  * SmemBk:    n <= SMALL_N, every matrix in ONE CTA's shared memory (ld = SM_LD),
 //               __syncthreads only (used by CTA 0 alone for the small projected
 //               matrices of configs 1-3, where cluster barriers would dominate).
 // ---------------------------------------------------------------------------
@@ -219,34 +219,71 @@ struct ClusterBk {
   }
 };
 
+// Single-CTA policy (n <= SMALL_N): column-major matrices with leading dimension
+// SM_LD = 52 (= 4 mod 16: the m8n8k4 fragment loads below are bank-conflict free),
+// zero-padded to NP = n rounded up to 8 (products of zero-padded operands keep the
+// padding zero, so the elementwise steps may stay on the n x n part).
+#define SM_LD 52
+__device__ __forceinline__ void dmma_8x8x4(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};\n"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
 struct SmemBk {
-  double *base;   // 10 matrices of n x n (ld = n) + a reduction scratch
+  double *base;   // 10 matrices of SM_LD x SMALL_N (ld = SM_LD) + reduction scratch
   int n_;
-  __device__ int ld() const { return n_; }
-  __device__ double *mat(int i) const { return base + (size_t)i * n_ * n_; }
+  __device__ int ld() const { return SM_LD; }
+  __device__ double *mat(int i) const { return base + (size_t)i * SM_LD * SMALL_N; }
   __device__ int gid() const { return threadIdx.x; }
   __device__ int gsz() const { return blockDim.x; }
   __device__ void sync() const { __syncthreads(); }
+  // zero the 10 matrices (padding included); call before the first use for this n
+  __device__ void clear() const {
+    for (int e = threadIdx.x; e < 10 * SM_LD * SMALL_N; e += blockDim.x) base[e] = 0.0;
+    __syncthreads();
+  }
+  // C = A B on the FP64 tensor cores: one warp per 8 x 8 output tile (up to 3 tiles
+  // per warp interleaved), k in steps of 4.  Fragments (PTX m8n8k4 .f64): A row
+  // g = lane/4, col t = lane%4; B row t, col g; C row g, cols 2t, 2t+1.
   __device__ void matmul(int n, const double *A, const double *B, double *C) const {
-    for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
-      const int i = e % n, j = e / n;
-      double s0 = 0.0, s1 = 0.0;
-      int k = 0;
-      for (; k + 1 < n; k += 2) {
-        s0 = fma(A[i + n * k], B[k + n * j], s0);
-        s1 = fma(A[i + n * (k + 1)], B[k + 1 + n * j], s1);
+    const int np = (n + 7) & ~7, nt = np >> 3, ntile = nt * nt;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int g = lane >> 2, tq = lane & 3;
+    for (int t0 = warp; t0 < ntile; t0 += 3 * nw) {
+      double c[3][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+      int ti[3], tj[3];
+      bool on[3];
+#pragma unroll
+      for (int u = 0; u < 3; u++) {
+        const int tt = t0 + u * nw;
+        on[u] = tt < ntile;
+        ti[u] = on[u] ? (tt % nt) * 8 : 0;
+        tj[u] = on[u] ? (tt / nt) * 8 : 0;
       }
-      if (k < n) s0 = fma(A[i + n * k], B[k + n * j], s0);
-      C[e] = s0 + s1;
+      for (int k0 = 0; k0 < np; k0 += 4) {
+#pragma unroll
+        for (int u = 0; u < 3; u++)
+          if (on[u]) {
+            const double a = A[(ti[u] + g) + SM_LD * (k0 + tq)];
+            const double b = B[(k0 + tq) + SM_LD * (tj[u] + g)];
+            dmma_8x8x4(c[u], a, b);
+          }
+      }
+#pragma unroll
+      for (int u = 0; u < 3; u++)
+        if (on[u]) {
+          C[(ti[u] + g) + SM_LD * (tj[u] + 2 * tq)] = c[u][0];
+          C[(ti[u] + g) + SM_LD * (tj[u] + 2 * tq + 1)] = c[u][1];
+        }
     }
     __syncthreads();
   }
   __device__ double norm1(int n, const double *A) const {
-    double *red = base + 10 * (size_t)n_ * n_;
+    double *red = base + 10 * (size_t)SM_LD * SMALL_N;
     double best = 0.0;
     for (int j = threadIdx.x; j < n; j += blockDim.x) {
       double s = 0.0;
-      for (int i = 0; i < n; i++) s += fabs(A[i + n * j]);
+      for (int i = 0; i < n; i++) s += fabs(A[i + SM_LD * j]);
       best = (s > best || s != s) ? s : best;
     }
     for (int o = 16; o > 0; o >>= 1) {
@@ -267,62 +304,129 @@ struct SmemBk {
   }
   // Q X = R in place (R <- X): Gaussian elimination with partial pivoting (first
   // maximal |pivot|) applied to the right-hand sides, then back substitution; Q is
-  // destroyed.  Multipliers are scaled by one reciprocal per pivot (measured faster
-  // than a per-element division and than a one-warp variant).  Returns 0 or -1.
+  // destroyed.  Static column ownership: warp c % nw owns column c of Q and of R, so
+  // the row swap and the update of a column need only __syncwarp.  Step k: the
+  // owner of column k has published the pivot row, 1/pivot and the multipliers
+  // (in place below the diagonal); after one __syncthreads every warp swaps rows
+  // k <-> pv in its columns and applies the multipliers, the owner of column k+1
+  // first, which then searches step k+1's pivot right away (look-ahead).
+  // Returns 0 or -1 (zero pivot), all threads.
   __device__ int solve(int n, double *Q, double *R) const {
-    __shared__ int s_piv, s_bad;
+    __shared__ int s_bad, s_piv[SMALL_N];
+    __shared__ double s_rd[SMALL_N];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     if (threadIdx.x == 0) s_bad = 0;
+    // pivot of step k on column k (up to date), by its owner warp.  First maximal
+    // |C[r]|, r >= k: |x| as a non-negative double orders like its bit pattern, so
+    // the max is two 32-bit warp reductions (high word, then low word among the
+    // ties) and the first row among equal maxima comes from two ballots.
+    auto pivot = [&](int k) {
+      double *C = Q + SM_LD * k;
+      const int ra = k + lane, rb = ra + 32;
+      const double va = ra < n ? fabs(C[ra]) : -1.0, vb = rb < n ? fabs(C[rb]) : -1.0;
+      const bool useb = vb > va;  // (equal: the lower row ra wins)
+      const double v = useb ? vb : va;
+      const unsigned long long bits = v >= 0.0 ? (unsigned long long)__double_as_longlong(v) : 0ull;
+      const unsigned hi = (unsigned)(bits >> 32), lo = (unsigned)bits;
+      const unsigned mhi = __reduce_max_sync(0xffffffffu, v >= 0.0 ? hi : 0u);
+      const bool onhi = v >= 0.0 && hi == mhi;
+      const unsigned mlo = __reduce_max_sync(0xffffffffu, onhi ? lo : 0u);
+      const bool top = onhi && lo == mlo;
+      const unsigned bA = __ballot_sync(0xffffffffu, top && !useb), bB = __ballot_sync(0xffffffffu, top && useb);
+      const int bi = bA ? k + __ffs(bA) - 1 : k + 32 + __ffs(bB) - 1;
+      const double best = __longlong_as_double((long long)(((unsigned long long)mhi << 32) | mlo));
+      if (!(best > 0.0) || (bA == 0u && bB == 0u)) {
+        if (lane == 0) s_bad = 1;
+        return;
+      }
+      const double piv = C[bi], ck = C[k];
+      __syncwarp();
+      if (lane == 0) { C[bi] = ck; C[k] = piv; }  // swap rows k and bi of column k
+      const double rp = __drcp_rn(piv);
+      // multipliers l_r = C'[r] / piv (C'[bi] = ck), written in place below the diagonal
+      if (ra > k && ra < n) C[ra] = (ra == bi ? ck : C[ra]) * rp;
+      if (rb < n) C[rb] = (rb == bi ? ck : C[rb]) * rp;
+      if (lane == 0) { s_piv[k] = bi; s_rd[k] = rp; }
+      __syncwarp();
+    };
+    // row swap k <-> pv and update of this warp's columns: Q columns cq + u nw
+    // (u < 3, cq + u nw < n) and R columns warp + u nw (u < 3, < n); all loads, one
+    // __syncwarp, all stores.  n <= SMALL_N = 48 = 3 nw.
+    auto update = [&](int cq, bool with_r, int k, int pv, double l0, double l1) {
+      const int r0 = k + 1 + lane, r1 = r0 + 32;
+      double xk[6], x0[6], x1[6];
+#pragma unroll
+      for (int u = 0; u < 6; u++) {
+        const int col = u < 3 ? cq + u * nw : warp + (u - 3) * nw;
+        const bool on = col < n && (u < 3 || with_r);
+        double *X = (u < 3 ? Q : R) + SM_LD * (on ? col : 0);
+        if (on) {
+          const double xo = X[k];
+          xk[u] = X[pv];  // new row k = old row pv, new row pv = old row k
+          x0[u] = r0 < n ? (r0 == pv ? xo : X[r0]) : 0.0;
+          x1[u] = r1 < n ? (r1 == pv ? xo : X[r1]) : 0.0;
+        }
+      }
+      __syncwarp();
+#pragma unroll
+      for (int u = 0; u < 6; u++) {
+        const int col = u < 3 ? cq + u * nw : warp + (u - 3) * nw;
+        const bool on = col < n && (u < 3 || with_r);
+        double *X = (u < 3 ? Q : R) + SM_LD * (on ? col : 0);
+        if (on) {
+          if (lane == 0) X[k] = xk[u];
+          if (r0 < n) X[r0] = x0[u] - l0 * xk[u];
+          if (r1 < n) X[r1] = x1[u] - l1 * xk[u];
+        }
+      }
+      __syncwarp();
+    };
+    if (warp == 0) pivot(0);
     __syncthreads();
     for (int k = 0; k < n; k++) {
-      if (threadIdx.x < 32) {
-        double best = -1.0;
-        int bi = n;
-        for (int r = k + threadIdx.x; r < n; r += 32) {
-          const double a = fabs(Q[r + n * k]);
-          if (a > best) { best = a; bi = r; }
-        }
-        for (int o = 16; o > 0; o >>= 1) {
-          const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-          const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-          if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
-        }
-        if (threadIdx.x == 0) { s_piv = bi; if (!(best > 0.0)) s_bad = 1; }
-      }
-      __syncthreads();
       if (s_bad) return -1;
-      const int pv = s_piv;
-      if (pv != k) {
-        for (int c = threadIdx.x; c < n; c += blockDim.x) {
-          double t = Q[k + n * c]; Q[k + n * c] = Q[pv + n * c]; Q[pv + n * c] = t;
-          t = R[k + n * c]; R[k + n * c] = R[pv + n * c]; R[pv + n * c] = t;
-        }
-        __syncthreads();
-      }
-      const int rows = n - k - 1;
-      const double rpiv = 1.0 / Q[k + n * k];
-      for (int r = k + 1 + threadIdx.x; r < n; r += blockDim.x) Q[r + n * k] *= rpiv;  // multipliers
-      __syncthreads();
-      for (int e = threadIdx.x; e < rows * (rows + n); e += blockDim.x) {
-        const int r = k + 1 + e % rows, cc = e / rows;
-        const double f = Q[r + n * k];
-        if (cc < rows) Q[r + n * (k + 1 + cc)] -= f * Q[k + n * (k + 1 + cc)];
-        else R[r + n * (cc - rows)] -= f * R[k + n * (cc - rows)];
+      const int pv = s_piv[k];
+      const int r0 = k + 1 + lane, r1 = r0 + 32;
+      const double l0 = r0 < n ? Q[r0 + SM_LD * k] : 0.0, l1 = r1 < n ? Q[r1 + SM_LD * k] : 0.0;
+      // first owned Q column > k; the owner of column k+1 updates its Q columns,
+      // searches step k+1's pivot, then updates its R columns
+      int c = k + 1 + ((warp - (k + 1)) % nw + nw) % nw;
+      if (c == k + 1 && c < n) {
+        update(c, false, k, pv, l0, l1);  // owned Q columns (k+1 among them)
+        pivot(k + 1);
+        update(n, true, k, pv, l0, l1);   // owned R columns
+      } else {
+        update(c, true, k, pv, l0, l1);
       }
       __syncthreads();
     }
-    for (int k = n - 1; k >= 0; k--) {
-      const double rd = 1.0 / Q[k + n * k];
-      for (int c = threadIdx.x; c < n; c += blockDim.x) R[k + n * c] *= rd;
-      __syncthreads();
-      for (int e = threadIdx.x; e < k * n; e += blockDim.x) {
-        const int r = e % k, c = e / k;
-        R[r + n * c] -= Q[r + n * k] * R[k + n * c];
+    // back substitution: U x = y, U = upper triangle of Q, 1/U[k,k] in s_rd
+    for (int c = warp; c < n; c += nw) {
+      double x0 = lane < n ? R[lane + SM_LD * c] : 0.0, x1 = lane + 32 < n ? R[lane + 32 + SM_LD * c] : 0.0;
+      for (int k = n - 1; k >= 0; k--) {
+        const double xk = __shfl_sync(0xffffffffu, k < 32 ? x0 : x1, k & 31) * s_rd[k];
+        if (lane == (k & 31)) { if (k < 32) x0 = xk; else x1 = xk; }
+        if (lane < k) x0 -= Q[lane + SM_LD * k] * xk;
+        if (lane + 32 < k) x1 -= Q[lane + 32 + SM_LD * k] * xk;
       }
-      __syncthreads();
+      if (lane < n) R[lane + SM_LD * c] = x0;
+      if (lane + 32 < n) R[lane + 32 + SM_LD * c] = x1;
     }
+    __syncthreads();
     return 0;
   }
 };
+
+// [m/m] Pade numerator coefficients p_m(x) = sum b_j x^j, b_j proportional to
+// (2m-j)! m! / ((2m)! j! (m-j)!), integer-scaled as tabulated by Higham (2005);
+// rows m = 3, 5, 7, 9, 13.
+__constant__ double kPade[5][14] = {
+    {120.0, 60.0, 12.0, 1.0},
+    {30240.0, 15120.0, 3360.0, 420.0, 30.0, 1.0},
+    {17297280.0, 8648640.0, 1995840.0, 277200.0, 25200.0, 1512.0, 56.0, 1.0},
+    {17643225600.0, 8821612800.0, 2075673600.0, 302702400.0, 30270240.0, 2162160.0, 110880.0, 3960.0, 90.0, 1.0},
+    {64764752532480000.0, 32382376266240000.0, 7771770303897600.0, 1187353796428800.0, 129060195264000.0,
+     10559470521600.0, 670442572800.0, 33522128640.0, 1323241920.0, 40840800.0, 960960.0, 16380.0, 182.0, 1.0}};
 
 // F = exp(scale * M) for n <= KMAXM+1: diagonal Pade approximant with scaling and
 // squaring ("[47]" = Higham 2005, Algorithm 2.3; R17).  Degree cascade
@@ -336,17 +440,12 @@ __device__ int pade_expm(const Bk &bk, int n, const double *M, double scale, dou
   const int ld = bk.ld();
   double *X = bk.mat(0), *X2 = bk.mat(1), *X4 = bk.mat(2), *X6 = bk.mat(3), *X8 = bk.mat(4), *U = bk.mat(5),
          *V = bk.mat(6), *T = bk.mat(7);
-  // [m/m] Pade numerator coefficients p_m(x) = sum b_j x^j, b_j proportional to
-  // (2m-j)! m! / ((2m)! j! (m-j)!), integer-scaled as tabulated by Higham (2005).
-  const double c3[4] = {120.0, 60.0, 12.0, 1.0};
-  const double c5[6] = {30240.0, 15120.0, 3360.0, 420.0, 30.0, 1.0};
-  const double c7[8] = {17297280.0, 8648640.0, 1995840.0, 277200.0, 25200.0, 1512.0, 56.0, 1.0};
-  const double c9[10] = {17643225600.0, 8821612800.0, 2075673600.0, 302702400.0, 30270240.0,
-                         2162160.0, 110880.0, 3960.0, 90.0, 1.0};
-  const double c13[14] = {64764752532480000.0, 32382376266240000.0, 7771770303897600.0,
-                          1187353796428800.0, 129060195264000.0, 10559470521600.0, 670442572800.0,
-                          33522128640.0, 1323241920.0, 40840800.0, 960960.0, 16380.0, 182.0, 1.0};
+  // [m/m] Pade numerator coefficients (kPade, constant memory: a per-thread local
+  // table indexed through a runtime pointer costs local-memory round trips).
   const int nn = n * n, g0 = bk.gid(), gs = bk.gsz();
+#ifdef KIOPS_PHASE_DEBUG
+  const long long c0 = clock64();
+#endif
   for (int e = g0; e < nn; e += gs) {
     const int i = e % n, j = e / n;
     X[i + (size_t)ld * j] = scale * M[i + (size_t)ld * j];
@@ -373,7 +472,7 @@ __device__ int pade_expm(const Bk &bk, int n, const double *M, double scale, dou
   if (deg >= 7) { bk.matmul(n, X2, X4, X6); mult++; }
   if (deg == 9) { bk.matmul(n, X4, X4, X8); mult++; }
   if (deg < 13) {
-    const double *b = deg == 3 ? c3 : deg == 5 ? c5 : deg == 7 ? c7 : c9;
+    const double *b = kPade[deg == 3 ? 0 : deg == 5 ? 1 : deg == 7 ? 2 : 3];
     for (int e = g0; e < nn; e += gs) {
       const int i = e % n, j = e / n;
       const size_t q = i + (size_t)ld * j;
@@ -388,7 +487,7 @@ __device__ int pade_expm(const Bk &bk, int n, const double *M, double scale, dou
     bk.sync();
     bk.matmul(n, X, T, U); mult++;   // U = X * odd part
   } else {
-    const double *b = c13;
+    const double *b = kPade[4];
     for (int e = g0; e < nn; e += gs) {
       const size_t q = (e % n) + (size_t)ld * (e / n);
       T[q] = b[13] * X6[q] + b[11] * X4[q] + b[9] * X2[q];
@@ -419,7 +518,13 @@ __device__ int pade_expm(const Bk &bk, int n, const double *M, double scale, dou
     F[q] = V[q] + U[q];
   }
   bk.sync();
+#ifdef KIOPS_PHASE_DEBUG
+  const long long c1 = clock64();
+#endif
   if (bk.solve(n, T, F) != 0) return -1;
+#ifdef KIOPS_PHASE_DEBUG
+  const long long c2 = clock64();
+#endif
   for (int k = 0; k < s; k++) {
     double *src = (k & 1) ? T : F, *dst = (k & 1) ? F : T;
     bk.matmul(n, src, src, dst); mult++;
@@ -431,6 +536,11 @@ __device__ int pade_expm(const Bk &bk, int n, const double *M, double scale, dou
     }
     bk.sync();
   }
+#ifdef KIOPS_PHASE_DEBUG
+  if (bk.gid() == 0)
+    printf("expm n=%d deg=%d s=%d mult=%d cycles: pade %lld solve %lld squaring %lld\n", n, deg, s, mult, c1 - c0,
+           c2 - c1, clock64() - c2);
+#endif
   return mult;
 }
 
@@ -444,10 +554,13 @@ __device__ int cl_expm(int n, const double *M, double scale, double *F, double *
   if (cl_rank() == 0) {
     SmemBk bk{sm, n};
     double *Ms = bk.mat(8), *Fs = bk.mat(9);
-    for (int e = threadIdx.x; e < n * n; e += blockDim.x) Ms[e] = M[(e % n) + (size_t)LDH * (e / n)];
+    bk.clear();
+    for (int j = threadIdx.x >> 6; j < n; j += blockDim.x >> 6)
+      for (int i = threadIdx.x & 63; i < n; i += 64) Ms[i + SM_LD * j] = M[i + (size_t)LDH * j];
     __syncthreads();
     const int r = pade_expm(bk, n, Ms, scale, Fs);
-    for (int e = threadIdx.x; e < n * n; e += blockDim.x) F[(e % n) + (size_t)LDH * (e / n)] = Fs[e];
+    for (int j = threadIdx.x >> 6; j < n; j += blockDim.x >> 6)
+      for (int i = threadIdx.x & 63; i < n; i += 64) F[i + (size_t)LDH * j] = Fs[i + SM_LD * j];
     if (threadIdx.x == 0) reinterpret_cast<int *>(scr + 11 * (size_t)LDH * LDH)[LDH + 1] = r;
   }
   cl_sync();

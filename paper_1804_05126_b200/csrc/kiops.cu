@@ -190,7 +190,7 @@ size_t ctrl_smem_bytes() {
   const size_t n = KMAXM + 1, cb = (n + CTRL_CL - 1) / CTRL_CL;
   const size_t solve = sizeof(double) * (n * n + n * cb);
   const size_t mm = sizeof(double) * 2 * (size_t)((n + 3) & ~3) * MM_KP;
-  const size_t small = sizeof(double) * (10 * (size_t)SMALL_N * SMALL_N + 64);  // single-CTA path
+  const size_t small = sizeof(double) * (10 * (size_t)SM_LD * SMALL_N + 64);  // single-CTA path
   return std::max(std::max(solve, mm), small);
 }
 
