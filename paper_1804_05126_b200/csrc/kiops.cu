@@ -37,6 +37,12 @@ constexpr int SM_COUNT_HINT = 148;
 #define T2D 2, 64, 16, 1
 #define T3D 3, 32, 8, 4
 #define L2YC 8
+#ifndef Q3Y
+#define Q3Y 7   // lock-step 3D pass: max tile rows (config 4 bands: 6-7 rows)
+#endif
+#ifndef Q3D
+#define Q3D 2   // planes in flight (p <= 2; p = 3, 4 use 1 to fit 2 CTAs/SM)
+#endif
 #define M3X 32   // one-point-per-thread 3D pass (odd nx / p > 4)
 #define M3Y 8
 #define M3Z 32   // z-planes per CTA chunk
@@ -139,12 +145,12 @@ Layout layout(const kiops_operator_desc *op, int p, const kiops_options *o) {
       break;
     case KIOPS_OP_STENCIL3D7_VARKAPPA:
       if (op->nx % 2 == 0 && op->nx >= 2 && p >= 1 && p <= 4) {  // lock-step persistent pair pass
-        using Q = LazyQ<2, 8, 2>;
+        using Q = LazyQ<2, Q3Y, 2>;
         int ntx, nb;
-        rc_tiles(op->nx, op->ny, Q::TILES, 8, &ntx, &nb);
-        L.grid_pass = ntx * nb * rc_zsplit(op->nx, op->ny, op->nz, Q::TILES, 8, Q::CTAS);
-        L.smem_pass = p == 1 ? LazyQ<1, 8, 2>::smem_bytes : p == 2 ? LazyQ<2, 8, 2>::smem_bytes
-                    : p == 3 ? LazyQ<3, 8, 2>::smem_bytes : LazyQ<4, 8, 2>::smem_bytes;
+        rc_tiles(op->nx, op->ny, Q::TILES, Q3Y, &ntx, &nb);
+        L.grid_pass = ntx * nb * rc_zsplit(op->nx, op->ny, op->nz, Q::TILES, Q3Y, Q::CTAS);
+        L.smem_pass = p == 1 ? LazyQ<1, Q3Y, 2, Q3D>::smem_bytes : p == 2 ? LazyQ<2, Q3Y, 2, Q3D>::smem_bytes
+                    : p == 3 ? LazyQ<3, Q3Y, 2, 1>::smem_bytes : LazyQ<4, Q3Y, 2, 1>::smem_bytes;
         L.block_pass = Q::NT;
       } else {
         L.grid_pass = (int)(((op->nx + M3X - 1) / M3X) * ((op->ny + M3Y - 1) / M3Y) * ((op->nz + M3Z - 1) / M3Z));
@@ -276,8 +282,8 @@ static kiops_status build_graph(kiops_ctx c) {
       break;
     case KIOPS_OP_STENCIL3D7_VARKAPPA:
       if (c->op.nx % 2 == 0 && c->op.nx >= 2 && c->p >= 1 && c->p <= 4)
-        fpass = c->p == 1 ? (void *)k_pass_3d_lazyq<1, 8, 2> : c->p == 2 ? (void *)k_pass_3d_lazyq<2, 8, 2>
-              : c->p == 3 ? (void *)k_pass_3d_lazyq<3, 8, 2> : (void *)k_pass_3d_lazyq<4, 8, 2>;
+        fpass = c->p == 1 ? (void *)k_pass_3d_lazyq<1, Q3Y, 2, Q3D> : c->p == 2 ? (void *)k_pass_3d_lazyq<2, Q3Y, 2, Q3D>
+              : c->p == 3 ? (void *)k_pass_3d_lazyq<3, Q3Y, 2, 1> : (void *)k_pass_3d_lazyq<4, Q3Y, 2, 1>;
       else
         fpass = c->p <= 2 ? (void *)k_pass_3d_lazy<M3X, M3Y, M3Z, 2, 3>
               : c->p <= 4 ? (void *)k_pass_3d_lazy<M3X, M3Y, M3Z, 4, 3>

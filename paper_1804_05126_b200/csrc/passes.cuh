@@ -631,23 +631,25 @@ __device__ __forceinline__ double2 stencil_pair(double2 xc, double2 kc, double x
 }
 
 // TYM: max tile rows; CPS: CTAs per SM (grid = CPS x 148, tiles target CPS/2 x 148)
-template <int PM, int TYM, int CPS>
+// DD planes in flight; the private ring slot holds r, x_{k-1}, x_{k-2}, kappa for the
+// NPAIR halo-1 pairs and B only for the NIN interior pairs.
+template <int PM, int TYM, int CPS, int DD = 1>
 struct LazyQ {
-  static constexpr int PX = 34, NPAIR = PX * (TYM + 2);
+  static constexpr int PX = 34, NPAIR = PX * (TYM + 2), NIN = 32 * TYM;
   static constexpr int NT = (NPAIR + 31) / 32 * 32;
-  static constexpr int D = 1, RD = D + 1, NOP = 4 + PM;
+  static constexpr int D = DD, RD = D + 1, SLOT = 4 * NPAIR + PM * NIN;
   static constexpr int TILES = RC_SMS * CPS / 2, CTAS = RC_SMS * CPS;
-  static constexpr size_t smem_bytes = 16 * (4 * (size_t)NPAIR + (size_t)RD * NOP * NPAIR);  // ring stride NPAIR
+  static constexpr size_t smem_bytes = 16 * (4 * (size_t)NPAIR + (size_t)RD * SLOT);
 };
 
-template <int PM, int TYM, int CPS>
-__global__ void __launch_bounds__(LazyQ<PM, TYM, CPS>::NT, CPS) k_pass_3d_lazyq(KParams P) {
-  using M = LazyQ<PM, TYM, CPS>;
-  constexpr int NT = M::NT, PX = M::PX, NPAIR = M::NPAIR, D = M::D, RD = M::RD, NOP = M::NOP;
+template <int PM, int TYM, int CPS, int DD>
+__global__ void __launch_bounds__(LazyQ<PM, TYM, CPS, DD>::NT, CPS) k_pass_3d_lazyq(KParams P) {
+  using M = LazyQ<PM, TYM, CPS, DD>;
+  constexpr int PX = M::PX, NPAIR = M::NPAIR, NIN = M::NIN, D = M::D, RD = M::RD, SLOT = M::SLOT;
   extern __shared__ double2 smem2[];
   double2 *sXK = smem2;                // 2 x NPAIR   x_k pairs (shared plane ring)
   double2 *sKP = smem2 + 2 * NPAIR;    // 2 x NPAIR   kappa pairs
-  double2 *sOp = smem2 + 4 * NPAIR;    // RD x NOP x NPAIR  thread-private operand ring (active threads)
+  double2 *sOp = smem2 + 4 * NPAIR;    // RD x SLOT   thread-private operand ring
 
   __shared__ PassScalars S;
   pass_guard(P);
@@ -690,12 +692,13 @@ __global__ void __launch_bounds__(LazyQ<PM, TYM, CPS>::NT, CPS) k_pass_3d_lazyq(
     const int o1 = act ? (int)(wrapc(ox - 2 + 2 * px, nx) + nx * wrapc(oy - 1 + py, ny)) : 0;
     const bool pin = act && py >= 1 && py <= hb && px >= 1 && px <= 32 && (ox - 2 + 2 * px) < nx;
     const long long oo = (ox - 2 + 2 * px) + nx * (oy - 1 + py);
+    const int ib = (py - 1) * 32 + (px - 1);  // interior index (B slots)
     // logical plane j (-1 .. nzc) -> physical plane offset; the march is in j
     const long long zstep = down ? -nxy : nxy, zwrap = nz * nxy;
     long long zoL = wrapc(down ? zhi : zlo - 1, nz) * nxy;  // plane j = -1
     auto issue = [&](int slot) {
       if (act) {
-        double2 *d = sOp + slot * NOP * NPAIR + t;
+        double2 *d = sOp + slot * SLOT + t;
         const long long g = zoL + o1;
         if (use_r) cp_async16(d, rin + g);
         cp_async16(d + NPAIR, xprev + g);
@@ -703,7 +706,7 @@ __global__ void __launch_bounds__(LazyQ<PM, TYM, CPS>::NT, CPS) k_pass_3d_lazyq(
         cp_async16(d + 3 * NPAIR, kap + g);
         if (pin)
 #pragma unroll
-          for (int c = 0; c < PM; c++) cp_async16(d + (4 + c) * NPAIR, Bc[c] + g);
+          for (int c = 0; c < PM; c++) cp_async16(sOp + slot * SLOT + 4 * NPAIR + c * NIN + ib, Bc[c] + g);
       }
       zoL += zstep;
       if (zoL < 0) zoL += zwrap;
@@ -723,7 +726,7 @@ __global__ void __launch_bounds__(LazyQ<PM, TYM, CPS>::NT, CPS) k_pass_3d_lazyq(
       if (i + D <= nzc + 1) issue(ri);
       cp_async_commit();
       cp_async_wait<D>();
-      const double2 *o = sOp + rs * NOP * NPAIR + t;
+      const double2 *o = sOp + rs * SLOT + t;
       const double2 xm = o[NPAIR], kc_p = o[3 * NPAIR];
       double2 xk_p = xm;
       if (use_r) {
@@ -740,7 +743,7 @@ __global__ void __launch_bounds__(LazyQ<PM, TYM, CPS>::NT, CPS) k_pass_3d_lazyq(
       if (pin)
 #pragma unroll
         for (int c = 0; c < PM; c++) {
-          const double2 b = o[(4 + c) * NPAIR];
+          const double2 b = sOp[rs * SLOT + 4 * NPAIR + c * NIN + ib];
           bt.x = fma(b.x, btc[c], bt.x);
           bt.y = fma(b.y, btc[c], bt.y);
         }
