@@ -1,0 +1,182 @@
+"""EPIRK exponential integrators on top of the oracle's KIOPS.
+
+TEST INFRASTRUCTURE ONLY (same rule as oracle.py: only tests/, __graft_entry__.smoke()
+and bench.py's reference legs import it; the product package never does).
+
+What it follows, step by step:
+  * the three-stage EPIRK template, Eq. 2 (Sec. 2), with the nonlinear
+    remainder r(u) = f(u) - f(u_n) - J_n (u - u_n);
+  * EPIRK4s3, Eq. 50 (= Eq. 9) and EPIRK4s3A, Eq. 51;
+  * the "mixed implementation" grouping of Sec. 2 (Eqs. 10-11): call 1 is a
+    Task-I KIOPS call, phi_1 at the two stage nodes T = [c_a, c_b] on b = h f(u_n) with
+    the 1/T^p scaling (Alg. 1 l.31-35); call 2 is a Task-II call at tau = 1 with
+    b_1 = h f(u_n), b_2 = 0 and b_3, b_4 written exactly as Eq. 11 prints them (for
+    EPIRK4s3A: read off Eq. 51 the same way);
+  * constant step size (Sec. 4: "implemented with constant time step
+    integration"); KIOPS's m warm-started from the previous step's final m of the same
+    call (Sec. 3.6 heuristic, reading E1 in DESIGN.md).
+The problems (Sec. 4): the 1D semilinear parabolic problem made autonomous
+by appending t to the state (reading E2), with the source discretised so that the
+semi-discrete system has the exact solution x(1-x)e^t (reading E3); and a periodic
+Allen-Cahn 2D problem (periodic instead of no-flow boundaries: reading E4).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from oracle import oracle as O
+
+# Eq. 50 / Eq. 51: stage nodes (U_{n2}, U_{n3}) and the final-stage combination
+SCHEMES = ("epirk4s3", "epirk4s3a")
+NODES = {"epirk4s3": (1.0 / 8.0, 1.0 / 9.0), "epirk4s3a": (1.0 / 2.0, 2.0 / 3.0)}
+
+
+def final_b34(scheme, h, r2, r3):
+    """b_3, b_4 of the Task-II call (Eq. 11 for EPIRK4s3; Eq. 51 for EPIRK4s3A), as printed."""
+    if scheme == "epirk4s3":
+        d = r3 - 2.0 * r2
+        b3 = 1892.0 * h * r2 + 1458.0 * h * d
+        b4 = -42336.0 * h * r2 - 34992.0 * h * d
+    elif scheme == "epirk4s3a":
+        b3 = 32.0 * h * r2 - 13.5 * h * r3
+        b4 = -144.0 * h * r2 + 81.0 * h * r3
+    else:
+        raise ValueError(scheme)
+    return b3, b4
+
+
+# ---------------------------------------------------------------------------
+# problems: f(y), J(y) as a KIOPS operator dict scaled by h, and J(y) x
+# ---------------------------------------------------------------------------
+class Semilinear1D:
+    """U_t - U_xx = int_0^1 U dx + Phi(x, t) on (0, 1), U = 0 at x = 0, 1.
+    Interior nodes x_i = i dx, dx = 1/(N+1); U_xx by the 3-point difference; the
+    integral by the trapezoid rule with the zero boundary values, dx sum_j U_j.
+    Phi_i(t) = e^t (x_i(1-x_i) + 2 - Q), Q = dx sum_j x_j(1-x_j): then
+    u_i(t) = x_i(1-x_i) e^t solves the semi-discrete system exactly (reading E3).
+    State y = (u_1..u_N, t) (autonomous form, reading E2)."""
+
+    def __init__(self, N=200):
+        self.N = N
+        self.dim = N + 1
+        dx = 1.0 / (N + 1)
+        self.x = dx * np.arange(1, N + 1)
+        A = np.zeros((N, N))
+        i = np.arange(N)
+        A[i, i] = -2.0 / dx ** 2
+        A[i[1:], i[:-1]] = 1.0 / dx ** 2
+        A[i[:-1], i[1:]] = 1.0 / dx ** 2
+        A += dx  # quadrature row: every row gets dx * sum_j u_j
+        self.A = A
+        self.g = self.x * (1.0 - self.x) + 2.0 - dx * np.sum(self.x * (1.0 - self.x))
+
+    def exact(self, t):
+        return np.r_[self.x * (1.0 - self.x) * np.exp(t), t]
+
+    def f(self, y):
+        u, t = y[:-1], y[-1]
+        return np.r_[self.A @ u + np.exp(t) * self.g, 1.0]
+
+    def jac_dense(self, y):
+        t = y[-1]
+        J = np.zeros((self.dim, self.dim))
+        J[:-1, :-1] = self.A
+        J[:-1, -1] = np.exp(t) * self.g  # d Phi / dt
+        return J
+
+    def jmul(self, y, x):
+        return self.jac_dense(y) @ x
+
+    def kiops_op(self, y, h):
+        return {"kind": "dense", "nx": self.dim, "ny": 1, "nz": 1, "dense": h * self.jac_dense(y)}
+
+
+class ReactionDiffusion2D:
+    """u_t = alpha lap(u) + R(u), R(u) = c0 + c1 u + c2 u^2 + c3 u^3, periodic n x n
+    grid of spacing dx (5-point Laplacian).  Allen-Cahn: alpha = 0.1,
+    R = u - u^3 on [-1, 1]^2 (dx = 2/n), u_0 = 0.1 + 0.1 cos(2 pi x) cos(2 pi y);
+    periodic boundaries (reading E4).  J(u) = alpha lap + diag(R'(u))."""
+
+    def __init__(self, n=64, ny=None, alpha=0.1, coef=(0.0, 1.0, 0.0, -1.0), length=2.0):
+        self.nx, self.ny = n, (ny or n)
+        self.dim = self.nx * self.ny
+        self.dx = length / self.nx
+        self.alpha = alpha
+        self.c = tuple(float(c) for c in coef)
+        self.wa = alpha / self.dx ** 2
+
+    def initial(self):
+        xs = -1.0 + self.dx * np.arange(self.nx)
+        ys = -1.0 + self.dx * np.arange(self.ny)
+        X, Y = np.meshgrid(xs, ys, indexing="xy")
+        return (0.1 + 0.1 * np.cos(2 * np.pi * X) * np.cos(2 * np.pi * Y)).ravel()
+
+    def lap(self, u):
+        U = u.reshape(self.ny, self.nx)
+        L = np.roll(U, 1, 1) + np.roll(U, -1, 1) + np.roll(U, 1, 0) + np.roll(U, -1, 0) - 4.0 * U
+        return self.wa * L.ravel()
+
+    def R(self, u):
+        c0, c1, c2, c3 = self.c
+        return c0 + u * (c1 + u * (c2 + u * c3))
+
+    def dR(self, u):
+        _, c1, c2, c3 = self.c
+        return c1 + u * (2.0 * c2 + u * 3.0 * c3)
+
+    def f(self, y):
+        return self.lap(y) + self.R(y)
+
+    def jmul(self, y, x):
+        return self.lap(x) + self.dR(y) * x
+
+    def kiops_op(self, y, h):
+        wa = h * self.wa
+        return {"kind": "stencil2d5", "nx": self.nx, "ny": self.ny, "nz": 1,
+                "w": [wa, wa, wa, wa, -4.0 * wa], "diag": h * self.dR(y)}
+
+
+# ---------------------------------------------------------------------------
+# one step / integration
+# ---------------------------------------------------------------------------
+def remainder(prob, yn, fn, y):
+    """r(y) = f(y) - f(y_n) - J_n (y - y_n)."""
+    return prob.f(y) - fn - prob.jmul(yn, y - yn)
+
+
+def step(prob, scheme, yn, h, tol=1e-12, m_hint=(10, 10), m_max=128):
+    """One EPIRK4s3 / EPIRK4s3A step with the two grouped KIOPS calls.
+    Returns (y_{n+1}, (final_m call 1, final_m call 2), [stats1, stats2])."""
+    ca, cb = NODES[scheme]
+    fn = prob.f(yn)
+    b1 = h * fn
+    op = prob.kiops_op(yn, h)  # the matrix argument is h J_n
+    zero = np.zeros_like(yn)
+    # call 1 (Task I): phi_1(T h J) h f at both nodes, T ascending, scaled by 1/T
+    T1 = np.array(sorted((ca, cb)))
+    w1, s1, _, rc = O.kiops(op, [zero, b1], T1, tol=tol, m_init=m_hint[0], m_min=min(10, m_hint[0]),
+                            m_max=m_max, task1=1)
+    assert rc == "OK", rc
+    phi = {T1[0]: w1[0], T1[1]: w1[1]}
+    U2 = yn + ca * phi[ca]
+    U3 = yn + cb * phi[cb]
+    r2 = remainder(prob, yn, fn, U2)
+    r3 = remainder(prob, yn, fn, U3)
+    b3, b4 = final_b34(scheme, h, r2, r3)
+    # call 2 (Task II at tau = 1): phi_1 b1 + phi_3 b3 + phi_4 b4 (b0 = b2 = 0)
+    w2, s2, _, rc = O.kiops(op, [zero, b1, zero, b3, b4], np.array([1.0]), tol=tol, m_init=m_hint[1],
+                            m_min=min(10, m_hint[1]), m_max=m_max)
+    assert rc == "OK", rc
+    return yn + w2[0], (s1["final_m"], s2["final_m"]), [s1, s2]
+
+
+def integrate(prob, scheme, y0, t0, t1, nsteps, tol=1e-12):
+    """Constant-step integration over [t0, t1] (Sec. 4); m chained across steps."""
+    h = (t1 - t0) / nsteps
+    y = np.array(y0, dtype=np.float64)
+    m = (10, 10)
+    kv = 0
+    for _ in range(nsteps):
+        y, m, st = step(prob, scheme, y, h, tol=tol, m_hint=m)
+        kv += st[0]["krylov_vectors"] + st[1]["krylov_vectors"]
+    return y, {"krylov_vectors": kv, "final_m": m}

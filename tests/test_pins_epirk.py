@@ -1,0 +1,141 @@
+"""Pins of the EPIRK oracle (oracle/epirk.py) against things other
+than itself: the exact solution of the 1D semilinear problem (order 4, SPEC's test
+idea S:540), the exact exponential of linear problems (scipy.linalg.expm, an
+independent routine), a naive per-phi-term evaluation of Eq. 50/51 with phi_k from
+scipy's expm of the block matrix [[M, v e_1^T], [0, J_k]], hand-expanded remainders,
+and finite-difference Jacobians."""
+import numpy as np
+import pytest
+import scipy.linalg as sla
+
+from oracle import epirk as E
+
+
+class Linear:
+    """f(y) = A y (dense): every remainder vanishes, so a step is exp(hA) y exactly."""
+
+    def __init__(self, A):
+        self.A = np.asarray(A, dtype=np.float64)
+        self.dim = self.A.shape[0]
+
+    def f(self, y):
+        return self.A @ y
+
+    def jmul(self, y, x):
+        return self.A @ x
+
+    def kiops_op(self, y, h):
+        return {"kind": "dense", "nx": self.dim, "ny": 1, "nz": 1, "dense": h * self.A}
+
+
+class Square:
+    """scalar f(u) = u^2 (SPEC's remainder example)."""
+
+    dim = 1
+
+    def f(self, y):
+        return y * y
+
+    def jmul(self, y, x):
+        return 2.0 * y * x
+
+
+def phi_k_v(M, v, k):
+    """phi_k(M) v from the exponential of the (n+k)-block matrix (independent of KIOPS)."""
+    n = len(v)
+    W = np.zeros((n + k, n + k))
+    W[:n, :n] = M
+    W[:n, n] = v
+    for i in range(k - 1):
+        W[n + i, n + i + 1] = 1.0
+    return sla.expm(W)[:n, n + k - 1]
+
+
+def naive_step(prob, scheme, y, h, J):
+    """Eq. 50 / Eq. 51 term by term, every phi_k(g h J) b evaluated separately."""
+    ca, cb = E.NODES[scheme]
+    fn = prob.f(y)
+    U2 = y + ca * phi_k_v(ca * h * J, h * fn, 1)
+    U3 = y + cb * phi_k_v(cb * h * J, h * fn, 1)
+    r2 = prob.f(U2) - fn - J @ (U2 - y)
+    r3 = prob.f(U3) - fn - J @ (U3 - y)
+    M = h * J
+    out = y + phi_k_v(M, h * fn, 1)
+    if scheme == "epirk4s3":
+        terms = [(1892.0, 3, r2), (-42336.0, 4, r2), (1458.0, 3, r3 - 2 * r2), (-34992.0, 4, r3 - 2 * r2)]
+    else:
+        terms = [(32.0, 3, r2), (-144.0, 4, r2), (-13.5, 3, r3), (81.0, 4, r3)]
+    for c, k, r in terms:
+        out = out + c * phi_k_v(M, h * r, k)
+    return out
+
+
+def test_remainder_pins():
+    sq = Square()
+    u_n = np.array([1.0])
+    h = 0.1
+    r = E.remainder(sq, u_n, sq.f(u_n), u_n + h)
+    assert abs(r[0] - h * h) <= 1e-15  # (1+h)^2 - 1 - 2h = h^2
+    for prob in (E.Semilinear1D(20), E.ReactionDiffusion2D(8)):
+        y = prob.exact(0.3) if hasattr(prob, "exact") else prob.initial()
+        assert not np.any(E.remainder(prob, y, prob.f(y), y))  # r(u_n) = 0 exactly
+
+
+@pytest.mark.parametrize("prob", [E.Semilinear1D(30), E.ReactionDiffusion2D(12)], ids=["semilinear", "allen_cahn"])
+def test_jacobian_matches_finite_differences(prob):
+    rng = np.random.default_rng(7)
+    y = prob.exact(0.2) if hasattr(prob, "exact") else prob.initial() + 0.05 * rng.standard_normal(prob.dim)
+    x = rng.standard_normal(prob.dim)
+    eps = 1e-6 * (1.0 + np.linalg.norm(y) / np.linalg.norm(x))
+    fd = (prob.f(y + eps * x) - prob.f(y - eps * x)) / (2 * eps)
+    jx = prob.jmul(y, x)
+    assert np.linalg.norm(fd - jx) <= 1e-5 * np.linalg.norm(jx)
+
+
+@pytest.mark.parametrize("scheme", E.SCHEMES)
+def test_linear_problem_step_is_the_exponential(scheme):
+    rng = np.random.default_rng(11)
+    n = 20
+    Q = rng.standard_normal((n, n))
+    A = -(Q @ Q.T) / n - 0.5 * np.eye(n) + 0.3 * (Q - Q.T) / np.sqrt(n)
+    prob = Linear(A)
+    y = rng.standard_normal(n)
+    h = 0.7
+    y1, _, _ = E.step(prob, scheme, y, h, tol=1e-13)
+    ref = sla.expm(h * A) @ y
+    assert np.linalg.norm(y1 - ref) <= 1e-9 * np.linalg.norm(ref)
+
+
+@pytest.mark.parametrize("scheme", E.SCHEMES)
+def test_scalar_decay(scheme):
+    prob = Linear([[-1.0]])
+    y, _ = E.integrate(prob, scheme, np.array([1.0]), 0.0, 1.0, 10, tol=1e-13)
+    assert abs(y[0] - np.exp(-1.0)) <= 1e-9
+
+
+@pytest.mark.parametrize("scheme", E.SCHEMES)
+def test_grouped_step_equals_naive_per_term_evaluation(scheme):
+    # stage-grouping equivalence (SPEC S:540 idea): the two grouped KIOPS calls give the
+    # same step as evaluating every phi_k(g h J) b of Eq. 50/51 separately
+    for prob, y, h in ((E.ReactionDiffusion2D(8, alpha=0.1), None, 0.05), (E.Semilinear1D(20), None, 0.1)):
+        y = prob.exact(0.0) if hasattr(prob, "exact") else prob.initial()
+        J = np.column_stack([prob.jmul(y, e) for e in np.eye(prob.dim)])
+        got, _, _ = E.step(prob, scheme, y, h, tol=1e-13)
+        ref = naive_step(prob, scheme, y, h, J)
+        assert np.linalg.norm(got - ref) <= 1e-9 * np.linalg.norm(ref), (scheme, np.linalg.norm(got - ref))
+
+
+@pytest.mark.parametrize("scheme", E.SCHEMES)
+def test_order_four_on_the_semilinear_problem(scheme):
+    # Sec. 4 problem with its exact solution x(1-x)e^t; SPEC's order test:
+    # slope 4 +- 0.3 under step halving
+    prob = E.Semilinear1D(200)
+    steps = [4, 8, 16, 32]
+    errs = []
+    for n in steps:
+        y, _ = E.integrate(prob, scheme, prob.exact(0.0), 0.0, 1.0, n, tol=1e-13)
+        ex = prob.exact(1.0)
+        errs.append(np.linalg.norm(y[:-1] - ex[:-1]) / np.linalg.norm(ex[:-1]))
+    slope = np.polyfit(np.log([1.0 / n for n in steps]), np.log(errs), 1)[0]
+    print(f"{scheme}: errors {['%.2e' % e for e in errs]}, observed order {slope:.2f}")
+    assert 3.7 <= slope <= 4.3, (slope, errs)
