@@ -167,6 +167,12 @@ kiops_status kiops_apply_hostloop(kiops_ctx c, const double *const *u, const dou
  * available (may exceed what fit). */
 kiops_status kiops_get_trace(kiops_ctx c, void *host_buf, size_t bytes, int64_t *rows);
 
+/* Initial Krylov size of the NEXT kiops_apply calls (Alg. 1 l.3 m_init; the Sec. 3.6
+ * warm start "use the final value of m_i from the previous time step": pass the
+ * previous call's stats.final_m).  0 restores options.m_init.  Clipped to
+ * [m_min, m_max] like m_init.  Errors: KIOPS_ERR_INVALID_ARG for a NULL ctx or m < 0. */
+kiops_status kiops_set_m_init(kiops_ctx ctx, int m_init);
+
 /* TEST HOOK (not for users): force the next applies to run attempt i with
  * substep tau[i] and Krylov size m[i], bypassing Alg. 4, and accept it if
  * accept == NULL or accept[i] != 0 (n = 0 clears).  tau, m, accept: HOST,
@@ -189,6 +195,58 @@ kiops_status kiops_destroy(kiops_ctx c);
 /* Static strings; never NULL. */
 const char *kiops_status_string(kiops_status s);
 const char *kiops_last_error(kiops_ctx c);
+
+
+/* ===========================================================================
+ * EPIRK exponential integrators on top of kiops_apply.
+ * EPIRK4s3 (Eq. 50) and EPIRK4s3A (Eq. 51) with the
+ * "mixed implementation" of Sec. 2 (Eqs. 9-11): per constant step h,
+ *   call 1 (Task I):  phi_1(c h J_n) h f(u_n) at both stage nodes c (one kiops_apply,
+ *                     p = 1, T = the two nodes ascending, 1/T scaling);
+ *   stages:           U_i = u_n + c_i * (call-1 output), r(U_i), b_3, b_4 (Eq. 11);
+ *   call 2 (Task II): phi_1(hJ_n) h f + phi_3(hJ_n) b_3 + phi_4(hJ_n) b_4 (p = 4, T = 1);
+ *   u_{n+1} = u_n + (call-2 output).
+ * Each call's m starts from the same call's final m of the previous step (Sec. 3.6).
+ * Problem class: u' = L u + R(u) on a periodic nx x ny grid, L a constant 5-point
+ * stencil, R a cubic polynomial applied pointwise (Allen-Cahn: alpha lap(u) + u - u^3,
+ * P:593-597).  J(u) = L + diag(R'(u)); for this class the remainder
+ * r(U) = f(U) - f(u_n) - J_n (U - u_n) equals R(U) - R(u_n) - R'(u_n)(U - u_n)
+ * exactly (the linear terms cancel), which is what the stage kernel evaluates.
+ * =========================================================================== */
+typedef enum { KIOPS_EPIRK4S3 = 1, KIOPS_EPIRK4S3A = 2 } kiops_epirk_scheme;
+
+typedef struct {
+  int64_t nx, ny;          /* periodic grid, N = nx*ny, x fastest                          */
+  double w[5];             /* L: {W, E, S, N, C} weights (alpha lap: alpha/dx^2 {1,1,1,1,-4}) */
+  double c[4];             /* R(u) = c[0] + c[1] u + c[2] u^2 + c[3] u^3                   */
+} kiops_rd_problem;
+
+typedef struct {
+  int64_t steps, krylov_vectors, passes, substeps, rejections, expm_calls;
+  int32_t final_m[2];      /* warm-start m of call 1 and call 2 after the last step         */
+  double kiops_ms;         /* device time in the two kiops_apply calls (%globaltimer sums)  */
+} kiops_epirk_stats;
+
+typedef struct kiops_epirk_s *kiops_epirk_ctx;
+
+/* Bytes of the caller-owned workspace for kiops_epirk_create (two kiops workspaces
+ * of m_max+3 vectors each plus 10 stage vectors; 1024^2: ~2.2 GB at m_max = 128). */
+kiops_status kiops_epirk_workspace_bytes(const kiops_rd_problem *pb, const kiops_options *o, size_t *bytes);
+
+/* pb, o: HOST, copied.  h > 0: the constant step.  scheme: KIOPS_EPIRK4S3[A].
+ * o: the KIOPS options of both calls (tol, m_*, max_attempts; task1 and staging are
+ * set internally).  workspace: DEVICE, 256-byte aligned, >= the queried bytes,
+ * borrowed for the ctx's life.  Errors as kiops_create. */
+kiops_status kiops_epirk_create(const kiops_rd_problem *pb, int scheme, double h, const kiops_options *o,
+                                void *cuda_stream, void *workspace, size_t workspace_bytes,
+                                kiops_epirk_ctx *out);
+
+/* nsteps constant steps from u (DEVICE, N doubles, updated in place).  Any KIOPS
+ * failure aborts with its status (the step index is in kiops_epirk_last_error). */
+kiops_status kiops_epirk_step(kiops_epirk_ctx ctx, double *u, int nsteps, kiops_epirk_stats *stats);
+
+kiops_status kiops_epirk_destroy(kiops_epirk_ctx ctx);
+const char *kiops_epirk_last_error(kiops_epirk_ctx ctx);
 
 #ifdef __cplusplus
 }

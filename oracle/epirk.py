@@ -130,6 +130,12 @@ class ReactionDiffusion2D:
     def jmul(self, y, x):
         return self.lap(x) + self.dR(y) * x
 
+    def remainder(self, yn, y):
+        """r(y) of P:85 for f = L u + R(u) with L linear: the L terms of
+        f(y) - f(y_n) - J_n (y - y_n) cancel identically, leaving the pointwise
+        R(y) - R(y_n) - R'(y_n)(y - y_n) (reading E7; no cancellation of large terms)."""
+        return self.R(y) - self.R(yn) - self.dR(yn) * (y - yn)
+
     def kiops_op(self, y, h):
         wa = h * self.wa
         return {"kind": "stencil2d5", "nx": self.nx, "ny": self.ny, "nz": 1,
@@ -140,7 +146,10 @@ class ReactionDiffusion2D:
 # one step / integration
 # ---------------------------------------------------------------------------
 def remainder(prob, yn, fn, y):
-    """r(y) = f(y) - f(y_n) - J_n (y - y_n)  (P:85)."""
+    """r(y) = f(y) - f(y_n) - J_n (y - y_n); problems with a linear part may
+    provide the identical pointwise form (reading E7)."""
+    if hasattr(prob, "remainder"):
+        return prob.remainder(yn, y)
     return prob.f(y) - fn - prob.jmul(yn, y - yn)
 
 

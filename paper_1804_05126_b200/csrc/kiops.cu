@@ -219,6 +219,7 @@ struct kiops_ctx_s {
   int forced_m[KIOPS_MAX_FORCED];
   int forced_acc[KIOPS_MAX_FORCED];
   long long last_attempts = 0;
+  int m_init_call = 0;           // kiops_set_m_init (0: options.m_init)
   void *fpass = nullptr;         // stencil pass kernel (NULL for CSR)
   std::string err;
 };
@@ -494,6 +495,7 @@ static void fill_call(kiops_ctx c, const double *const *u, const double *T, int 
     B.T[l] = l < n_out ? T[l] : 0.0;
   }
   B.n_out = n_out;
+  B.m_init = c->m_init_call;
   B.n_forced = c->n_forced;
   for (int i = 0; i < c->n_forced; i++) {
     B.forced_tau[i] = c->forced_tau[i];
@@ -590,6 +592,12 @@ kiops_status kiops_get_trace(kiops_ctx c, void *host_buf, size_t bytes, int64_t 
   return KIOPS_OK;
 }
 
+kiops_status kiops_set_m_init(kiops_ctx c, int m_init) {
+  if (!c || m_init < 0) return KIOPS_ERR_INVALID_ARG;
+  c->m_init_call = m_init;
+  return KIOPS_OK;
+}
+
 kiops_status kiops_set_forced_schedule(kiops_ctx c, const double *tau, const int32_t *m, const int32_t *accept,
                                        int n) {
   if (!c || n < 0 || n > KIOPS_MAX_FORCED || (n > 0 && (!tau || !m))) return KIOPS_ERR_INVALID_ARG;
@@ -639,3 +647,4 @@ const char *kiops_status_string(kiops_status s) {
 const char *kiops_last_error(kiops_ctx c) { return c ? c->err.c_str() : "NULL ctx"; }
 
 }  // extern "C"
+#include "epirk.cuh"

@@ -20,6 +20,7 @@ struct CallBlock {
   double *w[KMAXO];              // outputs (DEVICE)
   double T[KMAXO];               // output times
   int n_out;
+  int m_init;                    // > 0: this call's initial m (warm start, kiops_set_m_init)
   int n_forced;                  // test hook: forced schedule
   double forced_tau[KIOPS_MAX_FORCED];
   int forced_m[KIOPS_MAX_FORCED];

@@ -90,7 +90,8 @@ __global__ void __launch_bounds__(256) k_setup(KParams P) {
   const int n_out = call->n_out;
   st->t_end = call->T[n_out - 1];
   st->tau = st->t_end;                                     // Alg. 1 l.2
-  int m = P.m_init < P.m_max ? P.m_init : P.m_max;         // l.3
+  const int m0 = call->m_init > 0 ? call->m_init : P.m_init;  // (warm start: kiops_set_m_init)
+  int m = m0 < P.m_max ? m0 : P.m_max;                     // l.3
   st->m = m < P.m_min ? P.m_min : m;
   if (call->n_forced > 0) {
     st->tau = call->forced_tau[0];

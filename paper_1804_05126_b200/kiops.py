@@ -52,8 +52,23 @@ class TraceRow(C.Structure):
 
 
 SYMBOLS = ["kiops_options_default", "kiops_workspace_bytes", "kiops_create", "kiops_apply",
-           "kiops_apply_host", "kiops_apply_hostloop", "kiops_get_trace", "kiops_set_forced_schedule", "kiops_debug_basis",
-           "kiops_destroy", "kiops_status_string", "kiops_last_error"]
+           "kiops_apply_host", "kiops_apply_hostloop", "kiops_get_trace", "kiops_set_m_init",
+           "kiops_set_forced_schedule", "kiops_debug_basis", "kiops_destroy", "kiops_status_string", "kiops_last_error",
+           "kiops_epirk_workspace_bytes", "kiops_epirk_create", "kiops_epirk_step", "kiops_epirk_destroy",
+           "kiops_epirk_last_error"]
+
+
+class RDProblem(C.Structure):
+    _fields_ = [("nx", C.c_int64), ("ny", C.c_int64), ("w", C.c_double * 5), ("c", C.c_double * 4)]
+
+
+class EpirkStats(C.Structure):
+    _fields_ = [("steps", C.c_int64), ("krylov_vectors", C.c_int64), ("passes", C.c_int64),
+                ("substeps", C.c_int64), ("rejections", C.c_int64), ("expm_calls", C.c_int64),
+                ("final_m", C.c_int32 * 2), ("kiops_ms", C.c_double)]
+
+
+EPIRK_SCHEMES = {"epirk4s3": 1, "epirk4s3a": 2}
 
 _lib = None
 
@@ -79,13 +94,23 @@ def lib():
         L.kiops_set_forced_schedule.argtypes = [C.c_void_p, _dp, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
                                                 C.c_int]
         L.kiops_debug_basis.argtypes = [C.c_void_p, _dp, _dp, C.POINTER(C.c_int32)]
+        L.kiops_set_m_init.argtypes = [C.c_void_p, C.c_int]
+        L.kiops_epirk_workspace_bytes.argtypes = [C.POINTER(RDProblem), C.POINTER(Options), C.POINTER(C.c_size_t)]
+        L.kiops_epirk_create.argtypes = [C.POINTER(RDProblem), C.c_int, C.c_double, C.POINTER(Options), C.c_void_p,
+                                         C.c_void_p, C.c_size_t, C.POINTER(C.c_void_p)]
+        L.kiops_epirk_step.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.POINTER(EpirkStats)]
+        L.kiops_epirk_destroy.argtypes = [C.c_void_p]
+        L.kiops_epirk_last_error.argtypes = [C.c_void_p]
+        L.kiops_epirk_last_error.restype = C.c_char_p
         L.kiops_destroy.argtypes = [C.c_void_p]
         L.kiops_status_string.argtypes = [C.c_int]
         L.kiops_status_string.restype = C.c_char_p
         L.kiops_last_error.argtypes = [C.c_void_p]
         L.kiops_last_error.restype = C.c_char_p
         for name in ("kiops_workspace_bytes", "kiops_create", "kiops_apply", "kiops_apply_host", "kiops_apply_hostloop",
-                     "kiops_get_trace", "kiops_set_forced_schedule", "kiops_debug_basis", "kiops_destroy"):
+                     "kiops_get_trace", "kiops_set_m_init", "kiops_set_forced_schedule", "kiops_debug_basis",
+                     "kiops_destroy", "kiops_epirk_workspace_bytes", "kiops_epirk_create", "kiops_epirk_step",
+                     "kiops_epirk_destroy"):
             getattr(L, name).restype = C.c_int
         _lib = L
     return _lib
@@ -252,3 +277,62 @@ def _host_ptr(x):
     if isinstance(x, np.ndarray):
         return x.ctypes.data
     return x.data_ptr()  # pinned torch CPU tensor
+
+
+class KiopsEpirk:
+    """EPIRK4s3 / EPIRK4s3A (Eqs. 50-51) for u' = L u + R(u) on a periodic grid through
+    the kiops_epirk_* C ABI: problem {"nx", "ny", "w": 5 stencil weights {W,E,S,N,C},
+    "c": 4 cubic reaction coefficients}, constant step h, KIOPS options."""
+
+    def __init__(self, problem: dict, scheme: str, h: float, device="cuda:0", stream=None, **options):
+        import torch
+
+        if not torch.cuda.is_available():
+            raise RuntimeError("KIOPS B200 path needs a CUDA device (no CPU fallback)")
+        self.torch = torch
+        self.device = torch.device(device)
+        self.N = int(problem["nx"]) * int(problem["ny"])
+        pb = RDProblem()
+        pb.nx, pb.ny = int(problem["nx"]), int(problem["ny"])
+        for i in range(5):
+            pb.w[i] = float(problem["w"][i])
+        for i in range(4):
+            pb.c[i] = float(problem["c"][i])
+        self.pb = pb
+        self.opts = default_options(**options)
+        nb = C.c_size_t(0)
+        s = lib().kiops_epirk_workspace_bytes(C.byref(pb), C.byref(self.opts), C.byref(nb))
+        if s != 0:
+            raise KiopsError(s, "kiops_epirk_workspace_bytes")
+        self.workspace = torch.empty(nb.value + 256, dtype=torch.uint8, device=self.device)
+        aligned = (self.workspace.data_ptr() + 255) & ~255
+        self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
+        ctx = C.c_void_p()
+        s = lib().kiops_epirk_create(C.byref(pb), EPIRK_SCHEMES[scheme], float(h), C.byref(self.opts),
+                                     C.c_void_p(self.stream.cuda_stream), C.c_void_p(aligned), C.c_size_t(nb.value),
+                                     C.byref(ctx))
+        if s != 0:
+            raise KiopsError(s, "kiops_epirk_create")
+        self.ctx = ctx
+
+    def step(self, u, nsteps=1):
+        """u: CUDA float64 tensor (N,), advanced in place by nsteps constant steps."""
+        st = EpirkStats()
+        s = lib().kiops_epirk_step(self.ctx, C.c_void_p(u.data_ptr()), int(nsteps), C.byref(st))
+        if s != 0:
+            msg = lib().kiops_epirk_last_error(self.ctx)
+            raise KiopsError(s, f"kiops_epirk_step: {msg.decode() if msg else ''}")
+        out = {k: getattr(st, k) for k, _ in EpirkStats._fields_ if k != "final_m"}
+        out["final_m"] = (st.final_m[0], st.final_m[1])
+        return out
+
+    def close(self):
+        if getattr(self, "ctx", None):
+            lib().kiops_epirk_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -81,6 +81,16 @@ def test_remainder_pins():
         assert not np.any(E.remainder(prob, y, prob.f(y), y))  # r(u_n) = 0 exactly
 
 
+def test_pointwise_remainder_is_the_papers_definition():
+    # reading E7: for f = L u + R(u) the L terms of f(U) - f(u_n) - J_n (U - u_n) cancel
+    rng = np.random.default_rng(5)
+    prob = E.ReactionDiffusion2D(10, alpha=0.01)
+    yn = prob.initial()
+    y = yn + 0.1 * rng.standard_normal(prob.dim)
+    full = prob.f(y) - prob.f(yn) - prob.jmul(yn, y - yn)
+    assert np.linalg.norm(prob.remainder(yn, y) - full) <= 1e-12 * np.linalg.norm(full)
+
+
 @pytest.mark.parametrize("prob", [E.Semilinear1D(30), E.ReactionDiffusion2D(12)], ids=["semilinear", "allen_cahn"])
 def test_jacobian_matches_finite_differences(prob):
     rng = np.random.default_rng(7)
