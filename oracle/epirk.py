@@ -29,6 +29,13 @@ from oracle import oracle as O
 # Eq. 50 / Eq. 51: stage nodes (U_{n2}, U_{n3}) and the final-stage combination
 SCHEMES = ("epirk4s3", "epirk4s3a")
 NODES = {"epirk4s3": (1.0 / 8.0, 1.0 / 9.0), "epirk4s3a": (1.0 / 2.0, 2.0 / 3.0)}
+# fifth-order schemes, three KIOPS calls per step (Sec. 4)
+SCHEMES5 = ("epirk5p1", "exprb5s3")
+# Table 1, EPIRK5P1 coefficients as printed
+A11, A21, A22 = 0.3512959269505819, 0.8440547201165712, 1.690589160956896
+B1, B2, B3 = 1.0, 1.272712731735689, 2.271459926542262
+G11, G21, G22 = 0.3512959269505819, 0.8440547201165712, 1.0
+G31, G32, G33 = 1.0, 0.71111109536436687, 0.6237811195337149
 
 
 def final_b34(scheme, h, r2, r3):
@@ -179,13 +186,68 @@ def step(prob, scheme, yn, h, tol=1e-12, m_hint=(10, 10), m_max=128):
     return yn + w2[0], (s1["final_m"], s2["final_m"]), [s1, s2]
 
 
+def _task1(op, p, b, T, tol, m, m_max):
+    """Task I (Sec. 2): phi_p(T_l A) b for every T_l (ascending), from one KIOPS
+    call with u_p = b, all other u_k = 0, and the 1/T^p scaling (Alg. 1 l.31-35)."""
+    zero = np.zeros_like(b)
+    u = [zero] * p + [b]
+    w, st, _, rc = O.kiops(op, u, np.asarray(T, dtype=np.float64), tol=tol, m_init=m, m_min=min(10, m),
+                           m_max=m_max, task1=1)
+    assert rc == "OK", rc
+    return w, st
+
+
+def step5(prob, scheme, yn, h, tol=1e-12, m_hint=(10, 10, 10), m_max=128):
+    """One fifth-order step with three grouped KIOPS calls (Sec. 4: "fifth-order methods
+    require only three calls").
+    EPIRK5P1, Eq. 52 with Table 1 (the U_{n3} line's truncated "+ alpha_22" completed from
+    the Eq. 2 template as alpha_22 phi_1(g_22 h J) h r(U_{n2}), reading E8):
+      call 1: phi_1 on h f at T = [g11, g21, g31];  call 2: phi_1 on h r(U2) at [g32, g22];
+      call 3: phi_3 on h(-2 r(U2) + r(U3)) at [g33].
+    EXPRB5s3, Eq. 53:
+      call 1: phi_1 on h f at [1/2, 9/10];  call 2: phi_3 on h r(U2) at [1/2, 9/10];
+      call 3 (Task II, tau = 1): phi_1 h f + phi_3 b3 + phi_4 b4 with
+      b3 = 18 h r2 - 250/81 h r3, b4 = -60 h r2 + 500/27 h r3.
+    Returns (y_{n+1}, (final m of calls 1-3), [stats])."""
+    fn = prob.f(yn)
+    b1 = h * fn
+    op = prob.kiops_op(yn, h)
+    zero = np.zeros_like(yn)
+    if scheme == "epirk5p1":
+        w1, s1 = _task1(op, 1, b1, [G11, G21, G31], tol, m_hint[0], m_max)
+        U2 = yn + A11 * w1[0]
+        r2 = remainder(prob, yn, fn, U2)
+        w2, s2 = _task1(op, 1, h * r2, [G32, G22], tol, m_hint[1], m_max)
+        U3 = yn + A21 * w1[1] + A22 * w2[1]
+        r3 = remainder(prob, yn, fn, U3)
+        w3, s3 = _task1(op, 3, h * (-2.0 * r2 + r3), [G33], tol, m_hint[2], m_max)
+        y = yn + B1 * w1[2] + B2 * w2[0] + B3 * w3[0]
+    elif scheme == "exprb5s3":
+        w1, s1 = _task1(op, 1, b1, [0.5, 0.9], tol, m_hint[0], m_max)
+        U2 = yn + 0.5 * w1[0]
+        r2 = remainder(prob, yn, fn, U2)
+        w2, s2 = _task1(op, 3, h * r2, [0.5, 0.9], tol, m_hint[1], m_max)
+        U3 = yn + 0.9 * w1[1] + (27.0 / 25.0) * w2[0] + (729.0 / 125.0) * w2[1]
+        r3 = remainder(prob, yn, fn, U3)
+        b3 = 18.0 * h * r2 - (250.0 / 81.0) * h * r3
+        b4 = -60.0 * h * r2 + (500.0 / 27.0) * h * r3
+        w3, s3, _, rc = O.kiops(op, [zero, b1, zero, b3, b4], np.array([1.0]), tol=tol, m_init=m_hint[2],
+                                m_min=min(10, m_hint[2]), m_max=m_max)
+        assert rc == "OK", rc
+        y = yn + w3[0]
+    else:
+        raise ValueError(scheme)
+    return y, (s1["final_m"], s2["final_m"], s3["final_m"]), [s1, s2, s3]
+
+
 def integrate(prob, scheme, y0, t0, t1, nsteps, tol=1e-12):
     """Constant-step integration over [t0, t1] (Sec. 4); m chained across steps."""
     h = (t1 - t0) / nsteps
     y = np.array(y0, dtype=np.float64)
-    m = (10, 10)
+    five = scheme in SCHEMES5
+    m = (10, 10, 10) if five else (10, 10)
     kv = 0
     for _ in range(nsteps):
-        y, m, st = step(prob, scheme, y, h, tol=tol, m_hint=m)
-        kv += st[0]["krylov_vectors"] + st[1]["krylov_vectors"]
+        y, m, st = (step5 if five else step)(prob, scheme, y, h, tol=tol, m_hint=m)
+        kv += sum(s["krylov_vectors"] for s in st)
     return y, {"krylov_vectors": kv, "final_m": m}

@@ -149,3 +149,95 @@ def test_order_four_on_the_semilinear_problem(scheme):
     slope = np.polyfit(np.log([1.0 / n for n in steps]), np.log(errs), 1)[0]
     print(f"{scheme}: errors {['%.2e' % e for e in errs]}, observed order {slope:.2f}")
     assert 3.7 <= slope <= 4.3, (slope, errs)
+
+
+@pytest.mark.parametrize("scheme", E.SCHEMES5)
+def test_fifth_order_linear_step_is_the_exponential(scheme):
+    rng = np.random.default_rng(12)
+    n = 16
+    Q = rng.standard_normal((n, n))
+    A = -(Q @ Q.T) / n - 0.5 * np.eye(n)
+    prob = Linear(A)
+    y = rng.standard_normal(n)
+    y1, _, _ = E.step5(prob, scheme, y, 0.5, tol=1e-13)
+    ref = sla.expm(0.5 * A) @ y
+    assert np.linalg.norm(y1 - ref) <= 1e-9 * np.linalg.norm(ref)
+
+
+def test_fifth_order_grouping_equals_naive_per_term_evaluation():
+    # Eq. 52 / Eq. 53 term by term with the block-matrix phi_k
+    prob = E.ReactionDiffusion2D(8, alpha=0.1)
+    y = prob.initial()
+    h = 0.05
+    J = np.column_stack([prob.jmul(y, e) for e in np.eye(prob.dim)])
+    fn = prob.f(y)
+    M = h * J
+    r = lambda U: prob.f(U) - fn - J @ (U - y)  # noqa: E731
+    # EPIRK5P1
+    U2 = y + E.A11 * phi_k_v(E.G11 * M, h * fn, 1)
+    r2 = r(U2)
+    U3 = y + E.A21 * phi_k_v(E.G21 * M, h * fn, 1) + E.A22 * phi_k_v(E.G22 * M, h * r2, 1)
+    r3 = r(U3)
+    ref = (y + E.B1 * phi_k_v(E.G31 * M, h * fn, 1) + E.B2 * phi_k_v(E.G32 * M, h * r2, 1)
+           + E.B3 * phi_k_v(E.G33 * M, h * (-2 * r2 + r3), 3))
+    got, _, _ = E.step5(prob, "epirk5p1", y, h, tol=1e-13)
+    assert np.linalg.norm(got - ref) <= 1e-9 * np.linalg.norm(ref)
+    # EXPRB5s3
+    U2 = y + 0.5 * phi_k_v(0.5 * M, h * fn, 1)
+    r2 = r(U2)
+    U3 = (y + 0.9 * phi_k_v(0.9 * M, h * fn, 1) + 27 / 25 * phi_k_v(0.5 * M, h * r2, 3)
+          + 729 / 125 * phi_k_v(0.9 * M, h * r2, 3))
+    r3 = r(U3)
+    ref = (y + phi_k_v(M, h * fn, 1) + 18 * phi_k_v(M, h * r2, 3) - 60 * phi_k_v(M, h * r2, 4)
+           - 250 / 81 * phi_k_v(M, h * r3, 3) + 500 / 27 * phi_k_v(M, h * r3, 4))
+    got, _, _ = E.step5(prob, "exprb5s3", y, h, tol=1e-13)
+    assert np.linalg.norm(got - ref) <= 1e-9 * np.linalg.norm(ref)
+
+
+def test_table1_coefficients_as_printed():
+    # Table 1 round trip, SPEC's example values
+    assert E.A11 == 0.3512959269505819 and E.G33 == 0.6237811195337149 and E.G32 == 0.71111109536436687
+
+
+class Logistic:
+    """u' = u(1-u), u(0) = 0.1: exact 1/(1 + 9 e^-t); non-stiff, so every scheme shows
+    its classical order."""
+
+    dim = 1
+
+    def f(self, y):
+        return y * (1.0 - y)
+
+    def jmul(self, y, x):
+        return (1.0 - 2.0 * y) * x
+
+    def kiops_op(self, y, h):
+        return {"kind": "dense", "nx": 1, "ny": 1, "nz": 1, "dense": h * np.array([[1.0 - 2.0 * y[0]]])}
+
+
+def observed_order(prob, scheme, y0, t1, steps, exact, tol):
+    errs = []
+    for n in steps:
+        y, _ = E.integrate(prob, scheme, y0, 0.0, t1, n, tol=tol)
+        errs.append(np.linalg.norm(y - exact) / np.linalg.norm(exact))
+    return np.polyfit(np.log([t1 / n for n in steps]), np.log(errs), 1)[0], errs
+
+
+@pytest.mark.parametrize("scheme", E.SCHEMES5)
+def test_fifth_order_schemes_are_classically_fifth_order(scheme):
+    slope, errs = observed_order(Logistic(), scheme, np.array([0.1]), 2.0, [4, 8, 16],
+                                 np.array([1.0 / (1.0 + 9.0 * np.exp(-2.0))]), 1e-14)
+    print(f"{scheme} (logistic): errors {['%.2e' % e for e in errs]}, order {slope:.2f}")
+    assert slope >= 4.6, (slope, errs)
+
+
+def test_stiff_orders_on_the_semilinear_problem():
+    # EXPRB5s3 is stiffly accurate: order 5 on the stiff semi-discretisation (h <= 1/8);
+    # EPIRK5P1 is "classical (non-stiffly accurate)" (P:563): it reduces to ~3 there
+    prob = E.Semilinear1D(200)
+    ex = prob.exact(1.0)
+    s5, e5 = observed_order(prob, "exprb5s3", prob.exact(0.0), 1.0, [8, 16, 32], ex, 1e-14)
+    s1, e1 = observed_order(prob, "epirk5p1", prob.exact(0.0), 1.0, [8, 16, 32], ex, 1e-14)
+    print(f"exprb5s3: {['%.2e' % e for e in e5]} order {s5:.2f}; epirk5p1: {['%.2e' % e for e in e1]} order {s1:.2f}")
+    assert 4.6 <= s5 <= 5.4, (s5, e5)
+    assert 2.6 <= s1 <= 3.6, (s1, e1)
