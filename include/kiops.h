@@ -200,7 +200,9 @@ const char *kiops_last_error(kiops_ctx c);
 /* ===========================================================================
  * EPIRK exponential integrators on top of kiops_apply.
  * EPIRK4s3 (Eq. 50) and EPIRK4s3A (Eq. 51) with the
- * "mixed implementation" of Sec. 2 (Eqs. 9-11): per constant step h,
+ * "mixed implementation" of Sec. 2 (Eqs. 9-11); EPIRK5P1 (Eq. 52, Table 1)
+ * and EXPRB5s3 (Eq. 53) with three calls per step (Sec. 4; grouping in
+ * DESIGN.md readings E8-E9).  Fourth order, per constant step h,
  *   call 1 (Task I):  phi_1(c h J_n) h f(u_n) at both stage nodes c (one kiops_apply,
  *                     p = 1, T = the two nodes ascending, 1/T scaling);
  *   stages:           U_i = u_n + c_i * (call-1 output), r(U_i), b_3, b_4 (Eq. 11);
@@ -213,7 +215,7 @@ const char *kiops_last_error(kiops_ctx c);
  * r(U) = f(U) - f(u_n) - J_n (U - u_n) equals R(U) - R(u_n) - R'(u_n)(U - u_n)
  * exactly (the linear terms cancel), which is what the stage kernel evaluates.
  * =========================================================================== */
-typedef enum { KIOPS_EPIRK4S3 = 1, KIOPS_EPIRK4S3A = 2 } kiops_epirk_scheme;
+typedef enum { KIOPS_EPIRK4S3 = 1, KIOPS_EPIRK4S3A = 2, KIOPS_EPIRK5P1 = 3, KIOPS_EXPRB5S3 = 4 } kiops_epirk_scheme;
 
 typedef struct {
   int64_t nx, ny;          /* periodic grid, N = nx*ny, x fastest                          */
@@ -223,15 +225,18 @@ typedef struct {
 
 typedef struct {
   int64_t steps, krylov_vectors, passes, substeps, rejections, expm_calls;
-  int32_t final_m[2];      /* warm-start m of call 1 and call 2 after the last step         */
+  int32_t final_m[3];      /* warm-start m of calls 1-3 after the last step (4th order: 2 calls) */
   double kiops_ms;         /* device time in the two kiops_apply calls (%globaltimer sums)  */
 } kiops_epirk_stats;
 
 typedef struct kiops_epirk_s *kiops_epirk_ctx;
 
-/* Bytes of the caller-owned workspace for kiops_epirk_create (two kiops workspaces
- * of m_max+3 vectors each plus 10 stage vectors; 1024^2: ~2.2 GB at m_max = 128). */
-kiops_status kiops_epirk_workspace_bytes(const kiops_rd_problem *pb, const kiops_options *o, size_t *bytes);
+/* Bytes of the caller-owned workspace for kiops_epirk_create with this scheme (one kiops
+ * workspace of m_max+3 vectors per distinct call shape -- two for the fourth-order
+ * schemes and EPIRK5P1, three for EXPRB5s3 -- plus 11 stage vectors; 1024^2: ~2.3 GB
+ * at m_max = 128 for two shapes). */
+kiops_status kiops_epirk_workspace_bytes(const kiops_rd_problem *pb, int scheme, const kiops_options *o,
+                                         size_t *bytes);
 
 /* pb, o: HOST, copied.  h > 0: the constant step.  scheme: KIOPS_EPIRK4S3[A].
  * o: the KIOPS options of both calls (tol, m_*, max_attempts; task1 and staging are

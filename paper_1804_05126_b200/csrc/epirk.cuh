@@ -1,6 +1,8 @@
 // epirk.cuh -- SURVEY 8(f) row f1: EPIRK4s3 (Eq. 50) / EPIRK4s3A (Eq. 51) with the
-// two-call "mixed implementation" of Sec. 2 (Eqs. 9-11) on top of kiops_apply, for
-// u' = L u + R(u) (periodic 5-point L, cubic pointwise R; Allen-Cahn).
+// two-call "mixed implementation" of Sec. 2 (Eqs. 9-11), and the fifth-order EPIRK5P1
+// (Eq. 52, Table 1, reading E8) / EXPRB5s3 (Eq. 53) with three calls (reading E9), on
+// top of kiops_apply, for u' = L u + R(u) (periodic 5-point L, cubic pointwise R;
+// Allen-Cahn).
 // Included at the end of kiops.cu (one translation unit).  sm_100a, fp64.
 //
 // Per step (all on the ctx stream):
@@ -69,20 +71,87 @@ __global__ void __launch_bounds__(256) k_ep_update(long long N, const double *__
     u[i] += w[i];
 }
 
+// fifth-order stage kernels (oracle/epirk.py step5, operand for operand)
+#define EP_A11 0.3512959269505819
+#define EP_A21 0.8440547201165712
+#define EP_A22 1.690589160956896
+#define EP_B1 1.0
+#define EP_B2 1.272712731735689
+#define EP_B3 2.271459926542262
+__device__ __forceinline__ double ep_rem(const EpProblem &q, double un, double U) {
+  return ep_R(q, U) - ep_R(q, un) - ep_dR(q, un) * (U - un);
+}
+// EPIRK5P1 after call 1: t = h r(U2), U2 = u + a11 phi_1(g11 hJ) hf
+__global__ void __launch_bounds__(256) k_ep5p1_a(EpProblem q, const double *__restrict__ u, const double *__restrict__ o10,
+                                                 double *__restrict__ t) {
+  const long long N = q.nx * q.ny;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < N; i += (long long)gridDim.x * blockDim.x) {
+    const double un = u[i], U2 = un + EP_A11 * o10[i];
+    t[i] = q.h * ep_rem(q, un, U2);
+  }
+}
+// after call 2: U3 = u + a21 phi_1(g21 hJ) hf + a22 phi_1(g22 hJ) h r2; t = h (-2 r2 + r3)
+__global__ void __launch_bounds__(256) k_ep5p1_b(EpProblem q, const double *__restrict__ u, const double *__restrict__ o10,
+                                                 const double *__restrict__ o11, const double *__restrict__ o21,
+                                                 double *__restrict__ t) {
+  const long long N = q.nx * q.ny;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < N; i += (long long)gridDim.x * blockDim.x) {
+    const double un = u[i];
+    const double r2 = ep_rem(q, un, un + EP_A11 * o10[i]);
+    const double U3 = un + EP_A21 * o11[i] + EP_A22 * o21[i];
+    t[i] = q.h * (-2.0 * r2 + ep_rem(q, un, U3));
+  }
+}
+// after call 3: u = u + b1 phi_1(g31 hJ) hf + b2 phi_1(g32 hJ) h r2 + b3 phi_3(g33 hJ) h(-2 r2 + r3)
+__global__ void __launch_bounds__(256) k_ep5p1_c(long long N, const double *__restrict__ o12,
+                                                 const double *__restrict__ o20, const double *__restrict__ o3,
+                                                 double *__restrict__ u) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < N; i += (long long)gridDim.x * blockDim.x)
+    u[i] = u[i] + EP_B1 * o12[i] + EP_B2 * o20[i] + EP_B3 * o3[i];
+}
+// EXPRB5s3 after call 1: t = h r(U2), U2 = u + 1/2 phi_1(hJ/2) hf
+__global__ void __launch_bounds__(256) k_ex5_a(EpProblem q, const double *__restrict__ u, const double *__restrict__ o10,
+                                               double *__restrict__ t) {
+  const long long N = q.nx * q.ny;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < N; i += (long long)gridDim.x * blockDim.x) {
+    const double un = u[i];
+    t[i] = q.h * ep_rem(q, un, un + 0.5 * o10[i]);
+  }
+}
+// after call 2: U3 = u + 9/10 phi_1(9hJ/10) hf + 27/25 phi_3(hJ/2) h r2 + 729/125 phi_3(9hJ/10) h r2;
+// b3 = 18 h r2 - 250/81 h r3, b4 = -60 h r2 + 500/27 h r3 (Eq. 53)
+__global__ void __launch_bounds__(256) k_ex5_b(EpProblem q, const double *__restrict__ u, const double *__restrict__ o10,
+                                               const double *__restrict__ o11, const double *__restrict__ o20,
+                                               const double *__restrict__ o21, double *__restrict__ b3,
+                                               double *__restrict__ b4) {
+  const long long N = q.nx * q.ny;
+  const double h = q.h;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < N; i += (long long)gridDim.x * blockDim.x) {
+    const double un = u[i];
+    const double r2 = ep_rem(q, un, un + 0.5 * o10[i]);
+    const double U3 = un + 0.9 * o11[i] + (27.0 / 25.0) * o20[i] + (729.0 / 125.0) * o21[i];
+    const double r3 = ep_rem(q, un, U3);
+    b3[i] = 18.0 * h * r2 - (250.0 / 81.0) * h * r3;
+    b4[i] = -60.0 * h * r2 + (500.0 / 27.0) * h * r3;
+  }
+}
+
 struct kiops_epirk_s {
-  kiops_ctx k1 = nullptr, k2 = nullptr;
+  kiops_ctx kA = nullptr;        // p = 1, Task I (phi_1 at several T)
+  kiops_ctx kB = nullptr;        // p = 4, Task II at tau = 1      (4s3, 4s3A, EXPRB5s3)
+  kiops_ctx kC = nullptr;        // p = 3, Task I (phi_3)          (EPIRK5P1, EXPRB5s3)
   EpProblem q{};
   int scheme = 0;
-  double c2 = 0.0, c3 = 0.0;   // stage nodes of U_{n2}, U_{n3}
+  double c2 = 0.0, c3 = 0.0;     // fourth order: stage nodes of U_{n2}, U_{n3}
   cudaStream_t stream = nullptr;
-  double *d = nullptr, *b1 = nullptr, *zero = nullptr, *wa = nullptr, *wb = nullptr, *b3 = nullptr, *b4 = nullptr,
-         *w = nullptr;
-  int m1 = 0, m2 = 0;          // warm start of call 1 / call 2 (Sec. 3.6, reading E1)
+  double *d = nullptr, *b1 = nullptr, *zero = nullptr, *o1[3] = {}, *o2[2] = {}, *o3 = nullptr, *t1 = nullptr,
+         *t2 = nullptr;
+  int m[3] = {0, 0, 0};          // warm start of calls 1-3 (Sec. 3.6, reading E1)
   std::string err;
 };
 
 namespace {
-constexpr int EP_VECS = 8;
+constexpr int EP_VECS = 11;  // d, b1, zero, o1[3], o2[2], o3, t1, t2
 
 kiops_operator_desc ep_desc(const kiops_rd_problem *pb, double h, const double *d) {
   kiops_operator_desc o{};
@@ -94,30 +163,39 @@ kiops_operator_desc ep_desc(const kiops_rd_problem *pb, double h, const double *
   return o;
 }
 
-kiops_status ep_sizes(const kiops_rd_problem *pb, const kiops_options *o, size_t *b1, size_t *b2, size_t *vec) {
+bool ep_uses(int scheme, int which) {  // 0: kA, 1: kB, 2: kC
+  if (which == 0) return true;
+  if (which == 1) return scheme != KIOPS_EPIRK5P1;
+  return scheme == KIOPS_EPIRK5P1 || scheme == KIOPS_EXPRB5S3;
+}
+
+kiops_status ep_sizes(const kiops_rd_problem *pb, int scheme, const kiops_options *o, size_t b[3], size_t *vec) {
   if (!pb || !o || pb->nx < 1 || pb->ny < 1) return KIOPS_ERR_INVALID_ARG;
-  kiops_options o1 = *o, o2 = *o;
-  o1.task1 = 1; o1.host_staging = 0;
-  o2.task1 = 0; o2.host_staging = 0;
   const double fake = 0.0;
   kiops_operator_desc dsc = ep_desc(pb, 1.0, &fake);
-  kiops_status s = kiops_workspace_bytes(&dsc, 1, &o1, b1);
-  if (s != KIOPS_OK) return s;
-  s = kiops_workspace_bytes(&dsc, 4, &o2, b2);
-  if (s != KIOPS_OK) return s;
-  *b1 = (*b1 + 255) & ~(size_t)255;
-  *b2 = (*b2 + 255) & ~(size_t)255;
+  const int pk[3] = {1, 4, 3}, t1[3] = {1, 0, 1};
+  for (int i = 0; i < 3; i++) {
+    b[i] = 0;
+    if (!ep_uses(scheme, i)) continue;
+    kiops_options oi = *o;
+    oi.task1 = t1[i];
+    oi.host_staging = 0;
+    const kiops_status s = kiops_workspace_bytes(&dsc, pk[i], &oi, &b[i]);
+    if (s != KIOPS_OK) return s;
+    b[i] = (b[i] + 255) & ~(size_t)255;
+  }
   *vec = ((size_t)pb->nx * (size_t)pb->ny * sizeof(double) + 255) & ~(size_t)255;
   return KIOPS_OK;
 }
 }  // namespace
 
-kiops_status kiops_epirk_workspace_bytes(const kiops_rd_problem *pb, const kiops_options *o, size_t *bytes) {
-  if (!bytes) return KIOPS_ERR_INVALID_ARG;
-  size_t b1, b2, vec;
-  const kiops_status s = ep_sizes(pb, o, &b1, &b2, &vec);
+kiops_status kiops_epirk_workspace_bytes(const kiops_rd_problem *pb, int scheme, const kiops_options *o,
+                                         size_t *bytes) {
+  if (!bytes || scheme < KIOPS_EPIRK4S3 || scheme > KIOPS_EXPRB5S3) return KIOPS_ERR_INVALID_ARG;
+  size_t b[3], vec;
+  const kiops_status s = ep_sizes(pb, scheme, o, b, &vec);
   if (s != KIOPS_OK) return s;
-  *bytes = b1 + b2 + EP_VECS * vec;
+  *bytes = b[0] + b[1] + b[2] + EP_VECS * vec;
   return KIOPS_OK;
 }
 
@@ -125,13 +203,13 @@ kiops_status kiops_epirk_create(const kiops_rd_problem *pb, int scheme, double h
                                 void *cuda_stream, void *workspace, size_t workspace_bytes, kiops_epirk_ctx *out) {
   if (!out) return KIOPS_ERR_INVALID_ARG;
   *out = nullptr;
-  if (scheme != KIOPS_EPIRK4S3 && scheme != KIOPS_EPIRK4S3A) return KIOPS_ERR_INVALID_ARG;
+  if (scheme < KIOPS_EPIRK4S3 || scheme > KIOPS_EXPRB5S3) return KIOPS_ERR_INVALID_ARG;
   if (!(h > 0.0) || !std::isfinite(h)) return KIOPS_ERR_INVALID_ARG;
-  size_t b1, b2, vec;
-  kiops_status s = ep_sizes(pb, o, &b1, &b2, &vec);
+  size_t b[3], vec;
+  kiops_status s = ep_sizes(pb, scheme, o, b, &vec);
   if (s != KIOPS_OK) return s;
-  if (!workspace || ((uintptr_t)workspace & 255) || workspace_bytes < b1 + b2 + EP_VECS * vec)
-    return KIOPS_ERR_WORKSPACE;
+  const size_t kb = b[0] + b[1] + b[2];
+  if (!workspace || ((uintptr_t)workspace & 255) || workspace_bytes < kb + EP_VECS * vec) return KIOPS_ERR_WORKSPACE;
   kiops_epirk_ctx e = new (std::nothrow) kiops_epirk_s();
   if (!e) return KIOPS_ERR_WORKSPACE;
   e->scheme = scheme;
@@ -139,17 +217,24 @@ kiops_status kiops_epirk_create(const kiops_rd_problem *pb, int scheme, double h
   e->q.nx = pb->nx; e->q.ny = pb->ny; e->q.h = h;
   for (int i = 0; i < 5; i++) e->q.w[i] = pb->w[i];
   for (int i = 0; i < 4; i++) e->q.c[i] = pb->c[i];
-  if (scheme == KIOPS_EPIRK4S3) { e->c2 = 1.0 / 8.0; e->c3 = 1.0 / 9.0; }   // Eq. 50
-  else { e->c2 = 1.0 / 2.0; e->c3 = 2.0 / 3.0; }                             // Eq. 51
+  if (scheme == KIOPS_EPIRK4S3) { e->c2 = 1.0 / 8.0; e->c3 = 1.0 / 9.0; }        // Eq. 50
+  else if (scheme == KIOPS_EPIRK4S3A) { e->c2 = 1.0 / 2.0; e->c3 = 2.0 / 3.0; }  // Eq. 51
   unsigned char *ws = (unsigned char *)workspace;
-  double **vp[EP_VECS] = {&e->d, &e->b1, &e->zero, &e->wa, &e->wb, &e->b3, &e->b4, &e->w};
-  for (int i = 0; i < EP_VECS; i++) *vp[i] = (double *)(ws + b1 + b2 + (size_t)i * vec);
-  kiops_options o1 = *o, o2 = *o;
-  o1.task1 = 1; o1.host_staging = 0;
-  o2.task1 = 0; o2.host_staging = 0;
+  double **vp[EP_VECS] = {&e->d, &e->b1, &e->zero, &e->o1[0], &e->o1[1], &e->o1[2], &e->o2[0], &e->o2[1],
+                          &e->o3, &e->t1, &e->t2};
+  for (int i = 0; i < EP_VECS; i++) *vp[i] = (double *)(ws + kb + (size_t)i * vec);
   const kiops_operator_desc dsc = ep_desc(pb, h, e->d);
-  s = kiops_create(&dsc, 1, &o1, cuda_stream, ws, b1, &e->k1);
-  if (s == KIOPS_OK) s = kiops_create(&dsc, 4, &o2, cuda_stream, ws + b1, b2, &e->k2);
+  const int pk[3] = {1, 4, 3}, t1[3] = {1, 0, 1};
+  kiops_ctx *kc[3] = {&e->kA, &e->kB, &e->kC};
+  size_t off = 0;
+  for (int i = 0; i < 3 && s == KIOPS_OK; i++) {
+    if (!ep_uses(scheme, i)) continue;
+    kiops_options oi = *o;
+    oi.task1 = t1[i];
+    oi.host_staging = 0;
+    s = kiops_create(&dsc, pk[i], &oi, cuda_stream, ws + off, b[i], kc[i]);
+    off += b[i];
+  }
   if (s == KIOPS_OK) {
     const cudaError_t ce = cudaMemsetAsync(e->zero, 0, vec, e->stream);
     if (ce != cudaSuccess) { e->err = cudaGetErrorString(ce); s = KIOPS_ERR_CUDA; }
@@ -162,55 +247,98 @@ kiops_status kiops_epirk_create(const kiops_rd_problem *pb, int scheme, double h
   return KIOPS_OK;
 }
 
+namespace {
+// one kiops_apply of the step with warm start; accumulates the stats
+kiops_status ep_call(kiops_epirk_ctx e, kiops_ctx k, int call, int step, const double *const *u, const double *T,
+                     int n_out, double *const *w, kiops_epirk_stats *acc) {
+  kiops_stats st{};
+  kiops_set_m_init(k, e->m[call]);
+  const kiops_status s = kiops_apply(k, u, T, n_out, w, &st);
+  if (s != KIOPS_OK) {
+    e->err = "step " + std::to_string(step) + ", call " + std::to_string(call + 1) + ": " + kiops_last_error(k);
+    return s;
+  }
+  e->m[call] = st.final_m;
+  acc->krylov_vectors += st.krylov_vectors;
+  acc->passes += st.passes;
+  acc->substeps += st.substeps;
+  acc->rejections += st.rejections;
+  acc->expm_calls += st.expm_calls;
+  acc->kiops_ms += st.pass_ms + st.ctrl_ms + st.gemv_ms;
+  return KIOPS_OK;
+}
+}  // namespace
+
 kiops_status kiops_epirk_step(kiops_epirk_ctx e, double *u, int nsteps, kiops_epirk_stats *stats) {
   if (!e || !u || nsteps < 0) return KIOPS_ERR_INVALID_ARG;
   const long long N = e->q.nx * e->q.ny;
   const int grid = (int)std::min<long long>((N + 255) / 256, SM_COUNT_HINT * 8);
   kiops_epirk_stats acc{};
-  const bool asc = e->c2 < e->c3;  // call-1 outputs come in ascending T
-  const double T1[2] = {asc ? e->c2 : e->c3, asc ? e->c3 : e->c2};
-  double *w1[2] = {e->wa, e->wb};
-  const double *w2 = asc ? e->wa : e->wb, *w3 = asc ? e->wb : e->wa;
+  const double *z = e->zero;
+#define EP_LAUNCHED(name) \
+  if (cudaGetLastError() != cudaSuccess) { e->err = name " launch"; return KIOPS_ERR_CUDA; }
   for (int n = 0; n < nsteps; n++) {
+    kiops_status s;
     k_ep_f<<<grid, 256, 0, e->stream>>>(e->q, u, e->d, e->b1);
-    if (cudaGetLastError() != cudaSuccess) { e->err = "k_ep_f launch"; return KIOPS_ERR_CUDA; }
-    kiops_stats s1{}, s2{};
-    const double *u1[2] = {e->zero, e->b1};
-    kiops_set_m_init(e->k1, e->m1);
-    kiops_status s = kiops_apply(e->k1, u1, T1, 2, w1, &s1);
-    if (s != KIOPS_OK) { e->err = "step " + std::to_string(n) + ", call 1: " + kiops_last_error(e->k1); return s; }
-    e->m1 = s1.final_m;
-    k_ep_stage<<<grid, 256, 0, e->stream>>>(e->q, e->scheme, e->c2, e->c3, u, w2, w3, e->b3, e->b4);
-    if (cudaGetLastError() != cudaSuccess) { e->err = "k_ep_stage launch"; return KIOPS_ERR_CUDA; }
-    const double *u2[5] = {e->zero, e->b1, e->zero, e->b3, e->b4};
-    const double T2[1] = {1.0};
-    double *wo[1] = {e->w};
-    kiops_set_m_init(e->k2, e->m2);
-    s = kiops_apply(e->k2, u2, T2, 1, wo, &s2);
-    if (s != KIOPS_OK) { e->err = "step " + std::to_string(n) + ", call 2: " + kiops_last_error(e->k2); return s; }
-    e->m2 = s2.final_m;
-    k_ep_update<<<grid, 256, 0, e->stream>>>(N, e->w, u);
-    if (cudaGetLastError() != cudaSuccess) { e->err = "k_ep_update launch"; return KIOPS_ERR_CUDA; }
+    EP_LAUNCHED("k_ep_f");
+    const double *uf[2] = {z, e->b1};
+    if (e->scheme == KIOPS_EPIRK4S3 || e->scheme == KIOPS_EPIRK4S3A) {
+      const bool asc = e->c2 < e->c3;  // call-1 outputs come in ascending T
+      const double T1[2] = {asc ? e->c2 : e->c3, asc ? e->c3 : e->c2};
+      if ((s = ep_call(e, e->kA, 0, n, uf, T1, 2, e->o1, &acc)) != KIOPS_OK) return s;
+      k_ep_stage<<<grid, 256, 0, e->stream>>>(e->q, e->scheme, e->c2, e->c3, u, asc ? e->o1[0] : e->o1[1],
+                                              asc ? e->o1[1] : e->o1[0], e->t1, e->t2);
+      EP_LAUNCHED("k_ep_stage");
+      const double *u2[5] = {z, e->b1, z, e->t1, e->t2};
+      const double T2[1] = {1.0};
+      if ((s = ep_call(e, e->kB, 1, n, u2, T2, 1, &e->o3, &acc)) != KIOPS_OK) return s;
+      k_ep_update<<<grid, 256, 0, e->stream>>>(N, e->o3, u);
+      EP_LAUNCHED("k_ep_update");
+    } else if (e->scheme == KIOPS_EPIRK5P1) {  // Eq. 52, Table 1
+      const double T1[3] = {0.3512959269505819, 0.8440547201165712, 1.0};  // g11, g21, g31
+      if ((s = ep_call(e, e->kA, 0, n, uf, T1, 3, e->o1, &acc)) != KIOPS_OK) return s;
+      k_ep5p1_a<<<grid, 256, 0, e->stream>>>(e->q, u, e->o1[0], e->t1);
+      EP_LAUNCHED("k_ep5p1_a");
+      const double *u2[2] = {z, e->t1};
+      const double T2[2] = {0.71111109536436687, 1.0};  // g32, g22
+      if ((s = ep_call(e, e->kA, 1, n, u2, T2, 2, e->o2, &acc)) != KIOPS_OK) return s;
+      k_ep5p1_b<<<grid, 256, 0, e->stream>>>(e->q, u, e->o1[0], e->o1[1], e->o2[1], e->t1);
+      EP_LAUNCHED("k_ep5p1_b");
+      const double *u3[4] = {z, z, z, e->t1};
+      const double T3[1] = {0.6237811195337149};  // g33
+      if ((s = ep_call(e, e->kC, 2, n, u3, T3, 1, &e->o3, &acc)) != KIOPS_OK) return s;
+      k_ep5p1_c<<<grid, 256, 0, e->stream>>>(N, e->o1[2], e->o2[0], e->o3, u);
+      EP_LAUNCHED("k_ep5p1_c");
+    } else {  // EXPRB5s3, Eq. 53
+      const double T1[2] = {0.5, 0.9};
+      if ((s = ep_call(e, e->kA, 0, n, uf, T1, 2, e->o1, &acc)) != KIOPS_OK) return s;
+      k_ex5_a<<<grid, 256, 0, e->stream>>>(e->q, u, e->o1[0], e->t1);
+      EP_LAUNCHED("k_ex5_a");
+      const double *u2[4] = {z, z, z, e->t1};
+      if ((s = ep_call(e, e->kC, 1, n, u2, T1, 2, e->o2, &acc)) != KIOPS_OK) return s;
+      k_ex5_b<<<grid, 256, 0, e->stream>>>(e->q, u, e->o1[0], e->o1[1], e->o2[0], e->o2[1], e->t1, e->t2);
+      EP_LAUNCHED("k_ex5_b");
+      const double *u3[5] = {z, e->b1, z, e->t1, e->t2};
+      const double T3[1] = {1.0};
+      if ((s = ep_call(e, e->kB, 2, n, u3, T3, 1, &e->o3, &acc)) != KIOPS_OK) return s;
+      k_ep_update<<<grid, 256, 0, e->stream>>>(N, e->o3, u);
+      EP_LAUNCHED("k_ep_update");
+    }
     acc.steps++;
-    acc.krylov_vectors += s1.krylov_vectors + s2.krylov_vectors;
-    acc.passes += s1.passes + s2.passes;
-    acc.substeps += s1.substeps + s2.substeps;
-    acc.rejections += s1.rejections + s2.rejections;
-    acc.expm_calls += s1.expm_calls + s2.expm_calls;
-    acc.kiops_ms += s1.pass_ms + s1.ctrl_ms + s1.gemv_ms + s2.pass_ms + s2.ctrl_ms + s2.gemv_ms;
   }
+#undef EP_LAUNCHED
   const cudaError_t ce = cudaStreamSynchronize(e->stream);
   if (ce != cudaSuccess) { e->err = cudaGetErrorString(ce); return KIOPS_ERR_CUDA; }
-  acc.final_m[0] = e->m1;
-  acc.final_m[1] = e->m2;
+  for (int i = 0; i < 3; i++) acc.final_m[i] = e->m[i];
   if (stats) *stats = acc;
   return KIOPS_OK;
 }
 
 kiops_status kiops_epirk_destroy(kiops_epirk_ctx e) {
   if (!e) return KIOPS_ERR_INVALID_ARG;
-  if (e->k1) kiops_destroy(e->k1);
-  if (e->k2) kiops_destroy(e->k2);
+  if (e->kA) kiops_destroy(e->kA);
+  if (e->kB) kiops_destroy(e->kB);
+  if (e->kC) kiops_destroy(e->kC);
   delete e;
   return KIOPS_OK;
 }

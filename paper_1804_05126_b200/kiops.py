@@ -65,10 +65,10 @@ class RDProblem(C.Structure):
 class EpirkStats(C.Structure):
     _fields_ = [("steps", C.c_int64), ("krylov_vectors", C.c_int64), ("passes", C.c_int64),
                 ("substeps", C.c_int64), ("rejections", C.c_int64), ("expm_calls", C.c_int64),
-                ("final_m", C.c_int32 * 2), ("kiops_ms", C.c_double)]
+                ("final_m", C.c_int32 * 3), ("kiops_ms", C.c_double)]
 
 
-EPIRK_SCHEMES = {"epirk4s3": 1, "epirk4s3a": 2}
+EPIRK_SCHEMES = {"epirk4s3": 1, "epirk4s3a": 2, "epirk5p1": 3, "exprb5s3": 4}
 
 _lib = None
 
@@ -95,7 +95,8 @@ def lib():
                                                 C.c_int]
         L.kiops_debug_basis.argtypes = [C.c_void_p, _dp, _dp, C.POINTER(C.c_int32)]
         L.kiops_set_m_init.argtypes = [C.c_void_p, C.c_int]
-        L.kiops_epirk_workspace_bytes.argtypes = [C.POINTER(RDProblem), C.POINTER(Options), C.POINTER(C.c_size_t)]
+        L.kiops_epirk_workspace_bytes.argtypes = [C.POINTER(RDProblem), C.c_int, C.POINTER(Options),
+                                                  C.POINTER(C.c_size_t)]
         L.kiops_epirk_create.argtypes = [C.POINTER(RDProblem), C.c_int, C.c_double, C.POINTER(Options), C.c_void_p,
                                          C.c_void_p, C.c_size_t, C.POINTER(C.c_void_p)]
         L.kiops_epirk_step.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.POINTER(EpirkStats)]
@@ -291,6 +292,7 @@ class KiopsEpirk:
             raise RuntimeError("KIOPS B200 path needs a CUDA device (no CPU fallback)")
         self.torch = torch
         self.device = torch.device(device)
+        self.scheme = scheme
         self.N = int(problem["nx"]) * int(problem["ny"])
         pb = RDProblem()
         pb.nx, pb.ny = int(problem["nx"]), int(problem["ny"])
@@ -301,7 +303,7 @@ class KiopsEpirk:
         self.pb = pb
         self.opts = default_options(**options)
         nb = C.c_size_t(0)
-        s = lib().kiops_epirk_workspace_bytes(C.byref(pb), C.byref(self.opts), C.byref(nb))
+        s = lib().kiops_epirk_workspace_bytes(C.byref(pb), EPIRK_SCHEMES[scheme], C.byref(self.opts), C.byref(nb))
         if s != 0:
             raise KiopsError(s, "kiops_epirk_workspace_bytes")
         self.workspace = torch.empty(nb.value + 256, dtype=torch.uint8, device=self.device)
@@ -323,7 +325,7 @@ class KiopsEpirk:
             msg = lib().kiops_epirk_last_error(self.ctx)
             raise KiopsError(s, f"kiops_epirk_step: {msg.decode() if msg else ''}")
         out = {k: getattr(st, k) for k, _ in EpirkStats._fields_ if k != "final_m"}
-        out["final_m"] = (st.final_m[0], st.final_m[1])
+        out["final_m"] = tuple(st.final_m[i] for i in range(3 if self.scheme in ("epirk5p1", "exprb5s3") else 2))
         return out
 
     def close(self):

@@ -1,4 +1,5 @@
-"""EPIRK driver measurement: constant-step EPIRK4s3 / EPIRK4s3A on the
+"""EPIRK driver measurement: constant-step EPIRK4s3 / EPIRK4s3A /
+EPIRK5P1 / EXPRB5s3 on the
 periodic Allen-Cahn 2D problem (Sec. 4; reading E4) through kiops_epirk_step,
 timed with CUDA events on the ctx stream after warm-up steps; the oracle EPIRK
 (oracle/epirk.py, 1 thread) timed on a bounded sample of the same steps.  Prints one
@@ -18,7 +19,7 @@ from paper_1804_05126_b200 import KiopsEpirk  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--n", type=int, default=1024)
-ap.add_argument("--scheme", default="epirk4s3", choices=["epirk4s3", "epirk4s3a"])
+ap.add_argument("--scheme", default="epirk4s3", choices=["epirk4s3", "epirk4s3a", "epirk5p1", "exprb5s3"])
 ap.add_argument("--h", type=float, default=0.01)
 ap.add_argument("--tol", type=float, default=1e-10)
 ap.add_argument("--steps", type=int, default=5)
@@ -49,7 +50,7 @@ line = {"metric": f"{a.scheme} step time, Allen-Cahn 2D periodic (EPIRK driver, 
         "unit": "ms/step", "n_gpus": 1, "steps": a.steps, "warmup": a.warmup, "higher_is_better": False,
         "dtype": "f64", "data": "synthetic (paper's Allen-Cahn initial condition)",
         "config": {"workload": f"allen_cahn_2d_{n}x{n}", "N": n * n, "h": a.h, "tol": a.tol, "scheme": a.scheme,
-                   "kiops_calls_per_step": 2,
+                   "kiops_calls_per_step": 3 if a.scheme in ("epirk5p1", "exprb5s3") else 2,
                    "per_step": {"krylov_vectors": st["krylov_vectors"] / a.steps, "passes": st["passes"] / a.steps,
                                 "rejections": st["rejections"] / a.steps,
                                 "kiops_device_ms": st["kiops_ms"] / a.steps},
@@ -61,9 +62,10 @@ if a.oracle_steps > 0:
     prob = E.ReactionDiffusion2D(n, alpha=alpha)
     y = u0.copy()
     t0 = time.perf_counter()
-    m = (10, 10)
+    five = a.scheme in E.SCHEMES5
+    m = (10, 10, 10) if five else (10, 10)
     for _ in range(a.oracle_steps):
-        y, m, _ = E.step(prob, a.scheme, y, a.h, tol=a.tol, m_hint=m)
+        y, m, _ = (E.step5 if five else E.step)(prob, a.scheme, y, a.h, tol=a.tol, m_hint=m)
     cpu_ms = (time.perf_counter() - t0) * 1e3 / a.oracle_steps
     line["cpu_baseline"] = {"value": cpu_ms, "unit": "ms/step", "cores": 1, "kind": "oracle",
                             "sample": f"first {a.oracle_steps} step(s) of the same run from u_0 (oracle EPIRK over the C KIOPS oracle)"}

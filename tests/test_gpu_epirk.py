@@ -20,7 +20,7 @@ def rd(n, ny, alpha=0.1):
     return prob, {"nx": n, "ny": ny, "w": [wa, wa, wa, wa, -4.0 * wa], "c": list(prob.c)}
 
 
-@pytest.mark.parametrize("scheme", E.SCHEMES)
+@pytest.mark.parametrize("scheme", E.SCHEMES + E.SCHEMES5)
 @pytest.mark.parametrize("dims", [(48, 40), (64, 64)])
 def test_epirk_matches_oracle(scheme, dims):
     from paper_1804_05126_b200 import KiopsEpirk
