@@ -84,7 +84,8 @@ typedef struct {
 typedef struct {
   double tol;             /* Eq. 39 tolerance (absolute, 2-norm of the scaled augmented vector, R18) */
   int32_t m_init, m_min, m_max; /* 1 <= m_min <= m_max <= KIOPS_MAX_M                   */
-  int32_t iop_q;          /* IOP window; this build supports 2 (Alg. 2 as printed)       */
+  int32_t iop_q;          /* IOP window, 1 <= q <= m_max (q = m_max: full Arnoldi); q = 2 (Alg. 2
+                           * as printed) runs the fused kernels, other q a generic 4-launch pass */
   int32_t task1;          /* 1 => output l scaled by 1/T_l^p (Alg. 1 l.31-35) */
   int64_t max_attempts;   /* accepted + rejected attempts before KIOPS_ERR_NO_CONVERGENCE */
   int32_t host_staging;   /* 1 => workspace also holds device staging for kiops_apply_host */

@@ -665,11 +665,11 @@ __global__ void __cluster_dims__(CTRL_CL, 1, 1) __launch_bounds__(CTRL_THREADS, 
     return;
   }
   const int n1 = j + 1, g0 = cl_gtid(), gs = cl_gsize();
-  // R1 / Eq. 37: H~ = [[H(1:j,1:j), e_1],[0, 0]] from the IOP band (q = 2)
+  // R1 / Eq. 37: H~ = [[H(1:j,1:j), e_1],[0, 0]] from the IOP band (rows c-q+1 .. c+1)
   for (int e = g0; e < n1 * n1; e += gs) {
     const int r = e % n1, c = e / n1;
     double v = 0.0;
-    if (r < j && c < j && r >= c - 1 && r <= c + 1) v = P.H[r + (size_t)LDH * c];
+    if (r < j && c < j && r >= c - P.q + 1 && r <= c + 1) v = P.H[r + (size_t)LDH * c];  // IOP band
     if (r == 0 && c == j) v = 1.0;
     Mh[r + (size_t)LDH * c] = v;
   }
@@ -744,7 +744,7 @@ __global__ void __cluster_dims__(CTRL_CL, 1, 1) __launch_bounds__(CTRL_THREADS, 
     for (int k = 0; k < n_tau; k++) {
       for (int e = g0; e < j * j; e += gs) {
         const int r = e % j, c = e / j;
-        Mh[r + (size_t)LDH * c] = (r >= c - 1 && r <= c + 1) ? P.H[r + (size_t)LDH * c] : 0.0;
+        Mh[r + (size_t)LDH * c] = (r >= c - P.q + 1 && r <= c + 1) ? P.H[r + (size_t)LDH * c] : 0.0;
       }
       cl_sync();
       const double tt = call->T[l0 + k] - t_now;

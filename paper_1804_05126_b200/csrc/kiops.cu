@@ -25,6 +25,7 @@
 #include <vector>
 
 #include "controller.cuh"
+#include "passq.cuh"
 #include "kiops_internal.cuh"
 #include "passes.cuh"
 
@@ -49,7 +50,7 @@ constexpr int SM_COUNT_HINT = 148;
 
 struct Layout {
   size_t V, r, staging, state, call, H, sig, R2, tails, partials, npart, scratch, coef, trace, sell_off, sell_col,
-      sell_val, total;
+      sell_val, qa, gram, qpart, total;
   long long sell_entries;
   long long ldN;
   int grid_pass, grid_setup, grid_gemv, grid_form, grid_max;
@@ -70,7 +71,6 @@ kiops_status validate(const kiops_operator_desc *op, int p, const kiops_options 
   if (o->m_max > KIOPS_MAX_M) { err = "m_max > KIOPS_MAX_M (single-CTA exponential of (m_max+1)^2)"; return KIOPS_ERR_UNSUPPORTED; }
   if (o->m_init < 1) { err = "m_init must be >= 1"; return KIOPS_ERR_INVALID_ARG; }
   if (o->iop_q < 1 || o->iop_q > o->m_max) { err = "need 1 <= iop_q <= m_max"; return KIOPS_ERR_INVALID_ARG; }
-  if (o->iop_q != 2) { err = "this build implements the IOP window q = 2 (Alg. 2 as printed)"; return KIOPS_ERR_UNSUPPORTED; }
   if (o->max_attempts < 1) { err = "max_attempts must be >= 1"; return KIOPS_ERR_INVALID_ARG; }
   if (o->host_staging && (o->max_outputs < 1 || o->max_outputs > KIOPS_MAX_OUT)) {
     err = "max_outputs must be in [1, KIOPS_MAX_OUT]"; return KIOPS_ERR_INVALID_ARG;
@@ -180,6 +180,9 @@ Layout layout(const kiops_operator_desc *op, int p, const kiops_options *o) {
   L.scratch = off; off += al(sizeof(double) * NSCR * (size_t)LDH * LDH);
   L.coef = off; off += al(sizeof(double) * (KMAXO + 1) * (size_t)LDH);
   L.trace = off; off += al(sizeof(kiops_trace_row) * (size_t)KIOPS_TRACE_CAP);
+  L.qa = off; off += al(sizeof(double) * (size_t)LDH);                          // generic-q path
+  L.gram = off; off += al(sizeof(double) * (size_t)LDH * LDH);
+  L.qpart = off; off += al(sizeof(double) * (2 * (size_t)LDH + 2) * QG);
   L.sell_entries = 0;
   if (op->kind == KIOPS_OP_CSR) {  // SELL-32 copy: exact size from the row lengths
     const long long ns = (N + 31) / 32;
@@ -238,12 +241,12 @@ static kiops_status cuda_fail(kiops_ctx c, cudaError_t e, const char *what) {
   } while (0)
 
 static cudaError_t add_kernel(cudaGraph_t g, cudaGraphNode_t *node, const cudaGraphNode_t *deps, size_t nd,
-                              void *func, int grid, int block, size_t smem, KParams *P) {
+                              void *func, int grid, int block, size_t smem, KParams *P, int grid_y = 1) {
   cudaGraphNodeParams np = {};
   np.type = cudaGraphNodeTypeKernel;
   void *args[] = {P};
   np.kernel.func = func;
-  np.kernel.gridDim = dim3(grid);
+  np.kernel.gridDim = dim3(grid, grid_y);
   np.kernel.blockDim = dim3(block);
   np.kernel.sharedMemBytes = (unsigned)smem;
   np.kernel.kernelParams = args;
@@ -303,7 +306,13 @@ static kiops_status build_graph(kiops_ctx c) {
   CK(add_kernel(c->graph, &n_setup, nullptr, 0, (void *)k_setup, c->L.grid_setup, 256, 0, &P), "node setup");
   CK(add_cond(c->graph, &n_outer, &n_setup, 1, P.h_outer, cudaGraphCondTypeWhile, &b_outer), "node outer");
   CK(add_cond(b_outer, &n_inner, nullptr, 0, P.h_inner, cudaGraphCondTypeWhile, &b_inner), "node inner");
-  if (c->op.kind == KIOPS_OP_CSR) {
+  if (P.q != 2) {  // generic IOP window (passq.cuh): form, apply, window dots, finalise
+    cudaGraphNode_t n_c, n_d;
+    CK(add_kernel(b_inner, &n_a, nullptr, 0, (void *)k_q_form, c->L.grid_form, 256, 0, &P), "node q form");
+    CK(add_kernel(b_inner, &n_b, &n_a, 1, (void *)k_q_apply, QG, 256, 0, &P), "node q apply");
+    CK(add_kernel(b_inner, &n_c, &n_b, 1, (void *)k_q_dots, QG, 256, 0, &P, P.q), "node q dots");
+    CK(add_kernel(b_inner, &n_d, &n_c, 1, (void *)k_q_finalize, 1, 256, 0, &P), "node q finalize");
+  } else if (c->op.kind == KIOPS_OP_CSR) {
     CK(add_kernel(b_inner, &n_a, nullptr, 0, (void *)k_csr_form, c->L.grid_form, 256, 0, &P), "node form");
     CK(add_kernel(b_inner, &n_b, &n_a, 1, (void *)k_sell_spmv, c->L.grid_pass, 256, 0, &P), "node spmv");
   } else {
@@ -364,7 +373,10 @@ kiops_status kiops_create(const kiops_operator_desc *op, int p, const kiops_opti
   P.nx = op->nx; P.ny = op->ny; P.nz = op->nz;
   P.N = op_n(op);
   P.ldN = L.ldN;
-  for (int i = 0; i < 5; i++) P.w[i] = op->w[i];
+  for (int i = 0; i < 5; i++) P.w[i] = P.w5[i] = op->w[i];
+  if (op->kind == KIOPS_OP_STENCIL1D3) {  // 1D {W, C, E} -> {W, E, 0, 0, C}
+    P.w5[0] = op->w[0]; P.w5[1] = op->w[2]; P.w5[2] = 0.0; P.w5[3] = 0.0; P.w5[4] = op->w[1];
+  }
   if (op->kind == KIOPS_OP_STENCIL1D3 && op->nx % 2 == 0 && p <= 4) {
     // the 1D operator runs on the 2D warp-strip kernel (ny = 1): {W, E, S, N, C} = {W, E, 0, 0, C}
     P.w[0] = op->w[0]; P.w[1] = op->w[2]; P.w[2] = 0.0; P.w[3] = 0.0; P.w[4] = op->w[1];
@@ -394,6 +406,10 @@ kiops_status kiops_create(const kiops_operator_desc *op, int p, const kiops_opti
   P.scratch = (double *)(w + L.scratch);
   P.coef = (double *)(w + L.coef);
   P.trace = (kiops_trace_row *)(w + L.trace);
+  P.qa = (double *)(w + L.qa);
+  P.gram = (double *)(w + L.gram);
+  P.qpart = (double *)(w + L.qpart);
+  P.q = o->iop_q;
   if (op->kind == KIOPS_OP_CSR) {
     P.sell_off = (const long long *)(w + L.sell_off);
     P.sell_col = (const int *)(w + L.sell_col);
@@ -563,7 +579,13 @@ kiops_status kiops_apply_hostloop(kiops_ctx c, const double *const *u, const dou
   if ((s = read_conds(c, cond)) != KIOPS_OK) return s;
   while (cond[COND_OUTER]) {
     while (cond[COND_INNER]) {
-      if (c->op.kind == KIOPS_OP_CSR) {
+      if (P.q != 2) {
+        void *args[] = {&P};
+        if ((s = launch_plain(c, (void *)k_q_form, c->L.grid_form, 256, 0, &P)) != KIOPS_OK) return s;
+        if ((s = launch_plain(c, (void *)k_q_apply, QG, 256, 0, &P)) != KIOPS_OK) return s;
+        CK(cudaLaunchKernel((void *)k_q_dots, dim3(QG, P.q), dim3(256), args, 0, c->stream), "k_q_dots");
+        if ((s = launch_plain(c, (void *)k_q_finalize, 1, 256, 0, &P)) != KIOPS_OK) return s;
+      } else if (c->op.kind == KIOPS_OP_CSR) {
         if ((s = launch_plain(c, (void *)k_csr_form, c->L.grid_form, 256, 0, &P)) != KIOPS_OK) return s;
         if ((s = launch_plain(c, (void *)k_sell_spmv, c->L.grid_pass, 256, 0, &P)) != KIOPS_OK) return s;
       } else {

@@ -55,6 +55,7 @@ struct KParams {
   int kind;
   long long nx, ny, nz, N, ldN;
   double w[5];
+  double w5[5];       // 1D/2D weights as {W, E, S, N, C} for every nx (generic-q path)
   const double *diag, *kappa;
   double inv_h2;
   const long long *row_ptr;
@@ -81,6 +82,10 @@ struct KParams {
   double *coef;       // (KMAXO+1) x LDH    (GEMV coefficients)
   kiops_trace_row *trace;
   int grid_pass, grid_max;
+  int q;              // IOP window (2: fused kernels; else passq.cuh)
+  double *qa;         // generic q: formation coefficients of the next x (LDH)
+  double *gram;       // generic q: G(i,l) = x_i . x_l, LDH x LDH column-major
+  double *qpart;      // generic q: (2 LDH + 2) x QG dot partials
   int no_cond;        // 1: launched outside the graph (host-loop profiling hook)
   cudaGraphConditionalHandle h_outer, h_inner, h_accept;
 };

@@ -87,7 +87,7 @@ def test_workspace_bytes_layout(L):
 
 @pytest.mark.parametrize("bad,status", [
     ({"tol": 0.0}, 1), ({"m_min": 0}, 1), ({"m_min": 20, "m_max": 10}, 1), ({"iop_q": 0}, 1),
-    ({"iop_q": 3}, 2), ({"m_max": 200}, 2), ({"max_attempts": 0}, 1)])
+    ({"iop_q": 129}, 1), ({"m_max": 200}, 2), ({"max_attempts": 0}, 1)])
 def test_validation_before_any_launch(L, bad, status):
     from paper_1804_05126_b200 import kiops as K
     from workloads import configs as W

@@ -280,3 +280,14 @@ def test_config4_full_size_trace_vs_stored_oracle_run():
         assert gs[key] == ref["stats"][key], key
     for l, nrm in enumerate(ref["out_norms"]):
         assert abs(np.linalg.norm(g[l]) - nrm) <= 1e-10 * nrm, (l, np.linalg.norm(g[l]), nrm)
+
+
+# IOP windows q != 2 (generic path, passq.cuh) against the oracle's
+# general-q IOP (Alg. 2 with the window of l.7; q = m_max is full Arnoldi)
+@pytest.mark.parametrize("q", [1, 3, 5, 128])
+@pytest.mark.parametrize("make", [lambda: W.config1(), lambda: W.config2(64, 48), lambda: W.config3(96, 64),
+                                  lambda: W.config5(20, 20, 20), lambda: W.config4(16, 16, 16)],
+                         ids=["c1", "c2", "c3", "c5", "c4"])
+def test_iop_window_q(make, q):
+    c = make()
+    assert_parity(c, iop_q=q, strict=c["op"]["kind"] != "stencil3d7")
