@@ -7,7 +7,6 @@
 
 #define CTRL_THREADS 512
 #define CTRL_CL 8    // CTAs per controller cluster (portable maximum)
-#define MM_KP 32     // k-panel depth of the matmul (fewer barriers per product)
 
 // ---------------------------------------------------------------------------
 // Dense n x n (n <= KMAXM+1) linear algebra for ONE thread-block CLUSTER of
@@ -27,53 +26,64 @@ __device__ __forceinline__ unsigned cl_rank() {
 __device__ __forceinline__ int cl_gtid() { return (int)(cl_rank() * blockDim.x + threadIdx.x); }
 __device__ __forceinline__ int cl_gsize() { return (int)(CTRL_CL * blockDim.x); }
 
+// D += A B for one 8x8x4 FP64 tensor-core tile (mma.sync m8n8k4 .f64): fragments per
+// lane g = lane/4, t = lane%4: A(g, t), B(t, g), C(g, 2t), C(g, 2t+1).
+__device__ __forceinline__ void dmma_8x8x4(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};\n"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+// C = A B (ld LDH, no aliasing), n <= KMAXM+1, on the FP64 tensor cores.  CTA r owns
+// the 8-column output tiles r, r+8, ...: it stages ALL of A (n x np, ld MM_LD) and its
+// B column panels in shared memory (coalesced .cg loads -- other CTAs wrote them -- all
+// independent, so one L2 round trip instead of one per k-step), then its warps run
+// m8n8k4 DMMA from shared memory over the tile rows (zero-padded to multiples of 8).
+#define MM_LD 148  // >= KMAXM+1 rounded to 8, = 4 mod 16: the fragment loads are bank-conflict free
 __device__ void cl_matmul(int n, const double *__restrict__ A, const double *__restrict__ B, double *__restrict__ C,
                           double *sm) {
-  // C = A B (no aliasing).  4x4 register micro-tiles; tile t belongs to CTA t % CL.
-  const int np = (n + 3) & ~3, tr = np >> 2, ntiles = tr * tr;
-  const int rank = (int)cl_rank();
-  double *sA = sm;               // np x KP   sA[i + np*kk]
-  double *sB = sm + np * MM_KP;  // np x KP   sB[j + np*kk]  (transposed panel)
-  const int nmine = (ntiles - rank + CTRL_CL - 1) / CTRL_CL;
-  for (int r0 = 0; r0 < nmine; r0 += blockDim.x) {
-    const int tl = r0 + threadIdx.x;
-    const bool act = tl < nmine;
-    const int t = rank + CTRL_CL * tl;
-    const int ti = (t % tr) * 4, tj = (t / tr) * 4;
-    double acc[4][4];
-#pragma unroll
-    for (int a = 0; a < 4; a++)
-#pragma unroll
-      for (int b = 0; b < 4; b++) acc[a][b] = 0.0;
-    for (int k0 = 0; k0 < n; k0 += MM_KP) {
-      __syncthreads();
-      for (int e = threadIdx.x; e < np * MM_KP; e += blockDim.x) {
-        const int i = e % np, kk = e / np;
-        sA[e] = (i < n && k0 + kk < n) ? A[i + (size_t)LDH * (k0 + kk)] : 0.0;
-        sB[e] = (i < n && k0 + kk < n) ? B[(k0 + kk) + (size_t)LDH * i] : 0.0;
-      }
-      __syncthreads();
-      if (act) {
-#pragma unroll 8
-        for (int kk = 0; kk < MM_KP; kk++) {
-          const double2 a01 = *reinterpret_cast<const double2 *>(sA + ti + np * kk);
-          const double2 a23 = *reinterpret_cast<const double2 *>(sA + ti + 2 + np * kk);
-          const double2 b01 = *reinterpret_cast<const double2 *>(sB + tj + np * kk);
-          const double2 b23 = *reinterpret_cast<const double2 *>(sB + tj + 2 + np * kk);
-          const double a[4] = {a01.x, a01.y, a23.x, a23.y}, b[4] = {b01.x, b01.y, b23.x, b23.y};
-#pragma unroll
-          for (int x = 0; x < 4; x++)
-#pragma unroll
-            for (int y = 0; y < 4; y++) acc[x][y] = fma(a[x], b[y], acc[x][y]);
-        }
-      }
+  const int np = (n + 7) & ~7, nt = np >> 3;
+  const int rank = (int)cl_rank(), lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int g = lane >> 2, tq = lane & 3;
+  const int ncol = (nt - rank + CTRL_CL - 1) / CTRL_CL;  // tile columns tj = rank + CTRL_CL i
+  double *sA = sm;                          // np x np, ld MM_LD (A[i + ld k])
+  double *sB = sm + (size_t)MM_LD * np;     // np x (8 ncol), ld MM_LD (B[k + ld j_local])
+  if (ncol > 0) {
+    for (int c = warp; c < np; c += nw)
+      for (int r = lane; r < np; r += 32)
+        sA[r + MM_LD * c] = (r < n && c < n) ? __ldcg(A + r + (size_t)LDH * c) : 0.0;
+    for (int jl = warp; jl < 8 * ncol; jl += nw) {
+      const int j = (rank + CTRL_CL * (jl >> 3)) * 8 + (jl & 7);
+      for (int r = lane; r < np; r += 32)
+        sB[r + MM_LD * jl] = (r < n && j < n) ? __ldcg(B + r + (size_t)LDH * j) : 0.0;
     }
-    if (act)
+  }
+  __syncthreads();
+  const int ntile = nt * ncol;  // (tile row, local tile column)
+  for (int t0 = warp; t0 < ntile; t0 += 2 * nw) {
+    double c[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+    int ti[2], tl[2];
+    bool on[2];
 #pragma unroll
-      for (int x = 0; x < 4; x++)
+    for (int u = 0; u < 2; u++) {
+      const int tt = t0 + u * nw;
+      on[u] = tt < ntile;
+      ti[u] = on[u] ? (tt % nt) * 8 : 0;
+      tl[u] = on[u] ? (tt / nt) * 8 : 0;
+    }
+    for (int k0 = 0; k0 < np; k0 += 4) {
 #pragma unroll
-        for (int y = 0; y < 4; y++)
-          if (ti + x < n && tj + y < n) C[(ti + x) + (size_t)LDH * (tj + y)] = acc[x][y];
+      for (int u = 0; u < 2; u++)
+        if (on[u]) dmma_8x8x4(c[u], sA[(ti[u] + g) + MM_LD * (k0 + tq)], sB[(k0 + tq) + MM_LD * (tl[u] + g)]);
+    }
+#pragma unroll
+    for (int u = 0; u < 2; u++)
+      if (on[u]) {
+        const int r = ti[u] + g, jl = tl[u] + 2 * tq;
+        const int cc = (rank + CTRL_CL * (jl >> 3)) * 8 + (jl & 7);
+        if (r < n && cc < n) C[r + (size_t)LDH * cc] = c[u][0];
+        if (r < n && cc + 1 < n) C[r + (size_t)LDH * (cc + 1)] = c[u][1];
+      }
   }
   cl_sync();
 }
@@ -110,87 +120,197 @@ __device__ double cta_norm1(int n, const double *A, double *red) {
 // solves its own block of right-hand-side columns (one thread per column:
 // permutation, forward and back substitution from its shared-memory copy of L\U).
 // Returns 0, or -1 for a zero pivot (every CTA).
-__device__ int cl_solve(int n, const double *Qg, double *R, double *LUg, int *perm, int *flag, double *sm) {
+// Q X = R (n <= KMAXM+1, ld LDH, global): CTA 0 factors Q = P L U in shared memory with
+// partial pivoting (first maximal |pivot|), static column ownership (warp c mod nw owns
+// column c: swaps and updates need only __syncwarp), ONE __syncthreads per step, the
+// owner of column k+1 searching step k+1's pivot right after its update (look-ahead).
+// L is kept in elimination order (no later row swaps of its columns), so the forward
+// solve applies swap k right before eliminating with column k (LAPACK getrs order).
+// Then every CTA solves its block of right-hand-side columns, one warp per column, the
+// column in registers (rows lane + 32 j), pivots broadcast by shuffles.  Returns 0 or
+// -1 (zero pivot) in every thread of the cluster.
+#define CL_RS 5  // row slots per lane: n <= 160
+__device__ int cl_solve(int n, const double *Qg, double *R, double *LUg, int *piv, int *flag, double *sm) {
   double *sQ = sm;  // n x n, ld = n
   const int rank = (int)cl_rank();
-  __shared__ int s_piv;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  __shared__ int s_piv[LDH];
+  __shared__ int s_bad;
   if (rank == 0) {
-    for (int e = threadIdx.x; e < n * n; e += blockDim.x) sQ[e] = Qg[(e % n) + (size_t)LDH * (e / n)];
-    for (int i = threadIdx.x; i < n; i += blockDim.x) perm[i] = i;
-    if (threadIdx.x == 0) *flag = 0;
+    for (int c = warp; c < n; c += nw)
+      for (int r = lane; r < n; r += 32) sQ[r + n * c] = __ldcg(Qg + r + (size_t)LDH * c);
+    if (threadIdx.x == 0) s_bad = 0;
+    __syncthreads();
+    // pivot of step k on column k (up to date), by its owner warp
+    auto pivot = [&](int k) {
+      double *C = sQ + n * k;
+      double vb = -1.0;
+      int rb = n;
+#pragma unroll
+      for (int j = 0; j < CL_RS; j++) {
+        const int r = k + lane + 32 * j;
+        const double a = r < n ? fabs(C[r]) : -1.0;
+        if (a > vb) { vb = a; rb = r; }  // (rows ascend with j: ties keep the first)
+      }
+      const unsigned long long bits = vb >= 0.0 ? (unsigned long long)__double_as_longlong(vb) : 0ull;
+      const unsigned hi = (unsigned)(bits >> 32), lo = (unsigned)bits;
+      const unsigned mhi = __reduce_max_sync(0xffffffffu, vb >= 0.0 ? hi : 0u);
+      const bool onhi = vb >= 0.0 && hi == mhi;
+      const unsigned mlo = __reduce_max_sync(0xffffffffu, onhi ? lo : 0u);
+      const bool top = onhi && lo == mlo;
+      const int bi = (int)__reduce_min_sync(0xffffffffu, top ? (unsigned)rb : 0x7fffffffu);
+      const double best = __longlong_as_double((long long)(((unsigned long long)mhi << 32) | mlo));
+      if (!(best > 0.0) || bi >= n) {
+        if (lane == 0) s_bad = 1;
+        return;
+      }
+      const double pv = C[bi], ck = C[k];
+      __syncwarp();
+      if (lane == 0) { C[bi] = ck; C[k] = pv; }
+      __syncwarp();
+      const double rp = __drcp_rn(pv);
+#pragma unroll
+      for (int j = 0; j < CL_RS; j++) {
+        const int r = k + 1 + lane + 32 * j;
+        if (r < n) C[r] *= rp;  // multipliers l_r
+      }
+      if (lane == 0) s_piv[k] = bi;
+      __syncwarp();
+    };
+#ifdef KIOPS_PHASE_DEBUG
+    const long long f0 = clock64();
+#endif
+// swap rows k <-> pv of column X and subtract l_r x_k from rows r > k (__syncwarp only:
+// the column is this warp's; batching several columns per round trip spilled and was slower)
+#define CL_UPDATE(X)                                                 \
+  {                                                                  \
+    double *const Xc = (X);                                          \
+    const double xk = Xc[pv], xo = Xc[k];                            \
+    double xv[CL_RS];                                                \
+    _Pragma("unroll") for (int j = 0; j < CL_RS; j++) {              \
+      const int r = k + 1 + lane + 32 * j;                           \
+      xv[j] = r < n ? (r == pv ? xo : Xc[r]) : 0.0;                  \
+    }                                                                \
+    __syncwarp();                                                    \
+    if (lane == 0) Xc[k] = xk;                                       \
+    _Pragma("unroll") for (int j = 0; j < CL_RS; j++) {              \
+      const int r = k + 1 + lane + 32 * j;                           \
+      if (r < n) Xc[r] = xv[j] - l[j] * xk;                          \
+    }                                                                \
+    __syncwarp();                                                    \
+  }
+    if (warp == 0) pivot(0);
     __syncthreads();
     for (int k = 0; k < n; k++) {
-      if (threadIdx.x < 32) {
-        double best = -1.0;
-        int bi = n;
-        for (int r = k + threadIdx.x; r < n; r += 32) {
-          const double a = fabs(sQ[r + n * k]);
-          if (a > best) { best = a; bi = r; }
-        }
-        for (int o = 16; o > 0; o >>= 1) {
-          const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-          const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-          if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
-        }
-        if (threadIdx.x == 0) {
-          s_piv = bi;
-          if (!(best > 0.0)) *flag = 1;
-          if (bi != k) { const int tp = perm[k]; perm[k] = perm[bi]; perm[bi] = tp; }
-        }
+      if (s_bad) break;
+      const int pv = s_piv[k];
+      double l[CL_RS];
+#pragma unroll
+      for (int j = 0; j < CL_RS; j++) {
+        const int r = k + 1 + lane + 32 * j;
+        l[j] = r < n ? sQ[r + n * k] : 0.0;
       }
-      __syncthreads();
-      if (*flag) break;
-      const int pv = s_piv;
-      if (pv != k)
-        for (int c = threadIdx.x; c < n; c += blockDim.x) {
-          const double t = sQ[k + n * c]; sQ[k + n * c] = sQ[pv + n * c]; sQ[pv + n * c] = t;
-        }
-      __syncthreads();
-      const double piv = sQ[k + n * k];
-      for (int r = k + 1 + threadIdx.x; r < n; r += blockDim.x) sQ[r + n * k] = sQ[r + n * k] / piv;
-      __syncthreads();
-      const int rows = n - k - 1;
-      for (int e = threadIdx.x; e < rows * rows; e += blockDim.x) {
-        const int r = k + 1 + e % rows, c = k + 1 + e / rows;
-        sQ[r + n * c] -= sQ[r + n * k] * sQ[k + n * c];
+      int c = k + 1 + ((warp - (k + 1)) % nw + nw) % nw;  // first owned column > k
+      if (c == k + 1 && c < n) {
+        CL_UPDATE(sQ + n * c);
+        pivot(k + 1);
+        c += nw;
       }
+      for (; c < n; c += nw) CL_UPDATE(sQ + n * c);
       __syncthreads();
     }
-    for (int e = threadIdx.x; e < n * n; e += blockDim.x) LUg[e] = sQ[e];
+#undef CL_UPDATE
+#ifdef KIOPS_PHASE_DEBUG
+    if (threadIdx.x == 0) printf("cl_solve n=%d factor cycles %lld\n", n, clock64() - f0);
+#endif
+    // L into final row order: column c gets the swaps of the later steps k > c (thread
+    // per column), so P Q = L U with P from the same swap sequence
+    if (!s_bad)
+      for (int c = threadIdx.x; c < n - 1; c += blockDim.x)
+        for (int k = c + 1; k < n; k++) {
+          const int pk = s_piv[k];
+          if (pk != k) { const double t = sQ[k + n * c]; sQ[k + n * c] = sQ[pk + n * c]; sQ[pk + n * c] = t; }
+        }
+    __syncthreads();
+    for (int c = warp; c < n; c += nw)
+      for (int r = lane; r < n; r += 32) LUg[r + n * c] = sQ[r + n * c];
+    if (threadIdx.x == 0) {  // row i of P Q is row perm[i] of Q
+      for (int i = 0; i < n; i++) piv[i] = i;
+      for (int k = 0; k < n; k++) { const int pk = s_piv[k], t = piv[k]; piv[k] = piv[pk]; piv[pk] = t; }
+      *flag = s_bad;
+    }
   }
+#ifdef KIOPS_PHASE_DEBUG
+  const long long s0 = clock64();
+#endif
   cl_sync();
-  if (*flag) return -1;
+  if (__ldcg(flag)) return -1;
+#ifdef KIOPS_PHASE_DEBUG
+  const long long s1 = clock64();
+#endif
   const int cb = (n + CTRL_CL - 1) / CTRL_CL, c0 = rank * cb, c1 = min(n, c0 + cb);
-  double *sX = sm + n * n;  // n x cb right-hand-side block, column-major
-  for (int e = threadIdx.x; e < n * n; e += blockDim.x) sQ[e] = LUg[e];
-  for (int e = threadIdx.x; e < n * (c1 - c0); e += blockDim.x) {
-    const int i = e % n, c = e / n;
-    sX[i + n * c] = R[perm[i] + (size_t)LDH * (c0 + c)];  // apply the row permutation
+  if (c0 < n) {
+    for (int c = warp; c < n; c += nw)
+      for (int r = lane; r < n; r += 32) sQ[r + n * c] = __ldcg(LUg + r + n * c);
+    for (int k = threadIdx.x; k < n; k += blockDim.x) s_piv[k] = __ldcg(piv + k);
   }
   __syncthreads();
-  const int c = threadIdx.x;
-  if (c < c1 - c0) {
-    double *x = sX + n * c;
-    for (int i = 1; i < n; i++) {  // L y = P b (unit lower)
-      double s0 = x[i], s1 = 0.0;
-      int k = 0;
-      for (; k + 1 < i; k += 2) { s0 -= sQ[i + n * k] * x[k]; s1 -= sQ[i + n * (k + 1)] * x[k + 1]; }
-      if (k < i) s0 -= sQ[i + n * k] * x[k];
-      x[i] = s0 + s1;
-    }
-    for (int i = n - 1; i >= 0; i--) {  // U x = y
-      double s0 = x[i], s1 = 0.0;
-      int k = i + 1;
-      for (; k + 1 < n; k += 2) { s0 -= sQ[i + n * k] * x[k]; s1 -= sQ[i + n * (k + 1)] * x[k + 1]; }
-      if (k < n) s0 -= sQ[i + n * k] * x[k];
-      x[i] = (s0 + s1) / sQ[i + n * i];
-    }
-  }
+#ifdef KIOPS_PHASE_DEBUG
+  const long long s2 = clock64();
+#endif
+  // 1/U(k,k) for the back substitution
+  double *s_rdg = sm + (size_t)n * n;
+  if (c0 < n)
+    for (int k = threadIdx.x; k < n; k += blockDim.x) s_rdg[k] = 1.0 / sQ[k + n * k];
   __syncthreads();
-  for (int e = threadIdx.x; e < n * (c1 - c0); e += blockDim.x) {
-    const int i = e % n, cc = e / n;
-    R[i + (size_t)LDH * (c0 + cc)] = sX[i + n * cc];
+  static_assert(CL_RS == 5, "row slots");
+  for (int c = c0 + warp; c < c1; c += nw) {
+    double x[CL_RS];
+#pragma unroll
+    for (int j = 0; j < CL_RS; j++) {  // P b
+      const int r = lane + 32 * j;
+      x[j] = r < n ? __ldcg(R + s_piv[r] + (size_t)LDH * c) : 0.0;
+    }
+    // forward: L y = P b (unit lower); row block kb of the pivots is register x[kb]
+#pragma unroll
+    for (int kb = 0; kb < CL_RS; kb++)
+      for (int kk = 0; kk < 32; kk++) {
+        const int k = 32 * kb + kk;
+        if (k >= n) break;
+        const double xk = __shfl_sync(0xffffffffu, x[kb], kk);
+        const double *Lk = sQ + n * k;
+#pragma unroll
+        for (int j = kb; j < CL_RS; j++) {
+          const int r = lane + 32 * j;
+          if (r > k && r < n) x[j] -= Lk[r] * xk;
+        }
+      }
+    // back: U x = y
+#pragma unroll
+    for (int kb = CL_RS - 1; kb >= 0; kb--)
+      for (int kk = 31; kk >= 0; kk--) {
+        const int k = 32 * kb + kk;
+        if (k >= n) continue;
+        const double xk = __shfl_sync(0xffffffffu, x[kb], kk) * s_rdg[k];
+        const double *Uk = sQ + n * k;
+        if (lane == kk) x[kb] = xk;
+#pragma unroll
+        for (int j = 0; j <= kb; j++) {
+          const int r = lane + 32 * j;
+          if (r < k) x[j] -= Uk[r] * xk;
+        }
+      }
+#pragma unroll
+    for (int j = 0; j < CL_RS; j++) {
+      const int r = lane + 32 * j;
+      if (r < n) R[r + (size_t)LDH * c] = x[j];
+    }
   }
+#ifdef KIOPS_PHASE_DEBUG
+  const long long s3 = clock64();
+  if (threadIdx.x == 0 && (rank == 0 || rank == CTRL_CL - 1))
+    printf("cl_solve n=%d rank %d: wait %lld copy %lld trsv %lld\n", n, rank, s1 - s0, s2 - s1, s3 - s2);
+#endif
   cl_sync();
   return 0;
 }
@@ -224,11 +344,6 @@ struct ClusterBk {
 // zero-padded to NP = n rounded up to 8 (products of zero-padded operands keep the
 // padding zero, so the elementwise steps may stay on the n x n part).
 #define SM_LD 52
-__device__ __forceinline__ void dmma_8x8x4(double (&c)[2], double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};\n"
-               : "+d"(c[0]), "+d"(c[1])
-               : "d"(a), "d"(b));
-}
 struct SmemBk {
   double *base;   // 10 matrices of SM_LD x SMALL_N (ld = SM_LD) + reduction scratch
   int n_;

@@ -198,7 +198,8 @@ Layout layout(const kiops_operator_desc *op, int p, const kiops_options *o) {
 size_t ctrl_smem_bytes() {
   const size_t n = KMAXM + 1, cb = (n + CTRL_CL - 1) / CTRL_CL;
   const size_t solve = sizeof(double) * (n * n + n * cb);
-  const size_t mm = sizeof(double) * 2 * (size_t)((n + 3) & ~3) * MM_KP;
+  const size_t np = (n + 7) & ~(size_t)7;
+  const size_t mm = sizeof(double) * MM_LD * (np + 8 * ((np / 8 + CTRL_CL - 1) / CTRL_CL));  // A + B panels
   const size_t small = sizeof(double) * (10 * (size_t)SM_LD * SMALL_N + 64);  // single-CTA path
   return std::max(std::max(solve, mm), small);
 }
