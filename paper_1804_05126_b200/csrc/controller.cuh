@@ -417,83 +417,46 @@ struct SmemBk {
     __syncthreads();
     return r;
   }
-  // Q X = R in place (R <- X): Gaussian elimination with partial pivoting (first
-  // maximal |pivot|) applied to the right-hand sides, then back substitution; Q is
-  // destroyed.  Static column ownership: warp c % nw owns column c of Q and of R, so
-  // the row swap and the update of a column need only __syncwarp.  Step k: the
-  // owner of column k has published the pivot row, 1/pivot and the multipliers
-  // (in place below the diagonal); after one __syncthreads every warp swaps rows
-  // k <-> pv in its columns and applies the multipliers, the owner of column k+1
-  // first, which then searches step k+1's pivot right away (look-ahead).
+  // Q X = R in place (R <- X), n <= SMALL_N, everything in CTA 0's shared memory.  The
+  // same scheme as cl_solve: factor Q = P L U in place with partial pivoting (first
+  // maximal |pivot|), static column ownership (warp c mod nw owns column c; swaps and
+  // updates need only __syncwarp), one __syncthreads per step, the owner of column k+1
+  // searching step k+1's pivot right after its update; L brought into final row order;
+  // then one warp per right-hand-side column: P b, L y = P b, U x = y with the column in
+  // registers (rows lane, lane + 32) and pivots broadcast by shuffles.  Q is destroyed.
   // Returns 0 or -1 (zero pivot), all threads.
   __device__ int solve(int n, double *Q, double *R) const {
-    __shared__ int s_bad, s_piv[SMALL_N];
+    __shared__ int s_bad, s_piv[SMALL_N], s_perm[SMALL_N];
     __shared__ double s_rd[SMALL_N];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     if (threadIdx.x == 0) s_bad = 0;
-    // pivot of step k on column k (up to date), by its owner warp.  First maximal
-    // |C[r]|, r >= k: |x| as a non-negative double orders like its bit pattern, so
-    // the max is two 32-bit warp reductions (high word, then low word among the
-    // ties) and the first row among equal maxima comes from two ballots.
-    auto pivot = [&](int k) {
+    auto pivot = [&](int k) {  // owner warp of column k (up to date)
       double *C = Q + SM_LD * k;
       const int ra = k + lane, rb = ra + 32;
       const double va = ra < n ? fabs(C[ra]) : -1.0, vb = rb < n ? fabs(C[rb]) : -1.0;
       const bool useb = vb > va;  // (equal: the lower row ra wins)
       const double v = useb ? vb : va;
+      const int rv = useb ? rb : ra;
       const unsigned long long bits = v >= 0.0 ? (unsigned long long)__double_as_longlong(v) : 0ull;
       const unsigned hi = (unsigned)(bits >> 32), lo = (unsigned)bits;
       const unsigned mhi = __reduce_max_sync(0xffffffffu, v >= 0.0 ? hi : 0u);
       const bool onhi = v >= 0.0 && hi == mhi;
       const unsigned mlo = __reduce_max_sync(0xffffffffu, onhi ? lo : 0u);
       const bool top = onhi && lo == mlo;
-      const unsigned bA = __ballot_sync(0xffffffffu, top && !useb), bB = __ballot_sync(0xffffffffu, top && useb);
-      const int bi = bA ? k + __ffs(bA) - 1 : k + 32 + __ffs(bB) - 1;
+      const int bi = (int)__reduce_min_sync(0xffffffffu, top ? (unsigned)rv : 0x7fffffffu);
       const double best = __longlong_as_double((long long)(((unsigned long long)mhi << 32) | mlo));
-      if (!(best > 0.0) || (bA == 0u && bB == 0u)) {
+      if (!(best > 0.0) || bi >= n) {
         if (lane == 0) s_bad = 1;
         return;
       }
       const double piv = C[bi], ck = C[k];
       __syncwarp();
-      if (lane == 0) { C[bi] = ck; C[k] = piv; }  // swap rows k and bi of column k
+      if (lane == 0) { C[bi] = ck; C[k] = piv; }
+      __syncwarp();
       const double rp = __drcp_rn(piv);
-      // multipliers l_r = C'[r] / piv (C'[bi] = ck), written in place below the diagonal
-      if (ra > k && ra < n) C[ra] = (ra == bi ? ck : C[ra]) * rp;
-      if (rb < n) C[rb] = (rb == bi ? ck : C[rb]) * rp;
+      if (ra > k && ra < n) C[ra] *= rp;  // multipliers l_r
+      if (rb < n) C[rb] *= rp;
       if (lane == 0) { s_piv[k] = bi; s_rd[k] = rp; }
-      __syncwarp();
-    };
-    // row swap k <-> pv and update of this warp's columns: Q columns cq + u nw
-    // (u < 3, cq + u nw < n) and R columns warp + u nw (u < 3, < n); all loads, one
-    // __syncwarp, all stores.  n <= SMALL_N = 48 = 3 nw.
-    auto update = [&](int cq, bool with_r, int k, int pv, double l0, double l1) {
-      const int r0 = k + 1 + lane, r1 = r0 + 32;
-      double xk[6], x0[6], x1[6];
-#pragma unroll
-      for (int u = 0; u < 6; u++) {
-        const int col = u < 3 ? cq + u * nw : warp + (u - 3) * nw;
-        const bool on = col < n && (u < 3 || with_r);
-        double *X = (u < 3 ? Q : R) + SM_LD * (on ? col : 0);
-        if (on) {
-          const double xo = X[k];
-          xk[u] = X[pv];  // new row k = old row pv, new row pv = old row k
-          x0[u] = r0 < n ? (r0 == pv ? xo : X[r0]) : 0.0;
-          x1[u] = r1 < n ? (r1 == pv ? xo : X[r1]) : 0.0;
-        }
-      }
-      __syncwarp();
-#pragma unroll
-      for (int u = 0; u < 6; u++) {
-        const int col = u < 3 ? cq + u * nw : warp + (u - 3) * nw;
-        const bool on = col < n && (u < 3 || with_r);
-        double *X = (u < 3 ? Q : R) + SM_LD * (on ? col : 0);
-        if (on) {
-          if (lane == 0) X[k] = xk[u];
-          if (r0 < n) X[r0] = x0[u] - l0 * xk[u];
-          if (r1 < n) X[r1] = x1[u] - l1 * xk[u];
-        }
-      }
       __syncwarp();
     };
     if (warp == 0) pivot(0);
@@ -503,29 +466,58 @@ struct SmemBk {
       const int pv = s_piv[k];
       const int r0 = k + 1 + lane, r1 = r0 + 32;
       const double l0 = r0 < n ? Q[r0 + SM_LD * k] : 0.0, l1 = r1 < n ? Q[r1 + SM_LD * k] : 0.0;
-      // first owned Q column > k; the owner of column k+1 updates its Q columns,
-      // searches step k+1's pivot, then updates its R columns
-      int c = k + 1 + ((warp - (k + 1)) % nw + nw) % nw;
+      int c = k + 1 + ((warp - (k + 1)) % nw + nw) % nw;  // first owned column > k
+#define SB_UPDATE(X)                                                   \
+  {                                                                    \
+    double *const Xc = (X);                                            \
+    const double xk = Xc[pv], xo = Xc[k];                              \
+    const double x0 = r0 < n ? (r0 == pv ? xo : Xc[r0]) : 0.0;         \
+    const double x1 = r1 < n ? (r1 == pv ? xo : Xc[r1]) : 0.0;         \
+    __syncwarp();                                                      \
+    if (lane == 0) Xc[k] = xk;                                         \
+    if (r0 < n) Xc[r0] = x0 - l0 * xk;                                 \
+    if (r1 < n) Xc[r1] = x1 - l1 * xk;                                 \
+    __syncwarp();                                                      \
+  }
       if (c == k + 1 && c < n) {
-        update(c, false, k, pv, l0, l1);  // owned Q columns (k+1 among them)
+        SB_UPDATE(Q + SM_LD * c);
         pivot(k + 1);
-        update(n, true, k, pv, l0, l1);   // owned R columns
-      } else {
-        update(c, true, k, pv, l0, l1);
+        c += nw;
       }
+      for (; c < n; c += nw) SB_UPDATE(Q + SM_LD * c);
+#undef SB_UPDATE
       __syncthreads();
     }
-    // back substitution: U x = y, U = upper triangle of Q, 1/U[k,k] in s_rd
-    for (int c = warp; c < n; c += nw) {
-      double x0 = lane < n ? R[lane + SM_LD * c] : 0.0, x1 = lane + 32 < n ? R[lane + 32 + SM_LD * c] : 0.0;
-      for (int k = n - 1; k >= 0; k--) {
-        const double xk = __shfl_sync(0xffffffffu, k < 32 ? x0 : x1, k & 31) * s_rd[k];
-        if (lane == (k & 31)) { if (k < 32) x0 = xk; else x1 = xk; }
-        if (lane < k) x0 -= Q[lane + SM_LD * k] * xk;
-        if (lane + 32 < k) x1 -= Q[lane + 32 + SM_LD * k] * xk;
+    // L into final row order (thread per column), permutation of the right-hand sides
+    for (int c = threadIdx.x; c < n - 1; c += blockDim.x)
+      for (int k = c + 1; k < n; k++) {
+        const int pk = s_piv[k];
+        if (pk != k) { const double t = Q[k + SM_LD * c]; Q[k + SM_LD * c] = Q[pk + SM_LD * c]; Q[pk + SM_LD * c] = t; }
       }
-      if (lane < n) R[lane + SM_LD * c] = x0;
-      if (lane + 32 < n) R[lane + 32 + SM_LD * c] = x1;
+    if (threadIdx.x == 0) {
+      for (int i = 0; i < n; i++) s_perm[i] = i;
+      for (int k = 0; k < n; k++) { const int pk = s_piv[k], t = s_perm[k]; s_perm[k] = s_perm[pk]; s_perm[pk] = t; }
+    }
+    __syncthreads();
+    for (int c = warp; c < n; c += nw) {
+      double *Rc = R + SM_LD * c;
+      double x0 = lane < n ? Rc[s_perm[lane]] : 0.0, x1 = lane + 32 < n ? Rc[s_perm[lane + 32]] : 0.0;
+      for (int k = 0; k < n; k++) {  // L y = P b (unit lower)
+        const double xk = __shfl_sync(0xffffffffu, k < 32 ? x0 : x1, k & 31);
+        const double *Lk = Q + SM_LD * k;
+        if (lane > k && lane < n) x0 -= Lk[lane] * xk;
+        if (lane + 32 > k && lane + 32 < n) x1 -= Lk[lane + 32] * xk;
+      }
+      for (int k = n - 1; k >= 0; k--) {  // U x = y
+        const double xk = __shfl_sync(0xffffffffu, k < 32 ? x0 : x1, k & 31) * s_rd[k];
+        const double *Uk = Q + SM_LD * k;
+        if (lane == (k & 31)) { if (k < 32) x0 = xk; else x1 = xk; }
+        if (lane < k) x0 -= Uk[lane] * xk;
+        if (lane + 32 < k) x1 -= Uk[lane + 32] * xk;
+      }
+      __syncwarp();
+      if (lane < n) Rc[lane] = x0;
+      if (lane + 32 < n) Rc[lane + 32] = x1;
     }
     __syncthreads();
     return 0;
