@@ -122,3 +122,35 @@ def test_bad_operator_and_workspace(L):
     assert L.kiops_create(C.byref(d), 1, C.byref(o), None, None, 0, C.byref(ctx)) == 6
     assert L.kiops_create(C.byref(d), 1, C.byref(o), None, C.c_void_p(4096 + 8), 1 << 40, C.byref(ctx)) == 6
     assert L.kiops_create(C.byref(d), 1, C.byref(o), None, C.c_void_p(4096), 16, C.byref(ctx)) == 6
+
+
+def test_epirk_workspace_and_validation(L):
+    # host-only checks of the EPIRK entry points: sizes grow with the number of
+    # KIOPS call shapes per scheme; invalid scheme / h / workspace are rejected before any launch
+    from paper_1804_05126_b200 import kiops as K
+
+    pb = K.RDProblem()
+    pb.nx, pb.ny = 64, 48
+    for i, w in enumerate([1.0, 1.0, 1.0, 1.0, -4.0]):
+        pb.w[i] = w
+    for i, c in enumerate([0.0, 1.0, 0.0, -1.0]):
+        pb.c[i] = c
+    o = K.default_options(m_max=64)
+    sizes = {}
+    for name, sch in K.EPIRK_SCHEMES.items():
+        nb = C.c_size_t()
+        assert L.kiops_epirk_workspace_bytes(C.byref(pb), sch, C.byref(o), C.byref(nb)) == 0
+        sizes[name] = nb.value
+    # two call shapes (p = 1, 4) for the fourth-order schemes and EPIRK5P1 (p = 1, 3); three for EXPRB5s3
+    assert sizes["epirk4s3"] == sizes["epirk4s3a"]
+    assert sizes["exprb5s3"] > sizes["epirk4s3"] and sizes["exprb5s3"] > sizes["epirk5p1"]
+    nb = C.c_size_t()
+    assert L.kiops_epirk_workspace_bytes(C.byref(pb), 9, C.byref(o), C.byref(nb)) == 1
+    ctx = C.c_void_p()
+    assert L.kiops_epirk_create(C.byref(pb), 1, C.c_double(-0.1), C.byref(o), None, C.c_void_p(4096),
+                                C.c_size_t(1 << 40), C.byref(ctx)) == 1  # h <= 0
+    assert L.kiops_epirk_create(C.byref(pb), 1, C.c_double(0.1), C.byref(o), None, None, C.c_size_t(0),
+                                C.byref(ctx)) == 6  # no workspace
+    assert not ctx.value
+    bad = K.default_options(iop_q=0)
+    assert L.kiops_epirk_workspace_bytes(C.byref(pb), 1, C.byref(bad), C.byref(nb)) == 1

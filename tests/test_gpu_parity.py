@@ -250,8 +250,8 @@ def test_hostloop_hook_is_bitwise_identical():
     # the profiling hook runs the same kernels with host-side control flow
     from paper_1804_05126_b200 import Kiops
 
-    for c in (W.config4(24, 20, 16), W.config5(20, 20, 20), W.config1()):
-        k = Kiops(c["op"], c["p"], device=DEV, tol=c["tol"])
+    for c, q in ((W.config4(24, 20, 16), 2), (W.config5(20, 20, 20), 2), (W.config1(), 2), (W.config2(64, 48), 3)):
+        k = Kiops(c["op"], c["p"], device=DEV, tol=c["tol"], iop_q=q)
         u = [torch.as_tensor(x, device=DEV) for x in c["u"]]
         a, sa = k.apply(u, c["T"])
         a = [x.cpu().numpy() for x in a]
