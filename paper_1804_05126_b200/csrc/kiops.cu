@@ -28,6 +28,7 @@
 #include "passq.cuh"
 #include "kiops_internal.cuh"
 #include "passes.cuh"
+#include "inner.cuh"
 
 namespace {
 
@@ -175,7 +176,7 @@ Layout layout(const kiops_operator_desc *op, int p, const kiops_options *o) {
   L.sig = off; off += al(sizeof(double) * (LDH + 2));
   L.R2 = off; off += al(sizeof(double) * (LDH + 2));
   L.tails = off; off += al(sizeof(double) * (LDH + 2) * KMAXP);
-  L.partials = off; off += al(sizeof(double) * NDOT * (size_t)L.grid_max);
+  L.partials = off; off += al(sizeof(double) * 2 * NDOT * (size_t)L.grid_max);
   L.npart = off; off += al(sizeof(double) * KMAXP * (size_t)L.grid_max);
   L.scratch = off; off += al(sizeof(double) * NSCR * (size_t)LDH * LDH);
   L.coef = off; off += al(sizeof(double) * (KMAXO + 1) * (size_t)LDH);
@@ -225,6 +226,7 @@ struct kiops_ctx_s {
   long long last_attempts = 0;
   int m_init_call = 0;           // kiops_set_m_init (0: options.m_init)
   void *fpass = nullptr;         // stencil pass kernel (NULL for CSR)
+  void *finner = nullptr;        // persistent inner-loop kernel (inner.cuh), NULL if not used
   std::string err;
 };
 
@@ -299,6 +301,33 @@ static kiops_status build_graph(kiops_ctx c) {
   c->fpass = fpass;
   if (fpass && c->L.smem_pass > 0)
     CK(cudaFuncSetAttribute(fpass, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->L.smem_pass), "smem attr pass");
+
+  // persistent inner loop (inner.cuh) for the fused q = 2 stencil passes, when the whole
+  // pass grid is co-resident; KIOPS_PERSIST=0 in the environment keeps one launch per pass
+  void *finner = nullptr;
+  const char *pe = getenv("KIOPS_PERSIST");
+  if (P.q == 2 && !(pe && pe[0] == '0')) {
+    if (lazy2d && (c->op.kind == KIOPS_OP_STENCIL1D3 || c->op.kind == KIOPS_OP_STENCIL2D5))
+      finner = c->p == 0 ? (void *)k_inner_2d_lazy<L2YC, 0, 2> : c->p == 1 ? (void *)k_inner_2d_lazy<L2YC, 1, 2>
+             : c->p == 2 ? (void *)k_inner_2d_lazy<L2YC, 2, 2> : c->p == 3 ? (void *)k_inner_2d_lazy<L2YC, 3, 2>
+                         : (void *)k_inner_2d_lazy<L2YC, 4, 2>;
+    else if (c->op.kind == KIOPS_OP_STENCIL3D7_VARKAPPA && c->op.nx % 2 == 0 && c->op.nx >= 2 && c->p >= 1 &&
+             c->p <= 4)
+      finner = c->p == 1 ? (void *)k_inner_3d_lazyq<1, Q3Y, 2, Q3D> : c->p == 2 ? (void *)k_inner_3d_lazyq<2, Q3Y, 2, Q3D>
+             : c->p == 3 ? (void *)k_inner_3d_lazyq<3, Q3Y, 2, 1> : (void *)k_inner_3d_lazyq<4, Q3Y, 2, 1>;
+    if (finner) {
+      if (c->L.smem_pass > 0)
+        CK(cudaFuncSetAttribute(finner, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->L.smem_pass),
+           "smem attr inner");
+      int dev = 0, sms = 0, per_sm = 0;
+      CK(cudaGetDevice(&dev), "cudaGetDevice");
+      CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "SM count");
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, finner, c->L.block_pass, c->L.smem_pass),
+         "occupancy inner");
+      if ((long long)per_sm * sms < c->L.grid_pass) finner = nullptr;  // not co-resident: per-pass launches
+    }
+  }
+  c->finner = finner;
   CK(cudaFuncSetAttribute((void *)k_ctrl, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctrl_smem_bytes()),
      "smem attr ctrl");
 
@@ -316,6 +345,12 @@ static kiops_status build_graph(kiops_ctx c) {
   } else if (c->op.kind == KIOPS_OP_CSR) {
     CK(add_kernel(b_inner, &n_a, nullptr, 0, (void *)k_csr_form, c->L.grid_form, 256, 0, &P), "node form");
     CK(add_kernel(b_inner, &n_b, &n_a, 1, (void *)k_sell_spmv, c->L.grid_pass, 256, 0, &P), "node spmv");
+  } else if (finner) {  // the WHILE body runs once: the kernel loops over the passes itself
+    CK(add_kernel(b_inner, &n_a, nullptr, 0, finner, c->L.grid_pass, c->L.block_pass, c->L.smem_pass, &P),
+       "node inner");
+    cudaLaunchAttributeValue av = {};
+    av.cooperative = 1;
+    CK(cudaGraphKernelNodeSetAttribute(n_a, cudaLaunchAttributeCooperative, &av), "cooperative attr");
   } else {
     CK(add_kernel(b_inner, &n_a, nullptr, 0, fpass, c->L.grid_pass, c->L.block_pass, c->L.smem_pass, &P), "node pass");
   }
@@ -589,6 +624,11 @@ kiops_status kiops_apply_hostloop(kiops_ctx c, const double *const *u, const dou
       } else if (c->op.kind == KIOPS_OP_CSR) {
         if ((s = launch_plain(c, (void *)k_csr_form, c->L.grid_form, 256, 0, &P)) != KIOPS_OK) return s;
         if ((s = launch_plain(c, (void *)k_sell_spmv, c->L.grid_pass, 256, 0, &P)) != KIOPS_OK) return s;
+      } else if (c->finner) {
+        void *args[] = {&P};
+        CK(cudaLaunchCooperativeKernel(c->finner, dim3(c->L.grid_pass), dim3(c->L.block_pass), args, c->L.smem_pass,
+                                       c->stream),
+           "cudaLaunchCooperativeKernel inner");
       } else {
         if ((s = launch_plain(c, c->fpass, c->L.grid_pass, c->L.block_pass, c->L.smem_pass, &P)) != KIOPS_OK) return s;
       }

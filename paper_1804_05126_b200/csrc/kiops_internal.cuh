@@ -48,6 +48,7 @@ struct DevState {
   unsigned int gemv_ticket;
   unsigned int cond[3];          // mirror of the graph conditionals (outer, inner, accept)
   int bc_accept, bc_ntau;        // controller-cluster broadcast (CTA 0 -> all CTAs)
+  unsigned int bar_count, bar_gen;  // grid barrier of the persistent inner loop (inner.cuh)
 };
 
 // Frozen per-ctx parameters, passed BY VALUE to every kernel (graph node params).
@@ -76,7 +77,7 @@ struct KParams {
   double *sig;        // sig[k] = ||x_k||, k = 1..
   double *R2;         // R2[k] = ||A~ x_k||^2 (breakdown scale, R3)
   double *tails;      // tails[k*KMAXP + c] = tail entry N+c of x_k (unnormalised)
-  double *partials;   // NDOT x grid_max
+  double *partials;   // 2 x NDOT x grid_max (persistent inner loop: buffer k & 1)
   double *npart;      // KMAXP x grid_max   (setup: column abs sums)
   double *scratch;    // NSCR x LDH x LDH   (controller)
   double *coef;       // (KMAXO+1) x LDH    (GEMV coefficients)

@@ -644,19 +644,13 @@ struct LazyQ {
 };
 
 template <int PM, int TYM, int CPS, int DD>
-__global__ void __launch_bounds__(LazyQ<PM, TYM, CPS, DD>::NT, CPS) k_pass_3d_lazyq(KParams P) {
+__device__ __forceinline__ void body_3d_lazyq(const KParams &P, const PassScalars &S, double (&v)[NDOT]) {
   using M = LazyQ<PM, TYM, CPS, DD>;
   constexpr int PX = M::PX, NPAIR = M::NPAIR, NIN = M::NIN, D = M::D, RD = M::RD, SLOT = M::SLOT;
   extern __shared__ double2 smem2[];
   double2 *sXK = smem2;                // 2 x NPAIR   x_k pairs (shared plane ring)
   double2 *sKP = smem2 + 2 * NPAIR;    // 2 x NPAIR   kappa pairs
   double2 *sOp = smem2 + 4 * NPAIR;    // RD x SLOT   thread-private operand ring
-
-  __shared__ PassScalars S;
-  pass_guard(P);
-  if (threadIdx.x == 0) load_pass_scalars(P, S);
-  __syncthreads();
-  if (S.k == 0) return;
   const int k = S.k;
   const long long nx = P.nx, ny = P.ny, nz = P.nz, nxy = nx * ny;
   int ntx, nb;
@@ -776,8 +770,19 @@ __global__ void __launch_bounds__(LazyQ<PM, TYM, CPS, DD>::NT, CPS) k_pass_3d_la
     }
     cp_async_wait<0>();
   }
-  double v[NDOT] = {v0, v1, v2, v3, v4};
-  pass_epilogue(P, k, v);
+  v[0] += v0; v[1] += v1; v[2] += v2; v[3] += v3; v[4] += v4;
+}
+
+template <int PM, int TYM, int CPS, int DD>
+__global__ void __launch_bounds__(LazyQ<PM, TYM, CPS, DD>::NT, CPS) k_pass_3d_lazyq(KParams P) {
+  __shared__ PassScalars S;
+  pass_guard(P);
+  if (threadIdx.x == 0) load_pass_scalars(P, S);
+  __syncthreads();
+  if (S.k == 0) return;
+  double v[NDOT] = {0.0, 0.0, 0.0, 0.0, 0.0};
+  body_3d_lazyq<PM, TYM, CPS, DD>(P, S, v);
+  pass_epilogue(P, S.k, v);
 }
 
 // ---------------------------------------------------------------------------
@@ -795,14 +800,11 @@ struct Row2 {
   double2 r, xm, pp, d, b[PM > 0 ? PM : 1];
 };
 
-template <int YC, int PM, int MINB = 2>
-__global__ void __launch_bounds__(256, MINB) k_pass_2d_lazy(KParams P) {
+// One pass over this CTA's strips (vectors written by earlier passes of a persistent
+// launch are read through L2: __ldcg, never the non-coherent path).
+template <int YC, int PM>
+__device__ __forceinline__ void body_2d_lazy(const KParams &P, const PassScalars &S, double (&v)[NDOT]) {
   constexpr int IP = 30;  // interior pairs per warp strip
-  __shared__ PassScalars S;
-  pass_guard(P);
-  if (threadIdx.x == 0) load_pass_scalars(P, S);
-  __syncthreads();
-  if (S.k == 0) return;
   const int k = S.k;
   const long long nx = P.nx, ny = P.ny;
   const long long nsx = (nx + 2 * IP - 1) / (2 * IP), ncy = (ny + YC - 1) / YC;
@@ -829,9 +831,9 @@ __global__ void __launch_bounds__(256, MINB) k_pass_2d_lazy(KParams P) {
     const long long g = pxw + nx * wrapc(y, ny);
     const double2 z2 = make_double2(0.0, 0.0);
     o.r = z2; o.pp = z2; o.d = z2;
-    if (use_r) o.r = __ldg(reinterpret_cast<const double2 *>(rin + g));
-    o.xm = __ldg(reinterpret_cast<const double2 *>(S.xprev + g));
-    if (use_pp) o.pp = __ldg(reinterpret_cast<const double2 *>(S.xpp + g));
+    if (use_r) o.r = __ldcg(reinterpret_cast<const double2 *>(rin + g));
+    o.xm = __ldcg(reinterpret_cast<const double2 *>(S.xprev + g));
+    if (use_pp) o.pp = __ldcg(reinterpret_cast<const double2 *>(S.xpp + g));
     if (use_d) o.d = __ldg(reinterpret_cast<const double2 *>(P.diag + g));
 #pragma unroll
     for (int c = 0; c < PM; c++) o.b[c] = pin ? __ldg(reinterpret_cast<const double2 *>(Bc[c] + g)) : z2;
@@ -883,8 +885,19 @@ __global__ void __launch_bounds__(256, MINB) k_pass_2d_lazy(KParams P) {
       cur = ahead;
     }
   }
-  double v[NDOT] = {v0, v1, v2, v3, v4};
-  pass_epilogue(P, k, v);
+  v[0] += v0; v[1] += v1; v[2] += v2; v[3] += v3; v[4] += v4;
+}
+
+template <int YC, int PM, int MINB = 2>
+__global__ void __launch_bounds__(256, MINB) k_pass_2d_lazy(KParams P) {
+  __shared__ PassScalars S;
+  pass_guard(P);
+  if (threadIdx.x == 0) load_pass_scalars(P, S);
+  __syncthreads();
+  if (S.k == 0) return;
+  double v[NDOT] = {0.0, 0.0, 0.0, 0.0, 0.0};
+  body_2d_lazy<YC, PM>(P, S, v);
+  pass_epilogue(P, S.k, v);
 }
 
 // ---------------------------------------------------------------------------

@@ -291,3 +291,31 @@ def test_config4_full_size_trace_vs_stored_oracle_run():
 def test_iop_window_q(make, q):
     c = make()
     assert_parity(c, iop_q=q, strict=c["op"]["kind"] != "stencil3d7")
+
+
+@pytest.mark.parametrize("make", [lambda: W.config1(), lambda: W.config1(401), lambda: W.config2(64, 48),
+                                  lambda: W.config3(256, 96), lambda: W.config4(24, 20, 16),
+                                  lambda: W.config4(64, 38, 21)])
+def test_persistent_inner_loop_is_bitwise_identical(make, monkeypatch):
+    """inner.cuh: all passes of one Alg. 2 run in ONE cooperative launch (grid barrier,
+    every CTA finalises redundantly) must reproduce the one-launch-per-pass kernels
+    bit for bit (same block partials, same reduction order, same scalar arithmetic),
+    in the graph and through the host-loop hook."""
+    from paper_1804_05126_b200 import Kiops
+
+    c = make()
+    u = [torch.as_tensor(x, device=DEV) for x in c["u"]]
+    res = {}
+    for mode in ("1", "0"):
+        monkeypatch.setenv("KIOPS_PERSIST", mode)
+        k = Kiops(c["op"], c["p"], device=DEV, tol=c["tol"], m_init=c["m_init"], m_min=c["m_min"], m_max=c["m_max"])
+        a, sa = k.apply(u, c["T"])
+        b, sb = k.apply(u, c["T"], hostloop=True)
+        res[mode] = ([x.cpu().numpy() for x in a], sa, [x.cpu().numpy() for x in b], sb, k.trace())
+        k.close()
+    (a1, s1, b1, t1, tr1), (a0, s0, b0, t0, tr0) = res["1"], res["0"]
+    for x, y, z, q in zip(a1, a0, b1, b0):
+        assert np.array_equal(x, y) and np.array_equal(x, z) and np.array_equal(x, q)
+    for key in ("krylov_vectors", "passes", "substeps", "rejections", "expm_calls", "final_m"):
+        assert s1[key] == s0[key] == t1[key] == t0[key], key
+    assert [(r["j"], r["tau"], r["omega"]) for r in tr1] == [(r["j"], r["tau"], r["omega"]) for r in tr0]
