@@ -55,119 +55,169 @@ struct InnerCarry {
   double nu;
   const double *x1;
   int m, status_in, go, trip;
-  unsigned gen;
   unsigned long long launches;
 };
+// State counters CTA 0 keeps in registers and stores (never read back) every pass.
+struct InnerCounters {
+  long long passes, kv;
+  unsigned long long ns_pass, t0;
+};
 
-// pass_finalize (passes.cuh) on the carried scalars; wr: this CTA writes the state.
-// Sets C.go and, when going on, the PassScalars of pass k+1.
-__device__ __noinline__ void inner_finalize(const KParams &P, int k, const double (&v)[NDOT], InnerCarry &C, PassScalars &Sn,
-                               bool wr, unsigned long long &t0) {
+// Per-CTA dot records: recs[k & 1][cta][0..4] (64-byte slots).  A CTA writes its
+// block partials, then (release) adds 1 to the monotonic pass_count; one thread per
+// CTA waits (acquire) until pass_count reaches base + nb * (passes so far), then the
+// whole CTA reads the records in the fixed block order.  Two buffers suffice: a CTA
+// writes pass k+2's record only after every CTA has counted pass k+1, i.e. finished
+// reading pass k's records.
+__device__ __forceinline__ double *rec_ptr(const KParams &P, int buf, int cta) {
+  return P.recs + ((size_t)buf * (size_t)P.grid_max + (size_t)cta) * 8;
+}
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long *p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void red_release_add_u64(unsigned long long *p, unsigned long long v) {
+  asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// pass_finalize (passes.cuh) run by the 32 lanes of warp 0 with the same expressions
+// (bitwise identical results): every lane evaluates the shared chain sqrt -> h1 -> h2,
+// lane c < p the tail entry c of x_{k+1}, so the ~16 dependent fp64 divisions of the
+// serial version become a chain of ~4.  wr: this CTA (0) writes the state.
+__device__ __forceinline__ void finalize_warp(const KParams &P, int k, const double (&v0)[NDOT], InnerCarry &C,
+                                              PassScalars &Sn, bool wr, InnerCounters &K) {
   DevState *st = P.st;
-  const int p = P.p;
+  const int lane = threadIdx.x, p = P.p;
+  double v[NDOT];
+#pragma unroll
+  for (int q = 0; q < NDOT; q++) v[q] = __shfl_sync(0xffffffffu, v0[q], 0);
   double Kt[KMAXP];
-  for (int c = 0; c < p; c++) Kt[c] = (c + 1 < p) ? C.tk[c + 1] : 0.0;  // tail of A~ x_k (Alg. 2 l.5-6)
+#pragma unroll
+  for (int c = 0; c < KMAXP; c++) Kt[c] = (c + 1 < p) ? C.tk[c + 1 < KMAXP ? c + 1 : 0] : 0.0;
   double S = v[0], G = v[1], E1 = v[2], E2 = v[3], R = v[4];
-  for (int c = 0; c < p; c++) {
-    S += C.tk[c] * C.tk[c];
-    R += Kt[c] * Kt[c];
-    E2 += C.tk[c] * Kt[c];
-    if (k >= 2) { G += C.tkm1[c] * C.tk[c]; E1 += C.tkm1[c] * Kt[c]; }
-  }
-  C.go = 0;
-  if (wr) {
-    st->passes++;
+#pragma unroll
+  for (int c = 0; c < KMAXP; c++)
+    if (c < p) {
+      const double tkc = C.tk[c];
+      S += tkc * tkc;
+      R += Kt[c] * Kt[c];
+      E2 += tkc * Kt[c];
+      if (k >= 2) { G += C.tkm1[c] * tkc; E1 += C.tkm1[c] * Kt[c]; }
+    }
+  const bool l0 = lane == 0;
+  if (wr && l0) {
+    K.passes++;
+    st->passes = K.passes;
     st->npass = k;
     const unsigned long long t = gtimer();
-    st->ns_pass += t - t0;
-    t0 = t;
+    K.ns_pass += t - K.t0;
+    K.t0 = t;
+    st->ns_pass = K.ns_pass;
   }
   if (C.status_in != 0) {
-    if (wr) set_cond(P, COND_INNER, 0u);
+    if (wr && l0) set_cond(P, COND_INNER, 0u);
+    if (l0) C.go = 0;
     return;
   }
   if (!isfinite(S) || !isfinite(G) || !isfinite(E1) || !isfinite(E2) || !isfinite(R)) {
-    if (wr) {
+    if (wr && l0) {
       st->status = KIOPS_ERR_NONFINITE;  // R22
       set_cond(P, COND_INNER, 0u);
     }
+    if (l0) C.go = 0;
     return;
   }
   const double sk = sqrt(S);
   double *H = P.H;
 #define HH(i, j) H[((i)-1) + (size_t)((j)-1) * LDH]
-  double tn[KMAXP];
-  double a1, a2;
+  const int c = lane;  // this lane's tail entry
+  const double tkc = c < KMAXP ? C.tk[c] : 0.0, tkm1c = c < KMAXP ? C.tkm1[c] : 0.0;
+  double Ktc = 0.0;
+#pragma unroll
+  for (int q = 0; q < KMAXP; q++)
+    if (q == c) Ktc = Kt[q];
+  double tn = 0.0, a1 = 0.0, a2 = 0.0;
+  int go;
   if (k == 1) {  // beta = ||x_1|| (Alg. 1 l.14)
-    if (wr) {
+    if (wr && l0) {
       st->beta = sk;
       P.sig[1] = sk;
       P.R2[1] = R;
     }
     if (sk == 0.0) {  // R27
-      if (wr) {
+      if (wr && l0) {
         st->zero_start = 1;
         set_cond(P, COND_INNER, 0u);
       }
+      if (l0) C.go = 0;
       return;
     }
     const double h11 = E2 / (sk * sk);
-    if (wr) HH(1, 1) = h11;
-    for (int c = 0; c < p; c++) tn[c] = Kt[c] / sk - h11 * C.tk[c] / sk;
-    C.go = (1 < C.m + 1) ? 1 : 0;
-    a1 = h11 / sk;
-    a2 = 0.0;
+    if (wr && l0) HH(1, 1) = h11;
+    if (c < p) tn = Ktc / sk - h11 * tkc / sk;
+    go = (1 < C.m + 1) ? 1 : 0;
+    if (lane == 9) a1 = h11 / sk;
   } else {  // k >= 2 closes Alg. 2 iteration k-1
-    if (wr) st->kv++;
+    if (wr && l0) {
+      K.kv++;
+      st->kv = K.kv;
+    }
     const double skm1 = C.skm1;
     const double cn = sqrt(C.R2km1) / skm1;
     const double thr = fmax(1e-12 * cn, 1e-14);  // R3
     if (sk <= thr) {                             // Alg. 2 l.12-15
-      if (wr) {
+      if (wr && l0) {
         st->happy = 1;
         set_cond(P, COND_INNER, 0u);
       }
+      if (l0) C.go = 0;
       return;
     }
-    if (wr) {
+    if (wr && l0) {
       HH(k, k - 1) = sk;  // l.16 (R2)
       P.sig[k] = sk;
       P.R2[k] = R;
     }
     const double h1 = E1 / (skm1 * sk);
     const double h2 = E2 / (sk * sk) - h1 * G / (skm1 * sk);
-    if (wr) {
+    if (wr && l0) {
       HH(k - 1, k) = h1;
       HH(k, k) = h2;
     }
-    for (int c = 0; c < p; c++) tn[c] = Kt[c] / sk - h1 * C.tkm1[c] / skm1 - h2 * C.tk[c] / sk;
-    C.go = (k < C.m + 1) ? 1 : 0;
-    a1 = h2 / sk;   // = H(k,k)/sig[k]          (load_pass_scalars of pass k+1)
-    a2 = h1 / skm1; // = H(k-1,k)/sig[k-1]
+    if (c < p) tn = Ktc / sk - h1 * tkm1c / skm1 - h2 * tkc / sk;
+    go = (k < C.m + 1) ? 1 : 0;
+    if (lane == 9) a1 = h2 / sk;    // = H(k,k)/sig[k]      (load_pass_scalars of pass k+1)
+    if (lane == 10) a2 = h1 / skm1; // = H(k-1,k)/sig[k-1]
   }
 #undef HH
-  if (wr) {
-    double *tw = P.tails + (k + 1) * KMAXP;
-    for (int c = 0; c < p; c++) tw[c] = tn[c];
-    if (!C.go) set_cond(P, COND_INNER, 0u);
+  if (wr && c < p) P.tails[(k + 1) * KMAXP + c] = tn;
+  if (wr && l0 && !go) set_cond(P, COND_INNER, 0u);
+  double a0 = 0.0;
+  if (lane == 8) a0 = 1.0 / sk;
+  a0 = __shfl_sync(0xffffffffu, a0, 8);
+  a1 = __shfl_sync(0xffffffffu, a1, 9);
+  a2 = __shfl_sync(0xffffffffu, a2, 10);
+  if (l0) C.go = go;
+  if (!go) return;
+  if (c < KMAXP) {
+    Sn.btp[c] = c < p ? C.nu * tkc : 0.0;
+    Sn.btc[c] = c < p ? C.nu * tn : 0.0;
+    C.tkm1[c] = c < p ? tkc : 0.0;
+    C.tk[c] = c < p ? tn : 0.0;
   }
-  if (!C.go) return;
-  const int kn = k + 1;  // <= m + 1 <= m_max + 1
-  Sn.k = kn;
-  Sn.xprev = (k == 1) ? C.x1 : P.V + (size_t)(k - 1) * (size_t)P.ldN;
-  Sn.xpp = (kn >= 3) ? ((k - 1 == 1) ? C.x1 : P.V + (size_t)(k - 2) * (size_t)P.ldN) : nullptr;
-  Sn.xout = P.V + (size_t)(kn - 1) * (size_t)P.ldN;
-  Sn.a0 = 1.0 / sk;
-  Sn.a1 = a1;
-  Sn.a2 = a2;
-  for (int c = 0; c < KMAXP; c++) {
-    Sn.btp[c] = c < p ? C.nu * C.tk[c] : 0.0;
-    Sn.btc[c] = c < p ? C.nu * tn[c] : 0.0;
-    C.tkm1[c] = c < p ? C.tk[c] : 0.0;
-    C.tk[c] = c < p ? tn[c] : 0.0;
+  if (l0) {
+    const int kn = k + 1;  // <= m + 1 <= m_max + 1
+    Sn.k = kn;
+    Sn.xprev = (k == 1) ? C.x1 : P.V + (size_t)(k - 1) * (size_t)P.ldN;
+    Sn.xpp = (kn >= 3) ? ((k - 1 == 1) ? C.x1 : P.V + (size_t)(k - 2) * (size_t)P.ldN) : nullptr;
+    Sn.xout = P.V + (size_t)(kn - 1) * (size_t)P.ldN;
+    Sn.a0 = a0;
+    Sn.a1 = a1;
+    Sn.a2 = (k == 1) ? 0.0 : a2;
+    C.skm1 = sk;
+    C.R2km1 = R;
   }
-  C.skm1 = sk;
-  C.R2km1 = R;
 }
 
 // The loop.  body(S, v) streams pass S.k over this CTA's share and accumulates the
@@ -180,10 +230,15 @@ __device__ __forceinline__ void inner_loop(const KParams &P, Body &&body) {
   DevState *st = P.st;
   const unsigned nb = gridDim.x;
   const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
-  unsigned long long t0 = 0;
+  InnerCounters K{};
   unsigned gen = 0;
   if (threadIdx.x == 0) {
-    if (blockIdx.x == 0) t0 = gtimer();
+    if (blockIdx.x == 0) {
+      K.t0 = gtimer();
+      K.passes = st->passes;
+      K.kv = st->kv;
+      K.ns_pass = st->ns_pass;
+    }
     gen = ld_acquire_u32(&st->bar_gen);
     // loop guard (pass_guard), evaluated identically by every CTA
     C.launches = st->launches + 1;
@@ -204,48 +259,80 @@ __device__ __forceinline__ void inner_loop(const KParams &P, Body &&body) {
       C.R2km1 = k >= 2 ? P.R2[k - 1] : 0.0;
     }
   }
-  __syncthreads();
+  unsigned long long target = 0;
+  if (threadIdx.x == 0) target = st->pass_count;  // stable until every CTA passed the barrier below
+  // one grid barrier per launch: every CTA has read the launch and pass counters
+  grid_sync(st, nb, gen);
+  if (lead) st->launches = C.launches;
   if (C.trip || S.k == 0) {
-    grid_sync(st, nb, gen);  // every CTA has read the launch counter
-    if (lead) {
-      st->launches = C.launches;
-      if (C.trip) {
-        st->status = KIOPS_ERR_CUDA;
-        set_cond(P, COND_INNER, 0u);
-        set_cond(P, COND_OUTER, 0u);
-      }
+    if (lead && C.trip) {
+      st->status = KIOPS_ERR_CUDA;
+      set_cond(P, COND_INNER, 0u);
+      set_cond(P, COND_OUTER, 0u);
     }
     return;
   }
-  bool first = true;
+#ifdef KIOPS_PHASE_TIMERS  // debug build: CTA 0 prints body / barrier / finalise time per launch
+  const int k_first = S.k;
+  unsigned long long tb = 0, tw = 0, tf = 0, ta = gtimer(), tt;
+#define PHASE(acc) do { tt = gtimer(); acc += tt - ta; ta = tt; } while (0)
+#else
+#define PHASE(acc) do { } while (0)
+#endif
   for (;;) {
     const int k = S.k;
     double v[NDOT] = {0.0, 0.0, 0.0, 0.0, 0.0};
     body(S, v);
-    block_sum<NDOT>(v, red);
-    double *part = P.partials + (size_t)(k & 1) * NDOT * (size_t)P.grid_max;
-    if (threadIdx.x == 0)
+    block_sum<NDOT>(v, red);  // (its __syncthreads order every thread's vector writes before the fence)
+    PHASE(tb);
+    if (threadIdx.x == 0) {
+      double *mine = rec_ptr(P, k & 1, blockIdx.x);
 #pragma unroll
-      for (int q = 0; q < NDOT; q++) part[q * P.grid_max + blockIdx.x] = v[q];
-    grid_sync(st, nb, gen);
-    if (first && lead) st->launches = C.launches;
-    first = false;
+      for (int q = 0; q < NDOT; q++) __stcg(mine + q, v[q]);
+      __threadfence();  // release: this CTA's x_k, r_k (ordered by block_sum's barrier) and record
+      red_release_add_u64(&st->pass_count, 1ull);
+      target += nb;
+      while (ld_acquire_u64(&st->pass_count) < target) {
+      }
+      __threadfence();
+    }
+    __syncthreads();
+    // every CTA's record, in the fixed block order of pass_finalize
     double w[NDOT];
 #pragma unroll
     for (int q = 0; q < NDOT; q++) w[q] = 0.0;
-    for (int b = threadIdx.x; b < (int)nb; b += blockDim.x)
+    for (int b = threadIdx.x; b < (int)nb; b += blockDim.x) {
+      const double *rr = rec_ptr(P, k & 1, b);
 #pragma unroll
-      for (int q = 0; q < NDOT; q++) w[q] += __ldcg(&part[q * P.grid_max + b]);
+      for (int q = 0; q < NDOT; q++) w[q] += __ldcg(rr + q);
+    }
+    PHASE(tw);
     block_sum<NDOT>(w, red);
-    if (threadIdx.x == 0) inner_finalize(P, k, w, C, S, blockIdx.x == 0, t0);
+    if (threadIdx.x < 32) finalize_warp(P, k, w, C, S, blockIdx.x == 0, K);
     __syncthreads();
+    PHASE(tf);
     if (!C.go) break;
   }
+#ifdef KIOPS_PHASE_TIMERS
+  if (threadIdx.x == 0 && k_first == 1) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    printf("CTABODY %d %u %.2f %.2f\n", blockIdx.x, smid, tb * 1e-3, tw * 1e-3);
+  }
+  if (lead) printf("PHASES k_end %d body %.2f us barrier %.2f us finalise %.2f us (sums over the launch)\n", S.k,
+                   tb * 1e-3, tw * 1e-3, tf * 1e-3);
+#endif
+#undef PHASE
 }
 
-template <int YC, int PM, int MINB>
+template <int YC, int PM, int MINB, int DA = 0>
 __global__ void __launch_bounds__(256, MINB) k_inner_2d_lazy(KParams P) {
-  inner_loop(P, [&](const PassScalars &S, double (&v)[NDOT]) { body_2d_lazy<YC, PM>(P, S, v); });
+  inner_loop(P, [&](const PassScalars &S, double (&v)[NDOT]) {
+    if (DA > 0)
+      body_2d_async<YC, PM, (DA > 0 ? DA : 1)>(P, S, v);
+    else
+      body_2d_lazy<YC, PM>(P, S, v);
+  });
 }
 
 template <int PM, int TYM, int CPS, int DD>

@@ -50,7 +50,7 @@ constexpr int SM_COUNT_HINT = 148;
 #define M3Z 32   // z-planes per CTA chunk
 
 struct Layout {
-  size_t V, r, staging, state, call, H, sig, R2, tails, partials, npart, scratch, coef, trace, sell_off, sell_col,
+  size_t V, r, staging, state, call, H, sig, R2, tails, partials, recs, npart, scratch, coef, trace, sell_off, sell_col,
       sell_val, qa, gram, qpart, total;
   long long sell_entries;
   long long ldN;
@@ -135,7 +135,10 @@ Layout layout(const kiops_operator_desc *op, int p, const kiops_options *o) {
         const int yc = L2YC;
         const long long strips = (op->nx + 59) / 60 * ((op->ny + yc - 1) / yc);
         L.grid_pass = (int)((strips + 7) / 8);
-        L.smem_pass = 0;
+        const char *ev = getenv("KIOPS_2D_ASYNC");  // 0: register-prefetch body (A/B switch)
+        L.smem_pass = (ev && ev[0] == '0') ? 0
+                    : p == 0 ? Ring2<0, 2>::smem_bytes : p == 1 ? Ring2<1, 2>::smem_bytes
+                    : p == 2 ? Ring2<2, 2>::smem_bytes : p == 3 ? Ring2<3, 2>::smem_bytes : Ring2<4, 2>::smem_bytes;
       } else if (op->kind == KIOPS_OP_STENCIL1D3) {
         L.grid_pass = (int)((op->nx + 255) / 256);
         L.smem_pass = stencil_smem_bytes<T1D>();
@@ -176,7 +179,8 @@ Layout layout(const kiops_operator_desc *op, int p, const kiops_options *o) {
   L.sig = off; off += al(sizeof(double) * (LDH + 2));
   L.R2 = off; off += al(sizeof(double) * (LDH + 2));
   L.tails = off; off += al(sizeof(double) * (LDH + 2) * KMAXP);
-  L.partials = off; off += al(sizeof(double) * 2 * NDOT * (size_t)L.grid_max);
+  L.partials = off; off += al(sizeof(double) * NDOT * (size_t)L.grid_max);
+  L.recs = off; off += al(sizeof(double) * 2 * 8 * (size_t)L.grid_max);
   L.npart = off; off += al(sizeof(double) * KMAXP * (size_t)L.grid_max);
   L.scratch = off; off += al(sizeof(double) * NSCR * (size_t)LDH * LDH);
   L.coef = off; off += al(sizeof(double) * (KMAXO + 1) * (size_t)LDH);
@@ -280,10 +284,14 @@ static kiops_status build_graph(kiops_ctx c) {
   switch (c->op.kind) {
     case KIOPS_OP_STENCIL1D3:
     case KIOPS_OP_STENCIL2D5:
-      if (lazy2d)  // strip height 8, 2 CTAs/SM: measured best of YC 4/8/16 and 2-3 CTAs/SM
+      if (lazy2d && c->L.smem_pass == 0)  // strip height 8, 2 CTAs/SM: measured best of YC 4/8/16 and 2-3 CTAs/SM
         fpass = c->p == 0 ? (void *)k_pass_2d_lazy<L2YC, 0, 2> : c->p == 1 ? (void *)k_pass_2d_lazy<L2YC, 1, 2>
               : c->p == 2 ? (void *)k_pass_2d_lazy<L2YC, 2, 2> : c->p == 3 ? (void *)k_pass_2d_lazy<L2YC, 3, 2>
                           : (void *)k_pass_2d_lazy<L2YC, 4, 2>;
+      else if (lazy2d)  // cp.async ring, 2 rows in flight per warp
+        fpass = c->p == 0 ? (void *)k_pass_2d_lazy<L2YC, 0, 2, 2> : c->p == 1 ? (void *)k_pass_2d_lazy<L2YC, 1, 2, 2>
+              : c->p == 2 ? (void *)k_pass_2d_lazy<L2YC, 2, 2, 2> : c->p == 3 ? (void *)k_pass_2d_lazy<L2YC, 3, 2, 2>
+                          : (void *)k_pass_2d_lazy<L2YC, 4, 2, 2>;
       else
         fpass = c->op.kind == KIOPS_OP_STENCIL1D3 ? (void *)k_pass_stencil<T1D> : (void *)k_pass_stencil<T2D>;
       break;
@@ -307,10 +315,14 @@ static kiops_status build_graph(kiops_ctx c) {
   void *finner = nullptr;
   const char *pe = getenv("KIOPS_PERSIST");
   if (P.q == 2 && !(pe && pe[0] == '0')) {
-    if (lazy2d && (c->op.kind == KIOPS_OP_STENCIL1D3 || c->op.kind == KIOPS_OP_STENCIL2D5))
+    if (lazy2d && (c->op.kind == KIOPS_OP_STENCIL1D3 || c->op.kind == KIOPS_OP_STENCIL2D5) && c->L.smem_pass == 0)
       finner = c->p == 0 ? (void *)k_inner_2d_lazy<L2YC, 0, 2> : c->p == 1 ? (void *)k_inner_2d_lazy<L2YC, 1, 2>
              : c->p == 2 ? (void *)k_inner_2d_lazy<L2YC, 2, 2> : c->p == 3 ? (void *)k_inner_2d_lazy<L2YC, 3, 2>
                          : (void *)k_inner_2d_lazy<L2YC, 4, 2>;
+    else if (lazy2d && (c->op.kind == KIOPS_OP_STENCIL1D3 || c->op.kind == KIOPS_OP_STENCIL2D5))
+      finner = c->p == 0 ? (void *)k_inner_2d_lazy<L2YC, 0, 2, 2> : c->p == 1 ? (void *)k_inner_2d_lazy<L2YC, 1, 2, 2>
+             : c->p == 2 ? (void *)k_inner_2d_lazy<L2YC, 2, 2, 2> : c->p == 3 ? (void *)k_inner_2d_lazy<L2YC, 3, 2, 2>
+                         : (void *)k_inner_2d_lazy<L2YC, 4, 2, 2>;
     else if (c->op.kind == KIOPS_OP_STENCIL3D7_VARKAPPA && c->op.nx % 2 == 0 && c->op.nx >= 2 && c->p >= 1 &&
              c->p <= 4)
       finner = c->p == 1 ? (void *)k_inner_3d_lazyq<1, Q3Y, 2, Q3D> : c->p == 2 ? (void *)k_inner_3d_lazyq<2, Q3Y, 2, Q3D>
@@ -438,6 +450,7 @@ kiops_status kiops_create(const kiops_operator_desc *op, int p, const kiops_opti
   P.R2 = (double *)(w + L.R2);
   P.tails = (double *)(w + L.tails);
   P.partials = (double *)(w + L.partials);
+  P.recs = (double *)(w + L.recs);
   P.npart = (double *)(w + L.npart);
   P.scratch = (double *)(w + L.scratch);
   P.coef = (double *)(w + L.coef);

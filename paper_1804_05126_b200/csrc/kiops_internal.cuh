@@ -48,7 +48,8 @@ struct DevState {
   unsigned int gemv_ticket;
   unsigned int cond[3];          // mirror of the graph conditionals (outer, inner, accept)
   int bc_accept, bc_ntau;        // controller-cluster broadcast (CTA 0 -> all CTAs)
-  unsigned int bar_count, bar_gen;  // grid barrier of the persistent inner loop (inner.cuh)
+  unsigned int bar_count, bar_gen;  // launch-start grid barrier of the persistent inner loop (inner.cuh)
+  unsigned long long pass_count;    // per-pass arrivals of the persistent inner loop (monotonic)
 };
 
 // Frozen per-ctx parameters, passed BY VALUE to every kernel (graph node params).
@@ -77,7 +78,8 @@ struct KParams {
   double *sig;        // sig[k] = ||x_k||, k = 1..
   double *R2;         // R2[k] = ||A~ x_k||^2 (breakdown scale, R3)
   double *tails;      // tails[k*KMAXP + c] = tail entry N+c of x_k (unnormalised)
-  double *partials;   // 2 x NDOT x grid_max (persistent inner loop: buffer k & 1)
+  double *partials;   // NDOT x grid_max
+  double *recs;       // 2 x grid_max x 8: per-CTA dot records of the persistent inner loop (inner.cuh)
   double *npart;      // KMAXP x grid_max   (setup: column abs sums)
   double *scratch;    // NSCR x LDH x LDH   (controller)
   double *coef;       // (KMAXO+1) x LDH    (GEMV coefficients)

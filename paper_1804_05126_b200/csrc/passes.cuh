@@ -888,7 +888,121 @@ __device__ __forceinline__ void body_2d_lazy(const KParams &P, const PassScalars
   v[0] += v0; v[1] += v1; v[2] += v2; v[3] += v3; v[4] += v4;
 }
 
-template <int YC, int PM, int MINB = 2>
+// Same pass and arithmetic (identical operation order), with the operand rows
+// prefetched D rows ahead by 16-byte cp.async into a warp-private shared ring
+// (lane-private slots: no barriers), instead of one row ahead in registers: each
+// warp's row chain then waits ~1/D of an L2/HBM latency per row.
+template <int PM, int D>
+struct Ring2 {
+  static constexpr int NOP = 4 + PM, RD = D + 1;
+  static constexpr size_t smem_bytes = 16 * (size_t)8 * RD * NOP * 32;  // 8 warps per CTA
+};
+
+template <int YC, int PM, int D>
+__device__ __forceinline__ void body_2d_async(const KParams &P, const PassScalars &S, double (&v)[NDOT]) {
+  constexpr int IP = 30;  // interior pairs per warp strip
+  constexpr int NOP = Ring2<PM, D>::NOP, RD = Ring2<PM, D>::RD;
+  extern __shared__ double2 smem2[];
+  const int k = S.k;
+  const long long nx = P.nx, ny = P.ny;
+  const long long nsx = (nx + 2 * IP - 1) / (2 * IP), ncy = (ny + YC - 1) / YC;
+  const int lane = threadIdx.x & 31;
+  const long long w = (blockIdx.x * (long long)blockDim.x + threadIdx.x) / 32;
+  if (w >= nsx * ncy) return;  // warp-uniform
+  double2 *ring = smem2 + (size_t)(threadIdx.x >> 5) * RD * NOP * 32 + lane;
+  const long long sx = w % nsx, cy = w / nsx;
+  const long long x0 = sx * 2 * IP, y0 = cy * YC;
+  const long long y1 = (y0 + YC < ny) ? y0 + YC : ny;
+  const long long px = x0 - 2 + 2 * lane;
+  const long long pxw = wrapc(px, nx);
+  const bool pin = lane >= 1 && lane <= IP && px < nx;
+  const bool use_r = k >= 2, use_pp = S.xpp != nullptr, use_d = P.diag != nullptr;
+  const double *rin = P.r + (size_t)((k - 1) & 1) * (size_t)P.ldN;
+  double *rout = P.r + (size_t)(k & 1) * (size_t)P.ldN;
+  const double *xprev = S.xprev, *xpp = S.xpp;
+  double *xout = S.xout;
+  const double a0 = S.a0, a1 = S.a1, a2 = S.a2;
+  const double Ww = P.w[0], Ew = P.w[1], Sw = P.w[2], Nw = P.w[3], Cw = P.w[4];
+  double btc[PM > 0 ? PM : 1];
+  const double *Bc[PM > 0 ? PM : 1];
+#pragma unroll
+  for (int c = 0; c < PM; c++) { btc[c] = S.btc[c]; Bc[c] = S.B[c]; }
+  const int nrows = (int)(y1 - y0) + 2;  // logical row i = grid row y0 - 1 + i
+  long long yi = wrapc(y0 - 1, ny);      // next row to issue
+  int si = 0;                            // its ring slot
+  auto issue = [&]() {
+    const long long g = pxw + nx * yi;
+    double2 *d = ring + si * NOP * 32;
+    if (use_r) cp_async16(d, rin + g);
+    cp_async16(d + 32, xprev + g);
+    if (use_pp) cp_async16(d + 64, xpp + g);
+    if (use_d) cp_async16(d + 96, P.diag + g);
+    if (pin)
+#pragma unroll
+      for (int c = 0; c < PM; c++) cp_async16(d + (4 + c) * 32, Bc[c] + g);
+    yi = (yi + 1 == ny) ? 0 : yi + 1;
+    si = (si + 1 == RD) ? 0 : si + 1;
+  };
+#pragma unroll
+  for (int q = 0; q < D; q++) {
+    if (q < nrows) issue();
+    cp_async_commit();
+  }
+  const double2 z2 = make_double2(0.0, 0.0);
+  double2 xk_m = z2, xk_0 = z2, xm_0 = z2, d_0 = z2;
+  double2 b_0[PM > 0 ? PM : 1];
+#pragma unroll
+  for (int c = 0; c < PM; c++) b_0[c] = z2;
+  double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0, v4 = 0.0;
+  int sr = 0;  // slot of row i
+  long long y = y0 - 1;
+  for (int i = 0; i < nrows; i++, y++) {
+    if (i + D < nrows) issue();
+    cp_async_commit();
+    cp_async_wait<D>();
+    const double2 *o = ring + sr * NOP * 32;
+    sr = (sr + 1 == RD) ? 0 : sr + 1;
+    const double2 xm = o[32];
+    double2 xk_p = xm;
+    if (use_r) {
+      const double2 rr = o[0], pp = use_pp ? o[64] : z2;
+      xk_p.x = a0 * rr.x - a1 * xm.x - a2 * pp.x;
+      xk_p.y = a0 * rr.y - a1 * xm.y - a2 * pp.y;
+    }
+    if (i >= 2) {  // output row y - 1 (x_k of rows y-2, y-1, y are xk_m, xk_0, xk_p)
+      const double xl = __shfl_up_sync(0xffffffffu, xk_0.y, 1);
+      const double xr = __shfl_down_sync(0xffffffffu, xk_0.x, 1);
+      double ra = Ww * xl + Ew * xk_0.y + Sw * xk_m.x + Nw * xk_p.x + (Cw + d_0.x) * xk_0.x;
+      double rb = Ww * xk_0.x + Ew * xr + Sw * xk_m.y + Nw * xk_p.y + (Cw + d_0.y) * xk_0.y;
+#pragma unroll
+      for (int c = 0; c < PM; c++) {
+        ra = fma(b_0[c].x, btc[c], ra);
+        rb = fma(b_0[c].y, btc[c], rb);
+      }
+      if (pin) {
+        v0 = fma(xk_0.x, xk_0.x, fma(xk_0.y, xk_0.y, v0));
+        v1 = fma(xm_0.x, xk_0.x, fma(xm_0.y, xk_0.y, v1));
+        v2 = fma(xm_0.x, ra, fma(xm_0.y, rb, v2));
+        v3 = fma(xk_0.x, ra, fma(xk_0.y, rb, v3));
+        v4 = fma(ra, ra, fma(rb, rb, v4));
+        const long long g = px + nx * (y - 1);
+        if (xout) *reinterpret_cast<double2 *>(xout + g) = xk_0;
+        *reinterpret_cast<double2 *>(rout + g) = make_double2(ra, rb);
+      }
+    }
+    xk_m = xk_0;
+    xk_0 = xk_p;
+    xm_0 = xm;
+    d_0 = use_d ? o[96] : z2;
+    if (pin)
+#pragma unroll
+      for (int c = 0; c < PM; c++) b_0[c] = o[(4 + c) * 32];
+  }
+  cp_async_wait<0>();
+  v[0] += v0; v[1] += v1; v[2] += v2; v[3] += v3; v[4] += v4;
+}
+
+template <int YC, int PM, int MINB = 2, int DA = 0>
 __global__ void __launch_bounds__(256, MINB) k_pass_2d_lazy(KParams P) {
   __shared__ PassScalars S;
   pass_guard(P);
@@ -896,7 +1010,10 @@ __global__ void __launch_bounds__(256, MINB) k_pass_2d_lazy(KParams P) {
   __syncthreads();
   if (S.k == 0) return;
   double v[NDOT] = {0.0, 0.0, 0.0, 0.0, 0.0};
-  body_2d_lazy<YC, PM>(P, S, v);
+  if (DA > 0)
+    body_2d_async<YC, PM, (DA > 0 ? DA : 1)>(P, S, v);
+  else
+    body_2d_lazy<YC, PM>(P, S, v);
   pass_epilogue(P, S.k, v);
 }
 
