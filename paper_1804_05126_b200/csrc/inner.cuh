@@ -335,7 +335,7 @@ __global__ void __launch_bounds__(256, MINB) k_inner_2d_lazy(KParams P) {
   });
 }
 
-template <int PM, int TYM, int CPS, int DD>
-__global__ void __launch_bounds__(LazyQ<PM, TYM, CPS, DD>::NT, CPS) k_inner_3d_lazyq(KParams P) {
-  inner_loop(P, [&](const PassScalars &S, double (&v)[NDOT]) { body_3d_lazyq<PM, TYM, CPS, DD>(P, S, v); });
+template <int PM, int TYM, int CPS, int DD, int NH = 1>
+__global__ void __launch_bounds__(LazyQ<PM, TYM, CPS, DD, NH>::BLOCK, CPS / NH) k_inner_3d_lazyq(KParams P) {
+  inner_loop(P, [&](const PassScalars &S, double (&v)[NDOT]) { body_3d_lazyq<PM, TYM, CPS, DD, NH>(P, S, v); });
 }

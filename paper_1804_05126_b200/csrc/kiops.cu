@@ -56,6 +56,7 @@ struct Layout {
   long long ldN;
   int grid_pass, grid_setup, grid_gemv, grid_form, grid_max;
   int block_pass;
+  int nh3 = 1;  // 3D pair pass: z-parts per CTA
   size_t smem_pass;
 };
 
@@ -152,10 +153,13 @@ Layout layout(const kiops_operator_desc *op, int p, const kiops_options *o) {
         using Q = LazyQ<2, Q3Y, 2>;
         int ntx, nb;
         rc_tiles(op->nx, op->ny, Q::TILES, Q3Y, &ntx, &nb);
-        L.grid_pass = ntx * nb * rc_zsplit(op->nx, op->ny, op->nz, Q::TILES, Q3Y, Q::CTAS);
-        L.smem_pass = p == 1 ? LazyQ<1, Q3Y, 2, Q3D>::smem_bytes : p == 2 ? LazyQ<2, Q3Y, 2, Q3D>::smem_bytes
-                    : p == 3 ? LazyQ<3, Q3Y, 2, 1>::smem_bytes : LazyQ<4, Q3Y, 2, 1>::smem_bytes;
-        L.block_pass = Q::NT;
+        const int zs = rc_zsplit(op->nx, op->ny, op->nz, Q::TILES, Q3Y, Q::CTAS);
+        const char *ev = getenv("KIOPS_3D_NH");  // 1: one z-part per CTA (A/B switch)
+        L.nh3 = (zs % 2 == 0 && !(ev && ev[0] == '1')) ? 2 : 1;
+        L.grid_pass = ntx * nb * zs / L.nh3;
+        L.smem_pass = L.nh3 * (p == 1 ? LazyQ<1, Q3Y, 2, Q3D>::half_bytes : p == 2 ? LazyQ<2, Q3Y, 2, Q3D>::half_bytes
+                               : p == 3 ? LazyQ<3, Q3Y, 2, 1>::half_bytes : LazyQ<4, Q3Y, 2, 1>::half_bytes);
+        L.block_pass = L.nh3 * Q::NT;
       } else {
         L.grid_pass = (int)(((op->nx + M3X - 1) / M3X) * ((op->ny + M3Y - 1) / M3Y) * ((op->nz + M3Z - 1) / M3Z));
         L.smem_pass = sizeof(double) * (p <= 2 ? Lazy3<M3X, M3Y, 2>::smem_doubles
@@ -297,8 +301,11 @@ static kiops_status build_graph(kiops_ctx c) {
       break;
     case KIOPS_OP_STENCIL3D7_VARKAPPA:
       if (c->op.nx % 2 == 0 && c->op.nx >= 2 && c->p >= 1 && c->p <= 4)
-        fpass = c->p == 1 ? (void *)k_pass_3d_lazyq<1, Q3Y, 2, Q3D> : c->p == 2 ? (void *)k_pass_3d_lazyq<2, Q3Y, 2, Q3D>
-              : c->p == 3 ? (void *)k_pass_3d_lazyq<3, Q3Y, 2, 1> : (void *)k_pass_3d_lazyq<4, Q3Y, 2, 1>;
+        fpass = c->L.nh3 == 2
+                    ? (c->p == 1 ? (void *)k_pass_3d_lazyq<1, Q3Y, 2, Q3D, 2> : c->p == 2 ? (void *)k_pass_3d_lazyq<2, Q3Y, 2, Q3D, 2>
+                       : c->p == 3 ? (void *)k_pass_3d_lazyq<3, Q3Y, 2, 1, 2> : (void *)k_pass_3d_lazyq<4, Q3Y, 2, 1, 2>)
+                    : (c->p == 1 ? (void *)k_pass_3d_lazyq<1, Q3Y, 2, Q3D> : c->p == 2 ? (void *)k_pass_3d_lazyq<2, Q3Y, 2, Q3D>
+                       : c->p == 3 ? (void *)k_pass_3d_lazyq<3, Q3Y, 2, 1> : (void *)k_pass_3d_lazyq<4, Q3Y, 2, 1>);
       else
         fpass = c->p <= 2 ? (void *)k_pass_3d_lazy<M3X, M3Y, M3Z, 2, 3>
               : c->p <= 4 ? (void *)k_pass_3d_lazy<M3X, M3Y, M3Z, 4, 3>
@@ -325,8 +332,11 @@ static kiops_status build_graph(kiops_ctx c) {
                          : (void *)k_inner_2d_lazy<L2YC, 4, 2, 2>;
     else if (c->op.kind == KIOPS_OP_STENCIL3D7_VARKAPPA && c->op.nx % 2 == 0 && c->op.nx >= 2 && c->p >= 1 &&
              c->p <= 4)
-      finner = c->p == 1 ? (void *)k_inner_3d_lazyq<1, Q3Y, 2, Q3D> : c->p == 2 ? (void *)k_inner_3d_lazyq<2, Q3Y, 2, Q3D>
-             : c->p == 3 ? (void *)k_inner_3d_lazyq<3, Q3Y, 2, 1> : (void *)k_inner_3d_lazyq<4, Q3Y, 2, 1>;
+      finner = c->L.nh3 == 2
+                   ? (c->p == 1 ? (void *)k_inner_3d_lazyq<1, Q3Y, 2, Q3D, 2> : c->p == 2 ? (void *)k_inner_3d_lazyq<2, Q3Y, 2, Q3D, 2>
+                      : c->p == 3 ? (void *)k_inner_3d_lazyq<3, Q3Y, 2, 1, 2> : (void *)k_inner_3d_lazyq<4, Q3Y, 2, 1, 2>)
+                   : (c->p == 1 ? (void *)k_inner_3d_lazyq<1, Q3Y, 2, Q3D> : c->p == 2 ? (void *)k_inner_3d_lazyq<2, Q3Y, 2, Q3D>
+                      : c->p == 3 ? (void *)k_inner_3d_lazyq<3, Q3Y, 2, 1> : (void *)k_inner_3d_lazyq<4, Q3Y, 2, 1>);
     if (finner) {
       if (c->L.smem_pass > 0)
         CK(cudaFuncSetAttribute(finner, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->L.smem_pass),

@@ -634,29 +634,37 @@ __device__ __forceinline__ double2 stencil_pair(double2 xc, double2 kc, double x
 // TYM: max tile rows; CPS: CTAs per SM (grid = CPS x 148, tiles target CPS/2 x 148)
 // DD planes in flight; the private ring slot holds r, x_{k-1}, x_{k-2}, kappa for the
 // NPAIR halo-1 pairs and B only for the NIN interior pairs.
-template <int PM, int TYM, int CPS, int DD = 1>
+template <int PM, int TYM, int CPS, int DD = 1, int NH = 1>
 struct LazyQ {
   static constexpr int PX = 34, NPAIR = PX * (TYM + 2), NIN = 32 * TYM;
-  static constexpr int NT = (NPAIR + 31) / 32 * 32;
+  static constexpr int NT = (NPAIR + 31) / 32 * 32;  // threads of one z-part (a "half")
   static constexpr int D = DD, RD = D + 1, SLOT = 4 * NPAIR + PM * NIN;
   static constexpr int TILES = RC_SMS * CPS / 2, CTAS = RC_SMS * CPS;
-  static constexpr size_t smem_bytes = 16 * (4 * (size_t)NPAIR + (size_t)RD * SLOT);
+  static constexpr size_t half_bytes = 16 * (4 * (size_t)NPAIR + (size_t)RD * SLOT);
+  static constexpr size_t smem_bytes = NH * half_bytes;
+  static constexpr int BLOCK = NH * NT;
 };
 
-template <int PM, int TYM, int CPS, int DD>
+// NH = 2: one CTA runs the two z-parts of a tile as two thread halves that share the
+// per-plane __syncthreads.  Two independent CTAs per SM (NH = 1) measured ~8% apart in
+// speed (the second CTA placed on an SM is systematically slower), and the pass waits
+// for the slowest; the shared barrier keeps both parts in lock-step.  Every z-march
+// alternates direction with the pass parity, so a pass starts on the planes the
+// previous one touched last (measured: -37 MB of DRAM reads per pass at 256^3).
+template <int PM, int TYM, int CPS, int DD, int NH = 1>
 __device__ __forceinline__ void body_3d_lazyq(const KParams &P, const PassScalars &S, double (&v)[NDOT]) {
-  using M = LazyQ<PM, TYM, CPS, DD>;
-  constexpr int PX = M::PX, NPAIR = M::NPAIR, NIN = M::NIN, D = M::D, RD = M::RD, SLOT = M::SLOT;
+  using M = LazyQ<PM, TYM, CPS, DD, NH>;
+  constexpr int PX = M::PX, NPAIR = M::NPAIR, NIN = M::NIN, D = M::D, RD = M::RD, SLOT = M::SLOT, NT = M::NT;
   extern __shared__ double2 smem2[];
-  double2 *sXK = smem2;                // 2 x NPAIR   x_k pairs (shared plane ring)
-  double2 *sKP = smem2 + 2 * NPAIR;    // 2 x NPAIR   kappa pairs
-  double2 *sOp = smem2 + 4 * NPAIR;    // RD x SLOT   thread-private operand ring
+  const int h = threadIdx.x / NT, t = threadIdx.x % NT;  // half, thread within the half
+  double2 *sXK = smem2 + (size_t)h * (M::half_bytes / 16);  // 2 x NPAIR   x_k pairs (plane ring)
+  double2 *sKP = sXK + 2 * NPAIR;                               // 2 x NPAIR   kappa pairs
+  double2 *sOp = sXK + 4 * NPAIR;                               // RD x SLOT   thread-private operand ring
   const int k = S.k;
   const long long nx = P.nx, ny = P.ny, nz = P.nz, nxy = nx * ny;
   int ntx, nb;
   rc_tiles(nx, ny, M::TILES, TYM, &ntx, &nb);
   const int ntiles = ntx * nb, zsplit = rc_zsplit(nx, ny, nz, M::TILES, TYM, M::CTAS);
-  const int t = threadIdx.x;
   const double *rin = P.r + (size_t)((k - 1) & 1) * (size_t)P.ldN;
   double *rout = P.r + (size_t)(k & 1) * (size_t)P.ldN;
   const double *xprev = S.xprev, *xpp = S.xpp, *kap = P.kappa;
@@ -672,16 +680,21 @@ __device__ __forceinline__ void body_3d_lazyq(const KParams &P, const PassScalar
   }
   double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0, v4 = 0.0;
 
-  for (int w = blockIdx.x; w < ntiles * zsplit; w += gridDim.x) {
-    const int tile = w % ntiles, part = w / ntiles;
+  for (int w = blockIdx.x; w < ntiles * (zsplit / NH); w += gridDim.x) {
+    const int tile = w % ntiles, part = (w / ntiles) * NH + h;
     const long long ox = (long long)(tile % ntx) * 64, band = tile / ntx;
     const long long oy = band * ny / nb, hb = (band + 1) * ny / nb - oy;
     const long long zlo = part * nz / zsplit, zhi = (part + 1) * nz / zsplit;
     const int nzc = (int)(zhi - zlo);
-    // odd parts march downward.  (Reversing every direction on alternate passes, so
-    // that a pass starts on the planes the previous one touched last -- SURVEY f2(ii)
-    // -- measured no change in DRAM reads or call time.)
-    const bool down = part & 1;
+    int nzmax = 0;  // longest part of this CTA (the halves share the barriers)
+#pragma unroll
+    for (int q = 0; q < NH; q++) {
+      const int pq = (w / ntiles) * NH + q;
+      const int n = (int)((pq + 1) * nz / zsplit - pq * nz / zsplit);
+      nzmax = n > nzmax ? n : nzmax;
+    }
+    // odd parts march downward on odd passes' opposite: direction = part ^ pass parity
+    const bool down = ((part ^ k) & 1) != 0;
     const int px = t % PX, py = t / PX;
     const bool act = py < hb + 2;
     const int o1 = act ? (int)(wrapc(ox - 2 + 2 * px, nx) + nx * wrapc(oy - 1 + py, ny)) : 0;
@@ -709,7 +722,7 @@ __device__ __forceinline__ void body_3d_lazyq(const KParams &P, const PassScalar
     };
     __syncthreads();  // previous part's readers are done with the rings
     for (int q = 0; q < D; q++) {
-      issue(q);
+      if (q <= nzc + 1) issue(q);
       cp_async_commit();
     }
     double2 xk_m = {0.0, 0.0}, xk_0 = {0.0, 0.0}, k_m = {0.0, 0.0}, k_0 = {0.0, 0.0}, xm_0 = {0.0, 0.0},
@@ -717,7 +730,8 @@ __device__ __forceinline__ void body_3d_lazyq(const KParams &P, const PassScalar
     long long zo_out = (down ? zhi - 1 : zlo) * nxy;
     int rs = 0, ri = D;
 #pragma unroll 2
-    for (int i = 0; i <= nzc + 1; i++) {
+    for (int i = 0; i <= nzmax + 1; i++) {
+      const bool live = i <= nzc + 1;
       if (i + D <= nzc + 1) issue(ri);
       cp_async_commit();
       cp_async_wait<D>();
@@ -747,7 +761,7 @@ __device__ __forceinline__ void body_3d_lazyq(const KParams &P, const PassScalar
         sXK[(i & 1) * NPAIR + t] = xk_p;
         sKP[(i & 1) * NPAIR + t] = kc_p;
       }
-      if (i >= 2 && pin) {  // output logical plane i - 2 for both points of the pair
+      if (i >= 2 && pin && live) {  // output logical plane i - 2 for both points of the pair
         const double2 *X0 = sXK + ((i + 1) & 1) * NPAIR, *K0 = sKP + ((i + 1) & 1) * NPAIR;
         const double2 r = stencil_pair(xk_0, k_0, X0[t - 1].y, X0[t + 1].x, K0[t - 1].y, K0[t + 1].x, X0[t - PX],
                                        X0[t + PX], K0[t - PX], K0[t + PX], xk_m, k_m, xk_p, kc_p, hh, bt_0);
@@ -773,15 +787,15 @@ __device__ __forceinline__ void body_3d_lazyq(const KParams &P, const PassScalar
   v[0] += v0; v[1] += v1; v[2] += v2; v[3] += v3; v[4] += v4;
 }
 
-template <int PM, int TYM, int CPS, int DD>
-__global__ void __launch_bounds__(LazyQ<PM, TYM, CPS, DD>::NT, CPS) k_pass_3d_lazyq(KParams P) {
+template <int PM, int TYM, int CPS, int DD, int NH = 1>
+__global__ void __launch_bounds__(LazyQ<PM, TYM, CPS, DD, NH>::BLOCK, CPS / NH) k_pass_3d_lazyq(KParams P) {
   __shared__ PassScalars S;
   pass_guard(P);
   if (threadIdx.x == 0) load_pass_scalars(P, S);
   __syncthreads();
   if (S.k == 0) return;
   double v[NDOT] = {0.0, 0.0, 0.0, 0.0, 0.0};
-  body_3d_lazyq<PM, TYM, CPS, DD>(P, S, v);
+  body_3d_lazyq<PM, TYM, CPS, DD, NH>(P, S, v);
   pass_epilogue(P, S.k, v);
 }
 
