@@ -61,7 +61,15 @@ struct InnerCarry {
 struct InnerCounters {
   long long passes, kv;
   unsigned long long ns_pass, t0;
+#ifdef KIOPS_PHASE_TIMERS
+  long long d[6];
+#endif
 };
+#ifdef KIOPS_PHASE_TIMERS
+#define DSTAMP(i) do { const long long _c = clock64(); K.d[i] += _c - _cl; _cl = _c; } while (0)
+#else
+#define DSTAMP(i) do { } while (0)
+#endif
 
 // Per-CTA dot records: recs[k & 1][cta][0..4] (64-byte slots).  A CTA writes its
 // block partials, then (release) adds 1 to the monotonic pass_count; one thread per
@@ -82,28 +90,44 @@ __device__ __forceinline__ void red_release_add_u64(unsigned long long *p, unsig
 }
 
 // pass_finalize (passes.cuh) run by the 32 lanes of warp 0 with the same expressions
-// (bitwise identical results): every lane evaluates the shared chain sqrt -> h1 -> h2,
-// lane c < p the tail entry c of x_{k+1}, so the ~16 dependent fp64 divisions of the
-// serial version become a chain of ~4.  wr: this CTA (0) writes the state.
+// (bitwise identical results).  The serial version is a chain of ~16 dependent fp64
+// divisions (~3600 clk measured); here every quotient of one dependency level is one
+// lane's operand pair of a single warp-uniform division (no divergence), so the chain
+// is sqrt -> 3 divisions:
+//   level A: h1 = E1/(s'*s) | t = E2/(s*s) | a0 = 1/s | cn = sqrt(R2')/s' | A_c = Kt_c/s
+//   level B: u = (h1*G)/(s'*s) | a2 = h1/s' | B_c = (h1*t'_c)/s'        (h2 = t - u)
+//   level C: a1 = h2/s | C_c = (h2*t_c)/s                 tn_c = (A_c - B_c) - C_c
+// (k = 1: A: h11 = E2/(s*s), a0, A_c; B: a1 = h11/s, B_c = (h11*t_c)/s; tn_c = A_c - B_c.)
+// Lanes 4..4+KMAXP-1 own tail entry c = lane - 4.  wr: this CTA (0) writes the state.
+// n / d for d > 0, bitwise equal to IEEE n / d.  A zero numerator would send the
+// whole warp through the slow path of the fp64 division (the fast path handles normal
+// quotients only): divide 1 instead and return the signed zero (= n / d for d > 0).
+__device__ __forceinline__ double div_pos(double n, double d) {
+  const bool z = n == 0.0;
+  const double q = (z ? 1.0 : n) / d;
+  return z ? n : q;
+}
+
 __device__ __forceinline__ void finalize_warp(const KParams &P, int k, const double (&v0)[NDOT], InnerCarry &C,
                                               PassScalars &Sn, bool wr, InnerCounters &K) {
   DevState *st = P.st;
   const int lane = threadIdx.x, p = P.p;
+  const unsigned FULL = 0xffffffffu;
+#ifdef KIOPS_PHASE_TIMERS
+  long long _cl = clock64();
+#endif
   double v[NDOT];
 #pragma unroll
-  for (int q = 0; q < NDOT; q++) v[q] = __shfl_sync(0xffffffffu, v0[q], 0);
-  double Kt[KMAXP];
-#pragma unroll
-  for (int c = 0; c < KMAXP; c++) Kt[c] = (c + 1 < p) ? C.tk[c + 1 < KMAXP ? c + 1 : 0] : 0.0;
+  for (int q = 0; q < NDOT; q++) v[q] = __shfl_sync(FULL, v0[q], 0);
   double S = v[0], G = v[1], E1 = v[2], E2 = v[3], R = v[4];
 #pragma unroll
   for (int c = 0; c < KMAXP; c++)
     if (c < p) {
-      const double tkc = C.tk[c];
+      const double tkc = C.tk[c], ktc = (c + 1 < p) ? C.tk[c + 1 < KMAXP ? c + 1 : 0] : 0.0;
       S += tkc * tkc;
-      R += Kt[c] * Kt[c];
-      E2 += tkc * Kt[c];
-      if (k >= 2) { G += C.tkm1[c] * tkc; E1 += C.tkm1[c] * Kt[c]; }
+      R += ktc * ktc;
+      E2 += tkc * ktc;
+      if (k >= 2) { G += C.tkm1[c] * tkc; E1 += C.tkm1[c] * ktc; }
     }
   const bool l0 = lane == 0;
   if (wr && l0) {
@@ -128,16 +152,18 @@ __device__ __forceinline__ void finalize_warp(const KParams &P, int k, const dou
     if (l0) C.go = 0;
     return;
   }
+  DSTAMP(0);
   const double sk = sqrt(S);
+  const int c = lane - 4;  // tail entry owned by this lane
+  const bool own = c >= 0 && c < p;
+  const int cc = (c >= 0 && c < KMAXP) ? c : 0;
+  const double tkc = C.tk[cc], tkm1c = C.tkm1[cc];
+  const double ktc = (own && c + 1 < p) ? C.tk[cc + 1 < KMAXP ? cc + 1 : 0] : 0.0;
+  const double skm1 = C.skm1;
+  const double r2s = k >= 2 ? sqrt(C.R2km1) : 0.0;
   double *H = P.H;
 #define HH(i, j) H[((i)-1) + (size_t)((j)-1) * LDH]
-  const int c = lane;  // this lane's tail entry
-  const double tkc = c < KMAXP ? C.tk[c] : 0.0, tkm1c = c < KMAXP ? C.tkm1[c] : 0.0;
-  double Ktc = 0.0;
-#pragma unroll
-  for (int q = 0; q < KMAXP; q++)
-    if (q == c) Ktc = Kt[q];
-  double tn = 0.0, a1 = 0.0, a2 = 0.0;
+  double tn = 0.0, a0, a1, a2 = 0.0;
   int go;
   if (k == 1) {  // beta = ||x_1|| (Alg. 1 l.14)
     if (wr && l0) {
@@ -153,18 +179,32 @@ __device__ __forceinline__ void finalize_warp(const KParams &P, int k, const dou
       if (l0) C.go = 0;
       return;
     }
-    const double h11 = E2 / (sk * sk);
+    // level A
+    double num = lane == 1 ? E2 : (lane == 2 ? 1.0 : ktc);
+    double den = lane == 1 ? sk * sk : sk;
+    const double qa = div_pos(num, den);
+    const double h11 = __shfl_sync(FULL, qa, 1);
+    a0 = __shfl_sync(FULL, qa, 2);
     if (wr && l0) HH(1, 1) = h11;
-    if (c < p) tn = Ktc / sk - h11 * tkc / sk;
+    // level B
+    num = lane == 1 ? h11 : h11 * tkc;
+    const double qb = div_pos(num, sk);
+    a1 = __shfl_sync(FULL, qb, 1);
+    if (own) tn = qa - qb;
     go = (1 < C.m + 1) ? 1 : 0;
-    if (lane == 9) a1 = h11 / sk;
   } else {  // k >= 2 closes Alg. 2 iteration k-1
+    DSTAMP(1);
+    // level A
+    double num = lane == 0 ? E1 : lane == 1 ? E2 : lane == 2 ? 1.0 : lane == 3 ? r2s : ktc;
+    double den = lane == 0 ? skm1 * sk : lane == 1 ? sk * sk : lane == 3 ? skm1 : sk;
+    const double qa = div_pos(num, den);
+    const double h1 = __shfl_sync(FULL, qa, 0), tt = __shfl_sync(FULL, qa, 1), cn = __shfl_sync(FULL, qa, 3);
+    a0 = __shfl_sync(FULL, qa, 2);
     if (wr && l0) {
       K.kv++;
       st->kv = K.kv;
     }
-    const double skm1 = C.skm1;
-    const double cn = sqrt(C.R2km1) / skm1;
+    DSTAMP(2);
     const double thr = fmax(1e-12 * cn, 1e-14);  // R3
     if (sk <= thr) {                             // Alg. 2 l.12-15
       if (wr && l0) {
@@ -179,32 +219,35 @@ __device__ __forceinline__ void finalize_warp(const KParams &P, int k, const dou
       P.sig[k] = sk;
       P.R2[k] = R;
     }
-    const double h1 = E1 / (skm1 * sk);
-    const double h2 = E2 / (sk * sk) - h1 * G / (skm1 * sk);
+    // level B
+    num = lane == 0 ? h1 * G : lane == 3 ? h1 : h1 * tkm1c;
+    den = lane == 0 ? skm1 * sk : skm1;
+    const double qb = div_pos(num, den);
+    const double u = __shfl_sync(FULL, qb, 0);
+    a2 = __shfl_sync(FULL, qb, 3);
+    const double h2 = tt - u;
     if (wr && l0) {
       HH(k - 1, k) = h1;
       HH(k, k) = h2;
     }
-    if (c < p) tn = Ktc / sk - h1 * tkm1c / skm1 - h2 * tkc / sk;
+    // level C
+    num = lane == 1 ? h2 : h2 * tkc;
+    const double qc = div_pos(num, sk);
+    a1 = __shfl_sync(FULL, qc, 1);
+    if (own) tn = (qa - qb) - qc;
     go = (k < C.m + 1) ? 1 : 0;
-    if (lane == 9) a1 = h2 / sk;    // = H(k,k)/sig[k]      (load_pass_scalars of pass k+1)
-    if (lane == 10) a2 = h1 / skm1; // = H(k-1,k)/sig[k-1]
+    DSTAMP(3);
   }
 #undef HH
-  if (wr && c < p) P.tails[(k + 1) * KMAXP + c] = tn;
+  if (wr && own) P.tails[(k + 1) * KMAXP + c] = tn;
   if (wr && l0 && !go) set_cond(P, COND_INNER, 0u);
-  double a0 = 0.0;
-  if (lane == 8) a0 = 1.0 / sk;
-  a0 = __shfl_sync(0xffffffffu, a0, 8);
-  a1 = __shfl_sync(0xffffffffu, a1, 9);
-  a2 = __shfl_sync(0xffffffffu, a2, 10);
   if (l0) C.go = go;
   if (!go) return;
-  if (c < KMAXP) {
-    Sn.btp[c] = c < p ? C.nu * tkc : 0.0;
-    Sn.btc[c] = c < p ? C.nu * tn : 0.0;
-    C.tkm1[c] = c < p ? tkc : 0.0;
-    C.tk[c] = c < p ? tn : 0.0;
+  if (c >= 0 && c < KMAXP) {
+    Sn.btp[c] = own ? C.nu * tkc : 0.0;
+    Sn.btc[c] = own ? C.nu * tn : 0.0;
+    C.tkm1[c] = own ? tkc : 0.0;
+    C.tk[c] = own ? tn : 0.0;
   }
   if (l0) {
     const int kn = k + 1;  // <= m + 1 <= m_max + 1
@@ -214,10 +257,11 @@ __device__ __forceinline__ void finalize_warp(const KParams &P, int k, const dou
     Sn.xout = P.V + (size_t)(kn - 1) * (size_t)P.ldN;
     Sn.a0 = a0;
     Sn.a1 = a1;
-    Sn.a2 = (k == 1) ? 0.0 : a2;
+    Sn.a2 = a2;
     C.skm1 = sk;
     C.R2km1 = R;
   }
+  DSTAMP(4);
 }
 
 // The loop.  body(S, v) streams pass S.k over this CTA's share and accumulates the
@@ -231,6 +275,9 @@ __device__ __forceinline__ void inner_loop(const KParams &P, Body &&body) {
   const unsigned nb = gridDim.x;
   const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
   InnerCounters K{};
+#ifdef KIOPS_PHASE_TIMERS
+  for (int i = 0; i < 6; i++) K.d[i] = 0;
+#endif
   unsigned gen = 0;
   if (threadIdx.x == 0) {
     if (blockIdx.x == 0) {
@@ -274,7 +321,8 @@ __device__ __forceinline__ void inner_loop(const KParams &P, Body &&body) {
   }
 #ifdef KIOPS_PHASE_TIMERS  // debug build: CTA 0 prints body / barrier / finalise time per launch
   const int k_first = S.k;
-  unsigned long long tb = 0, tw = 0, tf = 0, ta = gtimer(), tt;
+  unsigned long long tb = 0, tw = 0, tf = 0, tp = 0, ta = gtimer(), tt;
+  long long cf1 = 0;
 #define PHASE(acc) do { tt = gtimer(); acc += tt - ta; ta = tt; } while (0)
 #else
 #define PHASE(acc) do { } while (0)
@@ -289,14 +337,15 @@ __device__ __forceinline__ void inner_loop(const KParams &P, Body &&body) {
       double *mine = rec_ptr(P, k & 1, blockIdx.x);
 #pragma unroll
       for (int q = 0; q < NDOT; q++) __stcg(mine + q, v[q]);
-      __threadfence();  // release: this CTA's x_k, r_k (ordered by block_sum's barrier) and record
+      // release (cumulative: covers the CTA's x_k, r_k writes ordered before block_sum's
+      // bar.sync) ... acquire on the counter, propagated to the CTA by the bar.sync below
       red_release_add_u64(&st->pass_count, 1ull);
       target += nb;
       while (ld_acquire_u64(&st->pass_count) < target) {
       }
-      __threadfence();
     }
     __syncthreads();
+    PHASE(tp);
     // every CTA's record, in the fixed block order of pass_finalize
     double w[NDOT];
 #pragma unroll
@@ -308,19 +357,35 @@ __device__ __forceinline__ void inner_loop(const KParams &P, Body &&body) {
     }
     PHASE(tw);
     block_sum<NDOT>(w, red);
+#ifdef KIOPS_PHASE_TIMERS
+    const long long c0 = clock64();
+#endif
     if (threadIdx.x < 32) finalize_warp(P, k, w, C, S, blockIdx.x == 0, K);
+#ifdef KIOPS_PHASE_TIMERS
+    const long long c1 = clock64();
+    cf1 += c1 - c0;
+#endif
     __syncthreads();
     PHASE(tf);
     if (!C.go) break;
   }
 #ifdef KIOPS_PHASE_TIMERS
+  if (threadIdx.x == 0 && blockIdx.x < 3) {
+    const long long q0 = clock64();
+    const unsigned long long g0 = gtimer();
+    const long long q1 = clock64();
+    const unsigned long long g1 = gtimer();
+    const long long q2 = clock64();
+    printf("CTA %d warp-0 finalise %lld clk; gtimer read %lld / %lld clk (dg %llu ns) stamps %lld %lld %lld %lld %lld\n", blockIdx.x, cf1, q1 - q0,
+           q2 - q1, g1 - g0, K.d[0], K.d[1], K.d[2], K.d[3], K.d[4]);
+  }
   if (threadIdx.x == 0 && k_first == 1) {
     unsigned smid;
     asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
     printf("CTABODY %d %u %.2f %.2f\n", blockIdx.x, smid, tb * 1e-3, tw * 1e-3);
   }
-  if (lead) printf("PHASES k_end %d body %.2f us barrier %.2f us finalise %.2f us (sums over the launch)\n", S.k,
-                   tb * 1e-3, tw * 1e-3, tf * 1e-3);
+  if (lead) printf("PHASES k_end %d body %.2f us poll %.2f us records %.2f us finalise %.2f us (warp-0 finalise %lld clk) (sums over the launch)\n", S.k,
+                   tb * 1e-3, tp * 1e-3, tw * 1e-3, tf * 1e-3, cf1);
 #endif
 #undef PHASE
 }

@@ -943,19 +943,22 @@ __device__ __forceinline__ void body_2d_async(const KParams &P, const PassScalar
   for (int c = 0; c < PM; c++) { btc[c] = S.btc[c]; Bc[c] = S.B[c]; }
   const int nrows = (int)(y1 - y0) + 2;  // logical row i = grid row y0 - 1 + i
   long long yi = wrapc(y0 - 1, ny);      // next row to issue
-  int si = 0;                            // its ring slot
+  int si = 0, ii = 0;                    // its ring slot and logical index
   auto issue = [&]() {
     const long long g = pxw + nx * yi;
     double2 *d = ring + si * NOP * 32;
     if (use_r) cp_async16(d, rin + g);
     cp_async16(d + 32, xprev + g);
     if (use_pp) cp_async16(d + 64, xpp + g);
-    if (use_d) cp_async16(d + 96, P.diag + g);
-    if (pin)
+    if (ii >= 1 && ii <= nrows - 2) {  // diag and B only on output rows (not the y-halo rows)
+      if (use_d) cp_async16(d + 96, P.diag + g);
+      if (pin)
 #pragma unroll
-      for (int c = 0; c < PM; c++) cp_async16(d + (4 + c) * 32, Bc[c] + g);
+        for (int c = 0; c < PM; c++) cp_async16(d + (4 + c) * 32, Bc[c] + g);
+    }
     yi = (yi + 1 == ny) ? 0 : yi + 1;
     si = (si + 1 == RD) ? 0 : si + 1;
+    ii++;
   };
 #pragma unroll
   for (int q = 0; q < D; q++) {
