@@ -235,7 +235,7 @@ def main():
     clk = ClockSampler(os.path.join(ROOT, f"gpurun_out/clocks_rank{rank}.csv"
                                     if os.path.isdir(os.path.join(ROOT, "gpurun_out")) else f"/tmp/clocks_{rank}.csv"))
     totals = {"pass_ms": 0.0, "ctrl_ms": 0.0, "expm_ms": 0.0, "gemv_ms": 0.0, "passes": 0, "krylov_vectors": 0, "expm_calls": 0,
-              "substeps": 0, "rejections": 0}
+              "substeps": 0, "rejections": 0, "pass_launches": 0}
     with clk:
         time.sleep(0.3)
         if world > 1:
@@ -275,7 +275,9 @@ def main():
     achieved = bpp * passes / (pass_ms * 1e-3) / 1e9 if pass_ms > 0 else None
     peak, peak_src = hbm_peak()
     per_step = {key: totals[key] / args.steps for key in totals}
-    launches_per_step = 1 + (2 if cfg["op"]["kind"] == "csr" else 1) * per_step["passes"] + \
+    # setup + pass kernels (per pass, or one persistent launch per Alg. 2 run; CSR: form + SpMV per
+    # pass) + one controller per attempt + one GEMV per accepted substep
+    launches_per_step = 1 + (2 if cfg["op"]["kind"] == "csr" else 1) * per_step["pass_launches"] + \
         (per_step["substeps"] + per_step["rejections"]) + per_step["substeps"]
     traffic = None
     tpath = os.path.join(ROOT, "profiles", f"ncu_traffic_config{args.config}.json")
@@ -301,12 +303,13 @@ def main():
                                 "kv_per_s": per_step["krylov_vectors"] / (ms_step * 1e-3)}},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                     "kernel": {"stencil3d7": "k_pass_3d_lazyq (fused IOP pass)",
-                                "stencil2d5": "k_pass_2d_lazy (fused IOP pass)",
-                                "stencil1d3": "k_pass_2d_lazy (fused IOP pass, ny = 1)",
+                     "kernel": {"stencil3d7": "k_inner_3d_lazyq (fused IOP pass, persistent inner loop)",
+                                "stencil2d5": "k_inner_2d_lazy (fused IOP pass, persistent inner loop)",
+                                "stencil1d3": "k_inner_2d_lazy (fused IOP pass, ny = 1, persistent inner loop)",
                                 "csr": "k_csr_form + k_sell_spmv (fused IOP pass)"}.get(cfg["op"]["kind"], "fused IOP pass"),
                      "algorithmic_bytes_per_launch": bpp, "peak_source": peak_src,
-                     "timing": "device %globaltimer accumulated per launch inside the graph, over the timed steps"},
+                     "timing": "device %globaltimer per pass (pass start to the end of its grid reduction and "
+                               "finalisation), accumulated inside the graph over the timed steps"},
         "gpu_launches": int(round(launches_per_step * args.steps)),
         "e2e": {"value": e2e_ms / world, "unit": "ms/call",
                 "h2d_bytes_per_step": 8 * cfg["N"] * (cfg["p"] + 1),

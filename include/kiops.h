@@ -106,6 +106,8 @@ typedef struct {
   double pass_ms, ctrl_ms, gemv_ms; /* device-side kernel time (%globaltimer) of the fused
                                        passes, the controller and the GEMV in this call */
   double expm_ms;                   /* part of ctrl_ms spent in the F = exp(tau H~) of Alg. 1 l.18 */
+  int64_t pass_launches;            /* launches of the pass kernel(s): one per pass, or one per Alg. 2
+                                       run with the persistent inner loop (KIOPS_PERSIST=0 disables it) */
 } kiops_stats;
 
 /* One row per attempt (accepted or rejected), for oracle <-> GPU trace parity. */

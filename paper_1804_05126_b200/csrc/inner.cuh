@@ -61,15 +61,7 @@ struct InnerCarry {
 struct InnerCounters {
   long long passes, kv;
   unsigned long long ns_pass, t0;
-#ifdef KIOPS_PHASE_TIMERS
-  long long d[6];
-#endif
 };
-#ifdef KIOPS_PHASE_TIMERS
-#define DSTAMP(i) do { const long long _c = clock64(); K.d[i] += _c - _cl; _cl = _c; } while (0)
-#else
-#define DSTAMP(i) do { } while (0)
-#endif
 
 // Per-CTA dot records: recs[k & 1][cta][0..4] (64-byte slots).  A CTA writes its
 // block partials, then (release) adds 1 to the monotonic pass_count; one thread per
@@ -113,9 +105,6 @@ __device__ __forceinline__ void finalize_warp(const KParams &P, int k, const dou
   DevState *st = P.st;
   const int lane = threadIdx.x, p = P.p;
   const unsigned FULL = 0xffffffffu;
-#ifdef KIOPS_PHASE_TIMERS
-  long long _cl = clock64();
-#endif
   double v[NDOT];
 #pragma unroll
   for (int q = 0; q < NDOT; q++) v[q] = __shfl_sync(FULL, v0[q], 0);
@@ -152,7 +141,6 @@ __device__ __forceinline__ void finalize_warp(const KParams &P, int k, const dou
     if (l0) C.go = 0;
     return;
   }
-  DSTAMP(0);
   const double sk = sqrt(S);
   const int c = lane - 4;  // tail entry owned by this lane
   const bool own = c >= 0 && c < p;
@@ -193,7 +181,6 @@ __device__ __forceinline__ void finalize_warp(const KParams &P, int k, const dou
     if (own) tn = qa - qb;
     go = (1 < C.m + 1) ? 1 : 0;
   } else {  // k >= 2 closes Alg. 2 iteration k-1
-    DSTAMP(1);
     // level A
     double num = lane == 0 ? E1 : lane == 1 ? E2 : lane == 2 ? 1.0 : lane == 3 ? r2s : ktc;
     double den = lane == 0 ? skm1 * sk : lane == 1 ? sk * sk : lane == 3 ? skm1 : sk;
@@ -204,7 +191,6 @@ __device__ __forceinline__ void finalize_warp(const KParams &P, int k, const dou
       K.kv++;
       st->kv = K.kv;
     }
-    DSTAMP(2);
     const double thr = fmax(1e-12 * cn, 1e-14);  // R3
     if (sk <= thr) {                             // Alg. 2 l.12-15
       if (wr && l0) {
@@ -236,7 +222,6 @@ __device__ __forceinline__ void finalize_warp(const KParams &P, int k, const dou
     a1 = __shfl_sync(FULL, qc, 1);
     if (own) tn = (qa - qb) - qc;
     go = (k < C.m + 1) ? 1 : 0;
-    DSTAMP(3);
   }
 #undef HH
   if (wr && own) P.tails[(k + 1) * KMAXP + c] = tn;
@@ -261,7 +246,6 @@ __device__ __forceinline__ void finalize_warp(const KParams &P, int k, const dou
     C.skm1 = sk;
     C.R2km1 = R;
   }
-  DSTAMP(4);
 }
 
 // The loop.  body(S, v) streams pass S.k over this CTA's share and accumulates the
@@ -275,9 +259,6 @@ __device__ __forceinline__ void inner_loop(const KParams &P, Body &&body) {
   const unsigned nb = gridDim.x;
   const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
   InnerCounters K{};
-#ifdef KIOPS_PHASE_TIMERS
-  for (int i = 0; i < 6; i++) K.d[i] = 0;
-#endif
   unsigned gen = 0;
   if (threadIdx.x == 0) {
     if (blockIdx.x == 0) {
@@ -346,7 +327,9 @@ __device__ __forceinline__ void inner_loop(const KParams &P, Body &&body) {
     }
     __syncthreads();
     PHASE(tp);
-    // every CTA's record, in the fixed block order of pass_finalize
+    // every CTA's record, in the fixed block order of pass_finalize.  (Issuing pass
+    // k+1's first loads here, before its scalars exist, measured slower: the extra
+    // traffic delays the record loads and the finalisation more than it hides.)
     double w[NDOT];
 #pragma unroll
     for (int q = 0; q < NDOT; q++) w[q] = 0.0;
@@ -370,15 +353,6 @@ __device__ __forceinline__ void inner_loop(const KParams &P, Body &&body) {
     if (!C.go) break;
   }
 #ifdef KIOPS_PHASE_TIMERS
-  if (threadIdx.x == 0 && blockIdx.x < 3) {
-    const long long q0 = clock64();
-    const unsigned long long g0 = gtimer();
-    const long long q1 = clock64();
-    const unsigned long long g1 = gtimer();
-    const long long q2 = clock64();
-    printf("CTA %d warp-0 finalise %lld clk; gtimer read %lld / %lld clk (dg %llu ns) stamps %lld %lld %lld %lld %lld\n", blockIdx.x, cf1, q1 - q0,
-           q2 - q1, g1 - g0, K.d[0], K.d[1], K.d[2], K.d[3], K.d[4]);
-  }
   if (threadIdx.x == 0 && k_first == 1) {
     unsigned smid;
     asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));

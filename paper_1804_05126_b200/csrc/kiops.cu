@@ -555,6 +555,7 @@ static kiops_status finish(kiops_ctx c, kiops_stats *stats) {
     stats->ctrl_ms = S.ns_ctrl * 1e-6;
     stats->gemv_ms = S.ns_gemv * 1e-6;
     stats->expm_ms = S.ns_expm * 1e-6;
+    stats->pass_launches = (int64_t)S.launches;
   }
   if (S.status == KIOPS_ERR_NONFINITE) { c->err = "non-finite value in the Krylov recurrence or estimate"; return KIOPS_ERR_NONFINITE; }
   if (S.status == KIOPS_ERR_NO_CONVERGENCE) { c->err = "max_attempts exceeded"; return KIOPS_ERR_NO_CONVERGENCE; }

@@ -912,26 +912,75 @@ struct Ring2 {
   static constexpr size_t smem_bytes = 16 * (size_t)8 * RD * NOP * 32;  // 8 warps per CTA
 };
 
+// Per-warp strip geometry of the async 2D pass and the row issue (one 16-byte cp.async
+// per operand and lane into ring slot si; diag and B only on output rows).
+template <int YC, int PM, int D>
+struct Strip2 {
+  static constexpr int IP = 30;  // interior pairs per warp strip
+  static constexpr int NOP = Ring2<PM, D>::NOP, RD = Ring2<PM, D>::RD;
+  bool act, pin;
+  int lane, nrows;
+  long long px, pxw, y0, y1;
+  double2 *ring;
+  __device__ __forceinline__ Strip2(const KParams &P) {
+    extern __shared__ double2 smem2[];
+    const long long nx = P.nx, ny = P.ny;
+    // 32-bit strip indices (strips < 2^31: N < 2^31 * 60 * YC)
+    const int nsx = (int)((nx + 2 * IP - 1) / (2 * IP)), ncy = (int)((ny + YC - 1) / YC);
+    lane = threadIdx.x & 31;
+    const int w = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    act = (long long)w < (long long)nsx * ncy;  // warp-uniform
+    ring = smem2 + (size_t)(threadIdx.x >> 5) * RD * NOP * 32 + lane;
+    const int cy = act ? w / nsx : 0, sx = act ? w - cy * nsx : 0;
+    const long long x0 = (long long)sx * 2 * IP;
+    y0 = (long long)cy * YC;
+    y1 = (y0 + YC < ny) ? y0 + YC : ny;
+    px = x0 - 2 + 2 * lane;
+    pxw = wrapc(px, nx);
+    pin = act && lane >= 1 && lane <= IP && px < nx;
+    nrows = (int)(y1 - y0) + 2;  // logical row i = grid row y0 - 1 + i
+  }
+  // issue logical row ii (grid row yi) into slot si
+  __device__ __forceinline__ void issue(const KParams &P, const double *rin, const double *xprev, const double *xpp,
+                                        const double *const *Bc, long long yi, int si, int ii) const {
+    const long long g = pxw + P.nx * yi;
+    double2 *d = ring + si * NOP * 32;
+    if (rin) cp_async16(d, rin + g);
+    cp_async16(d + 32, xprev + g);
+    if (xpp) cp_async16(d + 64, xpp + g);
+    if (ii >= 1 && ii <= nrows - 2) {  // diag and B only on output rows (not the y-halo rows)
+      if (P.diag) cp_async16(d + 96, P.diag + g);
+      if (pin)
+#pragma unroll
+        for (int c = 0; c < PM; c++) cp_async16(d + (4 + c) * 32, Bc[c] + g);
+    }
+  }
+  // the first D rows of pass k (one commit group each); rin = NULL for k = 1
+  __device__ __forceinline__ void prologue(const KParams &P, const double *rin, const double *xprev, const double *xpp,
+                                           const double *const *Bc) const {
+    if (!act) return;
+    long long yi = wrapc(y0 - 1, P.ny);
+#pragma unroll
+    for (int q = 0; q < D; q++) {
+      if (q < nrows) issue(P, rin, xprev, xpp, Bc, yi, q, q);
+      cp_async_commit();
+      yi = (yi + 1 == P.ny) ? 0 : yi + 1;
+    }
+  }
+};
+
 template <int YC, int PM, int D>
 __device__ __forceinline__ void body_2d_async(const KParams &P, const PassScalars &S, double (&v)[NDOT]) {
-  constexpr int IP = 30;  // interior pairs per warp strip
-  constexpr int NOP = Ring2<PM, D>::NOP, RD = Ring2<PM, D>::RD;
-  extern __shared__ double2 smem2[];
+  const Strip2<YC, PM, D> G(P);
+  constexpr int RD = Strip2<YC, PM, D>::RD, NOP = Strip2<YC, PM, D>::NOP;
+  if (!G.act) return;  // warp-uniform
   const int k = S.k;
   const long long nx = P.nx, ny = P.ny;
-  const long long nsx = (nx + 2 * IP - 1) / (2 * IP), ncy = (ny + YC - 1) / YC;
-  const int lane = threadIdx.x & 31;
-  const long long w = (blockIdx.x * (long long)blockDim.x + threadIdx.x) / 32;
-  if (w >= nsx * ncy) return;  // warp-uniform
-  double2 *ring = smem2 + (size_t)(threadIdx.x >> 5) * RD * NOP * 32 + lane;
-  const long long sx = w % nsx, cy = w / nsx;
-  const long long x0 = sx * 2 * IP, y0 = cy * YC;
-  const long long y1 = (y0 + YC < ny) ? y0 + YC : ny;
-  const long long px = x0 - 2 + 2 * lane;
-  const long long pxw = wrapc(px, nx);
-  const bool pin = lane >= 1 && lane <= IP && px < nx;
+  const bool pin = G.pin;
+  const long long px = G.px, y0 = G.y0;
+  const int nrows = G.nrows;
   const bool use_r = k >= 2, use_pp = S.xpp != nullptr, use_d = P.diag != nullptr;
-  const double *rin = P.r + (size_t)((k - 1) & 1) * (size_t)P.ldN;
+  const double *rin = use_r ? P.r + (size_t)((k - 1) & 1) * (size_t)P.ldN : nullptr;
   double *rout = P.r + (size_t)(k & 1) * (size_t)P.ldN;
   const double *xprev = S.xprev, *xpp = S.xpp;
   double *xout = S.xout;
@@ -941,30 +990,16 @@ __device__ __forceinline__ void body_2d_async(const KParams &P, const PassScalar
   const double *Bc[PM > 0 ? PM : 1];
 #pragma unroll
   for (int c = 0; c < PM; c++) { btc[c] = S.btc[c]; Bc[c] = S.B[c]; }
-  const int nrows = (int)(y1 - y0) + 2;  // logical row i = grid row y0 - 1 + i
-  long long yi = wrapc(y0 - 1, ny);      // next row to issue
-  int si = 0, ii = 0;                    // its ring slot and logical index
+  G.prologue(P, rin, xprev, xpp, Bc);
+  long long yi = wrapc(y0 - 1 + D, ny);  // next row to issue
+  int si = D % RD, ii = D;               // its ring slot and logical index
   auto issue = [&]() {
-    const long long g = pxw + nx * yi;
-    double2 *d = ring + si * NOP * 32;
-    if (use_r) cp_async16(d, rin + g);
-    cp_async16(d + 32, xprev + g);
-    if (use_pp) cp_async16(d + 64, xpp + g);
-    if (ii >= 1 && ii <= nrows - 2) {  // diag and B only on output rows (not the y-halo rows)
-      if (use_d) cp_async16(d + 96, P.diag + g);
-      if (pin)
-#pragma unroll
-        for (int c = 0; c < PM; c++) cp_async16(d + (4 + c) * 32, Bc[c] + g);
-    }
+    G.issue(P, rin, xprev, xpp, Bc, yi, si, ii);
     yi = (yi + 1 == ny) ? 0 : yi + 1;
     si = (si + 1 == RD) ? 0 : si + 1;
     ii++;
   };
-#pragma unroll
-  for (int q = 0; q < D; q++) {
-    if (q < nrows) issue();
-    cp_async_commit();
-  }
+  double2 *ring = G.ring;
   const double2 z2 = make_double2(0.0, 0.0);
   double2 xk_m = z2, xk_0 = z2, xm_0 = z2, d_0 = z2;
   double2 b_0[PM > 0 ? PM : 1];

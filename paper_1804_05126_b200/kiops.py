@@ -41,7 +41,7 @@ class Stats(C.Structure):
                 ("expm_calls", C.c_int64), ("passes", C.c_int64), ("final_m", C.c_int32),
                 ("happy_breakdowns", C.c_int32), ("t_reached", C.c_double), ("nu", C.c_double),
                 ("mu", C.c_double), ("pass_ms", C.c_double), ("ctrl_ms", C.c_double), ("gemv_ms", C.c_double),
-                ("expm_ms", C.c_double)]
+                ("expm_ms", C.c_double), ("pass_launches", C.c_int64)]
 
 
 class TraceRow(C.Structure):
