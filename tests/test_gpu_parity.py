@@ -319,3 +319,15 @@ def test_persistent_inner_loop_is_bitwise_identical(make, monkeypatch):
     for key in ("krylov_vectors", "passes", "substeps", "rejections", "expm_calls", "final_m"):
         assert s1[key] == s0[key] == t1[key] == t0[key], key
     assert [(r["j"], r["tau"], r["omega"]) for r in tr1] == [(r["j"], r["tau"], r["omega"]) for r in tr0]
+
+
+@pytest.mark.parametrize("env", [{"KIOPS_3D_NH": "1"}, {"KIOPS_PERSIST": "0"}, {"KIOPS_2D_ASYNC": "0"}])
+def test_alternative_pass_layouts(env, monkeypatch):
+    """The layout switches (one z-part per CTA in 3D, per-pass launches, the register-
+    prefetch 2D body) are the same method with a different reduction grouping: oracle
+    parity as for the defaults (replay for config 4)."""
+    for key, val in env.items():
+        monkeypatch.setenv(key, val)
+    assert_parity(W.config3(200, 72))
+    assert_parity(W.config1())
+    assert_replay_parity(W.config4(40, 36, 22))
