@@ -153,7 +153,10 @@ kiops_status kiops_apply(kiops_ctx c, const double *const *u, const double *tau_
 /* Same computation from HOST vectors: u is a HOST array of p+1 HOST pointers, w a
  * HOST array of n_out HOST pointers.  Needs options.host_staging = 1 and
  * n_out <= options.max_outputs at create.  The host<->device copies are part of
- * the call (cudaMemcpyAsync on the ctx stream; pinned host memory is fastest). */
+ * the call (cudaMemcpyAsync on the ctx stream; pinned host memory is fastest).  An
+ * output buffer in pinned, device-mapped host memory (cudaHostAlloc / cudaMallocHost /
+ * torch pin_memory on a UVA system) is written by the GEMV directly over the host link
+ * (no staging, no separate D2H copy); any other host buffer goes through staging. */
 kiops_status kiops_apply_host(kiops_ctx c, const double *const *u, const double *tau_out, int n_out,
                               double *const *w, kiops_stats *stats);
 

@@ -606,11 +606,20 @@ kiops_status kiops_apply_host(kiops_ctx c, const double *const *u, const double 
     ud[k] = stg + (size_t)k * c->L.ldN;
     CK(cudaMemcpyAsync((void *)ud[k], u[k], vb, cudaMemcpyHostToDevice, c->stream), "H2D u");
   }
-  for (int l = 0; l < n_out; l++) wd[l] = stg + (size_t)(c->p + 1 + l) * c->L.ldN;
+  bool direct[KMAXO];
+  for (int l = 0; l < n_out; l++) {
+    // pinned + device-mapped host output: the GEMV writes it over the host link
+    cudaPointerAttributes pa{};
+    direct[l] = cudaPointerGetAttributes(&pa, w[l]) == cudaSuccess && pa.type == cudaMemoryTypeHost &&
+                pa.devicePointer != nullptr;
+    if (!direct[l]) cudaGetLastError();  // clear a "not a CUDA pointer" error of the query
+    wd[l] = direct[l] ? (double *)pa.devicePointer : stg + (size_t)(c->p + 1 + l) * c->L.ldN;
+  }
   fill_call(c, ud, tau_out, n_out, wd);
   s = launch_and_finish(c, stats);
   if (s != KIOPS_OK) return s;
-  for (int l = 0; l < n_out; l++) CK(cudaMemcpyAsync(w[l], wd[l], vb, cudaMemcpyDeviceToHost, c->stream), "D2H w");
+  for (int l = 0; l < n_out; l++)
+    if (!direct[l]) CK(cudaMemcpyAsync(w[l], wd[l], vb, cudaMemcpyDeviceToHost, c->stream), "D2H w");
   return finish(c, stats);
 }
 

@@ -232,6 +232,18 @@ def test_host_api_matches_device_api():
     wd, _ = k.apply(u, c["T"])
     wh, _ = k.apply_host([np.ascontiguousarray(x) for x in c["u"]], c["T"])
     assert np.array_equal(wd[0].cpu().numpy(), wh[0])
+    # pinned (device-mapped) host outputs are written by the GEMV directly: same bits
+    hu = [torch.from_numpy(np.ascontiguousarray(x)).pin_memory() for x in c["u"]]
+    hw = [torch.full((c["N"],), np.nan, dtype=torch.float64).pin_memory() for _ in c["T"]]
+    k.apply_host(hu, c["T"], hw)
+    assert np.array_equal(wd[0].cpu().numpy(), hw[0].numpy())
+    c4 = W.config4(32, 24, 20)  # three output times: intermediate outputs written directly too
+    k4 = Kiops(c4["op"], c4["p"], device=DEV, tol=c4["tol"], m_max=c4["m_max"], host_staging=1, max_outputs=3)
+    wd4, _ = k4.apply([torch.as_tensor(x, device=DEV) for x in c4["u"]], c4["T"])
+    hw4 = [torch.full((c4["N"],), np.nan, dtype=torch.float64).pin_memory() for _ in c4["T"]]
+    k4.apply_host([torch.from_numpy(np.ascontiguousarray(x)).pin_memory() for x in c4["u"]], c4["T"], hw4)
+    for a, b in zip(wd4, hw4):
+        assert np.array_equal(a.cpu().numpy(), b.numpy())
 
 
 def test_repeatable_bitwise():
