@@ -314,6 +314,11 @@ __device__ __forceinline__ void inner_loop(const KParams &P, Body &&body) {
     body(S, v);
     block_sum<NDOT>(v, red);  // (its __syncthreads order every thread's vector writes before the fence)
     PHASE(tb);
+    double w[NDOT];
+    if (nb == 1) {  // one CTA: its block sum is the total (= the record path's sum, + 0.0 terms)
+#pragma unroll
+      for (int q = 0; q < NDOT; q++) w[q] = v[q];
+    } else {
     if (threadIdx.x == 0) {
       double *mine = rec_ptr(P, k & 1, blockIdx.x);
 #pragma unroll
@@ -330,7 +335,6 @@ __device__ __forceinline__ void inner_loop(const KParams &P, Body &&body) {
     // every CTA's record, in the fixed block order of pass_finalize.  (Issuing pass
     // k+1's first loads here, before its scalars exist, measured slower: the extra
     // traffic delays the record loads and the finalisation more than it hides.)
-    double w[NDOT];
 #pragma unroll
     for (int q = 0; q < NDOT; q++) w[q] = 0.0;
     for (int b = threadIdx.x; b < (int)nb; b += blockDim.x) {
@@ -340,6 +344,7 @@ __device__ __forceinline__ void inner_loop(const KParams &P, Body &&body) {
     }
     PHASE(tw);
     block_sum<NDOT>(w, red);
+    }
 #ifdef KIOPS_PHASE_TIMERS
     const long long c0 = clock64();
 #endif
