@@ -46,6 +46,27 @@ def hbm_peak():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+def box_copy_gbs(torch, dev):
+    """This box's copy bandwidth, measured like MEASURED_PEAKS.json (read + write bytes of a
+    1 GiB bf16 copy, best of 5, CUDA events): context for the roofline, since boxes of the
+    pool differ (the roofline's peak stays the driver-measured figure)."""
+    a = torch.empty(1 << 30, dtype=torch.bfloat16, device=dev)
+    b = torch.empty_like(a)
+    b.copy_(a)
+    best = None
+    for _ in range(5):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        b.copy_(a)
+        e1.record()
+        torch.cuda.synchronize()
+        t = e0.elapsed_time(e1) * 1e-3
+        best = t if best is None or t < best else best
+    del a, b
+    torch.cuda.empty_cache()
+    return 2 * (1 << 30) * 2 / best / 1e9
+
+
 def oracle_counts(idx):
     """The oracle's OWN counts for the full config (scripts/oracle_full_run.py)."""
     path = os.path.join(ROOT, "profiles", f"oracle_full_config{idx}.json")
@@ -274,6 +295,7 @@ def main():
     pass_ms = totals["pass_ms"] / args.steps
     achieved = bpp * passes / (pass_ms * 1e-3) / 1e9 if pass_ms > 0 else None
     peak, peak_src = hbm_peak()
+    box_gbs = box_copy_gbs(torch, dev)
     per_step = {key: totals[key] / args.steps for key in totals}
     # setup + pass kernels (per pass, or one persistent launch per Alg. 2 run; CSR: form + SpMV per
     # pass) + one controller per attempt + one GEMV per accepted substep
@@ -307,7 +329,8 @@ def main():
                                 "stencil2d5": "k_inner_2d_lazy (fused IOP pass, persistent inner loop)",
                                 "stencil1d3": "k_inner_2d_lazy (fused IOP pass, ny = 1, persistent inner loop)",
                                 "csr": "k_csr_form + k_sell_spmv (fused IOP pass)"}.get(cfg["op"]["kind"], "fused IOP pass"),
-                     "algorithmic_bytes_per_launch": bpp, "peak_source": peak_src,
+                     "algorithmic_bytes_per_pass": bpp, "passes_per_launch": (per_step["passes"] / per_step["pass_launches"]) if per_step["pass_launches"] else None, "peak_source": peak_src,
+                     "box_copy_gbs": box_gbs, "frac_of_box_copy": (achieved / box_gbs) if achieved else None,
                      "timing": "device %globaltimer per pass (pass start to the end of its grid reduction and "
                                "finalisation), accumulated inside the graph over the timed steps"},
         "gpu_launches": int(round(launches_per_step * args.steps)),
