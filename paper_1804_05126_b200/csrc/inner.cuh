@@ -369,8 +369,8 @@ __device__ __forceinline__ void inner_loop(const KParams &P, Body &&body) {
 #undef PHASE
 }
 
-template <int YC, int PM, int MINB, int DA = 0>
-__global__ void __launch_bounds__(256, MINB) k_inner_2d_lazy(KParams P) {
+template <int YC, int PM, int MINB, int DA = 0, int NTH = 256>
+__global__ void __launch_bounds__(NTH, MINB) k_inner_2d_lazy(KParams P) {
   inner_loop(P, [&](const PassScalars &S, double (&v)[NDOT]) {
     if (DA > 0)
       body_2d_async<YC, PM, (DA > 0 ? DA : 1)>(P, S, v);

@@ -57,6 +57,7 @@ struct Layout {
   int grid_pass, grid_setup, grid_gemv, grid_form, grid_max;
   int block_pass;
   int nh3 = 1;  // 3D pair pass: z-parts per CTA
+  int w2d = 8;  // 2D async pass: warps per CTA
   size_t smem_pass;
 };
 
@@ -135,11 +136,19 @@ Layout layout(const kiops_operator_desc *op, int p, const kiops_options *o) {
       if (op->nx % 2 == 0 && p <= 4) {  // warp-strip lazy kernel (16-byte pairs)
         const int yc = L2YC;
         const long long strips = (op->nx + 59) / 60 * ((op->ny + yc - 1) / yc);
-        L.grid_pass = (int)((strips + 7) / 8);
         const char *ev = getenv("KIOPS_2D_ASYNC");  // 0: register-prefetch body (A/B switch)
+        // warps per CTA: 16 (one 512-thread CTA per SM: half the per-CTA dot records to gather
+        // per pass) when that still fills >= 128 SMs -- config 3: 144 CTAs, pass 14.8 -> 13.6 us
+        // (measured); else 8.  KIOPS_2D_WARPS=8|16 forces (async body only).
+        const char *ew = getenv("KIOPS_2D_WARPS");
+        L.w2d = (ew && (atoi(ew) == 8 || atoi(ew) == 16)) ? atoi(ew) : ((strips + 15) / 16 >= 128 ? 16 : 8);
+        if (ev && ev[0] == '0') L.w2d = 8;
+        L.block_pass = 32 * L.w2d;
+        L.grid_pass = (int)((strips + L.w2d - 1) / L.w2d);
         L.smem_pass = (ev && ev[0] == '0') ? 0
-                    : p == 0 ? Ring2<0, 2>::smem_bytes : p == 1 ? Ring2<1, 2>::smem_bytes
-                    : p == 2 ? Ring2<2, 2>::smem_bytes : p == 3 ? Ring2<3, 2>::smem_bytes : Ring2<4, 2>::smem_bytes;
+                    : (L.w2d / 8) * (p == 0 ? Ring2<0, 2>::smem_bytes : p == 1 ? Ring2<1, 2>::smem_bytes
+                                   : p == 2 ? Ring2<2, 2>::smem_bytes : p == 3 ? Ring2<3, 2>::smem_bytes
+                                                                          : Ring2<4, 2>::smem_bytes);
       } else if (op->kind == KIOPS_OP_STENCIL1D3) {
         L.grid_pass = (int)((op->nx + 255) / 256);
         L.smem_pass = stencil_smem_bytes<T1D>();
@@ -292,6 +301,10 @@ static kiops_status build_graph(kiops_ctx c) {
         fpass = c->p == 0 ? (void *)k_pass_2d_lazy<L2YC, 0, 2> : c->p == 1 ? (void *)k_pass_2d_lazy<L2YC, 1, 2>
               : c->p == 2 ? (void *)k_pass_2d_lazy<L2YC, 2, 2> : c->p == 3 ? (void *)k_pass_2d_lazy<L2YC, 3, 2>
                           : (void *)k_pass_2d_lazy<L2YC, 4, 2>;
+      else if (lazy2d && c->L.w2d == 16)
+        fpass = c->p == 0 ? (void *)k_pass_2d_lazy<L2YC, 0, 1, 2, 512> : c->p == 1 ? (void *)k_pass_2d_lazy<L2YC, 1, 1, 2, 512>
+              : c->p == 2 ? (void *)k_pass_2d_lazy<L2YC, 2, 1, 2, 512> : c->p == 3 ? (void *)k_pass_2d_lazy<L2YC, 3, 1, 2, 512>
+                          : (void *)k_pass_2d_lazy<L2YC, 4, 1, 2, 512>;
       else if (lazy2d)  // cp.async ring, 2 rows in flight per warp
         fpass = c->p == 0 ? (void *)k_pass_2d_lazy<L2YC, 0, 2, 2> : c->p == 1 ? (void *)k_pass_2d_lazy<L2YC, 1, 2, 2>
               : c->p == 2 ? (void *)k_pass_2d_lazy<L2YC, 2, 2, 2> : c->p == 3 ? (void *)k_pass_2d_lazy<L2YC, 3, 2, 2>
@@ -326,6 +339,10 @@ static kiops_status build_graph(kiops_ctx c) {
       finner = c->p == 0 ? (void *)k_inner_2d_lazy<L2YC, 0, 2> : c->p == 1 ? (void *)k_inner_2d_lazy<L2YC, 1, 2>
              : c->p == 2 ? (void *)k_inner_2d_lazy<L2YC, 2, 2> : c->p == 3 ? (void *)k_inner_2d_lazy<L2YC, 3, 2>
                          : (void *)k_inner_2d_lazy<L2YC, 4, 2>;
+    else if (lazy2d && (c->op.kind == KIOPS_OP_STENCIL1D3 || c->op.kind == KIOPS_OP_STENCIL2D5) && c->L.w2d == 16)
+      finner = c->p == 0 ? (void *)k_inner_2d_lazy<L2YC, 0, 1, 2, 512> : c->p == 1 ? (void *)k_inner_2d_lazy<L2YC, 1, 1, 2, 512>
+             : c->p == 2 ? (void *)k_inner_2d_lazy<L2YC, 2, 1, 2, 512> : c->p == 3 ? (void *)k_inner_2d_lazy<L2YC, 3, 1, 2, 512>
+                         : (void *)k_inner_2d_lazy<L2YC, 4, 1, 2, 512>;
     else if (lazy2d && (c->op.kind == KIOPS_OP_STENCIL1D3 || c->op.kind == KIOPS_OP_STENCIL2D5))
       finner = c->p == 0 ? (void *)k_inner_2d_lazy<L2YC, 0, 2, 2> : c->p == 1 ? (void *)k_inner_2d_lazy<L2YC, 1, 2, 2>
              : c->p == 2 ? (void *)k_inner_2d_lazy<L2YC, 2, 2, 2> : c->p == 3 ? (void *)k_inner_2d_lazy<L2YC, 3, 2, 2>

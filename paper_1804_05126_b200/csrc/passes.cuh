@@ -1054,8 +1054,8 @@ __device__ __forceinline__ void body_2d_async(const KParams &P, const PassScalar
   v[0] += v0; v[1] += v1; v[2] += v2; v[3] += v3; v[4] += v4;
 }
 
-template <int YC, int PM, int MINB = 2, int DA = 0>
-__global__ void __launch_bounds__(256, MINB) k_pass_2d_lazy(KParams P) {
+template <int YC, int PM, int MINB = 2, int DA = 0, int NTH = 256>
+__global__ void __launch_bounds__(NTH, MINB) k_pass_2d_lazy(KParams P) {
   __shared__ PassScalars S;
   pass_guard(P);
   if (threadIdx.x == 0) load_pass_scalars(P, S);

@@ -333,7 +333,8 @@ def test_persistent_inner_loop_is_bitwise_identical(make, monkeypatch):
     assert [(r["j"], r["tau"], r["omega"]) for r in tr1] == [(r["j"], r["tau"], r["omega"]) for r in tr0]
 
 
-@pytest.mark.parametrize("env", [{"KIOPS_3D_NH": "1"}, {"KIOPS_PERSIST": "0"}, {"KIOPS_2D_ASYNC": "0"}])
+@pytest.mark.parametrize("env", [{"KIOPS_3D_NH": "1"}, {"KIOPS_PERSIST": "0"}, {"KIOPS_2D_ASYNC": "0"},
+                                 {"KIOPS_2D_WARPS": "16"}, {"KIOPS_2D_WARPS": "8"}])
 def test_alternative_pass_layouts(env, monkeypatch):
     """The layout switches (one z-part per CTA in 3D, per-pass launches, the register-
     prefetch 2D body) are the same method with a different reduction grouping: oracle
