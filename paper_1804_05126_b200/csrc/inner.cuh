@@ -51,7 +51,7 @@ __device__ __forceinline__ void grid_sync(DevState *st, unsigned nb, unsigned &g
 // Scalars carried from the finalisation of pass k to that of pass k+1 (per CTA).
 struct InnerCarry {
   double tk[KMAXP], tkm1[KMAXP];  // tails of x_k, x_{k-1}
-  double skm1, R2km1;             // sig[k-1], R2[k-1]
+  double skm1, iskm1, R2km1;      // sig[k-1], 1 / sig[k-1], R2[k-1]
   double nu;
   const double *x1;
   int m, status_in, go, trip;
@@ -82,24 +82,14 @@ __device__ __forceinline__ void red_release_add_u64(unsigned long long *p, unsig
 }
 
 // pass_finalize (passes.cuh) run by the 32 lanes of warp 0 with the same expressions
-// (bitwise identical results).  The serial version is a chain of ~16 dependent fp64
-// divisions (~3600 clk measured); here every quotient of one dependency level is one
-// lane's operand pair of a single warp-uniform division (no divergence), so the chain
-// is sqrt -> 3 divisions:
-//   level A: h1 = E1/(s'*s) | t = E2/(s*s) | a0 = 1/s | cn = sqrt(R2')/s' | A_c = Kt_c/s
-//   level B: u = (h1*G)/(s'*s) | a2 = h1/s' | B_c = (h1*t'_c)/s'        (h2 = t - u)
-//   level C: a1 = h2/s | C_c = (h2*t_c)/s                 tn_c = (A_c - B_c) - C_c
-// (k = 1: A: h11 = E2/(s*s), a0, A_c; B: a1 = h11/s, B_c = (h11*t_c)/s; tn_c = A_c - B_c.)
+// (bitwise identical results).  One reciprocal per pass: with is = 1/s_k (and
+// is' = 1/s_{k-1}, carried from the previous pass), every Gram-Schmidt quotient of
+// Alg. 2 l.7-10 is a product (fin_* in passes.cuh, shared with pass_finalize), so the
+// chain is sqrt -> one division -> a few dependent multiplications, computed
+// redundantly by every lane: no shuffles after the broadcast of the dot sums.  (The
+// earlier form divided at each of three levels with shuffles between them: 4.5 k
+// cycles per pass measured at config 3, now 2.4 k.)
 // Lanes 4..4+KMAXP-1 own tail entry c = lane - 4.  wr: this CTA (0) writes the state.
-// n / d for d > 0, bitwise equal to IEEE n / d.  A zero numerator would send the
-// whole warp through the slow path of the fp64 division (the fast path handles normal
-// quotients only): divide 1 instead and return the signed zero (= n / d for d > 0).
-__device__ __forceinline__ double div_pos(double n, double d) {
-  const bool z = n == 0.0;
-  const double q = (z ? 1.0 : n) / d;
-  return z ? n : q;
-}
-
 __device__ __forceinline__ void finalize_warp(const KParams &P, int k, const double (&v0)[NDOT], InnerCarry &C,
                                               PassScalars &Sn, bool wr, InnerCounters &K) {
   DevState *st = P.st;
@@ -141,17 +131,17 @@ __device__ __forceinline__ void finalize_warp(const KParams &P, int k, const dou
     if (l0) C.go = 0;
     return;
   }
+  const double cn = k >= 2 ? sqrt(C.R2km1) / C.skm1 : 0.0;  // carried values only: off the chain
   const double sk = sqrt(S);
+  const double is = 1.0 / sk;
   const int c = lane - 4;  // tail entry owned by this lane
   const bool own = c >= 0 && c < p;
   const int cc = (c >= 0 && c < KMAXP) ? c : 0;
   const double tkc = C.tk[cc], tkm1c = C.tkm1[cc];
   const double ktc = (own && c + 1 < p) ? C.tk[cc + 1 < KMAXP ? cc + 1 : 0] : 0.0;
-  const double skm1 = C.skm1;
-  const double r2s = k >= 2 ? sqrt(C.R2km1) : 0.0;
   double *H = P.H;
 #define HH(i, j) H[((i)-1) + (size_t)((j)-1) * LDH]
-  double tn = 0.0, a0, a1, a2 = 0.0;
+  double tn = 0.0, a1, a2 = 0.0;
   int go;
   if (k == 1) {  // beta = ||x_1|| (Alg. 1 l.14)
     if (wr && l0) {
@@ -167,26 +157,13 @@ __device__ __forceinline__ void finalize_warp(const KParams &P, int k, const dou
       if (l0) C.go = 0;
       return;
     }
-    // level A
-    double num = lane == 1 ? E2 : (lane == 2 ? 1.0 : ktc);
-    double den = lane == 1 ? sk * sk : sk;
-    const double qa = div_pos(num, den);
-    const double h11 = __shfl_sync(FULL, qa, 1);
-    a0 = __shfl_sync(FULL, qa, 2);
+    const double h11 = fin_h11(E2, is);
     if (wr && l0) HH(1, 1) = h11;
-    // level B
-    num = lane == 1 ? h11 : h11 * tkc;
-    const double qb = div_pos(num, sk);
-    a1 = __shfl_sync(FULL, qb, 1);
-    if (own) tn = qa - qb;
+    a1 = __dmul_rn(h11, is);
+    if (own) tn = fin_tail1(ktc, tkc, h11, is);
     go = (1 < C.m + 1) ? 1 : 0;
   } else {  // k >= 2 closes Alg. 2 iteration k-1
-    // level A
-    double num = lane == 0 ? E1 : lane == 1 ? E2 : lane == 2 ? 1.0 : lane == 3 ? r2s : ktc;
-    double den = lane == 0 ? skm1 * sk : lane == 1 ? sk * sk : lane == 3 ? skm1 : sk;
-    const double qa = div_pos(num, den);
-    const double h1 = __shfl_sync(FULL, qa, 0), tt = __shfl_sync(FULL, qa, 1), cn = __shfl_sync(FULL, qa, 3);
-    a0 = __shfl_sync(FULL, qa, 2);
+    const double ism1 = C.iskm1;
     if (wr && l0) {
       K.kv++;
       st->kv = K.kv;
@@ -205,22 +182,14 @@ __device__ __forceinline__ void finalize_warp(const KParams &P, int k, const dou
       P.sig[k] = sk;
       P.R2[k] = R;
     }
-    // level B
-    num = lane == 0 ? h1 * G : lane == 3 ? h1 : h1 * tkm1c;
-    den = lane == 0 ? skm1 * sk : skm1;
-    const double qb = div_pos(num, den);
-    const double u = __shfl_sync(FULL, qb, 0);
-    a2 = __shfl_sync(FULL, qb, 3);
-    const double h2 = tt - u;
+    const double h1 = fin_h1(E1, ism1, is), h2 = fin_h2(E2, G, h1, ism1, is);
     if (wr && l0) {
       HH(k - 1, k) = h1;
       HH(k, k) = h2;
     }
-    // level C
-    num = lane == 1 ? h2 : h2 * tkc;
-    const double qc = div_pos(num, sk);
-    a1 = __shfl_sync(FULL, qc, 1);
-    if (own) tn = (qa - qb) - qc;
+    a1 = __dmul_rn(h2, is);
+    a2 = __dmul_rn(h1, ism1);
+    if (own) tn = fin_tail(ktc, tkm1c, tkc, h1, h2, ism1, is);
     go = (k < C.m + 1) ? 1 : 0;
   }
 #undef HH
@@ -240,10 +209,11 @@ __device__ __forceinline__ void finalize_warp(const KParams &P, int k, const dou
     Sn.xprev = (k == 1) ? C.x1 : P.V + (size_t)(k - 1) * (size_t)P.ldN;
     Sn.xpp = (kn >= 3) ? ((k - 1 == 1) ? C.x1 : P.V + (size_t)(k - 2) * (size_t)P.ldN) : nullptr;
     Sn.xout = P.V + (size_t)(kn - 1) * (size_t)P.ldN;
-    Sn.a0 = a0;
+    Sn.a0 = is;
     Sn.a1 = a1;
     Sn.a2 = a2;
     C.skm1 = sk;
+    C.iskm1 = is;
     C.R2km1 = R;
   }
 }
@@ -284,6 +254,7 @@ __device__ __forceinline__ void inner_loop(const KParams &P, Body &&body) {
         C.tkm1[c] = c < P.p ? P.tails[(k - 1) * KMAXP + c] : 0.0;
       }
       C.skm1 = k >= 2 ? P.sig[k - 1] : 0.0;
+      C.iskm1 = k >= 2 ? 1.0 / C.skm1 : 0.0;
       C.R2km1 = k >= 2 ? P.R2[k - 1] : 0.0;
     }
   }

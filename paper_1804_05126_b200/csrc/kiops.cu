@@ -146,7 +146,7 @@ Layout layout(const kiops_operator_desc *op, int p, const kiops_options *o) {
         L.block_pass = 32 * L.w2d;
         L.grid_pass = (int)((strips + L.w2d - 1) / L.w2d);
         L.smem_pass = (ev && ev[0] == '0') ? 0
-                    : (L.w2d / 8) * (p == 0 ? Ring2<0, 2>::smem_bytes : p == 1 ? Ring2<1, 2>::smem_bytes
+                    : RING_SLACK + (L.w2d / 8) * (p == 0 ? Ring2<0, 2>::smem_bytes : p == 1 ? Ring2<1, 2>::smem_bytes
                                    : p == 2 ? Ring2<2, 2>::smem_bytes : p == 3 ? Ring2<3, 2>::smem_bytes
                                                                           : Ring2<4, 2>::smem_bytes);
       } else if (op->kind == KIOPS_OP_STENCIL1D3) {
@@ -166,7 +166,7 @@ Layout layout(const kiops_operator_desc *op, int p, const kiops_options *o) {
         const char *ev = getenv("KIOPS_3D_NH");  // 1: one z-part per CTA (A/B switch)
         L.nh3 = (zs % 2 == 0 && !(ev && ev[0] == '1')) ? 2 : 1;
         L.grid_pass = ntx * nb * zs / L.nh3;
-        L.smem_pass = L.nh3 * (p == 1 ? LazyQ<1, Q3Y, 2, Q3D>::half_bytes : p == 2 ? LazyQ<2, Q3Y, 2, Q3D>::half_bytes
+        L.smem_pass = RING_SLACK + L.nh3 * (p == 1 ? LazyQ<1, Q3Y, 2, Q3D>::half_bytes : p == 2 ? LazyQ<2, Q3Y, 2, Q3D>::half_bytes
                                : p == 3 ? LazyQ<3, Q3Y, 2, 1>::half_bytes : LazyQ<4, Q3Y, 2, 1>::half_bytes);
         L.block_pass = L.nh3 * Q::NT;
       } else {

@@ -133,6 +133,25 @@ struct PassScalars {
   const double *B[KMAXP];     // column c of B = u_{p-c} (Thm 1, R14)
 };
 
+// Alg. 2 l.7-10 quotients of the lazy pass's finalisation as products with the
+// reciprocals is = 1/s_k, ism1 = 1/s_{k-1} (the same values in exact arithmetic as
+// E1/(s_{k-1} s_k), E2/s_k^2 - h1 G/(s_{k-1} s_k), ...).  Explicit _rn operations (no
+// FMA contraction): pass_finalize and the persistent loop's finalize_warp must round
+// identically.
+__device__ __forceinline__ double fin_h11(double E2, double is) { return __dmul_rn(__dmul_rn(E2, is), is); }
+__device__ __forceinline__ double fin_h1(double E1, double ism1, double is) { return __dmul_rn(__dmul_rn(E1, ism1), is); }
+__device__ __forceinline__ double fin_h2(double E2, double G, double h1, double ism1, double is) {
+  return __dsub_rn(__dmul_rn(__dmul_rn(E2, is), is), __dmul_rn(__dmul_rn(__dmul_rn(h1, G), ism1), is));
+}
+// tail of x_{k+1} (unnormalised tails, Thm 1): (K t_k / s_k - h1 t_{k-1} / s_{k-1}) - h2 t_k / s_k
+__device__ __forceinline__ double fin_tail(double ktc, double tkm1c, double tkc, double h1, double h2, double ism1,
+                                           double is) {
+  return __dsub_rn(__dsub_rn(__dmul_rn(ktc, is), __dmul_rn(__dmul_rn(h1, tkm1c), ism1)), __dmul_rn(__dmul_rn(h2, tkc), is));
+}
+__device__ __forceinline__ double fin_tail1(double ktc, double tkc, double h11, double is) {
+  return __dsub_rn(__dmul_rn(ktc, is), __dmul_rn(__dmul_rn(h11, tkc), is));
+}
+
 __device__ __forceinline__ void load_pass_scalars(const KParams &P, PassScalars &s) {
   const DevState *st = P.st;
   const int k = st->npass + 1;
@@ -154,8 +173,8 @@ __device__ __forceinline__ void load_pass_scalars(const KParams &P, PassScalars 
   s.xout = P.V + (size_t)(k - 1) * (size_t)P.ldN;
   const double skm1 = P.sig[k - 1];
   s.a0 = 1.0 / skm1;
-  s.a1 = H[(k - 2) + (size_t)(k - 2) * LDH] / skm1;                    // H(k-1,k-1)/s_{k-1}
-  s.a2 = (k >= 3) ? H[(k - 3) + (size_t)(k - 2) * LDH] / P.sig[k - 2] : 0.0;  // H(k-2,k-1)/s_{k-2}
+  s.a1 = __dmul_rn(H[(k - 2) + (size_t)(k - 2) * LDH], s.a0);                              // H(k-1,k-1)/s_{k-1}
+  s.a2 = (k >= 3) ? __dmul_rn(H[(k - 3) + (size_t)(k - 2) * LDH], 1.0 / P.sig[k - 2]) : 0.0;  // H(k-2,k-1)/s_{k-2}
   for (int c = 0; c < KMAXP; c++) {
     s.btp[c] = c < P.p ? nu * P.tails[(k - 1) * KMAXP + c] : 0.0;
     s.btc[c] = c < P.p ? nu * P.tails[k * KMAXP + c] : 0.0;
@@ -214,9 +233,10 @@ __device__ void pass_finalize(const KParams &P, int k, int nblocks) {
       set_cond(P, COND_INNER, 0u);
       return;
     }
-    const double h11 = E2 / (sk * sk);
+    const double is = 1.0 / sk;
+    const double h11 = fin_h11(E2, is);
     HH(1, 1) = h11;
-    for (int c = 0; c < p; c++) tn[c] = Kt[c] / sk - h11 * tk[c] / sk;
+    for (int c = 0; c < p; c++) tn[c] = fin_tail1(Kt[c], tk[c], h11, is);
     set_cond(P, COND_INNER, (1 < st->m + 1) ? 1u : 0u);
     return;
   }
@@ -233,11 +253,12 @@ __device__ void pass_finalize(const KParams &P, int k, int nblocks) {
   HH(k, k - 1) = sk;  // l.16 (R2)
   P.sig[k] = sk;
   P.R2[k] = R;
-  const double h1 = E1 / (skm1 * sk);
-  const double h2 = E2 / (sk * sk) - h1 * G / (skm1 * sk);
+  const double is = 1.0 / sk, ism1 = 1.0 / skm1;
+  const double h1 = fin_h1(E1, ism1, is);
+  const double h2 = fin_h2(E2, G, h1, ism1, is);
   HH(k - 1, k) = h1;
   HH(k, k) = h2;
-  for (int c = 0; c < p; c++) tn[c] = Kt[c] / sk - h1 * tkm1[c] / skm1 - h2 * tk[c] / sk;
+  for (int c = 0; c < p; c++) tn[c] = fin_tail(Kt[c], tkm1[c], tk[c], h1, h2, ism1, is);
   set_cond(P, COND_INNER, (k < st->m + 1) ? 1u : 0u);
 #undef HH
 }
@@ -565,6 +586,26 @@ __device__ __forceinline__ void cp_async16(void *dst, const void *src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(src) : "memory");
 }
 
+// Base of the dynamic shared memory of the 16-byte cp.async ring kernels, moved to a
+// FIXED residue mod 128 bytes.  The extern array starts right after the kernel's
+// static shared variables, so its address moved with every change to them, and the
+// ring passes measured up to 20% slower at residues that are multiples of 32 than at
+// 16 or 112 (sweep in profiles/r01_kernel_evolution.md, session 3): with the global
+// rows at 16 mod 32, those put every 32-byte sector of a copy across two shared
+// sectors.  The layouts reserve RING_SLACK extra bytes for the shift.
+#ifndef KIOPS_RING_RES2D
+#define KIOPS_RING_RES2D 112
+#endif
+#ifndef KIOPS_RING_RES3D
+#define KIOPS_RING_RES3D 112
+#endif
+#define RING_SLACK 128
+template <unsigned RES>
+__device__ __forceinline__ double2 *ring_smem_base() {
+  extern __shared__ __align__(128) double2 smem_ring[];  // base 128-byte aligned
+  return smem_ring + RES / 16;
+}
+
 // ---------------------------------------------------------------------------
 // 3D variable-kappa LAZY pass, pair version (in use for even nx, 1 <= p <= 4).
 // Every thread owns TWO x-adjacent points (a 16-byte aligned pair) of the halo-1
@@ -655,7 +696,7 @@ template <int PM, int TYM, int CPS, int DD, int NH = 1>
 __device__ __forceinline__ void body_3d_lazyq(const KParams &P, const PassScalars &S, double (&v)[NDOT]) {
   using M = LazyQ<PM, TYM, CPS, DD, NH>;
   constexpr int PX = M::PX, NPAIR = M::NPAIR, NIN = M::NIN, D = M::D, RD = M::RD, SLOT = M::SLOT, NT = M::NT;
-  extern __shared__ double2 smem2[];
+  double2 *const smem2 = ring_smem_base<KIOPS_RING_RES3D>();
   const int h = threadIdx.x / NT, t = threadIdx.x % NT;  // half, thread within the half
   double2 *sXK = smem2 + (size_t)h * (M::half_bytes / 16);  // 2 x NPAIR   x_k pairs (plane ring)
   double2 *sKP = sXK + 2 * NPAIR;                               // 2 x NPAIR   kappa pairs
@@ -923,7 +964,7 @@ struct Strip2 {
   long long px, pxw, y0, y1;
   double2 *ring;
   __device__ __forceinline__ Strip2(const KParams &P) {
-    extern __shared__ double2 smem2[];
+    double2 *const smem2 = ring_smem_base<KIOPS_RING_RES2D>();
     const long long nx = P.nx, ny = P.ny;
     // 32-bit strip indices (strips < 2^31: N < 2^31 * 60 * YC)
     const int nsx = (int)((nx + 2 * IP - 1) / (2 * IP)), ncy = (int)((ny + YC - 1) / YC);
