@@ -90,24 +90,18 @@ __device__ __forceinline__ void red_release_add_u64(unsigned long long *p, unsig
 // earlier form divided at each of three levels with shuffles between them: 4.5 k
 // cycles per pass measured at config 3, now 2.4 k.)
 // Lanes 4..4+KMAXP-1 own tail entry c = lane - 4.  wr: this CTA (0) writes the state.
-__device__ __forceinline__ void finalize_warp(const KParams &P, int k, const double (&v0)[NDOT], InnerCarry &C,
-                                              PassScalars &Sn, bool wr, InnerCounters &K) {
+__device__ __forceinline__ void finalize_warp(const KParams &P, int k, const double (&v0)[NDOT],
+                                              const double *ts, InnerCarry &C, PassScalars &Sn, bool wr,
+                                              InnerCounters &K) {
   DevState *st = P.st;
   const int lane = threadIdx.x, p = P.p;
   const unsigned FULL = 0xffffffffu;
   double v[NDOT];
 #pragma unroll
   for (int q = 0; q < NDOT; q++) v[q] = __shfl_sync(FULL, v0[q], 0);
-  double S = v[0], G = v[1], E1 = v[2], E2 = v[3], R = v[4];
-#pragma unroll
-  for (int c = 0; c < KMAXP; c++)
-    if (c < p) {
-      const double tkc = C.tk[c], ktc = (c + 1 < p) ? C.tk[c + 1 < KMAXP ? c + 1 : 0] : 0.0;
-      S += tkc * tkc;
-      R += ktc * ktc;
-      E2 += tkc * ktc;
-      if (k >= 2) { G += C.tkm1[c] * tkc; E1 += C.tkm1[c] * ktc; }
-    }
+  // + the tails' share (tail_dots, computed during the pass body)
+  const double S = __dadd_rn(v[0], ts[0]), G = __dadd_rn(v[1], ts[1]), E1 = __dadd_rn(v[2], ts[2]),
+               E2 = __dadd_rn(v[3], ts[3]), R = __dadd_rn(v[4], ts[4]);
   const bool l0 = lane == 0;
   if (wr && l0) {
     K.passes++;
@@ -225,6 +219,7 @@ __device__ __forceinline__ void inner_loop(const KParams &P, Body &&body) {
   __shared__ PassScalars S;
   __shared__ InnerCarry C;
   __shared__ double red[NDOT * 32];
+  __shared__ double ts[NDOT];
   DevState *st = P.st;
   const unsigned nb = gridDim.x;
   const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
@@ -282,6 +277,12 @@ __device__ __forceinline__ void inner_loop(const KParams &P, Body &&body) {
   for (;;) {
     const int k = S.k;
     double v[NDOT] = {0.0, 0.0, 0.0, 0.0, 0.0};
+    if (threadIdx.x == 0) {  // the tails' share of this pass's dots, kept in shared memory (not
+      double t[NDOT];        // in registers across the body, whose allocation it would change)
+      tail_dots(k, P.p, C.tk, C.tkm1, t);
+#pragma unroll
+      for (int q = 0; q < NDOT; q++) ts[q] = t[q];
+    }
     body(S, v);
     block_sum<NDOT>(v, red);  // (its __syncthreads order every thread's vector writes before the fence)
     PHASE(tb);
@@ -319,7 +320,7 @@ __device__ __forceinline__ void inner_loop(const KParams &P, Body &&body) {
 #ifdef KIOPS_PHASE_TIMERS
     const long long c0 = clock64();
 #endif
-    if (threadIdx.x < 32) finalize_warp(P, k, w, C, S, blockIdx.x == 0, K);
+    if (threadIdx.x < 32) finalize_warp(P, k, w, ts, C, S, blockIdx.x == 0, K);
 #ifdef KIOPS_PHASE_TIMERS
     const long long c1 = clock64();
     cf1 += c1 - c0;

@@ -145,6 +145,29 @@ __device__ __forceinline__ double fin_h1(double E1, double ism1, double is) { re
 __device__ __forceinline__ double fin_h2(double E2, double G, double h1, double ism1, double is) {
   return __dsub_rn(__dmul_rn(__dmul_rn(E2, is), is), __dmul_rn(__dmul_rn(__dmul_rn(h1, G), ism1), is));
 }
+// The p-entry tails' share of the five dots of pass k (x_k = [top; t_k], A~ x_k tail =
+// K t_k): S_t = t_k.t_k, G_t = t_{k-1}.t_k, E1_t = t_{k-1}.K t_k, E2_t = t_k.K t_k,
+// R_t = |K t_k|^2 (G_t, E1_t for k >= 2 only), summed apart from the grid-reduced top
+// parts and added once (S = S_top + S_t, ...).  They depend only on tails known when
+// pass k starts, so the persistent loop computes them during the pass body, off the
+// finalisation chain; pass_finalize uses the same order.
+__device__ __forceinline__ void tail_dots(int k, int p, const double *tk, const double *tkm1, double (&t)[NDOT]) {
+#pragma unroll
+  for (int q = 0; q < NDOT; q++) t[q] = 0.0;
+#pragma unroll
+  for (int c = 0; c < KMAXP; c++)
+    if (c < p) {
+      const double tkc = tk[c], ktc = (c + 1 < p) ? tk[c + 1 < KMAXP ? c + 1 : 0] : 0.0;
+      t[0] = __fma_rn(tkc, tkc, t[0]);
+      t[4] = __fma_rn(ktc, ktc, t[4]);
+      t[3] = __fma_rn(tkc, ktc, t[3]);
+      if (k >= 2) {
+        t[1] = __fma_rn(tkm1[c], tkc, t[1]);
+        t[2] = __fma_rn(tkm1[c], ktc, t[2]);
+      }
+    }
+}
+
 // tail of x_{k+1} (unnormalised tails, Thm 1): (K t_k / s_k - h1 t_{k-1} / s_{k-1}) - h2 t_k / s_k
 __device__ __forceinline__ double fin_tail(double ktc, double tkm1c, double tkc, double h1, double h2, double ism1,
                                            double is) {
@@ -215,11 +238,21 @@ __device__ void pass_finalize(const KParams &P, int k, int nblocks) {
   double Kt[KMAXP];
   for (int c = 0; c < p; c++) Kt[c] = (c + 1 < p) ? tk[c + 1] : 0.0;  // tail of A~ x_k: K t_k (Alg. 2 l.5-6)
   double S = v[0], G = v[1], E1 = v[2], E2 = v[3], R = v[4];
-  for (int c = 0; c < p; c++) {
-    S += tk[c] * tk[c];
-    R += Kt[c] * Kt[c];
-    E2 += tk[c] * Kt[c];
-    if (k >= 2) { G += tkm1[c] * tk[c]; E1 += tkm1[c] * Kt[c]; }
+  if (RECIP) {  // same order as the persistent loop's finalize_warp
+    double t[NDOT];
+    tail_dots(k, p, tk, tkm1, t);
+    S = __dadd_rn(S, t[0]);
+    G = __dadd_rn(G, t[1]);
+    E1 = __dadd_rn(E1, t[2]);
+    E2 = __dadd_rn(E2, t[3]);
+    R = __dadd_rn(R, t[4]);
+  } else {
+    for (int c = 0; c < p; c++) {
+      S += tk[c] * tk[c];
+      R += Kt[c] * Kt[c];
+      E2 += tk[c] * Kt[c];
+      if (k >= 2) { G += tkm1[c] * tk[c]; E1 += tkm1[c] * Kt[c]; }
+    }
   }
   st->passes++;
   st->npass = k;
