@@ -125,6 +125,7 @@ __device__ __forceinline__ void finalize_warp(const KParams &P, int k, const dou
     if (l0) C.go = 0;
     return;
   }
+  const double cn = k >= 2 ? sqrt(C.R2km1) / C.skm1 : 0.0;  // carried values only: off the chain
   const double sk = sqrt(S);
   const double is = 1.0 / sk;
   const int c = lane - 4;  // tail entry owned by this lane
@@ -161,7 +162,7 @@ __device__ __forceinline__ void finalize_warp(const KParams &P, int k, const dou
       K.kv++;
       st->kv = K.kv;
     }
-    const double thr = ts[NDOT];  // R3: fmax(1e-12 ||A~ v_{k-1}||, 1e-14), from pass start
+    const double thr = fmax(1e-12 * cn, 1e-14);  // R3
     if (sk <= thr) {                             // Alg. 2 l.12-15
       if (wr && l0) {
         st->happy = 1;
@@ -218,7 +219,7 @@ __device__ __forceinline__ void inner_loop(const KParams &P, Body &&body) {
   __shared__ PassScalars S;
   __shared__ InnerCarry C;
   __shared__ double red[NDOT * 32];
-  __shared__ double ts[NDOT + 1];  // tails' dot shares, R3 threshold
+  __shared__ double ts[NDOT];
   DevState *st = P.st;
   const unsigned nb = gridDim.x;
   const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
@@ -281,8 +282,6 @@ __device__ __forceinline__ void inner_loop(const KParams &P, Body &&body) {
       tail_dots(k, P.p, C.tk, C.tkm1, t);
 #pragma unroll
       for (int q = 0; q < NDOT; q++) ts[q] = t[q];
-      // R3 breakdown threshold of iteration k-1: carried values only
-      ts[NDOT] = k >= 2 ? fmax(1e-12 * (sqrt(C.R2km1) / C.skm1), 1e-14) : 0.0;
     }
     body(S, v);
     block_sum<NDOT>(v, red);  // (its __syncthreads order every thread's vector writes before the fence)
