@@ -827,16 +827,17 @@ __device__ __forceinline__ void body_3d_lazyq(const KParams &P, const PassScalar
       if (q <= nzc + 1) issue(q);
       cp_async_commit();
     }
-    double2 xk_m = {0.0, 0.0}, xk_0 = {0.0, 0.0}, k_m = {0.0, 0.0}, k_0 = {0.0, 0.0}, xm_0 = {0.0, 0.0},
-            bt_0 = {0.0, 0.0};
+    // late issue: plane i + D is issued at the END of iteration i, into the slot of plane
+    // i - 1, so during iteration i that slot (x_{k-1}, B at the output plane) and the x_k /
+    // kappa shared rings (output plane's centre) still hold what the output needs: only
+    // the plane below the output (x_k, kappa) is carried in registers.
+    double2 xk_m = {0.0, 0.0}, k_m = {0.0, 0.0};
     long long zo_out = (down ? zhi - 1 : zlo) * nxy;
-    int rs = 0, ri = D;
+    int rs = 0, ri = D, rp = RD - 1;  // slots of planes i, i + D, i - 1
 #pragma unroll 2
     for (int i = 0; i <= nzmax + 1; i++) {
       const bool live = i <= nzc + 1;
-      if (i + D <= nzc + 1) issue(ri);
-      cp_async_commit();
-      cp_async_wait<D>();
+      cp_async_wait<D - 1>();
       const double2 *o = sOp + rs * SLOT + t;
       const double2 xm = o[NPAIR], kc_p = o[3 * NPAIR];
       double2 xk_p = xm;
@@ -850,23 +851,25 @@ __device__ __forceinline__ void body_3d_lazyq(const KParams &P, const PassScalar
           xk_p.y -= a2 * pp.y;
         }
       }
-      double2 bt = {0.0, 0.0};
-      if (pin)
-#pragma unroll
-        for (int c = 0; c < PM; c++) {
-          const double2 b = sOp[rs * SLOT + 4 * NPAIR + c * NIN + ib];
-          bt.x = fma(b.x, btc[c], bt.x);
-          bt.y = fma(b.y, btc[c], bt.y);
-        }
       __syncthreads();  // the output that read slot (i & 1) has finished everywhere
       if (act) {
         sXK[(i & 1) * NPAIR + t] = xk_p;
         sKP[(i & 1) * NPAIR + t] = kc_p;
       }
+      const double2 *X0 = sXK + ((i + 1) & 1) * NPAIR, *K0 = sKP + ((i + 1) & 1) * NPAIR;
+      const double2 xk_0 = X0[t], k_0 = K0[t];
       if (i >= 2 && pin && live) {  // output logical plane i - 2 for both points of the pair
-        const double2 *X0 = sXK + ((i + 1) & 1) * NPAIR, *K0 = sKP + ((i + 1) & 1) * NPAIR;
+        const double2 *op = sOp + rp * SLOT;
+        double2 bt = {0.0, 0.0};
+#pragma unroll
+        for (int c = 0; c < PM; c++) {
+          const double2 b = op[4 * NPAIR + c * NIN + ib];
+          bt.x = fma(b.x, btc[c], bt.x);
+          bt.y = fma(b.y, btc[c], bt.y);
+        }
+        const double2 xm_0 = op[NPAIR + t];
         const double2 r = stencil_pair(xk_0, k_0, X0[t - 1].y, X0[t + 1].x, K0[t - 1].y, K0[t + 1].x, X0[t - PX],
-                                       X0[t + PX], K0[t - PX], K0[t + PX], xk_m, k_m, xk_p, kc_p, hh, bt_0);
+                                       X0[t + PX], K0[t - PX], K0[t + PX], xk_m, k_m, xk_p, kc_p, hh, bt);
         const double2 xc = xk_0;
         v0 = fma(xc.x, xc.x, fma(xc.y, xc.y, v0));
         v1 = fma(xm_0.x, xc.x, fma(xm_0.y, xc.y, v1));
@@ -877,10 +880,11 @@ __device__ __forceinline__ void body_3d_lazyq(const KParams &P, const PassScalar
         *reinterpret_cast<double2 *>(rout + zo_out + oo) = r;
       }
       if (i >= 2) zo_out += zstep;
-      xk_m = xk_0; xk_0 = xk_p;
-      k_m = k_0; k_0 = kc_p;
-      xm_0 = xm;
-      bt_0 = bt;
+      xk_m = xk_0;
+      k_m = k_0;
+      if (i + D <= nzc + 1) issue(ri);  // into the slot of plane i - 1 (= ri)
+      cp_async_commit();
+      rp = rs;
       rs = rs + 1 == RD ? 0 : rs + 1;
       ri = ri + 1 == RD ? 0 : ri + 1;
     }

@@ -50,7 +50,7 @@ def test_persistent_3d_pass_spill_stack_small():
 
 def test_p2_persistent_3d_pass_stack_in_measured_fast_range():
     (fn, (reg, stack, _)), = _find(_res_usage(), r"k_inner_3d_lazyqILi2ELi7ELi2ELi2ELi2E").items()
-    assert stack <= 72, f"{fn}: stack {stack} bytes (measured fast: 64-72)"
+    assert stack <= 72, f"{fn}: stack {stack} bytes (measured fast: 56-72)"
 
 
 def test_sell_spmv_keeps_its_register_schedule():
