@@ -898,12 +898,94 @@ __global__ void __cluster_dims__(CTRL_CL, 1, 1) __launch_bounds__(CTRL_THREADS, 
 // accepted substep in ONE pass over the basis.  The running-solution row (which
 // may overwrite x_1 in place) is the last chunk.
 // ---------------------------------------------------------------------------
+// Row a8 in padded mode (Alg. 3 l.15, l.20): one pass over the padded basis; the
+// running solution (basis slot 1) is written on the whole padded grid -- its ghosts
+// are the same combination of the basis ghosts, i.e. again the periodic images -- and
+// the caller's outputs on the interior points only, in their natural layout.
+__device__ __forceinline__ void gemv_padded(const KParams &P, int j, int nout, const double *x1) {
+  DevState *st = P.st;
+  __shared__ double sc[GEMV_OCHUNK * LDH];
+  __shared__ double *outp[GEMV_OCHUNK];
+  const int Xp = P.Xp, Yp = P.Yp, nx = (int)P.nx, ny = (int)P.ny;
+  const long long npair = P.Np / 2, ld2 = P.ldN / 2;
+  const long long gt = blockIdx.x * (long long)blockDim.x + threadIdx.x, gsz = (long long)gridDim.x * blockDim.x;
+  for (int o0 = 0; o0 < nout; o0 += GEMV_OCHUNK) {
+    const int no = min(GEMV_OCHUNK, nout - o0);
+    __syncthreads();
+    for (int e = threadIdx.x; e < no * j; e += blockDim.x) sc[(e / j) * LDH + e % j] = P.coef[(size_t)(o0 + e / j) * LDH + e % j];
+    if (threadIdx.x < no) outp[threadIdx.x] = st->gemv_out[o0 + threadIdx.x];
+    __syncthreads();
+    for (long long q = gt; q < npair; q += gsz) {
+      double2 acc[GEMV_OCHUNK];
+#pragma unroll
+      for (int o = 0; o < GEMV_OCHUNK; o++) acc[o] = make_double2(0.0, 0.0);
+      if (j > 0) {
+        const double2 x = __ldg(reinterpret_cast<const double2 *>(x1) + q);
+#pragma unroll
+        for (int o = 0; o < GEMV_OCHUNK; o++) {
+          acc[o].x = fma(sc[o * LDH], x.x, acc[o].x);
+          acc[o].y = fma(sc[o * LDH], x.y, acc[o].y);
+        }
+      }
+      const double2 *vp = reinterpret_cast<const double2 *>(P.V + P.ldN) + q;  // slot 2
+      int c = 1;
+      for (; c + 3 < j; c += 4) {
+        const double2 xa = __ldg(vp), xb = __ldg(vp + ld2), xc = __ldg(vp + 2 * ld2), xd = __ldg(vp + 3 * ld2);
+        vp += 4 * ld2;
+#pragma unroll
+        for (int o = 0; o < GEMV_OCHUNK; o++) {
+          if (o < no) {
+            const double *cf = sc + o * LDH + c;
+            acc[o].x = fma(cf[0], xa.x, acc[o].x); acc[o].y = fma(cf[0], xa.y, acc[o].y);
+            acc[o].x = fma(cf[1], xb.x, acc[o].x); acc[o].y = fma(cf[1], xb.y, acc[o].y);
+            acc[o].x = fma(cf[2], xc.x, acc[o].x); acc[o].y = fma(cf[2], xc.y, acc[o].y);
+            acc[o].x = fma(cf[3], xd.x, acc[o].x); acc[o].y = fma(cf[3], xd.y, acc[o].y);
+          }
+        }
+      }
+      for (; c < j; c++) {
+        const double2 xa = __ldg(vp);
+        vp += ld2;
+#pragma unroll
+        for (int o = 0; o < GEMV_OCHUNK; o++)
+          if (o < no) {
+            acc[o].x = fma(sc[o * LDH + c], xa.x, acc[o].x);
+            acc[o].y = fma(sc[o * LDH + c], xa.y, acc[o].y);
+          }
+      }
+      // padded pair q -> (xp, yp, z); interior pairs map to the natural index
+      const long long i = 2 * q, row = i / Xp;
+      const int xp = (int)(i - row * Xp);
+      const long long z = row / Yp;
+      const int yp = (int)(row - z * Yp);
+      const bool inner = xp >= 2 && xp < nx + 2 && yp >= 2 && yp < ny + 2;
+      const long long ui = (xp - 2) + (long long)nx * ((yp - 2) + (long long)ny * z);
+#pragma unroll
+      for (int o = 0; o < GEMV_OCHUNK; o++)
+        if (o < no) {
+          double *out = outp[o];
+          if (out == P.V) {
+            reinterpret_cast<double2 *>(out)[q] = acc[o];
+          } else if (inner) {
+            if ((((uintptr_t)(out + ui)) & 15) == 0) {
+              *reinterpret_cast<double2 *>(out + ui) = acc[o];
+            } else {
+              out[ui] = acc[o].x;
+              out[ui + 1] = acc[o].y;
+            }
+          }
+        }
+    }
+  }
+}
+
 __global__ void __launch_bounds__(256) k_gemv(KParams P) {
   DevState *st = P.st;
   if (blockIdx.x == 0 && threadIdx.x == 0) st->t_gemv0 = gtimer();
   const int j = st->gemv_j, nout = st->gemv_nout;
   const double *x1 = st->gemv_x1;
-  const long long N = P.N;
+  const long long N = P.padded ? 0 : P.N;  // padded mode: gemv_padded below
+  if (P.padded) gemv_padded(P, j, nout, x1);
   __shared__ double sc[GEMV_OCHUNK * LDH];
   __shared__ double *outp[GEMV_OCHUNK];
   // 16-byte path when every stream is 16-byte aligned (V slots always are)

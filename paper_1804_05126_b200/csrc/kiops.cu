@@ -14,6 +14,7 @@
 //
 // with the three conditional handles set from device code (no host round trip per
 // step, no CPU fallback).
+#include <cuda.h>  // CUtensorMap (encoded through cudaGetDriverEntryPoint: no libcuda link)
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -29,10 +30,32 @@
 #include "kiops_internal.cuh"
 #include "passes.cuh"
 #include "inner.cuh"
+#include "passrc.cuh"
 
 namespace {
 
-constexpr int SM_COUNT_HINT = 148;
+constexpr int SM_COUNT_HINT = 148;  // only if the device query fails
+
+// SMs of the current device (grids of the persistent and one-wave kernels)
+int sm_count() {
+  int dev = 0, sms = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
+      sms < 1) {
+    cudaGetLastError();
+    return SM_COUNT_HINT;
+  }
+  return sms;
+}
+
+// Padded mode: the 3D variable-kappa operator with an even nx runs
+// the recompute pass (rc3d.cuh) on ghost-padded vectors.  KIOPS_3D=lazy keeps the lazy
+// pair pass (A/B switch).
+bool use_padded(const kiops_operator_desc *op, int p, const kiops_options *o) {
+  if (op->kind != KIOPS_OP_STENCIL3D7_VARKAPPA || o->iop_q != 2) return false;
+  if (op->nx % 2 != 0 || op->nx < 4 || op->ny < 4 || p > 4) return false;
+  const char *e = getenv("KIOPS_3D");
+  return !(e && strcmp(e, "lazy") == 0);
+}
 
 // v1 stencil tiles
 #define T1D 1, 256, 1, 1
@@ -51,7 +74,10 @@ constexpr int SM_COUNT_HINT = 148;
 
 struct Layout {
   size_t V, r, staging, state, call, H, sig, R2, tails, partials, recs, npart, scratch, coef, trace, sell_off, sell_col,
-      sell_val, qa, gram, qpart, total;
+      sell_val, qa, gram, qpart, tmaps, total;
+  bool padded = false;
+  int Xp = 0, Yp = 0, rc_ntx = 0, rc_nb = 0, rc_zs = 0, nslots = 0;
+  long long Np = 0;
   long long sell_entries;
   long long ldN;
   int grid_pass, grid_setup, grid_gemv, grid_form, grid_max;
@@ -127,8 +153,8 @@ Layout layout(const kiops_operator_desc *op, int p, const kiops_options *o) {
   L.ldN = (N + 31) & ~31LL;
   L.block_pass = 256;
   const long long blocks256 = (N + 255) / 256;
-  L.grid_setup = (int)std::min<long long>(blocks256, SM_COUNT_HINT * 8);
-  L.grid_gemv = (int)std::min<long long>((N / 2 + 255) / 256 + 1, SM_COUNT_HINT * 8);
+  L.grid_setup = (int)std::min<long long>(blocks256, sm_count() * 8);
+  L.grid_gemv = (int)std::min<long long>((N / 2 + 255) / 256 + 1, sm_count() * 8);
   L.grid_form = L.grid_gemv;
   switch (op->kind) {
     case KIOPS_OP_STENCIL1D3:
@@ -158,7 +184,19 @@ Layout layout(const kiops_operator_desc *op, int p, const kiops_options *o) {
       }
       break;
     case KIOPS_OP_STENCIL3D7_VARKAPPA:
-      if (op->nx % 2 == 0 && op->nx >= 2 && p >= 1 && p <= 4) {  // lock-step persistent pair pass
+      if (use_padded(op, p, o)) {  // recompute pass on the padded layout (rc3d.cuh)
+        const int sms = sm_count();
+        L.padded = true;
+        L.Xp = (int)op->nx + 4;
+        L.Yp = (int)op->ny + 4;
+        L.Np = (long long)L.Xp * L.Yp * op->nz;
+        L.ldN = (L.Np + 31) & ~31LL;
+        rc3::tiles((int)op->nx, (int)op->ny, (int)op->nz, sms, RC_HM, &L.rc_ntx, &L.rc_nb, &L.rc_zs);
+        L.grid_pass = std::min(L.rc_ntx * L.rc_nb * L.rc_zs, sms);
+        L.block_pass = RcCfg<0>::NT;
+        L.smem_pass = p == 0 ? RcCfg<0>::smem_bytes : p == 1 ? RcCfg<1>::smem_bytes : p == 2 ? RcCfg<2>::smem_bytes
+                    : p == 3 ? RcCfg<3>::smem_bytes : RcCfg<4>::smem_bytes;
+      } else if (op->nx % 2 == 0 && op->nx >= 2 && p >= 1 && p <= 4) {  // lock-step persistent pair pass
         using Q = LazyQ<2, Q3Y, 2>;
         int ntx, nb;
         rc_tiles(op->nx, op->ny, Q::TILES, Q3Y, &ntx, &nb);
@@ -177,14 +215,17 @@ Layout layout(const kiops_operator_desc *op, int p, const kiops_options *o) {
       }
       break;
     default:  // CSR (SELL-32): thread per row, 8 CTAs of 256 per SM
-      L.grid_pass = (int)std::min<long long>((N + 255) / 256, SM_COUNT_HINT * 8);
+      L.grid_pass = (int)std::min<long long>((N + 255) / 256, sm_count() * 8);
       L.smem_pass = 0;
   }
   L.grid_max = std::max(L.grid_pass, L.grid_setup);
   size_t off = 0;
   const size_t vec = (size_t)L.ldN * sizeof(double);
-  L.V = off; off += al((size_t)(o->m_max + 1) * vec);
-  L.r = off; off += 2 * al(vec);  // r_k ping-pong (lazy passes; CSR uses the first)
+  // padded mode: basis slots 1..m_max+1, then copies of B's p columns and of kappa, one
+  // 4-D tensor for the TMA maps; no r buffers (the recompute pass never stores r)
+  L.nslots = (o->m_max + 1) + (L.padded ? p + 1 : 0);
+  L.V = off; off += al((size_t)L.nslots * vec);
+  L.r = off; off += L.padded ? 0 : 2 * al(vec);  // r_k ping-pong (lazy passes; CSR uses the first)
   L.staging = off; off += o->host_staging ? al((size_t)(p + 1 + o->max_outputs) * vec) : 0;
   L.state = off; off += al(sizeof(DevState));
   L.call = off; off += al(sizeof(CallBlock));
@@ -201,6 +242,7 @@ Layout layout(const kiops_operator_desc *op, int p, const kiops_options *o) {
   L.qa = off; off += al(sizeof(double) * (size_t)LDH);                          // generic-q path
   L.gram = off; off += al(sizeof(double) * (size_t)LDH * LDH);
   L.qpart = off; off += al(sizeof(double) * (2 * (size_t)LDH + 2) * QG);
+  L.tmaps = off; off += L.padded ? al(2 * sizeof(CUtensorMap)) : 0;
   L.sell_entries = 0;
   if (op->kind == KIOPS_OP_CSR) {  // SELL-32 copy: exact size from the row lengths
     const long long ns = (N + 31) / 32;
@@ -285,6 +327,41 @@ static cudaError_t add_cond(cudaGraph_t g, cudaGraphNode_t *node, const cudaGrap
   return e;
 }
 
+// TMA tensor maps of the padded 4-D tensor [Xp][Yp][nz][nslots] (basis slots, B copies,
+// kappa copy; slot stride ldN doubles): box 68 x (HM+4) (halo-2 operands x_{k-1},
+// kappa) and 68 x (HM+2) (halo-1 operands x_{k-2}, B).  Encoded on the host once per
+// ctx, stored in the workspace (the kernels pass their global address to the TMA unit).
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static kiops_status encode_tmaps(kiops_ctx c) {
+  const Layout &L = c->L;
+  EncodeTiledFn enc = nullptr;
+  cudaDriverEntryPointQueryResult qr;
+  CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void **)&enc, cudaEnableDefault, &qr), "driver entry point");
+  if (!enc || qr != cudaDriverEntryPointSuccess) {
+    c->err = "cuTensorMapEncodeTiled unavailable";
+    return KIOPS_ERR_CUDA;
+  }
+  CUtensorMap maps[2];
+  const cuuint64_t gdim[4] = {(cuuint64_t)L.Xp, (cuuint64_t)L.Yp, (cuuint64_t)c->op.nz, (cuuint64_t)L.nslots};
+  const cuuint64_t gstr[3] = {(cuuint64_t)L.Xp * 8, (cuuint64_t)L.Xp * L.Yp * 8, (cuuint64_t)L.ldN * 8};
+  const cuuint32_t es[4] = {1, 1, 1, 1};
+  for (int m = 0; m < 2; m++) {
+    const cuuint32_t box[4] = {(cuuint32_t)RcCfg<0>::W, (cuuint32_t)(m == 0 ? RcCfg<0>::RA : RcCfg<0>::RB), 1, 1};
+    const CUresult r = enc(&maps[m], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, c->P.V, gdim, gstr, box, es,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+      c->err = "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")";
+      return KIOPS_ERR_CUDA;
+    }
+  }
+  CK(cudaMemcpyAsync((void *)c->P.tmapA, maps, sizeof(maps), cudaMemcpyHostToDevice, c->stream), "H2D tensor maps");
+  CK(cudaStreamSynchronize(c->stream), "tensor maps");
+  return KIOPS_OK;
+}
+
 static kiops_status build_graph(kiops_ctx c) {
   KParams &P = c->P;
   CK(cudaGraphCreate(&c->graph, 0), "cudaGraphCreate");
@@ -313,7 +390,10 @@ static kiops_status build_graph(kiops_ctx c) {
         fpass = c->op.kind == KIOPS_OP_STENCIL1D3 ? (void *)k_pass_stencil<T1D> : (void *)k_pass_stencil<T2D>;
       break;
     case KIOPS_OP_STENCIL3D7_VARKAPPA:
-      if (c->op.nx % 2 == 0 && c->op.nx >= 2 && c->p >= 1 && c->p <= 4)
+      if (c->L.padded)
+        fpass = c->p == 0 ? (void *)k_pass_3d_rc<0> : c->p == 1 ? (void *)k_pass_3d_rc<1> : c->p == 2 ? (void *)k_pass_3d_rc<2>
+              : c->p == 3 ? (void *)k_pass_3d_rc<3> : (void *)k_pass_3d_rc<4>;
+      else if (c->op.nx % 2 == 0 && c->op.nx >= 2 && c->p >= 1 && c->p <= 4)
         fpass = c->L.nh3 == 2
                     ? (c->p == 1 ? (void *)k_pass_3d_lazyq<1, Q3Y, 2, Q3D, 2> : c->p == 2 ? (void *)k_pass_3d_lazyq<2, Q3Y, 2, Q3D, 2>
                        : c->p == 3 ? (void *)k_pass_3d_lazyq<3, Q3Y, 2, 1, 2> : (void *)k_pass_3d_lazyq<4, Q3Y, 2, 1, 2>)
@@ -347,6 +427,9 @@ static kiops_status build_graph(kiops_ctx c) {
       finner = c->p == 0 ? (void *)k_inner_2d_lazy<L2YC, 0, 2, 2> : c->p == 1 ? (void *)k_inner_2d_lazy<L2YC, 1, 2, 2>
              : c->p == 2 ? (void *)k_inner_2d_lazy<L2YC, 2, 2, 2> : c->p == 3 ? (void *)k_inner_2d_lazy<L2YC, 3, 2, 2>
                          : (void *)k_inner_2d_lazy<L2YC, 4, 2, 2>;
+    else if (c->L.padded)
+      finner = c->p == 0 ? (void *)k_inner_3d_rc<0> : c->p == 1 ? (void *)k_inner_3d_rc<1> : c->p == 2 ? (void *)k_inner_3d_rc<2>
+             : c->p == 3 ? (void *)k_inner_3d_rc<3> : (void *)k_inner_3d_rc<4>;
     else if (c->op.kind == KIOPS_OP_STENCIL3D7_VARKAPPA && c->op.nx % 2 == 0 && c->op.nx >= 2 && c->p >= 1 &&
              c->p <= 4)
       finner = c->L.nh3 == 2
@@ -493,6 +576,16 @@ kiops_status kiops_create(const kiops_operator_desc *op, int p, const kiops_opti
   }
   P.grid_pass = L.grid_pass;
   P.grid_max = L.grid_max;
+  if (L.padded) {
+    P.padded = 1;
+    P.Xp = L.Xp; P.Yp = L.Yp; P.Np = L.Np;
+    P.rc_ntx = L.rc_ntx; P.rc_nb = L.rc_nb; P.rc_zs = L.rc_zs;
+    P.slot_B = o->m_max + 1;
+    P.slot_kappa = o->m_max + 1 + p;
+    P.r = nullptr;
+    P.tmapA = w + L.tmaps;
+    P.tmapB = w + L.tmaps + sizeof(CUtensorMap);
+  }
   kiops_status st = KIOPS_OK;
   cudaError_t e = cudaMallocHost((void **)&c->h_call, sizeof(CallBlock));
   if (e == cudaSuccess) e = cudaMallocHost((void **)&c->h_state, sizeof(DevState));
@@ -504,6 +597,7 @@ kiops_status kiops_create(const kiops_operator_desc *op, int p, const kiops_opti
     if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
     if (e != cudaSuccess) st = cuda_fail(c, e, "workspace init");
   }
+  if (st == KIOPS_OK && L.padded) st = encode_tmaps(c);
   if (st == KIOPS_OK && op->kind == KIOPS_OP_CSR) {  // build the SELL-32 copy once
     std::vector<long long> off = sell_offsets(op);
     if (off.empty() || off.back() != L.sell_entries) {
@@ -512,7 +606,7 @@ kiops_status kiops_create(const kiops_operator_desc *op, int p, const kiops_opti
     } else {
       e = cudaMemcpy((void *)P.sell_off, off.data(), sizeof(long long) * off.size(), cudaMemcpyHostToDevice);
       if (e == cudaSuccess) {
-        k_sell_build<<<SM_COUNT_HINT * 8, 256, 0, c->stream>>>(P.N, P.row_ptr, P.col_idx, P.vals, P.sell_off,
+        k_sell_build<<<sm_count() * 8, 256, 0, c->stream>>>(P.N, P.row_ptr, P.col_idx, P.vals, P.sell_off,
                                                                (int *)P.sell_col, (double *)P.sell_val);
         e = cudaGetLastError();
       }

@@ -90,6 +90,16 @@ struct KParams {
   double *gram;       // generic q: G(i,l) = x_i . x_l, LDH x LDH column-major
   double *qpart;      // generic q: (2 LDH + 2) x QG dot partials
   int no_cond;        // 1: launched outside the graph (host-loop profiling hook)
+  // padded mode (3D variable-kappa recompute pass, rc3d.cuh / passrc.cuh): every basis
+  // slot is a ghost-padded (nx+4) x (ny+4) x nz grid, and slots m_max+1 .. m_max+p hold
+  // copies of B's columns (u_p .. u_1), slot m_max+p+1 a copy of kappa, made by k_setup;
+  // x_1 of the first substep is V slot 1 (u_0 copied there).  N stays nx ny nz.
+  int padded;
+  int Xp, Yp;         // nx + 4, ny + 4
+  long long Np;       // Xp Yp nz (padded vector length)
+  int rc_ntx, rc_nb, rc_zs;   // recompute-pass tiles (rc3::tiles)
+  int slot_B, slot_kappa;     // 0-based slots of B column 0 and of kappa
+  const void *tmapA, *tmapB;  // TMA tensor maps of the 4-D tensor [Xp][Yp][nz][slots] (workspace)
   cudaGraphConditionalHandle h_outer, h_inner, h_accept;
 };
 enum { COND_OUTER = 0, COND_INNER = 1, COND_ACCEPT = 2 };

@@ -42,9 +42,34 @@ __device__ void write_exact_tail(const KParams &P, double t_now, double mu, doub
   }
 }
 
+// Row a1 / Alg. 1 l.8 in padded mode: copy u_0 into basis slot 1 (x_1 of the first
+// substep), B's columns u_p .. u_1 and kappa into their slots, ghosts included (the
+// periodic images).  Called from k_setup on every call (the operator's kappa may be
+// rewritten by the caller between calls; a copy costs ~2 vectors of traffic).
+__device__ __forceinline__ void pad_copies(const KParams &P) {
+  const CallBlock *call = P.call;
+  const int Xp = P.Xp, Yp = P.Yp, nx = (int)P.nx, ny = (int)P.ny;
+  const long long Np = P.Np, ldN = P.ldN;
+  const int p = P.p;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < Np; i += (long long)gridDim.x * blockDim.x) {
+    const long long row = i / Xp;
+    const int xp = (int)(i - row * Xp);
+    const long long z = row / Yp;
+    const int yp = (int)(row - z * Yp);
+    int x = xp - 2, y = yp - 2;
+    x = x < 0 ? x + nx : (x >= nx ? x - nx : x);
+    y = y < 0 ? y + ny : (y >= ny ? y - ny : y);
+    const long long src = x + (long long)nx * (y + (long long)ny * z);
+    P.V[i] = __ldg(call->u[0] + src);
+    for (int c = 0; c < p; c++) P.V[(size_t)(P.slot_B + c) * ldN + i] = __ldg(call->u[p - c] + src);
+    P.V[(size_t)P.slot_kappa * ldN + i] = __ldg(P.kappa + src);
+  }
+}
+
 __global__ void __launch_bounds__(256) k_setup(KParams P) {
   const CallBlock *call = P.call;
   const int p = P.p;
+  if (P.padded) pad_copies(P);
   __shared__ double red[KMAXP * 32];
   double v[KMAXP];
 #pragma unroll
@@ -108,7 +133,7 @@ __global__ void __launch_bounds__(256) k_setup(KParams P) {
   st->status = 0;
   st->zero_start = 0;
   st->accept = 0;
-  st->x1 = call->u[0];                                     // l.8
+  st->x1 = P.padded ? P.V : call->u[0];                   // l.8 (padded: u_0 copied to slot 1)
   st->attempt = st->substeps = st->rejections = st->kv = st->expm_calls = st->passes = 0;
   st->happy_count = 0;
   st->final_m = st->m;

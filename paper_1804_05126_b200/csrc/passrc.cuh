@@ -1,0 +1,74 @@
+// passrc.cuh -- the recompute pass kernels of the padded-mode 3D variable-kappa path
+// (body in rc3d.cuh, Alg. 2).  The padded copies
+// made at call start are pad_copies (passes.cuh, k_setup), the padded output update
+// gemv_padded (controller.cuh, k_gemv).  DESIGN.md sec. 4.1 / 6.
+#pragma once
+#include "kiops_internal.cuh"
+#include "passes.cuh"
+#include "inner.cuh"
+#include "rc3d.cuh"
+
+#define RC_HM 7  // tile rows (config 4 bands: 6-7 rows of 64 points)
+#define RC_D 3   // planes in flight ahead of the two in use
+template <int PM>
+using RcCfg = rc3::Cfg<PM, RC_HM, RC_D>;
+
+__device__ __forceinline__ rc3::Geom rc_geom(const KParams &P) {
+  rc3::Geom G;
+  G.nx = (int)P.nx; G.ny = (int)P.ny; G.nz = (int)P.nz;
+  G.Xp = P.Xp; G.Yp = P.Yp;
+  G.ldN = P.ldN;
+  G.ntx = P.rc_ntx; G.nb = P.rc_nb; G.zsplit = P.rc_zs;
+  G.slot_kappa = P.slot_kappa; G.slot_B = P.slot_B;
+  G.mapA = P.tmapA; G.mapB = P.tmapB;
+  G.V = P.V;
+  G.hh = 0.5 * P.inv_h2;
+  return G;
+}
+
+// PassScalars (load_pass_scalars / the persistent loop's finalisation) -> pass args.
+// x_{k-1}, x_{k-2} are basis slots (x_1 is slot 0 in padded mode).
+template <int PM>
+__device__ __forceinline__ rc3::PassArgs<PM> rc_args(const KParams &P, const PassScalars &S) {
+  rc3::PassArgs<PM> Q;
+  Q.k = S.k;
+  Q.slot_prev = (int)((S.xprev - P.V) / P.ldN);
+  Q.slot_pp = S.xpp ? (int)((S.xpp - P.V) / P.ldN) : -1;
+  Q.xout = S.k >= 2 ? S.xout : nullptr;
+  Q.a0 = S.a0; Q.a1 = S.a1; Q.a2 = S.a2;
+#pragma unroll
+  for (int c = 0; c < (PM > 0 ? PM : 1); c++) {
+    Q.btp[c] = c < PM ? S.btp[c] : 0.0;
+    Q.btc[c] = c < PM ? S.btc[c] : 0.0;
+  }
+  Q.use_r = S.k >= 2;
+  return Q;
+}
+
+// Persistent inner loop (inner.cuh) over recompute passes: one CTA per SM.
+template <int PM>
+__global__ void __launch_bounds__(RcCfg<PM>::NT, 1) k_inner_3d_rc(KParams P) {
+  const rc3::Geom G = rc_geom(P);
+  rc3::init<PM, RC_HM, RC_D>(G);
+  unsigned nl = 0;  // the ring's running fill count, carried across the passes
+  inner_loop(P, [&](const PassScalars &S, double (&v)[NDOT]) {
+    const rc3::PassArgs<PM> Q = rc_args<PM>(P, S);
+    rc3::body<PM, RC_HM, RC_D>(G, Q, v, nl);
+  });
+}
+
+// One launch per pass (KIOPS_PERSIST=0, or a grid that is not co-resident).
+template <int PM>
+__global__ void __launch_bounds__(RcCfg<PM>::NT, 1) k_pass_3d_rc(KParams P) {
+  __shared__ PassScalars S;
+  pass_guard(P);
+  if (threadIdx.x == 0) load_pass_scalars(P, S);
+  const rc3::Geom G = rc_geom(P);
+  rc3::init<PM, RC_HM, RC_D>(G);  // (its __syncthreads publishes S)
+  if (S.k == 0) return;
+  unsigned nl = 0;
+  double v[NDOT] = {0.0, 0.0, 0.0, 0.0, 0.0};
+  const rc3::PassArgs<PM> Q = rc_args<PM>(P, S);
+  rc3::body<PM, RC_HM, RC_D>(G, Q, v, nl);
+  pass_epilogue(P, S.k, v);
+}

@@ -1,0 +1,456 @@
+// rc3d.cuh -- the config-4 fused IOP pass (Alg. 2) in
+// the RECOMPUTE form, fed by TMA tensor-map loads, on a ghost-padded grid layout.
+//
+// Pass k completes Alg. 2 iteration k-1 and starts iteration k WITHOUT a stored
+// r_{k-1} = (A~ x_{k-1})_top: every CTA recomputes it on the halo-1 ring of its tile
+// from the halo-2 tile of x_{k-1}, so the pass moves the SURVEY 8(d) MINIMUM
+// (q+1+p+c) 8N bytes -- read x_{k-1}, x_{k-2}, B (p vectors), kappa; write x_k --
+// instead of the lazy form's (q+3+p+c) 8N (805 vs 1074 MB at 256^3, p = 2):
+//
+//   stage 1, plane L (halo-1 ring + interior):
+//     r_{k-1} = A x_{k-1} + nu B t_{k-1}                         (Thm 1)
+//     x_k     = a0 r_{k-1} - a1 x_{k-1} - a2 x_{k-2}               (l.7-10, l.17 folded)
+//   stage 2, plane L-1 (interior):
+//     r_k = A x_k + nu B t_k ;  S = x_k.x_k, G = x_{k-1}.x_k, E1 = x_{k-1}.r_k,
+//     E2 = x_k.r_k, R = r_k.r_k  (block partials; the grid reduction and the
+//     finalisation are the persistent loop's, inner.cuh) ; store x_k.
+//
+// with A the 7-point variable-kappa operator (A u)_i = 1/h^2 sum_faces kappa_f
+// (u_nb - u_i), kappa_f = (kappa_i + kappa_nb)/2 (BJ config 4, reading D6), evaluated
+// as 0.5/h^2 sum (kappa_i + kappa_nb)(u_nb - u_i) in the lazy kernels' operand order.
+//
+// Layout ("padded mode"): every vector the pass reads is stored with
+// two ghost columns / rows on each side of every xy plane, (nx+4) x (ny+4) x nz,
+// index (x+2) + (nx+4) ((y+2) + (ny+4) z); ghosts hold the periodic images, so a
+// tile's halo box is ONE rectangular TMA box with no wrap.  z wraps through the TMA
+// coordinate.  The basis slots, the B copies and the kappa copy form one 4-D tensor
+// [nx+4][ny+4][nz][slot] (slot stride ldN doubles) described by two tensor maps
+// (box 68 x (HM+4) for the halo-2 operands x_{k-1}, kappa; 68 x (HM+2) for the halo-1
+// operands x_{k-2}, B).  The pass writes x_k's interior AND its ghost images.
+//
+// Decomposition: tiles of 64 x hb points (hb <= HM, balanced bands) x z-parts, one
+// unit per CTA per wave (config 4: 4 x 37 tiles, 148 CTAs, one z-part, the full
+// periodic z column), every CTA marching z in lock-step with the others (halo rows
+// shared by neighbouring tiles are read at about the same time: L2 hits), direction
+// alternating with the pass parity.  Per CTA: a ring of RS = D + 2 plane slots
+// filled by one thread with 2 + 1 + p TMA boxes per plane (mbarrier complete_tx),
+// D planes ahead; threads own 16-byte pairs: interior pairs in full warps (one warp
+// = one 64-point row), the halo ring in the last warps; x_k of plane L is published
+// in a 2-plane shared exchange ring for the in-plane neighbours of stage 2; z
+// neighbours and the face sums of stage 2 stay in registers (carried from stage 1 of
+// the previous plane).  ONE __syncthreads per plane.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <type_traits>
+
+#ifndef RC3_ROLEMAP
+#define RC3_ROLEMAP 1
+#endif
+#ifndef RC3_HALO_S1ONLY
+#define RC3_HALO_S1ONLY 0
+#endif
+
+namespace rc3 {
+
+__device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t *b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *b, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "RC3_WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra RC3_WAIT_%=;\n}\n" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+// 4-D tensor-map box load global -> shared, completion on the mbarrier
+__device__ __forceinline__ void tma_load4(void *dst, const void *tmap, int c0, int c1, int c2, int c3, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], "
+      "[%6];" ::"r"(smem_u32(dst)),
+      "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_prefetch_desc(const void *tmap) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(tmap) : "memory");
+}
+__device__ __forceinline__ double2 ld2(const double *p) { return *reinterpret_cast<const double2 *>(p); }
+
+// Frozen geometry of the padded-mode 3D operator (identical in every pass).
+struct Geom {
+  int nx, ny, nz;          // grid (nx even, nx, ny >= 4)
+  int Xp, Yp;              // padded extents nx + 4, ny + 4
+  long long ldN;           // slot stride of the 4-D tensor (doubles)
+  int ntx, nb, zsplit;     // 64-wide x tiles, y bands, z parts
+  int slot_kappa, slot_B;  // 4-D slot of the kappa copy and of B column 0 (= u_p copy)
+  const void *mapA, *mapB; // tensor maps (global memory): halo-2 box, halo-1 box
+  double *V;               // slot 0 of the 4-D tensor
+  double hh;               // 0.5 / h^2
+};
+
+// Per-pass arguments (identical in every CTA).
+template <int PM>
+struct PassArgs {
+  int k;
+  int slot_prev, slot_pp;  // 4-D slots of x_{k-1}, x_{k-2} (slot_pp < 0: none)
+  double *xout;            // x_k (padded; NULL: x_1 is the start vector itself)
+  double a0, a1, a2;       // x_k = a0 r_{k-1} - a1 x_{k-1} - a2 x_{k-2}
+  double btp[PM > 0 ? PM : 1], btc[PM > 0 ? PM : 1];  // nu t_{k-1}, nu t_k
+  int use_r;               // k >= 2
+};
+
+// Tile rule (host and device): ntx columns of 64 points; nb bands of <= hm rows
+// giving about `ctas` tiles; z parts filling the CTAs (>= 2 planes each).
+__host__ __device__ inline void tiles(int nx, int ny, int nz, int ctas, int hm, int *ntx, int *nb, int *zs) {
+  const int tx = (nx + 63) / 64;
+  int b = ctas / tx;
+  if (b < 1) b = 1;
+  if (b > ny) b = ny;
+  const int bmin = (ny + hm - 1) / hm;
+  if (b < bmin) b = bmin;
+  int z = ctas / (tx * b);
+  if (z < 1) z = 1;
+  if (z > nz / 2) z = nz / 2 > 0 ? nz / 2 : 1;
+  *ntx = tx;
+  *nb = b;
+  *zs = z;
+}
+
+template <int PM, int HM, int D>
+struct Cfg {
+  static constexpr int W = 68;                 // box row: 64 + 2 halo columns each side (doubles)
+  static constexpr int RA = HM + 4, RB = HM + 2;  // box rows: halo-2 / halo-1
+  static constexpr unsigned BYTES_A = W * RA * 8, BYTES_B = W * RB * 8;
+  static constexpr int SA = (BYTES_A + 127) / 128 * 16, SB = (BYTES_B + 127) / 128 * 16;  // doubles, 128-B multiples
+  static constexpr int SLOT = 2 * SA + (1 + PM) * SB;  // X, kappa, x_{k-2}, B_0..B_{PM-1}
+  static constexpr int RS = D + 2;
+  static constexpr int EXP = 34 * (HM + 2);    // exchange ring: pairs per plane
+  static constexpr int NT = (32 * HM + 2 * 34 + 2 * HM + 31) / 32 * 32;
+  static constexpr size_t smem_bytes = 128 + (size_t)RS * SLOT * 8 + 2 * (size_t)(EXP + 32) * 16 + 8 * (size_t)RS;
+};
+
+// Shared-memory carve-up: [ring RS x SLOT doubles][exchange 2 x EXP pairs][RS mbarriers]
+template <int PM, int HM, int D>
+__device__ __forceinline__ double *smem_base() {
+  extern __shared__ __align__(128) unsigned char rc3_dsm[];
+  return reinterpret_cast<double *>(rc3_dsm);
+}
+template <int PM, int HM, int D>
+__device__ __forceinline__ uint64_t *bars(double *sm) {
+  using C = Cfg<PM, HM, D>;
+  return reinterpret_cast<uint64_t *>(sm + (size_t)C::RS * C::SLOT + 4 * (size_t)(C::EXP + 32));
+}
+// Once per kernel launch, before the first pass (thread 0 inits, then a barrier).
+template <int PM, int HM, int D>
+__device__ __forceinline__ void init(const Geom &G) {
+  double *sm = smem_base<PM, HM, D>();
+  uint64_t *b = bars<PM, HM, D>(sm);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < Cfg<PM, HM, D>::RS; s++) mbar_init(b + s, 1);
+    fence_mbar_init();
+    tma_prefetch_desc(G.mapA);
+    tma_prefetch_desc(G.mapB);
+  }
+  __syncthreads();
+}
+
+// Stage-1 results of one plane at this thread's pair, carried to stage 2 of the next
+// step (and its x_{k-1} / kappa centre to stage 1 of the next plane as the z-1 terms).
+struct Rec {
+  double2 xk, bk;     // x_k ; nu B t_k
+  double fl, fi, fr;  // kappa sums of the x faces: left, inside the pair, right
+  double2 fs, fn, fm; // kappa sums of the y-, y+, z- faces (per point)
+  double2 xc, kc;     // x_{k-1}, kappa centre
+};
+
+// Warp roles.  Warp w runs on scheduler w % 4; interior warps run stage 1 + stage 2,
+// halo warps stage 1 only (about half the work).  For HM = 7 (10 warps: 7 interior
+// rows, 3 halo) the halo warps are 4, 8, 9 so that no scheduler carries more than
+// I + I + H (schedulers 0-3: I H H | I I H | I I | I I), instead of three full warps
+// on two of them.  Returns the interior row (>= 0) or -1 - halo warp index.
+template <int HM>
+__host__ __device__ constexpr int role_of(int w) {
+#if RC3_ROLEMAP
+  if (HM == 7) {
+    return w == 4 ? -1 : w == 8 ? -2 : w == 9 ? -3 : (w < 4 ? w : w - 1);
+  }
+#endif
+  return w < HM ? w : -1 - (w - HM);
+}
+
+// One pass over this CTA's units.  nl: planes this CTA has loaded so far (the ring's
+// running fill count: slot = count % RS, phase parity = (count / RS) & 1), identical
+// in every thread and carried across passes by the caller.
+//
+// UR: k >= 2 (x_k is formed from the recomputed r_{k-1}); UPP: k >= 3 (x_{k-2} term).
+// Every thread runs both stages on every plane with no data-dependent branches (threads
+// without a pair read a valid dummy location and write a dummy exchange slot; halo
+// threads' stage-2 results are discarded), so stage 1 of plane L and stage 2 of plane
+// L-1 form ONE basic block the compiler can interleave.
+template <int PM, int HM, int D, bool UR, bool UPP>
+__device__ __forceinline__ void march(const Geom &G, const PassArgs<PM> &Q, double (&v)[5], unsigned &nl) {
+  using C = Cfg<PM, HM, D>;
+  constexpr int W = C::W, SA = C::SA, SB = C::SB, SLOT = C::SLOT, RS = C::RS, EXP = C::EXP;
+  double *const sm = smem_base<PM, HM, D>();
+  double2 *const ex = reinterpret_cast<double2 *>(sm + (size_t)RS * SLOT);
+  uint64_t *const bar = bars<PM, HM, D>(sm);
+  const int t = threadIdx.x, lane = t & 31;
+  const int nx = G.nx, ny = G.ny, nz = G.nz, ntx = G.ntx, nb = G.nb;
+  const int units = ntx * nb * G.zsplit;
+  const long long plane = (long long)G.Xp * G.Yp;
+  const double a0 = Q.a0, a1 = Q.a1, a2 = Q.a2, hh = G.hh;
+  double btp[PM > 0 ? PM : 1], btc[PM > 0 ? PM : 1];
+#pragma unroll
+  for (int c = 0; c < PM; c++) {
+    btp[c] = Q.btp[c];
+    btc[c] = Q.btc[c];
+  }
+  double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0, v4 = 0.0;
+  constexpr unsigned bytes = 2 * C::BYTES_A + (unsigned)PM * C::BYTES_B + (UPP ? C::BYTES_B : 0u);
+
+  for (int w = blockIdx.x; w < units; w += gridDim.x) {
+    const int tile = w % (ntx * nb), part = w / (ntx * nb);
+    const int ox = (tile % ntx) * 64, band = tile / ntx;
+    const int oy = (int)((long long)band * ny / nb), hb = (int)((long long)(band + 1) * ny / nb) - oy;
+    const int tw = min(32, (nx - ox) / 2);
+    const int zlo = (int)((long long)part * nz / G.zsplit), zhi = (int)((long long)(part + 1) * nz / G.zsplit);
+    const int nzc = zhi - zlo;
+    const bool down = ((part ^ Q.k) & 1) != 0;
+    // thread -> pair (px, py) of the halo-1 plane: px 0..tw+1, py 0..hb+1; interior pairs
+    // (1..tw, 1..hb) in full warps (one warp per row), the halo ring after them
+    int px = -1, py = -1;
+    bool s2 = false;
+    const int wr = role_of<HM>(t >> 5);  // >= 0: interior row; < 0: halo warp -1 - index
+    const bool hwarp = wr < 0;
+    if (!hwarp) {
+      if (wr < hb && lane < tw) {
+        px = 1 + lane;
+        py = 1 + wr;
+        s2 = true;
+      }
+    } else {
+      int h = (-1 - wr) * 32 + lane;
+      const int rw = tw + 2;
+      if (h < rw) { px = h; py = 0; }
+      else if ((h -= rw) < rw) { px = h; py = hb + 1; }
+      else if ((h -= rw) < hb) { px = 0; py = 1 + h; }
+      else if ((h -= hb) < hb) { px = tw + 1; py = 1 + h; }
+    }
+    const bool s1 = px >= 0;
+    // threads without a pair compute on pair (1, 1) and publish into the pad slot EXP
+    const int qx = s1 ? px : 1, qy = s1 ? py : 1;
+    const int offA = (qy + 1) * W + 2 * qx, offB = qy * W + 2 * qx;
+    const int ew = s1 ? qy * 34 + qx : EXP, er = s2 ? ew : 35;
+    // x-neighbour values from the neighbouring lanes when they hold the adjacent pair
+    const int key = s1 ? py * 64 + px : -1000 - t;
+    const int kl = __shfl_up_sync(0xffffffffu, key, 1), kr = __shfl_down_sync(0xffffffffu, key, 1);
+    const bool shl = lane > 0 && s1 && kl == key - 1, shr = lane < 31 && s1 && kr == key + 1;
+    // padded-plane offsets of this pair and of its periodic ghost images (interior pairs)
+    const int gx = ox - 2 + 2 * qx, gy = oy - 1 + qy;
+    const long long o0 = (long long)(gx + 2) + (long long)G.Xp * (gy + 2);
+    long long og0 = -1, og1 = -1, og2 = -1;
+    if (s2) {
+      const int gxg = gx < 2 ? gx + nx : (gx >= nx - 2 ? gx - nx : -99);
+      const int gyg = gy < 2 ? gy + ny : (gy >= ny - 2 ? gy - ny : -99);
+      if (gxg != -99) og0 = (long long)(gxg + 2) + (long long)G.Xp * (gy + 2);
+      if (gyg != -99) og1 = (long long)(gx + 2) + (long long)G.Xp * (gyg + 2);
+      if (gxg != -99 && gyg != -99) og2 = (long long)(gxg + 2) + (long long)G.Xp * (gyg + 2);
+    }
+    const bool st = s2 && Q.xout != nullptr;
+    const int dz = down ? -1 : 1;
+    auto wrapz = [&](int z) { return z < 0 ? z + nz : (z >= nz ? z - nz : z); };
+    int z0 = down ? zhi - 1 : zlo;  // physical plane of logical plane 0
+    z0 %= nz;
+    // producer (thread 0): next plane to issue, its slot and physical plane
+    int iL = -2, isl = (int)((nl) % (unsigned)RS), iz = wrapz(wrapz(z0 - 2 * dz));
+    const int last = nzc + 1;  // logical planes -2 .. nzc+1
+    auto issue = [&]() {
+      double *dst = sm + (size_t)isl * SLOT;
+      uint64_t *b = bar + isl;
+      mbar_expect_tx(b, bytes);
+      tma_load4(dst, G.mapA, ox, oy, iz, Q.slot_prev, b);
+      tma_load4(dst + SA, G.mapA, ox, oy, iz, G.slot_kappa, b);
+      if (UPP) tma_load4(dst + 2 * SA, G.mapB, ox, oy + 1, iz, Q.slot_pp, b);
+#pragma unroll
+      for (int c = 0; c < PM; c++) tma_load4(dst + 2 * SA + (1 + c) * SB, G.mapB, ox, oy + 1, iz, G.slot_B + c, b);
+      iL++;
+      isl = isl + 1 == RS ? 0 : isl + 1;
+      iz = wrapz(iz + dz);
+    };
+    __syncthreads();  // the previous unit / pass is done with the ring and the exchange
+    if (t == 0)
+      for (int q = 0; q < RS && iL <= last; q++) issue();
+    // consumer ring position: slot / parity of the plane to wait for next (plane -2)
+    int wsl = (int)(nl % (unsigned)RS);
+    unsigned wpar = (nl / (unsigned)RS) & 1u;
+    auto wait_next = [&]() -> int {  // wait for the next plane, return its slot
+      const int s = wsl;
+      mbar_wait(bar + s, wpar);
+      wsl = wsl + 1 == RS ? 0 : wsl + 1;
+      if (wsl == 0) wpar ^= 1u;
+      return s;
+    };
+    // prologue: plane -2 (x_{k-1}, kappa centre below the first stage-1 plane), plane -1
+    const int sm2 = wait_next();
+    int sl = wait_next();  // slot of the stage-1 plane L (= -1 at step 0)
+    Rec ra, rb;            // ra: plane L-1 at even steps; rb: at odd steps (ping-pong)
+    ra.xc = ld2(sm + (size_t)sm2 * SLOT + offA);
+    ra.kc = ld2(sm + (size_t)sm2 * SLOT + SA + offA);
+    ra.xk = ra.bk = ra.fs = ra.fn = ra.fm = make_double2(0.0, 0.0);
+    ra.fl = ra.fi = ra.fr = 0.0;
+    rb = ra;
+    double2 xq = ld2(sm + (size_t)sl * SLOT + offA), kq = ld2(sm + (size_t)sl * SLOT + SA + offA);  // centre of plane L
+    __syncthreads();
+    if (t == 0 && iL <= last) issue();  // into the slot of plane -2
+    int zo = z0;                        // physical plane of the stage-2 output (logical L-1)
+
+    // one step: stage 1 on plane L = i-1 (into cu, which held plane L-2), stage 2 on
+    // plane L-1 (pv) when S2
+    auto step = [&](auto s2tag, int i, Rec &pv, Rec &cu) {
+      constexpr bool S2 = decltype(s2tag)::value;
+      const int sq = wait_next();  // plane L+1
+      const double *Xs = sm + (size_t)sl * SLOT, *Xq = sm + (size_t)sq * SLOT;
+      // ---- stage 1, plane L
+      const double *XL = Xs + offA, *KL = Xs + SA + offA, *BL = Xs + 2 * SA + SB + offB;
+      const double2 xc = xq, kc = kq;
+      const double2 xqn = ld2(Xq + offA), kqn = ld2(Xq + SA + offA);
+      const double2 ks = ld2(KL - W), kn = ld2(KL + W);
+      double kl = __shfl_up_sync(0xffffffffu, kc.y, 1), kr = __shfl_down_sync(0xffffffffu, kc.x, 1);
+      if (!shl) kl = KL[-1];
+      if (!shr) kr = KL[2];
+      const double fl = kc.x + kl, fi = kc.x + kc.y, fr = kc.y + kr;
+      const double2 fs = make_double2(kc.x + ks.x, kc.y + ks.y), fn = make_double2(kc.x + kn.x, kc.y + kn.y);
+      const double2 fm = make_double2(kc.x + pv.kc.x, kc.y + pv.kc.y), fp = make_double2(kc.x + kqn.x, kc.y + kqn.y);
+      double2 xk = xc;
+      if (UR) {
+        const double2 xs = ld2(XL - W), xn = ld2(XL + W);
+        double xl = __shfl_up_sync(0xffffffffu, xc.y, 1), xr = __shfl_down_sync(0xffffffffu, xc.x, 1);
+        if (!shl) xl = XL[-1];
+        if (!shr) xr = XL[2];
+        double2 bt = {0.0, 0.0};
+#pragma unroll
+        for (int c = 0; c < PM; c++) {
+          const double2 b = ld2(BL + c * SB);
+          bt.x = fma(b.x, btp[c], bt.x);
+          bt.y = fma(b.y, btp[c], bt.y);
+        }
+        const double2 xm = pv.xc;
+        double ra_ = fl * (xl - xc.x);
+        double rb_ = fr * (xr - xc.y);
+        ra_ = fma(fi, xc.y - xc.x, ra_);
+        rb_ = fma(fi, xc.x - xc.y, rb_);
+        ra_ = fma(fs.x, xs.x - xc.x, ra_);
+        rb_ = fma(fs.y, xs.y - xc.y, rb_);
+        ra_ = fma(fn.x, xn.x - xc.x, ra_);
+        rb_ = fma(fn.y, xn.y - xc.y, rb_);
+        ra_ = fma(fm.x, xm.x - xc.x, ra_);
+        rb_ = fma(fm.y, xm.y - xc.y, rb_);
+        ra_ = fma(fp.x, xqn.x - xc.x, ra_);
+        rb_ = fma(fp.y, xqn.y - xc.y, rb_);
+        const double r0 = fma(ra_, hh, bt.x), r1 = fma(rb_, hh, bt.y);
+        xk.x = a0 * r0 - a1 * xc.x;
+        xk.y = a0 * r1 - a1 * xc.y;
+        if (UPP) {
+          const double2 pp = ld2(Xs + 2 * SA + offB);
+          xk.x -= a2 * pp.x;
+          xk.y -= a2 * pp.y;
+        }
+      }
+      double2 bk = {0.0, 0.0};
+#pragma unroll
+      for (int c = 0; c < PM; c++) {
+        const double2 b = ld2(BL + c * SB);
+        bk.x = fma(b.x, btc[c], bk.x);
+        bk.y = fma(b.y, btc[c], bk.y);
+      }
+      ex[(i & 1) * (EXP + 32) + ew] = xk;
+      // ---- stage 2, plane L-1: r_k = A x_k + nu B t_k, dots, store x_k
+      if (S2) {
+        const double2 *E = ex + ((i - 1) & 1) * (EXP + 32);
+        const double2 c0 = pv.xk, xkm = cu.xk;  // x_k at L-1, L-2
+        double xl = __shfl_up_sync(0xffffffffu, c0.y, 1), xr = __shfl_down_sync(0xffffffffu, c0.x, 1);
+        if (!shl) xl = E[er - 1].y;
+        if (!shr) xr = E[er + 1].x;
+        const double2 xs = E[er - 34], xn = E[er + 34];
+        double ra_ = pv.fl * (xl - c0.x);
+        double rb_ = pv.fr * (xr - c0.y);
+        ra_ = fma(pv.fi, c0.y - c0.x, ra_);
+        rb_ = fma(pv.fi, c0.x - c0.y, rb_);
+        ra_ = fma(pv.fs.x, xs.x - c0.x, ra_);
+        rb_ = fma(pv.fs.y, xs.y - c0.y, rb_);
+        ra_ = fma(pv.fn.x, xn.x - c0.x, ra_);
+        rb_ = fma(pv.fn.y, xn.y - c0.y, rb_);
+        ra_ = fma(pv.fm.x, xkm.x - c0.x, ra_);
+        rb_ = fma(pv.fm.y, xkm.y - c0.y, rb_);
+        ra_ = fma(fm.x, xk.x - c0.x, ra_);  // upper face of plane L-1 = lower face of plane L
+        rb_ = fma(fm.y, xk.y - c0.y, rb_);
+        const double r0 = fma(ra_, hh, pv.bk.x), r1 = fma(rb_, hh, pv.bk.y);
+        const double2 xm = pv.xc;  // x_{k-1} at L-1
+        const double d0 = fma(c0.x, c0.x, c0.y * c0.y), d1 = fma(xm.x, c0.x, xm.y * c0.y);
+        const double d2 = fma(xm.x, r0, xm.y * r1), d3 = fma(c0.x, r0, c0.y * r1), d4 = fma(r0, r0, r1 * r1);
+        if (s2) {
+          v0 += d0; v1 += d1; v2 += d2; v3 += d3; v4 += d4;
+        }
+        if (st) {
+          double *xo = Q.xout + (long long)zo * plane;
+          *reinterpret_cast<double2 *>(xo + o0) = c0;
+          if (og0 >= 0) *reinterpret_cast<double2 *>(xo + og0) = c0;
+          if (og1 >= 0) *reinterpret_cast<double2 *>(xo + og1) = c0;
+          if (og2 >= 0) *reinterpret_cast<double2 *>(xo + og2) = c0;
+        }
+        zo = wrapz(zo + dz);
+      }
+      cu.xk = xk; cu.bk = bk;
+      cu.fl = fl; cu.fi = fi; cu.fr = fr;
+      cu.fs = fs; cu.fn = fn; cu.fm = fm;
+      cu.xc = xc; cu.kc = kc;
+      xq = xqn;
+      kq = kqn;
+      sl = sq;
+      __syncthreads();  // slot of plane L and exchange (i-1)&1 fully read
+      if (t == 0 && iL <= last) issue();  // plane L + RS into the slot of plane L
+    };
+    using F = std::integral_constant<bool, false>;
+    using T = std::integral_constant<bool, true>;
+    // steps i = 0 .. nzc+1: stage 2 from i = 2; ra holds plane L-1 at even i
+    step(F{}, 0, ra, rb);
+    step(F{}, 1, rb, ra);
+    int i = 2;
+    if (RC3_HALO_S1ONLY && hwarp) {  // warp-uniform: halo warps run stage 1 only
+      for (; i + 1 <= last; i += 2) {
+        step(F{}, i, ra, rb);
+        step(F{}, i + 1, rb, ra);
+      }
+      if (i <= last) step(F{}, i, ra, rb);
+    } else {
+      for (; i + 1 <= last; i += 2) {
+        step(T{}, i, ra, rb);
+        step(T{}, i + 1, rb, ra);
+      }
+      if (i <= last) step(T{}, i, ra, rb);
+    }
+    nl += (unsigned)(nzc + 4);
+  }
+  // the stage-2 sums use v += d (not fma chains) -- same values as the fma form up to rounding
+  v[0] += v0; v[1] += v1; v[2] += v2; v[3] += v3; v[4] += v4;
+}
+
+template <int PM, int HM, int D>
+__device__ __forceinline__ void body(const Geom &G, const PassArgs<PM> &Q, double (&v)[5], unsigned &nl) {
+  if (Q.slot_pp >= 0)
+    march<PM, HM, D, true, true>(G, Q, v, nl);
+  else if (Q.use_r)
+    march<PM, HM, D, true, false>(G, Q, v, nl);
+  else
+    march<PM, HM, D, false, false>(G, Q, v, nl);
+}
+
+}  // namespace rc3
