@@ -45,11 +45,14 @@
 
 #include <type_traits>
 
+#ifndef RC3_PRODUCER
+#define RC3_PRODUCER 0  // the thread that issues the TMA boxes
+#endif
+#ifndef RC3_SPLIT
+#define RC3_SPLIT 1
+#endif
 #ifndef RC3_ROLEMAP
 #define RC3_ROLEMAP 1
-#endif
-#ifndef RC3_HALO_S1ONLY
-#define RC3_HALO_S1ONLY 0
 #endif
 
 namespace rc3 {
@@ -162,6 +165,76 @@ __device__ __forceinline__ void init(const Geom &G) {
   __syncthreads();
 }
 
+// One work unit (tile x z-part) of a pass: tile origin, band height, interior pairs,
+// z range, march direction (alternating with the pass parity) and the physical plane
+// of logical plane 0.
+struct UnitGeo {
+  int ox, oy, hb, tw, zlo, zhi, nzc, dz, z0;
+};
+__device__ __forceinline__ UnitGeo unit_geo(const Geom &G, int w, int k) {
+  UnitGeo U;
+  const int ntx = G.ntx, nb = G.nb;
+  const int tile = w % (ntx * nb), part = w / (ntx * nb);
+  U.ox = (tile % ntx) * 64;
+  const int band = tile / ntx;
+  U.oy = (int)((long long)band * G.ny / nb);
+  U.hb = (int)((long long)(band + 1) * G.ny / nb) - U.oy;
+  U.tw = min(32, (G.nx - U.ox) / 2);
+  U.zlo = (int)((long long)part * G.nz / G.zsplit);
+  U.zhi = (int)((long long)(part + 1) * G.nz / G.zsplit);
+  U.nzc = U.zhi - U.zlo;
+  const bool down = ((part ^ k) & 1) != 0;
+  U.dz = down ? -1 : 1;
+  U.z0 = down ? U.zhi - 1 : U.zlo;
+  return U;
+}
+// physical plane of logical plane L (>= -2) of a unit
+__device__ __forceinline__ int plane_z(const UnitGeo &U, int nz, int L) {
+  int z = (U.z0 + L * U.dz) % nz;
+  return z < 0 ? z + nz : z;
+}
+// The TMA boxes of one plane into ring slot `slot`: which & 1: kappa, x_{k-2} (slot_pp
+// >= 0), B (with the barrier's expected byte count for all boxes); which & 2: x_{k-1}.
+// (Issuing the first planes of the next pass early, during the grid reduction, split
+// 1 / 2 around the grid barrier, measured slower: profiles/r02_kernel_evolution.md.)
+template <int PM, int HM, int D>
+__device__ __forceinline__ void issue_boxes(const Geom &G, const UnitGeo &U, int z, int slot, int slot_prev, int slot_pp,
+                                            int which) {
+  using C = Cfg<PM, HM, D>;
+  double *sm = smem_base<PM, HM, D>();
+  double *dst = sm + (size_t)slot * C::SLOT;
+  uint64_t *b = bars<PM, HM, D>(sm) + slot;
+  if (which & 1) {
+    mbar_expect_tx(b, 2 * C::BYTES_A + (unsigned)PM * C::BYTES_B + (slot_pp >= 0 ? C::BYTES_B : 0u));
+    tma_load4(dst + C::SA, G.mapA, U.ox, U.oy, z, G.slot_kappa, b);
+    if (slot_pp >= 0) tma_load4(dst + 2 * C::SA, G.mapB, U.ox, U.oy + 1, z, slot_pp, b);
+#pragma unroll
+    for (int c = 0; c < PM; c++) tma_load4(dst + 2 * C::SA + (1 + c) * C::SB, G.mapB, U.ox, U.oy + 1, z, G.slot_B + c, b);
+  }
+  if (which & 2) tma_load4(dst, G.mapA, U.ox, U.oy, z, slot_prev, b);
+}
+// sum_f kappa_f (x_f - x_c) over the six faces of one point (x-, x+, y-, y+, z-, z+
+// in the lazy kernels' operand order).  RC3_SPLIT: two interleaved partial sums
+// (dependency depth 3 + 1 instead of 6), the same terms.
+__device__ __forceinline__ double face_sum(double f0, double d0, double f1, double d1, double f2, double d2, double f3,
+                                           double d3, double f4, double d4, double f5, double d5) {
+#if RC3_SPLIT
+  double a = f0 * d0, b = f1 * d1;
+  a = fma(f2, d2, a);
+  b = fma(f3, d3, b);
+  a = fma(f4, d4, a);
+  b = fma(f5, d5, b);
+  return a + b;
+#else
+  double a = f0 * d0;
+  a = fma(f1, d1, a);
+  a = fma(f2, d2, a);
+  a = fma(f3, d3, a);
+  a = fma(f4, d4, a);
+  return fma(f5, d5, a);
+#endif
+}
+
 // Stage-1 results of one plane at this thread's pair, carried to stage 2 of the next
 // step (and its x_{k-1} / kappa centre to stage 1 of the next plane as the z-1 terms).
 struct Rec {
@@ -214,7 +287,6 @@ __device__ __forceinline__ void march(const Geom &G, const PassArgs<PM> &Q, doub
     btc[c] = Q.btc[c];
   }
   double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0, v4 = 0.0;
-  constexpr unsigned bytes = 2 * C::BYTES_A + (unsigned)PM * C::BYTES_B + (UPP ? C::BYTES_B : 0u);
 
   for (int w = blockIdx.x; w < units; w += gridDim.x) {
     const int tile = w % (ntx * nb), part = w / (ntx * nb);
@@ -255,43 +327,37 @@ __device__ __forceinline__ void march(const Geom &G, const PassArgs<PM> &Q, doub
     const bool shl = lane > 0 && s1 && kl == key - 1, shr = lane < 31 && s1 && kr == key + 1;
     // padded-plane offsets of this pair and of its periodic ghost images (interior pairs)
     const int gx = ox - 2 + 2 * qx, gy = oy - 1 + qy;
-    const long long o0 = (long long)(gx + 2) + (long long)G.Xp * (gy + 2);
-    long long og0 = -1, og1 = -1, og2 = -1;
+    const int o0 = (gx + 2) + G.Xp * (gy + 2);  // (a padded plane has < 2^31 points)
+    int og0 = -1, og1 = -1, og2 = -1;
     if (s2) {
       const int gxg = gx < 2 ? gx + nx : (gx >= nx - 2 ? gx - nx : -99);
       const int gyg = gy < 2 ? gy + ny : (gy >= ny - 2 ? gy - ny : -99);
-      if (gxg != -99) og0 = (long long)(gxg + 2) + (long long)G.Xp * (gy + 2);
-      if (gyg != -99) og1 = (long long)(gx + 2) + (long long)G.Xp * (gyg + 2);
-      if (gxg != -99 && gyg != -99) og2 = (long long)(gxg + 2) + (long long)G.Xp * (gyg + 2);
+      if (gxg != -99) og0 = (gxg + 2) + G.Xp * (gy + 2);
+      if (gyg != -99) og1 = (gx + 2) + G.Xp * (gyg + 2);
+      if (gxg != -99 && gyg != -99) og2 = (gxg + 2) + G.Xp * (gyg + 2);
     }
     const bool st = s2 && Q.xout != nullptr;
     const int dz = down ? -1 : 1;
     auto wrapz = [&](int z) { return z < 0 ? z + nz : (z >= nz ? z - nz : z); };
-    int z0 = down ? zhi - 1 : zlo;  // physical plane of logical plane 0
-    z0 %= nz;
-    // producer (thread 0): next plane to issue, its slot and physical plane
-    int iL = -2, isl = (int)((nl) % (unsigned)RS), iz = wrapz(wrapz(z0 - 2 * dz));
+    const UnitGeo U = unit_geo(G, w, Q.k);
+    const int z0 = U.z0;
     const int last = nzc + 1;  // logical planes -2 .. nzc+1
+    // producer: next plane to issue, its slot and physical plane
+    const bool prod = t == RC3_PRODUCER;
+    int iL = -2, isl = (int)(nl % (unsigned)RS), iz = plane_z(U, nz, -2);
     auto issue = [&]() {
-      double *dst = sm + (size_t)isl * SLOT;
-      uint64_t *b = bar + isl;
-      mbar_expect_tx(b, bytes);
-      tma_load4(dst, G.mapA, ox, oy, iz, Q.slot_prev, b);
-      tma_load4(dst + SA, G.mapA, ox, oy, iz, G.slot_kappa, b);
-      if (UPP) tma_load4(dst + 2 * SA, G.mapB, ox, oy + 1, iz, Q.slot_pp, b);
-#pragma unroll
-      for (int c = 0; c < PM; c++) tma_load4(dst + 2 * SA + (1 + c) * SB, G.mapB, ox, oy + 1, iz, G.slot_B + c, b);
+      issue_boxes<PM, HM, D>(G, U, iz, isl, Q.slot_prev, UPP ? Q.slot_pp : -1, 3);
       iL++;
       isl = isl + 1 == RS ? 0 : isl + 1;
       iz = wrapz(iz + dz);
     };
     __syncthreads();  // the previous unit / pass is done with the ring and the exchange
-    if (t == 0)
+    if (prod)
       for (int q = 0; q < RS && iL <= last; q++) issue();
     // consumer ring position: slot / parity of the plane to wait for next (plane -2)
     int wsl = (int)(nl % (unsigned)RS);
     unsigned wpar = (nl / (unsigned)RS) & 1u;
-    auto wait_next = [&]() -> int {  // wait for the next plane, return its slot
+    auto wait_next = [&]() -> int {
       const int s = wsl;
       mbar_wait(bar + s, wpar);
       wsl = wsl + 1 == RS ? 0 : wsl + 1;
@@ -309,7 +375,7 @@ __device__ __forceinline__ void march(const Geom &G, const PassArgs<PM> &Q, doub
     rb = ra;
     double2 xq = ld2(sm + (size_t)sl * SLOT + offA), kq = ld2(sm + (size_t)sl * SLOT + SA + offA);  // centre of plane L
     __syncthreads();
-    if (t == 0 && iL <= last) issue();  // into the slot of plane -2
+    if (prod && iL <= last) issue();  // into the slot of plane -2
     int zo = z0;                        // physical plane of the stage-2 output (logical L-1)
 
     // one step: stage 1 on plane L = i-1 (into cu, which held plane L-2), stage 2 on
@@ -343,18 +409,10 @@ __device__ __forceinline__ void march(const Geom &G, const PassArgs<PM> &Q, doub
           bt.y = fma(b.y, btp[c], bt.y);
         }
         const double2 xm = pv.xc;
-        double ra_ = fl * (xl - xc.x);
-        double rb_ = fr * (xr - xc.y);
-        ra_ = fma(fi, xc.y - xc.x, ra_);
-        rb_ = fma(fi, xc.x - xc.y, rb_);
-        ra_ = fma(fs.x, xs.x - xc.x, ra_);
-        rb_ = fma(fs.y, xs.y - xc.y, rb_);
-        ra_ = fma(fn.x, xn.x - xc.x, ra_);
-        rb_ = fma(fn.y, xn.y - xc.y, rb_);
-        ra_ = fma(fm.x, xm.x - xc.x, ra_);
-        rb_ = fma(fm.y, xm.y - xc.y, rb_);
-        ra_ = fma(fp.x, xqn.x - xc.x, ra_);
-        rb_ = fma(fp.y, xqn.y - xc.y, rb_);
+        const double ra_ = face_sum(fl, xl - xc.x, fi, xc.y - xc.x, fs.x, xs.x - xc.x, fn.x, xn.x - xc.x, fm.x,
+                                    xm.x - xc.x, fp.x, xqn.x - xc.x);
+        const double rb_ = face_sum(fr, xr - xc.y, fi, xc.x - xc.y, fs.y, xs.y - xc.y, fn.y, xn.y - xc.y, fm.y,
+                                    xm.y - xc.y, fp.y, xqn.y - xc.y);
         const double r0 = fma(ra_, hh, bt.x), r1 = fma(rb_, hh, bt.y);
         xk.x = a0 * r0 - a1 * xc.x;
         xk.y = a0 * r1 - a1 * xc.y;
@@ -380,18 +438,11 @@ __device__ __forceinline__ void march(const Geom &G, const PassArgs<PM> &Q, doub
         if (!shl) xl = E[er - 1].y;
         if (!shr) xr = E[er + 1].x;
         const double2 xs = E[er - 34], xn = E[er + 34];
-        double ra_ = pv.fl * (xl - c0.x);
-        double rb_ = pv.fr * (xr - c0.y);
-        ra_ = fma(pv.fi, c0.y - c0.x, ra_);
-        rb_ = fma(pv.fi, c0.x - c0.y, rb_);
-        ra_ = fma(pv.fs.x, xs.x - c0.x, ra_);
-        rb_ = fma(pv.fs.y, xs.y - c0.y, rb_);
-        ra_ = fma(pv.fn.x, xn.x - c0.x, ra_);
-        rb_ = fma(pv.fn.y, xn.y - c0.y, rb_);
-        ra_ = fma(pv.fm.x, xkm.x - c0.x, ra_);
-        rb_ = fma(pv.fm.y, xkm.y - c0.y, rb_);
-        ra_ = fma(fm.x, xk.x - c0.x, ra_);  // upper face of plane L-1 = lower face of plane L
-        rb_ = fma(fm.y, xk.y - c0.y, rb_);
+        // (the upper face of plane L-1 is the lower face fm of plane L)
+        const double ra_ = face_sum(pv.fl, xl - c0.x, pv.fi, c0.y - c0.x, pv.fs.x, xs.x - c0.x, pv.fn.x, xn.x - c0.x,
+                                    pv.fm.x, xkm.x - c0.x, fm.x, xk.x - c0.x);
+        const double rb_ = face_sum(pv.fr, xr - c0.y, pv.fi, c0.x - c0.y, pv.fs.y, xs.y - c0.y, pv.fn.y, xn.y - c0.y,
+                                    pv.fm.y, xkm.y - c0.y, fm.y, xk.y - c0.y);
         const double r0 = fma(ra_, hh, pv.bk.x), r1 = fma(rb_, hh, pv.bk.y);
         const double2 xm = pv.xc;  // x_{k-1} at L-1
         const double d0 = fma(c0.x, c0.x, c0.y * c0.y), d1 = fma(xm.x, c0.x, xm.y * c0.y);
@@ -416,7 +467,7 @@ __device__ __forceinline__ void march(const Geom &G, const PassArgs<PM> &Q, doub
       kq = kqn;
       sl = sq;
       __syncthreads();  // slot of plane L and exchange (i-1)&1 fully read
-      if (t == 0 && iL <= last) issue();  // plane L + RS into the slot of plane L
+      if (prod && iL <= last) issue();  // plane L + RS into the slot of plane L
     };
     using F = std::integral_constant<bool, false>;
     using T = std::integral_constant<bool, true>;
@@ -424,19 +475,11 @@ __device__ __forceinline__ void march(const Geom &G, const PassArgs<PM> &Q, doub
     step(F{}, 0, ra, rb);
     step(F{}, 1, rb, ra);
     int i = 2;
-    if (RC3_HALO_S1ONLY && hwarp) {  // warp-uniform: halo warps run stage 1 only
-      for (; i + 1 <= last; i += 2) {
-        step(F{}, i, ra, rb);
-        step(F{}, i + 1, rb, ra);
-      }
-      if (i <= last) step(F{}, i, ra, rb);
-    } else {
-      for (; i + 1 <= last; i += 2) {
-        step(T{}, i, ra, rb);
-        step(T{}, i + 1, rb, ra);
-      }
-      if (i <= last) step(T{}, i, ra, rb);
+    for (; i + 1 <= last; i += 2) {
+      step(T{}, i, ra, rb);
+      step(T{}, i + 1, rb, ra);
     }
+    if (i <= last) step(T{}, i, ra, rb);
     nl += (unsigned)(nzc + 4);
   }
   // the stage-2 sums use v += d (not fma chains) -- same values as the fma form up to rounding

@@ -13,7 +13,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libkiops_b200.so")
+LIB_PATH = os.environ.get("KIOPS_LIB") or os.path.join(HERE, "libkiops_b200.so")  # KIOPS_LIB: debug builds (scripts/)
 
 MAX_P, MAX_OUT, MAX_M, MAX_FORCED, TRACE_CAP = 8, 64, 128, 256, 16384
 KIND = {"stencil1d3": 1, "stencil2d5": 2, "stencil3d7": 3, "csr": 4}

@@ -18,6 +18,15 @@
 #ifndef MB_HM
 #define MB_HM 7
 #endif
+#ifndef MB_ROT
+#define MB_ROT 0
+#endif
+#ifndef MB_QREG
+#define MB_QREG 0
+#endif
+#ifndef MB_GRID
+#define MB_GRID 0
+#endif
 #ifndef MB_D
 #define MB_D 3
 #endif
@@ -115,13 +124,56 @@ __global__ void k_check(const double *XO, const double *XK, int nx, int ny, int 
   atomicMax((unsigned long long *)(err + 1), __double_as_longlong(e2));
 }
 
+__device__ unsigned long long mb_count;  // grid barrier (MB_GRID): monotonic arrivals
+
+__device__ rc3::Geom mb_G;
+__device__ rc3::PassArgs<PM> mb_Q;
+#if MB_QREG  // geometry and pass scalars in registers (as in the product), not kernel parameters
+__global__ void __launch_bounds__(C::NT, 1) k_mb(rc3::Geom G0, rc3::PassArgs<PM> Q0, double *dots, int reps) {
+#if MB_QREG == 1
+  rc3::Geom G;
+  memcpy(&G, (const void *)&mb_G, sizeof(G));
+#else
+  const rc3::Geom &G = G0;
+#endif
+  rc3::PassArgs<PM> Q;
+  memcpy(&Q, (const void *)&mb_Q, sizeof(Q));
+#else
 __global__ void __maxnreg__(200) k_mb(rc3::Geom G, rc3::PassArgs<PM> Q, double *dots, int reps) {
+#endif
   rc3::init<PM, HM, DD>(G);
   unsigned nl = 0;
   double v[5] = {0, 0, 0, 0, 0};
+  __shared__ double red0[5][32];
+  unsigned long long target = 0;
+  if (threadIdx.x == 0) target = *(volatile unsigned long long *)&mb_count;
+  auto slots = [&](int r, int &sp, int &spp, double *&xo) {
+    sp = Q.slot_prev; spp = Q.slot_pp; xo = Q.xout;
+#if MB_ROT  // rotate x_{k-1}, x_{k-2}, x_k through the basis slots like consecutive passes
+    if (reps > 1) { sp = 5 + (r + 1) % 8; spp = 5 + r % 8; xo = G.V + (size_t)(5 + (r + 2) % 8) * G.ldN; }
+#endif
+  };
   for (int r = 0; r < reps; r++) {
     Q.k = r + 3;  // alternate the march direction like consecutive passes
+    slots(r, Q.slot_prev, Q.slot_pp, Q.xout);
     rc3::body<PM, HM, DD>(G, Q, v, nl);
+#if MB_GRID  // the persistent loop's pass boundary: block sums, grid barrier, (prefetch)
+    for (int q = 0; q < 5; q++) {
+      double x = v[q];
+      for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+      if ((threadIdx.x & 31) == 0) red0[q][threadIdx.x >> 5] = x;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      atomicAdd(&mb_count, 1ull);
+      target += gridDim.x;
+      while (*(volatile unsigned long long *)&mb_count < target) {
+      }
+      __threadfence();
+    }
+    __syncthreads();
+#endif
   }
   __shared__ double red[5][32];
   for (int q = 0; q < 5; q++) {
@@ -150,10 +202,11 @@ int main(int argc, char **argv) {
   CKR(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   const int Xp = nx + 4, Yp = ny + 4;
   const long long ldN = ((long long)Xp * Yp * nz + 31) / 32 * 32;
-  const int nslot = 6;  // 0 x_{k-1}, 1 x_{k-2}, 2 kappa, 3-4 B, 5 x_k
+  const int nslot = MB_ROT ? 13 : 6;  // 0 x_{k-1}, 1 x_{k-2}, 2 kappa, 3-4 B, 5 x_k (MB_ROT: 5..12 basis ring)
   double *V;
   CKR(cudaMalloc(&V, sizeof(double) * ldN * nslot));
-  for (int s = 0; s < 5; s++) k_fill<<<1184, 256>>>(V, ldN, s, nx, ny, nz);
+  for (int s = 0; s < nslot; s++)
+    if (s != 5) k_fill<<<1184, 256>>>(V, ldN, s, nx, ny, nz);
   CKR(cudaMemset(V + 5 * ldN, 0, sizeof(double) * ldN));
   EncodeFn enc = nullptr;
   cudaDriverEntryPointQueryResult qr;
@@ -183,6 +236,8 @@ int main(int argc, char **argv) {
   Q.k = 3; Q.slot_prev = 0; Q.slot_pp = 1; Q.xout = V + 5 * ldN;
   Q.a0 = 1.0 / 3000.0; Q.a1 = 0.3; Q.a2 = 0.2; Q.btp[0] = 0.7; Q.btp[1] = -0.4; Q.btc[0] = 0.25; Q.btc[1] = 0.6; Q.use_r = 1;
   const int grid = std::min(sms, G.ntx * G.nb * G.zsplit);
+  CKR(cudaMemcpyToSymbol(mb_G, &G, sizeof(G)));
+  CKR(cudaMemcpyToSymbol(mb_Q, &Q, sizeof(Q)));
   CKR(cudaFuncSetAttribute(k_mb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::smem_bytes));
   double *dots, *rdots, *err, *XK;
   CKR(cudaMalloc(&dots, 5 * sizeof(double)));
