@@ -212,10 +212,18 @@ __device__ __forceinline__ void finalize_warp(const KParams &P, int k, const dou
   }
 }
 
+// Optional pass-boundary hooks: prefetch(S, C, 1) right after pass S.k's body,
+// prefetch(S, C, 2) once every CTA has finished pass S.k (its records are readable),
+// settle(go) after the finalisation (go: pass S.k + 1 takes place).
+struct NoHooks {
+  __device__ __forceinline__ void prefetch(const PassScalars &, const InnerCarry &, int) {}
+  __device__ __forceinline__ void settle(bool) {}
+};
+
 // The loop.  body(S, v) streams pass S.k over this CTA's share and accumulates the
 // five dot partials into v.  All CTAs take identical control decisions.
-template <class Body>
-__device__ __forceinline__ void inner_loop(const KParams &P, Body &&body) {
+template <class Body, class Hooks = NoHooks>
+__device__ __forceinline__ void inner_loop(const KParams &P, Body &&body, Hooks &&hooks = Hooks{}) {
   __shared__ PassScalars S;
   __shared__ InnerCarry C;
   __shared__ double red[NDOT * 32];
@@ -284,6 +292,7 @@ __device__ __forceinline__ void inner_loop(const KParams &P, Body &&body) {
       for (int q = 0; q < NDOT; q++) ts[q] = t[q];
     }
     body(S, v);
+    hooks.prefetch(S, C, 1);
     block_sum<NDOT>(v, red);  // (its __syncthreads order every thread's vector writes before the fence)
     PHASE(tb);
     double w[NDOT];
@@ -304,6 +313,7 @@ __device__ __forceinline__ void inner_loop(const KParams &P, Body &&body) {
     }
     __syncthreads();
     PHASE(tp);
+    hooks.prefetch(S, C, 2);
     // every CTA's record, in the fixed block order of pass_finalize.  (Issuing pass
     // k+1's first loads here, before its scalars exist, measured slower: the extra
     // traffic delays the record loads and the finalisation more than it hides.)
@@ -317,6 +327,7 @@ __device__ __forceinline__ void inner_loop(const KParams &P, Body &&body) {
     PHASE(tw);
     block_sum<NDOT>(w, red);
     }
+    if (nb == 1) hooks.prefetch(S, C, 2);
 #ifdef KIOPS_PHASE_TIMERS
     const long long c0 = clock64();
 #endif
@@ -327,6 +338,7 @@ __device__ __forceinline__ void inner_loop(const KParams &P, Body &&body) {
 #endif
     __syncthreads();
     PHASE(tf);
+    hooks.settle(C.go != 0);
     if (!C.go) break;
   }
 #ifdef KIOPS_PHASE_TIMERS

@@ -8,8 +8,12 @@
 #include "inner.cuh"
 #include "rc3d.cuh"
 
+#ifndef RC_HM
 #define RC_HM 7  // tile rows (config 4 bands: 6-7 rows of 64 points)
-#define RC_D 3   // planes in flight ahead of the two in use
+#endif
+#ifndef RC_D
+#define RC_D 3  // planes in flight ahead of the two in use
+#endif
 template <int PM>
 using RcCfg = rc3::Cfg<PM, RC_HM, RC_D>;
 
@@ -45,16 +49,51 @@ __device__ __forceinline__ rc3::PassArgs<PM> rc_args(const KParams &P, const Pas
   return Q;
 }
 
+#ifndef RC_PREFETCH
+#define RC_PREFETCH 0  // measured neutral at config 4 (same-box A/B, profiles/r02_kernel_evolution.md)
+#endif
+// Pass-boundary prefetch: during pass k's grid reduction the first ring planes of pass
+// k+1 are issued (kappa, B, x_{k-1} boxes at once; the x_k boxes once every CTA has
+// finished pass k), so pass k+1 starts on landed data.  If the Alg. 2 run ends instead
+// (breakdown, non-finite, status), the planes are drained.
+template <int PM>
+struct RcHooks {
+  const KParams &P;
+  const rc3::Geom &G;
+  unsigned &nl;
+  int &pre;
+  int npend;
+  __device__ __forceinline__ void prefetch(const PassScalars &S, const InnerCarry &C, int which) {
+    if (!RC_PREFETCH) return;
+    const int k = S.k;
+    if (which == 1) npend = 0;
+    if (C.status_in != 0 || k >= C.m + 1 || k + 1 > P.m_max + 1 || (which == 2 && npend == 0)) return;
+    // pass k+1 reads x_k (slot k-1; x_1 is slot 0) and x_{k-1} (slot k-2, from k+1 = 3)
+    npend = rc3::preissue<PM, RC_HM, RC_D>(G, k + 1, k - 1, k >= 2 ? k - 2 : -1, nl, which, pre);
+  }
+  __device__ __forceinline__ void settle(bool go) {
+    if (!go && npend > 0) {
+      rc3::drain<PM, RC_HM, RC_D>(nl, npend);
+      pre = 0;
+    }
+    npend = 0;
+  }
+};
+
 // Persistent inner loop (inner.cuh) over recompute passes: one CTA per SM.
 template <int PM>
 __global__ void __launch_bounds__(RcCfg<PM>::NT, 1) k_inner_3d_rc(KParams P) {
   const rc3::Geom G = rc_geom(P);
   rc3::init<PM, RC_HM, RC_D>(G);
   unsigned nl = 0;  // the ring's running fill count, carried across the passes
-  inner_loop(P, [&](const PassScalars &S, double (&v)[NDOT]) {
-    const rc3::PassArgs<PM> Q = rc_args<PM>(P, S);
-    rc3::body<PM, RC_HM, RC_D>(G, Q, v, nl);
-  });
+  int pre = 0;      // ring planes of the next pass already issued (producer thread)
+  inner_loop(
+      P,
+      [&](const PassScalars &S, double (&v)[NDOT]) {
+        const rc3::PassArgs<PM> Q = rc_args<PM>(P, S);
+        rc3::body<PM, RC_HM, RC_D>(G, Q, v, nl, pre);
+      },
+      RcHooks<PM>{P, G, nl, pre, 0});
 }
 
 // One launch per pass (KIOPS_PERSIST=0, or a grid that is not co-resident).
@@ -67,8 +106,9 @@ __global__ void __launch_bounds__(RcCfg<PM>::NT, 1) k_pass_3d_rc(KParams P) {
   rc3::init<PM, RC_HM, RC_D>(G);  // (its __syncthreads publishes S)
   if (S.k == 0) return;
   unsigned nl = 0;
+  int pre = 0;
   double v[NDOT] = {0.0, 0.0, 0.0, 0.0, 0.0};
   const rc3::PassArgs<PM> Q = rc_args<PM>(P, S);
-  rc3::body<PM, RC_HM, RC_D>(G, Q, v, nl);
+  rc3::body<PM, RC_HM, RC_D>(G, Q, v, nl, pre);
   pass_epilogue(P, S.k, v);
 }

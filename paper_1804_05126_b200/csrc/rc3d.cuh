@@ -195,8 +195,7 @@ __device__ __forceinline__ int plane_z(const UnitGeo &U, int nz, int L) {
 }
 // The TMA boxes of one plane into ring slot `slot`: which & 1: kappa, x_{k-2} (slot_pp
 // >= 0), B (with the barrier's expected byte count for all boxes); which & 2: x_{k-1}.
-// (Issuing the first planes of the next pass early, during the grid reduction, split
-// 1 / 2 around the grid barrier, measured slower: profiles/r02_kernel_evolution.md.)
+
 template <int PM, int HM, int D>
 __device__ __forceinline__ void issue_boxes(const Geom &G, const UnitGeo &U, int z, int slot, int slot_prev, int slot_pp,
                                             int which) {
@@ -213,6 +212,39 @@ __device__ __forceinline__ void issue_boxes(const Geom &G, const UnitGeo &U, int
   }
   if (which & 2) tma_load4(dst, G.mapA, U.ox, U.oy, z, slot_prev, b);
 }
+// Pass-boundary prefetch (persistent loop, RC_PREFETCH): the producer issues the first
+// ring planes of this CTA's first unit of pass k while pass k-1's grid reduction runs:
+// which = 1 before the grid barrier (kappa, B and x_{k-2} boxes: independent of pass
+// k-1), which = 2 after it (x_{k-1} boxes: pass k-1's output).  Returns the number of
+// planes (identical in every thread); pre = that number in the producer thread.
+template <int PM, int HM, int D>
+__device__ __forceinline__ int preissue(const Geom &G, int k, int slot_prev, int slot_pp, unsigned nl, int which,
+                                        int &pre) {
+  using C = Cfg<PM, HM, D>;
+  if ((int)blockIdx.x >= G.ntx * G.nb * G.zsplit) return 0;
+  const UnitGeo U = unit_geo(G, blockIdx.x, k);
+  const int n = min(C::RS, U.nzc + 4);
+  if (threadIdx.x == RC3_PRODUCER) {
+    for (int q = 0; q < n; q++)
+      issue_boxes<PM, HM, D>(G, U, plane_z(U, G.nz, q - 2), (int)((nl + (unsigned)q) % (unsigned)C::RS), slot_prev,
+                             slot_pp, which);
+    pre = n;
+  }
+  return n;
+}
+// Planes pre-issued for a pass that does not take place (the Alg. 2 run ended): wait
+// for them in every thread (keeps the barrier phases in step) and advance the ring.
+template <int PM, int HM, int D>
+__device__ __forceinline__ void drain(unsigned &nl, int n) {
+  using C = Cfg<PM, HM, D>;
+  uint64_t *b = bars<PM, HM, D>(smem_base<PM, HM, D>());
+  for (int q = 0; q < n; q++) {
+    const unsigned c = nl + (unsigned)q;
+    mbar_wait(b + c % (unsigned)C::RS, (c / (unsigned)C::RS) & 1u);
+  }
+  nl += (unsigned)n;
+}
+
 // sum_f kappa_f (x_f - x_c) over the six faces of one point (x-, x+, y-, y+, z-, z+
 // in the lazy kernels' operand order).  RC3_SPLIT: two interleaved partial sums
 // (dependency depth 3 + 1 instead of 6), the same terms.
@@ -269,7 +301,7 @@ __host__ __device__ constexpr int role_of(int w) {
 // threads' stage-2 results are discarded), so stage 1 of plane L and stage 2 of plane
 // L-1 form ONE basic block the compiler can interleave.
 template <int PM, int HM, int D, bool UR, bool UPP>
-__device__ __forceinline__ void march(const Geom &G, const PassArgs<PM> &Q, double (&v)[5], unsigned &nl) {
+__device__ __forceinline__ void march(const Geom &G, const PassArgs<PM> &Q, double (&v)[5], unsigned &nl, int &pre) {
   using C = Cfg<PM, HM, D>;
   constexpr int W = C::W, SA = C::SA, SB = C::SB, SLOT = C::SLOT, RS = C::RS, EXP = C::EXP;
   double *const sm = smem_base<PM, HM, D>();
@@ -342,9 +374,11 @@ __device__ __forceinline__ void march(const Geom &G, const PassArgs<PM> &Q, doub
     const UnitGeo U = unit_geo(G, w, Q.k);
     const int z0 = U.z0;
     const int last = nzc + 1;  // logical planes -2 .. nzc+1
-    // producer: next plane to issue, its slot and physical plane
+    // producer: next plane to issue, its slot and physical plane; the first `pre` planes
+    // of the CTA's first unit may have been issued by preissue() already
     const bool prod = t == RC3_PRODUCER;
-    int iL = -2, isl = (int)(nl % (unsigned)RS), iz = plane_z(U, nz, -2);
+    const int npre = (prod && w == (int)blockIdx.x) ? pre : 0;
+    int iL = -2 + npre, isl = (int)((nl + (unsigned)npre) % (unsigned)RS), iz = plane_z(U, nz, -2 + npre);
     auto issue = [&]() {
       issue_boxes<PM, HM, D>(G, U, iz, isl, Q.slot_prev, UPP ? Q.slot_pp : -1, 3);
       iL++;
@@ -352,8 +386,10 @@ __device__ __forceinline__ void march(const Geom &G, const PassArgs<PM> &Q, doub
       iz = wrapz(iz + dz);
     };
     __syncthreads();  // the previous unit / pass is done with the ring and the exchange
-    if (prod)
-      for (int q = 0; q < RS && iL <= last; q++) issue();
+    if (prod) {
+      pre = 0;
+      for (int q = npre; q < RS && iL <= last; q++) issue();
+    }
     // consumer ring position: slot / parity of the plane to wait for next (plane -2)
     int wsl = (int)(nl % (unsigned)RS);
     unsigned wpar = (nl / (unsigned)RS) & 1u;
@@ -487,13 +523,13 @@ __device__ __forceinline__ void march(const Geom &G, const PassArgs<PM> &Q, doub
 }
 
 template <int PM, int HM, int D>
-__device__ __forceinline__ void body(const Geom &G, const PassArgs<PM> &Q, double (&v)[5], unsigned &nl) {
+__device__ __forceinline__ void body(const Geom &G, const PassArgs<PM> &Q, double (&v)[5], unsigned &nl, int &pre) {
   if (Q.slot_pp >= 0)
-    march<PM, HM, D, true, true>(G, Q, v, nl);
+    march<PM, HM, D, true, true>(G, Q, v, nl, pre);
   else if (Q.use_r)
-    march<PM, HM, D, true, false>(G, Q, v, nl);
+    march<PM, HM, D, true, false>(G, Q, v, nl, pre);
   else
-    march<PM, HM, D, false, false>(G, Q, v, nl);
+    march<PM, HM, D, false, false>(G, Q, v, nl, pre);
 }
 
 }  // namespace rc3

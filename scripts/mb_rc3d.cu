@@ -143,6 +143,7 @@ __global__ void __maxnreg__(200) k_mb(rc3::Geom G, rc3::PassArgs<PM> Q, double *
 #endif
   rc3::init<PM, HM, DD>(G);
   unsigned nl = 0;
+  int pre = 0;
   double v[5] = {0, 0, 0, 0, 0};
   __shared__ double red0[5][32];
   unsigned long long target = 0;
@@ -156,7 +157,7 @@ __global__ void __maxnreg__(200) k_mb(rc3::Geom G, rc3::PassArgs<PM> Q, double *
   for (int r = 0; r < reps; r++) {
     Q.k = r + 3;  // alternate the march direction like consecutive passes
     slots(r, Q.slot_prev, Q.slot_pp, Q.xout);
-    rc3::body<PM, HM, DD>(G, Q, v, nl);
+    rc3::body<PM, HM, DD>(G, Q, v, nl, pre);
 #if MB_GRID  // the persistent loop's pass boundary: block sums, grid barrier, (prefetch)
     for (int q = 0; q < 5; q++) {
       double x = v[q];
