@@ -76,13 +76,31 @@ def oracle_counts(idx):
     return None, None
 
 
-def cpu_sample(cfg, idx, n_kv=6):
-    """Oracle as it stands on the host cores (1 thread).  If one full oracle call of
-    this workload takes < 20 s (profiles/oracle_full_config<k>.json), time the full
-    call (median of up to 3).  Otherwise a bounded sample of the same workload:
-    Alg. 2 for n_kv Krylov vectors at full size from the real start vector, plus one
-    Pade exponential of a 129^2 H~ from the oracle's own Alg. 2 on the same-weights
-    48^3 grid, scaled to one call by the oracle's own full-size counts."""
+def host_cpu():
+    """CPU model and core count of the host (reported beside every oracle timing)."""
+    model = None
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"cpu_model": model or (os.uname().machine if hasattr(os, "uname") else "?"), "nproc": os.cpu_count()}
+
+
+def cpu_sample(cfg, idx, n_kv=4, proj_frac=16):
+    """Oracle as it stands on the host cores (1 thread).  If one full oracle call of this
+    workload takes < 20 s (profiles/oracle_full_config<k>.json), time the full call
+    (median of up to 3).  Otherwise a bounded sample of the same workload, every part
+    of a call measured at full size and scaled by the oracle's own full-size counts:
+      * Alg. 2: n_kv Krylov vectors from the real start vector;
+      * one Pade-13 exponential of a 129^2 H~ (the oracle's Alg. 2 on the same-weights
+        48^3 grid);
+      * Alg. 3's projection w = beta V f (the oracle's own loop, exported as or_project)
+        over 1/proj_frac of the rows of a full-size basis with 129 columns (the same
+        column stride N + p), times proj_frac, per projection, scaled by j/129, for every
+        accepted substep and every crossed output time of the oracle's trace."""
     from oracle import oracle as O
     from workloads import configs as W
 
@@ -95,8 +113,10 @@ def cpu_sample(cfg, idx, n_kv=6):
                     m_max=cfg["m_max"], iop_q=cfg["iop_q"])
             ts.append(time.perf_counter() - t0)
         v = float(np.median(ts)) * 1e3
-        return {"value": v, "unit": "ms/call", "cores": 1, "kind": "oracle",
-                "sample": f"full oracle call (Alg. 1-4, 1 thread), median of {len(ts)}"}
+        return dict({"value": v, "unit": "ms/call", "cores": 1, "kind": "oracle",
+                     "sample": f"full oracle call (Alg. 1-4, 1 thread), median of {len(ts)}"}, **host_cpu())
+    if st is None:
+        return None
     p, N = cfg["p"], cfg["N"]
     nu, mu = O.normalisation(cfg["u"])
     v0 = np.r_[cfg["u"][0], np.zeros(max(p - 1, 0)), [mu] if p else []]
@@ -115,16 +135,30 @@ def cpu_sample(cfg, idx, n_kv=6):
     t0 = time.perf_counter()
     O.expm(Ht, tau)
     t_exp = time.perf_counter() - t0
-    st, wall = oracle_counts(idx)
-    if st is None:
-        return None
-    est_ms = 1e3 * (t_kv * st["krylov_vectors"] + t_exp * st["expm_calls"])
-    return {"value": est_ms, "unit": "ms/call", "cores": 1, "kind": "oracle",
-            "sample": f"oracle Alg.2 {n_kv} Krylov vectors at full size ({t_kv*1e3:.1f} ms/KV) + one "
-                      f"{j+1}^2 Pade-13 expm ({t_exp*1e3:.1f} ms), scaled by the oracle's own full-size "
-                      f"counts ({st['krylov_vectors']} KVs, {st['expm_calls']} expm; GEMVs not counted, so a "
-                      f"lower bound)" + (f"; one measured full oracle call took {wall:.1f} s" if wall else ""),
-            "t_kv_ms": t_kv * 1e3, "t_expm_ms": t_exp * 1e3}
+    # projection sample: rows 0 .. N/proj_frac of a (N+p) x 129 column-major basis
+    ld, jc, rows = N + p, 129, N // proj_frac
+    Vb = np.empty(ld * jc)  # virtual; only the sampled rows are touched
+    for c in range(jc):
+        Vb[c * ld:c * ld + rows] = 1.0 / (c + 1)
+    f = np.linspace(1.0, 2.0, jc)
+    O.project(Vb, ld, rows, f)  # warm
+    t0 = time.perf_counter()
+    O.project(Vb, ld, rows, f)
+    t_proj = (time.perf_counter() - t0) * proj_frac
+    del Vb
+    tr = json.load(open(os.path.join(ROOT, "profiles", f"oracle_full_config{idx}.json"))).get("trace", [])
+    acc_j = [r["j"] for r in tr if r["accept"]]
+    n_cross = len(cfg["T"]) - 1
+    j_proj = acc_j + [max(acc_j) if acc_j else jc] * n_cross
+    t_gemv = sum(t_proj * jj / jc for jj in j_proj)
+    est_ms = 1e3 * (t_kv * st["krylov_vectors"] + t_exp * st["expm_calls"] + t_gemv)
+    return dict({"value": est_ms, "unit": "ms/call", "cores": 1, "kind": "oracle",
+                 "sample": f"oracle at full size, 1 thread: {n_kv} Krylov vectors ({t_kv*1e3:.0f} ms/KV), one {j+1}^2 "
+                           f"Pade-13 expm ({t_exp*1e3:.1f} ms), the Alg. 3 projection on 1/{proj_frac} of the rows of a "
+                           f"129-column basis ({t_proj:.1f} s per full projection); scaled by the oracle's own counts "
+                           f"({st['krylov_vectors']} KVs, {st['expm_calls']} expm, {len(j_proj)} projections)"
+                           + (f"; one measured full oracle call took {wall:.1f} s on the build host" if wall else ""),
+                 "t_kv_ms": t_kv * 1e3, "t_expm_ms": t_exp * 1e3, "t_proj_s": t_proj}, **host_cpu())
 
 
 class ClockSampler:
@@ -186,6 +220,43 @@ def bytes_per_pass(cfg):
     return W.algorithmic_bytes_per_pass(cfg)
 
 
+def secondary_config3(torch, dev, Kiops, W, peak, box_gbs, steps=10):
+    """BASELINE config 3 (2D Allen-Cahn Jacobian, 1024^2, p = 3), the other roofline
+    target of north_star, timed in the same process right after config 4: ms/call
+    (CUDA events, inputs resident) and the fused-pass roofline fraction (per-pass device
+    timer, algorithmic bytes).  Its 75 MB per-pass working set fits the 126 MB L2, so
+    the 'hbm' fraction is partly an L2 figure."""
+    c = W.make(3)
+    u = [torch.as_tensor(x).to(dev) for x in c["u"]]
+    k = Kiops(c["op"], c["p"], device=dev, tol=c["tol"], m_init=c["m_init"], m_min=c["m_min"], m_max=c["m_max"],
+              iop_q=c["iop_q"])
+    w = [torch.empty(c["N"], dtype=torch.float64, device=dev) for _ in c["T"]]
+    for _ in range(3):
+        k.apply(u, c["T"], w)
+    torch.cuda.synchronize()
+    tot = {"pass_ms": 0.0, "ctrl_ms": 0.0, "gemv_ms": 0.0, "passes": 0}
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(k.stream)
+    for _ in range(steps):
+        _, st = k.apply(u, c["T"], w)
+        for key in tot:
+            tot[key] += st[key]
+    e1.record(k.stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    k.close()
+    bpp = bytes_per_pass(c)
+    ach = bpp * tot["passes"] / (tot["pass_ms"] * 1e-3) / 1e9
+    return {"workload": c["name"], "value": ms, "unit": "ms/call", "steps": steps,
+            "passes_per_call": tot["passes"] / steps, "pass_us": 1e3 * tot["pass_ms"] / tot["passes"],
+            "device_ms": {"fused_pass": tot["pass_ms"] / steps, "controller": tot["ctrl_ms"] / steps,
+                          "gemv": tot["gemv_ms"] / steps},
+            "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                         "frac_of_box_copy": ach / box_gbs, "kernel": "k_inner_2d_lazy (fused IOP pass, persistent)",
+                         "algorithmic_bytes_per_pass": bpp,
+                         "note": "75 MB per-pass working set < 126 MB L2: partly an L2 figure (D10)"}}
+
+
 def run_reference(args):
     from workloads import configs as W
 
@@ -220,7 +291,8 @@ def main():
     ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--impl", default="kiops", choices=["kiops", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-secondary", action="store_true", help="skip the config-3 secondary line")
     ap.add_argument("--hostloop", action="store_true",
                     help="profiling only: same kernels, host-driven loop (ncu cannot see kernels in conditional graphs)")
     args = ap.parse_args()
@@ -283,12 +355,15 @@ def main():
     torch.cuda.synchronize()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
+    e2e_dev = 0.0
     e0.record(stream)
     for _ in range(args.e2e_steps):
-        k.apply_host(hu, cfg["T"], hw)
+        _, st2 = k.apply_host(hu, cfg["T"], hw)
+        e2e_dev += st2["pass_ms"] + st2["ctrl_ms"] + st2["gemv_ms"]
     e1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = max_over_ranks(e0.elapsed_time(e1) / args.e2e_steps, dist if world > 1 else None, dev)
+    e2e_dev /= args.e2e_steps
 
     bpp = bytes_per_pass(cfg)
     passes = totals["passes"] / args.steps
@@ -325,7 +400,9 @@ def main():
                                 "kv_per_s": per_step["krylov_vectors"] / (ms_step * 1e-3)}},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                     "kernel": {"stencil3d7": "k_inner_3d_lazyq (fused IOP pass, persistent inner loop)",
+                     "kernel": {"stencil3d7": ("k_inner_3d_lazyq (fused IOP pass, persistent inner loop)" if
+                                               os.environ.get("KIOPS_3D") == "lazy" else
+                                               "k_inner_3d_rc (fused IOP pass, recompute form, TMA-fed, persistent inner loop)"),
                                 "stencil2d5": "k_inner_2d_lazy (fused IOP pass, persistent inner loop)",
                                 "stencil1d3": "k_inner_2d_lazy (fused IOP pass, ny = 1, persistent inner loop)",
                                 "csr": "k_csr_form + k_sell_spmv (fused IOP pass)"}.get(cfg["op"]["kind"], "fused IOP pass"),
@@ -336,9 +413,17 @@ def main():
         "gpu_launches": int(round(launches_per_step * args.steps)),
         "e2e": {"value": e2e_ms / world, "unit": "ms/call",
                 "h2d_bytes_per_step": 8 * cfg["N"] * (cfg["p"] + 1),
-                "d2h_bytes_per_step": 8 * cfg["N"] * len(cfg["T"])},
+                "d2h_bytes_per_step": 8 * cfg["N"] * len(cfg["T"]),
+                "steps": args.e2e_steps,
+                "device_kernel_ms": e2e_dev,
+                "note": "kiops_apply_host: H2D of u_0..u_p from pinned memory, then the graph; outputs are pinned "
+                        "device-mapped host buffers written by the GEMV over the host link (no staging + D2H). "
+                        "device_kernel_ms = the in-graph %globaltimer sums (passes + controller + GEMV) of these "
+                        "calls; the rest of the call is the H2D copies, k_setup and the host-link output writes"},
         "clocks": clk.summary(local),
     }
+    if rank == 0 and args.config == 4 and not args.no_secondary:
+        line["secondary"] = secondary_config3(torch, dev, Kiops, W, peak, box_gbs)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             line["cpu_baseline"] = cpu_sample(cfg, args.config)

@@ -46,7 +46,8 @@ typedef struct kiops_ctx_s *kiops_ctx; /* opaque; created by kiops_create */
 typedef enum {
   KIOPS_OK = 0,
   KIOPS_ERR_INVALID_ARG = 1,    /* argument outside the domain of R21; nothing launched     */
-  KIOPS_ERR_UNSUPPORTED = 2,    /* valid for the method, not implemented here (e.g. q != 2) */
+  KIOPS_ERR_UNSUPPORTED = 2,    /* valid for the method, not implemented here (m_max > 128, */
+                                /* 3D planes >= 2^31 points, non-periodic stencils)          */
   KIOPS_ERR_CUDA = 3,           /* a CUDA call failed; text in kiops_last_error             */
   KIOPS_ERR_NO_CONVERGENCE = 4, /* > max_attempts attempts (R22); stats filled, w undefined */
   KIOPS_ERR_NONFINITE = 5,      /* NaN/Inf in a reduced dot, beta, H, eps or omega (R22)    */
@@ -145,8 +146,13 @@ kiops_status kiops_create(const kiops_operator_desc *op, int p, const kiops_opti
  *  w:      HOST array of n_out DEVICE pointers (N doubles each), written with
  *          w(T_l); must not alias any u[k] or each other.
  *  stats:  HOST, nullable.
- * Errors: INVALID_ARG (bad times, n_out outside 1..KIOPS_MAX_OUT, NULL pointers),
- * NO_CONVERGENCE / NONFINITE (stats filled, w undefined), CUDA. */
+ * Alignment: u[k] (and, at create, op->diag / op->kappa) must be 16-byte aligned for
+ * the periodic stencils with an even nx (1D/2D, and 3D with KIOPS_3D=lazy), whose
+ * passes read them as 16-byte pairs; a misaligned pointer is rejected with
+ * INVALID_ARG before any launch.  w and the CSR / padded-3D inputs have no alignment
+ * requirement beyond 8 bytes.
+ * Errors: INVALID_ARG (bad times, n_out outside 1..KIOPS_MAX_OUT, NULL or misaligned
+ * pointers), NO_CONVERGENCE / NONFINITE (stats filled, w undefined), CUDA. */
 kiops_status kiops_apply(kiops_ctx c, const double *const *u, const double *tau_out, int n_out,
                          double *const *w, kiops_stats *stats);
 
@@ -244,7 +250,8 @@ typedef struct kiops_epirk_s *kiops_epirk_ctx;
 kiops_status kiops_epirk_workspace_bytes(const kiops_rd_problem *pb, int scheme, const kiops_options *o,
                                          size_t *bytes);
 
-/* pb, o: HOST, copied.  h > 0: the constant step.  scheme: KIOPS_EPIRK4S3[A].
+/* pb, o: HOST, copied.  h > 0: the constant step.  scheme: KIOPS_EPIRK4S3,
+ * KIOPS_EPIRK4S3A (two grouped calls per step), KIOPS_EPIRK5P1, KIOPS_EXPRB5S3 (three).
  * o: the KIOPS options of both calls (tol, m_*, max_attempts; task1 and staging are
  * set internally).  workspace: DEVICE, 256-byte aligned, >= the queried bytes,
  * borrowed for the ctx's life.  Errors as kiops_create. */

@@ -394,6 +394,11 @@ static void project(int64_t N, int64_t ld, int j, const double *V, const double 
   }
 }
 
+/* the same projection, exported for the CPU-baseline timing sample (bench.py) */
+void or_project(int64_t N, int64_t ld, int j, const double *V, const double *f, double beta, double *w) {
+  project(N, ld, j, V, f, beta, w);
+}
+
 int or_kiops(const or_operator *op, int p, const double *const *u, int n_out, const double *T,
              double *const *w, const or_options *o, or_stats *st, or_trace_row *trace,
              int64_t trace_cap, int64_t *trace_len) {

@@ -106,6 +106,8 @@ int or_adapt(int happy, int accept, int j, int m, int m_min, int m_max, double t
 /* Alg. 1 + 3 + 4: w_l = sum_k T_l^k phi_k(T_l A) u_k for every output time.
  * u: p+1 input vectors u_0..u_p (N each).  T: n_out strictly increasing > 0.
  * w: n_out output vectors (N each).  trace may be NULL.                     */
+/* w(0:N) = beta V(0:N, 0:j) f(0:j), V column-major with leading dimension ld (Eq. 33) */
+void or_project(int64_t N, int64_t ld, int j, const double *V, const double *f, double beta, double *w);
 int or_kiops(const or_operator *op, int p, const double *const *u, int n_out,
              const double *T, double *const *w, const or_options *o, or_stats *st,
              or_trace_row *trace, int64_t trace_cap, int64_t *trace_len);

@@ -20,6 +20,8 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 SRC = os.path.join(HERE, "kiops_oracle.c")
 LIB = os.path.join(HERE, "libkiops_oracle.so")
+if os.environ.get("KIOPS_ORACLE_LIB"):  # mutation checks (scripts/oracle_mutations.py) load a scratch build
+    LIB = os.environ["KIOPS_ORACLE_LIB"]
 
 KIND = {"stencil1d3": 1, "stencil2d5": 2, "stencil3d7": 3, "csr": 4, "dense": 5}
 STATUS = {0: "OK", 1: "INVALID_ARG", 4: "NO_CONVERGENCE", 5: "NONFINITE", 6: "ALLOC"}
@@ -93,6 +95,7 @@ def lib():
         L.or_kiops.argtypes = [C.POINTER(_Op), C.c_int, C.POINTER(_dp), C.c_int, _dp,
                                C.POINTER(_dp), C.POINTER(_Opts), C.POINTER(_Stats),
                                C.POINTER(_Trace), C.c_int64, C.POINTER(C.c_int64)]
+        L.or_project.argtypes = [C.c_int64, C.c_int64, C.c_int, _dp, _dp, C.c_double, _dp]
         L.or_dense_phi_combination.argtypes = [C.POINTER(_Op), C.c_int, C.POINTER(_dp),
                                                C.c_double, _dp]
         _lib = L
@@ -200,6 +203,14 @@ def iop(op, u, nu, v0, m, q=2):
     j = lib().or_iop(op.ref, op.N, p, arr, float(nu), _ptr(v0), int(m), int(q), _ptr(V), _ptr(H),
                      C.byref(happy))
     return V.reshape((op.N + p, m + 1), order="F"), H.reshape((m + 1, m), order="F"), j, happy.value
+
+
+def project(V, ld, rows, f, beta=1.0):
+    """w = beta V(0:rows, 0:j) f on a column-major V (flat, leading dimension ld)."""
+    f = _f64(f)
+    w = np.empty(rows)
+    lib().or_project(int(rows), int(ld), len(f), _ptr(V), _ptr(f), float(beta), _ptr(w))
+    return w
 
 
 def adapt(happy, accept, j, m, m_min, m_max, tau, omega, t_now, t_end, hist_valid=0,

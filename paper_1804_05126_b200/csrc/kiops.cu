@@ -284,6 +284,7 @@ struct kiops_ctx_s {
   int forced_acc[KIOPS_MAX_FORCED];
   long long last_attempts = 0;
   int m_init_call = 0;           // kiops_set_m_init (0: options.m_init)
+  int align16 = 0;               // the chosen pass kernels read u, diag, kappa as 16-byte pairs
   void *fpass = nullptr;         // stencil pass kernel (NULL for CSR)
   void *finner = nullptr;        // persistent inner-loop kernel (inner.cuh), NULL if not used
   std::string err;
@@ -597,6 +598,17 @@ kiops_status kiops_create(const kiops_operator_desc *op, int p, const kiops_opti
     if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
     if (e != cudaSuccess) st = cuda_fail(c, e, "workspace init");
   }
+  // the lazy pair kernels (1D/2D with even nx, 3D lazy with even nx) read u, diag and kappa
+  // with 16-byte loads: a misaligned device pointer would fault (sticky CUDA error), so it
+  // is rejected here and in check_call instead (kiops.h, "alignment")
+  c->align16 = (o->iop_q == 2 && op->nx % 2 == 0 && !L.padded &&
+                ((op->kind == KIOPS_OP_STENCIL1D3 || op->kind == KIOPS_OP_STENCIL2D5) && p <= 4 ||
+                 (op->kind == KIOPS_OP_STENCIL3D7_VARKAPPA && p >= 1 && p <= 4)))
+                   ? 1 : 0;
+  if (st == KIOPS_OK && c->align16 && (((uintptr_t)op->diag & 15) || ((uintptr_t)op->kappa & 15))) {
+    c->err = "diag / kappa must be 16-byte aligned for this operator (even nx: 16-byte pair loads)";
+    st = KIOPS_ERR_INVALID_ARG;
+  }
   if (st == KIOPS_OK && L.padded) st = encode_tmaps(c);
   if (st == KIOPS_OK && op->kind == KIOPS_OP_CSR) {  // build the SELL-32 copy once
     std::vector<long long> off = sell_offsets(op);
@@ -634,8 +646,13 @@ static kiops_status check_call(kiops_ctx c, const double *const *u, const double
     }
     if (!w[l]) { c->err = "NULL output pointer"; return KIOPS_ERR_INVALID_ARG; }
   }
-  for (int k = 0; k <= c->p; k++)
+  for (int k = 0; k <= c->p; k++) {
     if (!u[k]) { c->err = "NULL input vector"; return KIOPS_ERR_INVALID_ARG; }
+    if (c->align16 && ((uintptr_t)u[k] & 15)) {  // 16-byte pair loads (kiops.h: alignment)
+      c->err = "input vectors must be 16-byte aligned for this operator (even nx: 16-byte pair loads)";
+      return KIOPS_ERR_INVALID_ARG;
+    }
+  }
   return KIOPS_OK;
 }
 

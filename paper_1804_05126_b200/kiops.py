@@ -227,7 +227,15 @@ class Kiops:
         T = [float(t) for t in T]
         if w is None:
             w = [torch.empty(self.N, dtype=torch.float64, device=self.device) for _ in T]
-        uarr = (C.c_void_p * (self.p + 1))(*[x.data_ptr() for x in u])
+        if len(u) != self.p + 1:
+            raise ValueError(f"need p + 1 = {self.p + 1} input vectors u_0..u_p, got {len(u)}")
+        dev_index = self.device.index if self.device.index is not None else torch.cuda.current_device()
+        for name, xs in (("u", u), ("w", w)):
+            for i, x in enumerate(xs):
+                if not isinstance(x, torch.Tensor) or x.dtype != torch.float64 or not x.is_contiguous() \
+                        or x.device.type != "cuda" or x.device.index != dev_index or x.numel() != self.N:
+                    raise ValueError(f"{name}[{i}] must be a contiguous float64 tensor of {self.N} elements on "
+                                     f"{self.device}")
         warr = (C.c_void_p * len(T))(*[x.data_ptr() for x in w])
         Tarr = (C.c_double * len(T))(*T)
         st = Stats()

@@ -20,9 +20,20 @@ t0 = time.time()
 w, st, tr, rc = O.kiops(c["op"], c["u"], c["T"], tol=c["tol"], m_init=c["m_init"], m_min=c["m_min"],
                         m_max=c["m_max"], iop_q=c["iop_q"])
 t_call = time.time() - t0
+cpu = platform.processor() or platform.machine()
+try:
+    cpu = next(ln.split(":", 1)[1].strip() for ln in open("/proc/cpuinfo") if ln.startswith("model name"))
+except (OSError, StopIteration):
+    pass
+SAMPLE_STRIDE = 257  # element-wise check of the GPU outputs at full size (tests/test_gpu_parity.py)
 out = {"config": c["name"], "status": rc, "wall_s": t_call, "gen_s": t_gen, "threads": 1,
-       "cpu": platform.processor() or platform.machine(), "nproc": os.cpu_count(), "stats": st,
-       "trace": tr, "out_norms": [float((x * x).sum() ** 0.5) for x in w]}
+       "cpu": cpu, "nproc": os.cpu_count(), "stats": st,
+       "trace": tr, "out_norms": [float((x * x).sum() ** 0.5) for x in w],
+       "sample_stride": SAMPLE_STRIDE, "sample_file": f"oracle_full_config{idx}_sample.npz"}
 os.makedirs("profiles", exist_ok=True)
+import numpy as np  # noqa: E402
+
+np.savez_compressed(f"profiles/oracle_full_config{idx}_sample.npz",
+                    **{f"w{l}": np.asarray(x)[::SAMPLE_STRIDE] for l, x in enumerate(w)})
 json.dump(out, open(f"profiles/oracle_full_config{idx}.json", "w"), indent=1)
 print(json.dumps({k: out[k] for k in ("config", "status", "wall_s", "stats")}))

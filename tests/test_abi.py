@@ -80,8 +80,11 @@ def test_workspace_bytes_layout(L):
     # full-size config 4 (descriptor only): the basis dominates, (m_max+1) vectors of N doubles
     d.nx = d.ny = d.nz = 256
     assert L.kiops_workspace_bytes(C.byref(d), 2, C.byref(o), C.byref(nb)) == 0
-    # basis (m_max + 1 vectors) + the r_k ping-pong pair + small state
-    assert 131 * 8 * 256 ** 3 <= nb.value <= 131 * 8 * 256 ** 3 + 64 * 2 ** 20
+    # padded mode (3D recompute pass): (m_max + 1) basis slots + the p
+    # copies of B's columns + the kappa copy, each a ghost-padded 260 x 260 x 256 grid
+    # (rounded to 32 doubles), + small state; no r_k buffers
+    vec = (260 * 260 * 256 + 31) // 32 * 32 * 8
+    assert (129 + 2 + 1) * vec <= nb.value <= (129 + 2 + 1) * vec + 64 * 2 ** 20
     assert small < nb.value
 
 

@@ -63,3 +63,15 @@ def test_ring_kernels_static_shared_is_128_aligned():
     # padded to a multiple of 128 bytes by that alignment
     for fn, (_, _, shared) in _find(_res_usage(), r"k_inner_(2d|3d)_lazy").items():
         assert shared % 128 == 0, (fn, shared)
+
+
+def test_recompute_3d_pass_no_spills_and_tma():
+    # k_inner_3d_rc<PM> (config 4's pass since round 2): 10 warps per CTA, 168-register cap
+    # (3 warps on two of the four schedulers); no spill stack, and its loads are TMA
+    # tensor-map loads (UTMALDG) with mbarrier completion, no cp.async (LDGSTS)
+    for fn, (reg, stack, _) in _find(_res_usage(), r"k_inner_3d_rcILi\dE").items():
+        assert reg <= 168, (fn, reg)
+        assert stack == 0, (fn, stack)
+    out = subprocess.run([CUOBJDUMP, "-sass", "-fun", "_Z13k_inner_3d_rcILi2EEv7KParams", LIB], capture_output=True,
+                         text=True).stdout
+    assert "UTMALDG" in out and "SYNCS" in out and "LDGSTS" not in out

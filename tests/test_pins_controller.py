@@ -66,3 +66,36 @@ def test_property_suite_clipping():
             assert tn == min(tau, rem)
             if not accept:
                 assert mn >= j or mn == m_max
+
+
+def test_golden_eq43_branch_discriminates():
+    """The Eq. 43 order estimate (same j, different tau; R4) is reached by the golden
+    cases in BOTH gamma branches with an unclipped tau_new, so an inverted Eq. 43, a
+    missing ord >= 1 floor or a missing j/4 fallback changes tau_new (hand-evaluated
+    values in tests/golden/paper_examples.json, P:486-496)."""
+    cases = [ex for ex in G["adapt"] if ex["hist"] and ex["hist"]["j_old"] == ex["j"] and ex["hist"]["tau_old"] != ex["tau"]]
+    assert len(cases) >= 5
+    branches = set()
+    for ex in cases:
+        h = ex["hist"]
+        tn, mn = O.adapt(ex["happy"], ex["accept"], ex["j"], ex["m"], ex["m_min"], ex["m_max"], ex["tau"], ex["omega"],
+                         ex["t_now"], ex["t_end"], 1, h["omega_old"], h["tau_old"], h["j_old"])
+        assert mn == ex["m_new"] and abs(tn - ex["tau_new"]) <= 4e-15 * ex["tau_new"], ex["note"]
+        # the value is strictly inside the clip interval, i.e. it depends on the exponent
+        lo, hi = ex["tau"] / 5, 5 * ex["tau"]
+        assert lo < tn < hi, ex["note"]
+        branches.add(ex["omega"] > 1.4)
+    assert branches == {True, False}
+
+
+def test_golden_r3_breakdown_threshold():
+    """R3 (Alg. 2 l.12 "s ~ 0"): happy breakdown iff s <= max(1e-12 c, 1e-14),
+    on nonzero residuals just below / above the relative threshold and the floor."""
+    for ex in G["r3_threshold"]:
+        a, dl = ex["a"], ex["delta"]
+        A = np.diag([a, a * (1.0 + dl)])
+        x = np.array([1.0, 1.0])
+        V, H, j, happy = O.iop({"kind": "dense", "nx": 2, "dense": A}, [x], 1.0, x, 1, 2)
+        assert bool(happy) == ex["happy_at_j1"], ex["note"]
+        if not happy:  # the stored subdiagonal is the residual norm s = a delta / 2
+            assert abs(H[1, 0] - a * dl / 2) <= 1e-3 * a * dl
