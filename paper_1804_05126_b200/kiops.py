@@ -236,6 +236,7 @@ class Kiops:
                         or x.device.type != "cuda" or x.device.index != dev_index or x.numel() != self.N:
                     raise ValueError(f"{name}[{i}] must be a contiguous float64 tensor of {self.N} elements on "
                                      f"{self.device}")
+        uarr = (C.c_void_p * (self.p + 1))(*[x.data_ptr() for x in u])
         warr = (C.c_void_p * len(T))(*[x.data_ptr() for x in w])
         Tarr = (C.c_double * len(T))(*T)
         st = Stats()
