@@ -960,6 +960,9 @@ __device__ __forceinline__ void gemv_padded(const KParams &P, int j, int nout, c
       const int yp = (int)(row - z * Yp);
       const bool inner = xp >= 2 && xp < nx + 2 && yp >= 2 && yp < ny + 2;
       const long long ui = (xp - 2) + (long long)nx * ((yp - 2) + (long long)ny * z);
+#ifdef KIOPS_BOUNDS_CHECK
+      assert(xp % 2 == 0 && (!inner || (ui >= 0 && ui + 1 < P.N)) && 2 * q + 1 < P.Np);
+#endif
 #pragma unroll
       for (int o = 0; o < GEMV_OCHUNK; o++)
         if (o < no) {

@@ -6,6 +6,10 @@
 
 #include "../../include/kiops.h"
 
+#ifdef KIOPS_BOUNDS_CHECK  // debug builds: device-side index asserts (rc3d.cuh, pad_copies, gemv_padded)
+#include <cassert>
+#endif
+
 #define KMAXP KIOPS_MAX_P
 #define KMAXO KIOPS_MAX_OUT
 #define KMAXM KIOPS_MAX_M

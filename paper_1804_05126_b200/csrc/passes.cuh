@@ -60,6 +60,9 @@ __device__ __forceinline__ void pad_copies(const KParams &P) {
     x = x < 0 ? x + nx : (x >= nx ? x - nx : x);
     y = y < 0 ? y + ny : (y >= ny ? y - ny : y);
     const long long src = x + (long long)nx * (y + (long long)ny * z);
+#ifdef KIOPS_BOUNDS_CHECK
+    assert(x >= 0 && x < nx && y >= 0 && y < ny && src < P.N);
+#endif
     P.V[i] = __ldg(call->u[0] + src);
     for (int c = 0; c < p; c++) P.V[(size_t)(P.slot_B + c) * ldN + i] = __ldg(call->u[p - c] + src);
     P.V[(size_t)P.slot_kappa * ldN + i] = __ldg(P.kappa + src);

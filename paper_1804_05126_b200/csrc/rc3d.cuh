@@ -45,6 +45,16 @@
 
 #include <type_traits>
 
+// KIOPS_BOUNDS_CHECK (debug builds, scripts/sanitize_run.py): device asserts on every
+// shared-memory offset, ring slot, TMA coordinate and global store offset of the pass
+// (compute-sanitizer is not available on this GPU pool).
+#ifdef KIOPS_BOUNDS_CHECK
+#include <cassert>
+#define RC3_ASSERT(c) assert(c)
+#else
+#define RC3_ASSERT(c) do { } while (0)
+#endif
+
 #ifndef RC3_PRODUCER
 #define RC3_PRODUCER 0  // the thread that issues the TMA boxes
 #endif
@@ -353,6 +363,10 @@ __device__ __forceinline__ void march(const Geom &G, const PassArgs<PM> &Q, doub
     const int qx = s1 ? px : 1, qy = s1 ? py : 1;
     const int offA = (qy + 1) * W + 2 * qx, offB = qy * W + 2 * qx;
     const int ew = s1 ? qy * 34 + qx : EXP, er = s2 ? ew : 35;
+    RC3_ASSERT(offA - W >= 0 && offA - 1 >= 0 && offA + W + 1 < C::RA * W);  // halo-2 box: x +-1, y +-1
+    RC3_ASSERT(offB >= 0 && offB + 1 < C::RB * W);
+    RC3_ASSERT(ew >= 0 && ew < EXP + 32 && er - 34 >= 0 && er + 34 < EXP && er - 1 >= 0);
+    RC3_ASSERT(qx <= 33 && qy <= HM + 1);
     // x-neighbour values from the neighbouring lanes when they hold the adjacent pair
     const int key = s1 ? py * 64 + px : -1000 - t;
     const int kl = __shfl_up_sync(0xffffffffu, key, 1), kr = __shfl_down_sync(0xffffffffu, key, 1);
@@ -380,6 +394,7 @@ __device__ __forceinline__ void march(const Geom &G, const PassArgs<PM> &Q, doub
     const int npre = (prod && w == (int)blockIdx.x) ? pre : 0;
     int iL = -2 + npre, isl = (int)((nl + (unsigned)npre) % (unsigned)RS), iz = plane_z(U, nz, -2 + npre);
     auto issue = [&]() {
+      RC3_ASSERT(iz >= 0 && iz < nz && isl >= 0 && isl < RS && iL >= -2 && iL <= last);
       issue_boxes<PM, HM, D>(G, U, iz, isl, Q.slot_prev, UPP ? Q.slot_pp : -1, 3);
       iL++;
       isl = isl + 1 == RS ? 0 : isl + 1;
@@ -487,6 +502,8 @@ __device__ __forceinline__ void march(const Geom &G, const PassArgs<PM> &Q, doub
           v0 += d0; v1 += d1; v2 += d2; v3 += d3; v4 += d4;
         }
         if (st) {
+          RC3_ASSERT(zo >= 0 && zo < nz && o0 >= 0 && o0 + 1 < plane && og0 + 1 < plane && og1 + 1 < plane &&
+                     og2 + 1 < plane);
           double *xo = Q.xout + (long long)zo * plane;
           *reinterpret_cast<double2 *>(xo + o0) = c0;
           if (og0 >= 0) *reinterpret_cast<double2 *>(xo + og0) = c0;
