@@ -263,6 +263,32 @@ kiops_status kiops_epirk_create(const kiops_rd_problem *pb, int scheme, double h
  * failure aborts with its status (the step index is in kiops_epirk_last_error). */
 kiops_status kiops_epirk_step(kiops_epirk_ctx ctx, double *u, int nsteps, kiops_epirk_stats *stats);
 
+/* Per-call decision history of the last kiops_epirk_step (TEST / diagnostics hook; off by
+ * default).  With kiops_epirk_record_history(ctx, 1), every KIOPS call of a step appends
+ * one record: its step index (0-based within the last kiops_epirk_step), call index
+ * (0..2), the call's counts and final m (the next call's warm start, reading E1), and the
+ * Krylov size j, acceptance, omega and m_new of its first KIOPS_EPIRK_HIST_ATTEMPTS attempts (from
+ * kiops_get_trace of the call's context right after it; the call has synchronised the
+ * stream already).  kiops_epirk_history copies up to `cap` records into buf (HOST) and
+ * sets *rows to the number available. */
+#define KIOPS_EPIRK_HIST_ATTEMPTS 64
+typedef struct {
+  int32_t step, call, final_m, n_attempts;
+  int64_t krylov_vectors, substeps, rejections;
+  int16_t j[KIOPS_EPIRK_HIST_ATTEMPTS];
+  int16_t m_new[KIOPS_EPIRK_HIST_ATTEMPTS];
+  int8_t accept[KIOPS_EPIRK_HIST_ATTEMPTS];
+  double omega[KIOPS_EPIRK_HIST_ATTEMPTS];  /* Eq. 39 of each attempt */
+} kiops_epirk_call_record;
+kiops_status kiops_epirk_record_history(kiops_epirk_ctx ctx, int on);
+/* TEST HOOK (trace replay, R26): the forced schedule (tau_i, m_i, accept_i), i < n, of
+ * call `call` (0..2) of step `step` (0-based within the next kiops_epirk_step), applied
+ * with kiops_set_forced_schedule to that call only.  n = 0 with step = -1 clears every
+ * schedule.  HOST arrays, copied. */
+kiops_status kiops_epirk_set_forced_schedule(kiops_epirk_ctx ctx, int step, int call, const double *tau,
+                                            const int32_t *m, const int32_t *accept, int n);
+kiops_status kiops_epirk_history(kiops_epirk_ctx ctx, kiops_epirk_call_record *buf, int64_t cap, int64_t *rows);
+
 kiops_status kiops_epirk_destroy(kiops_epirk_ctx ctx);
 const char *kiops_epirk_last_error(kiops_epirk_ctx ctx);
 

@@ -170,9 +170,10 @@ def step(prob, scheme, yn, h, tol=1e-12, m_hint=(10, 10), m_max=128):
     zero = np.zeros_like(yn)
     # call 1 (Task I): phi_1(T h J) h f at both nodes, T ascending, scaled by 1/T
     T1 = np.array(sorted((ca, cb)))
-    w1, s1, _, rc = O.kiops(op, [zero, b1], T1, tol=tol, m_init=m_hint[0], m_min=min(10, m_hint[0]),
-                            m_max=m_max, task1=1)
+    w1, s1, tr1, rc = O.kiops(op, [zero, b1], T1, tol=tol, m_init=m_hint[0], m_min=min(10, m_hint[0]),
+                              m_max=m_max, task1=1)
     assert rc == "OK", rc
+    s1["trace"] = tr1  # the call's decision trace (GPU parity compares it call by call)
     phi = {T1[0]: w1[0], T1[1]: w1[1]}
     U2 = yn + ca * phi[ca]
     U3 = yn + cb * phi[cb]
@@ -180,9 +181,10 @@ def step(prob, scheme, yn, h, tol=1e-12, m_hint=(10, 10), m_max=128):
     r3 = remainder(prob, yn, fn, U3)
     b3, b4 = final_b34(scheme, h, r2, r3)
     # call 2 (Task II at tau = 1): phi_1 b1 + phi_3 b3 + phi_4 b4 (b0 = b2 = 0)
-    w2, s2, _, rc = O.kiops(op, [zero, b1, zero, b3, b4], np.array([1.0]), tol=tol, m_init=m_hint[1],
-                            m_min=min(10, m_hint[1]), m_max=m_max)
+    w2, s2, tr2, rc = O.kiops(op, [zero, b1, zero, b3, b4], np.array([1.0]), tol=tol, m_init=m_hint[1],
+                              m_min=min(10, m_hint[1]), m_max=m_max)
     assert rc == "OK", rc
+    s2["trace"] = tr2
     return yn + w2[0], (s1["final_m"], s2["final_m"]), [s1, s2]
 
 
@@ -191,9 +193,10 @@ def _task1(op, p, b, T, tol, m, m_max):
     call with u_p = b, all other u_k = 0, and the 1/T^p scaling (Alg. 1 l.31-35)."""
     zero = np.zeros_like(b)
     u = [zero] * p + [b]
-    w, st, _, rc = O.kiops(op, u, np.asarray(T, dtype=np.float64), tol=tol, m_init=m, m_min=min(10, m),
-                           m_max=m_max, task1=1)
+    w, st, tr, rc = O.kiops(op, u, np.asarray(T, dtype=np.float64), tol=tol, m_init=m, m_min=min(10, m),
+                            m_max=m_max, task1=1)
     assert rc == "OK", rc
+    st["trace"] = tr
     return w, st
 
 
@@ -231,9 +234,10 @@ def step5(prob, scheme, yn, h, tol=1e-12, m_hint=(10, 10, 10), m_max=128):
         r3 = remainder(prob, yn, fn, U3)
         b3 = 18.0 * h * r2 - (250.0 / 81.0) * h * r3
         b4 = -60.0 * h * r2 + (500.0 / 27.0) * h * r3
-        w3, s3, _, rc = O.kiops(op, [zero, b1, zero, b3, b4], np.array([1.0]), tol=tol, m_init=m_hint[2],
-                                m_min=min(10, m_hint[2]), m_max=m_max)
+        w3, s3, tr3, rc = O.kiops(op, [zero, b1, zero, b3, b4], np.array([1.0]), tol=tol, m_init=m_hint[2],
+                                  m_min=min(10, m_hint[2]), m_max=m_max)
         assert rc == "OK", rc
+        s3["trace"] = tr3
         y = yn + w3[0]
     else:
         raise ValueError(scheme)
@@ -247,7 +251,9 @@ def integrate(prob, scheme, y0, t0, t1, nsteps, tol=1e-12):
     five = scheme in SCHEMES5
     m = (10, 10, 10) if five else (10, 10)
     kv = 0
-    for _ in range(nsteps):
+    calls = []  # per step, per call: counts, final m and the decision trace
+    for n in range(nsteps):
         y, m, st = (step5 if five else step)(prob, scheme, y, h, tol=tol, m_hint=m)
         kv += sum(s["krylov_vectors"] for s in st)
-    return y, {"krylov_vectors": kv, "final_m": m}
+        calls += [dict(s, step=n, call=c) for c, s in enumerate(st)]
+    return y, {"krylov_vectors": kv, "final_m": m, "calls": calls}

@@ -147,6 +147,14 @@ struct kiops_epirk_s {
   double *d = nullptr, *b1 = nullptr, *zero = nullptr, *o1[3] = {}, *o2[2] = {}, *o3 = nullptr, *t1 = nullptr,
          *t2 = nullptr;
   int m[3] = {0, 0, 0};          // warm start of calls 1-3 (Sec. 3.6, reading E1)
+  bool record = false;           // kiops_epirk_record_history
+  struct Forced {
+    int step, call;
+    std::vector<double> tau;
+    std::vector<int32_t> m, acc;
+  };
+  std::vector<Forced> forced;    // kiops_epirk_set_forced_schedule (test hook)
+  std::vector<kiops_epirk_call_record> hist;  // per-call records of the last kiops_epirk_step
   std::string err;
 };
 
@@ -253,12 +261,47 @@ kiops_status ep_call(kiops_epirk_ctx e, kiops_ctx k, int call, int step, const d
                      int n_out, double *const *w, kiops_epirk_stats *acc) {
   kiops_stats st{};
   kiops_set_m_init(k, e->m[call]);
+  {  // test hook: replay a forced schedule on this call, else free-running
+    const kiops_epirk_s::Forced *f = nullptr;
+    for (const auto &x : e->forced)
+      if (x.step == step && x.call == call) f = &x;
+    const kiops_status fs = f ? kiops_set_forced_schedule(k, f->tau.data(), f->m.data(), f->acc.data(), (int)f->tau.size())
+                              : kiops_set_forced_schedule(k, nullptr, nullptr, nullptr, 0);
+    if (fs != KIOPS_OK) {
+      e->err = "forced schedule rejected";
+      return fs;
+    }
+  }
   const kiops_status s = kiops_apply(k, u, T, n_out, w, &st);
   if (s != KIOPS_OK) {
     e->err = "step " + std::to_string(step) + ", call " + std::to_string(call + 1) + ": " + kiops_last_error(k);
     return s;
   }
   e->m[call] = st.final_m;
+  if (e->record) {  // the decision history of this call (kiops_apply has synchronised)
+    kiops_epirk_call_record r{};
+    r.step = step;
+    r.call = call;
+    r.final_m = st.final_m;
+    r.krylov_vectors = st.krylov_vectors;
+    r.substeps = st.substeps;
+    r.rejections = st.rejections;
+    kiops_trace_row tr[KIOPS_EPIRK_HIST_ATTEMPTS];
+    int64_t rows = 0;
+    const kiops_status ts = kiops_get_trace(k, tr, sizeof(tr), &rows);
+    if (ts != KIOPS_OK) {
+      e->err = "history: kiops_get_trace failed";
+      return ts;
+    }
+    r.n_attempts = (int32_t)rows;
+    for (int64_t a = 0; a < rows && a < KIOPS_EPIRK_HIST_ATTEMPTS; a++) {
+      r.j[a] = (int16_t)tr[a].j;
+      r.m_new[a] = (int16_t)tr[a].m_new;
+      r.accept[a] = (int8_t)tr[a].accept;
+      r.omega[a] = tr[a].omega;
+    }
+    e->hist.push_back(r);
+  }
   acc->krylov_vectors += st.krylov_vectors;
   acc->passes += st.passes;
   acc->substeps += st.substeps;
@@ -274,6 +317,7 @@ kiops_status kiops_epirk_step(kiops_epirk_ctx e, double *u, int nsteps, kiops_ep
   const long long N = e->q.nx * e->q.ny;
   const int grid = (int)std::min<long long>((N + 255) / 256, SM_COUNT_HINT * 8);
   kiops_epirk_stats acc{};
+  e->hist.clear();
   const double *z = e->zero;
 #define EP_LAUNCHED(name) \
   if (cudaGetLastError() != cudaSuccess) { e->err = name " launch"; return KIOPS_ERR_CUDA; }
@@ -331,6 +375,35 @@ kiops_status kiops_epirk_step(kiops_epirk_ctx e, double *u, int nsteps, kiops_ep
   if (ce != cudaSuccess) { e->err = cudaGetErrorString(ce); return KIOPS_ERR_CUDA; }
   for (int i = 0; i < 3; i++) acc.final_m[i] = e->m[i];
   if (stats) *stats = acc;
+  return KIOPS_OK;
+}
+
+kiops_status kiops_epirk_record_history(kiops_epirk_ctx e, int on) {
+  if (!e) return KIOPS_ERR_INVALID_ARG;
+  e->record = on != 0;
+  return KIOPS_OK;
+}
+
+kiops_status kiops_epirk_set_forced_schedule(kiops_epirk_ctx e, int step, int call, const double *tau,
+                                            const int32_t *m, const int32_t *accept, int n) {
+  if (!e) return KIOPS_ERR_INVALID_ARG;
+  if (n == 0 && step < 0) {
+    e->forced.clear();
+    return KIOPS_OK;
+  }
+  if (step < 0 || call < 0 || call > 2 || n < 1 || n > KIOPS_MAX_FORCED || !tau || !m) return KIOPS_ERR_INVALID_ARG;
+  kiops_epirk_s::Forced f{step, call, std::vector<double>(tau, tau + n), std::vector<int32_t>(m, m + n),
+                          std::vector<int32_t>(n, 1)};
+  if (accept)
+    for (int i = 0; i < n; i++) f.acc[i] = accept[i] != 0;
+  e->forced.push_back(f);
+  return KIOPS_OK;
+}
+
+kiops_status kiops_epirk_history(kiops_epirk_ctx e, kiops_epirk_call_record *buf, int64_t cap, int64_t *rows) {
+  if (!e || !rows || cap < 0 || (cap > 0 && !buf)) return KIOPS_ERR_INVALID_ARG;
+  *rows = (int64_t)e->hist.size();
+  for (int64_t i = 0; i < cap && i < *rows; i++) buf[i] = e->hist[(size_t)i];
   return KIOPS_OK;
 }
 

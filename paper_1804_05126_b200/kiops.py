@@ -68,6 +68,16 @@ class EpirkStats(C.Structure):
                 ("final_m", C.c_int32 * 3), ("kiops_ms", C.c_double)]
 
 
+EPIRK_HIST_ATTEMPTS = 64
+
+
+class EpirkCallRecord(C.Structure):
+    _fields_ = [("step", C.c_int32), ("call", C.c_int32), ("final_m", C.c_int32), ("n_attempts", C.c_int32),
+                ("krylov_vectors", C.c_int64), ("substeps", C.c_int64), ("rejections", C.c_int64),
+                ("j", C.c_int16 * EPIRK_HIST_ATTEMPTS), ("m_new", C.c_int16 * EPIRK_HIST_ATTEMPTS),
+                ("accept", C.c_int8 * EPIRK_HIST_ATTEMPTS), ("omega", C.c_double * EPIRK_HIST_ATTEMPTS)]
+
+
 EPIRK_SCHEMES = {"epirk4s3": 1, "epirk4s3a": 2, "epirk5p1": 3, "exprb5s3": 4}
 
 _lib = None
@@ -100,6 +110,10 @@ def lib():
         L.kiops_epirk_create.argtypes = [C.POINTER(RDProblem), C.c_int, C.c_double, C.POINTER(Options), C.c_void_p,
                                          C.c_void_p, C.c_size_t, C.POINTER(C.c_void_p)]
         L.kiops_epirk_step.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.POINTER(EpirkStats)]
+        L.kiops_epirk_record_history.argtypes = [C.c_void_p, C.c_int]
+        L.kiops_epirk_history.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.POINTER(C.c_int64)]
+        L.kiops_epirk_set_forced_schedule.argtypes = [C.c_void_p, C.c_int, C.c_int, _dp, C.POINTER(C.c_int32),
+                                                      C.POINTER(C.c_int32), C.c_int]
         L.kiops_epirk_destroy.argtypes = [C.c_void_p]
         L.kiops_epirk_last_error.argtypes = [C.c_void_p]
         L.kiops_epirk_last_error.restype = C.c_char_p
@@ -111,6 +125,7 @@ def lib():
         for name in ("kiops_workspace_bytes", "kiops_create", "kiops_apply", "kiops_apply_host", "kiops_apply_hostloop",
                      "kiops_get_trace", "kiops_set_m_init", "kiops_set_forced_schedule", "kiops_debug_basis",
                      "kiops_destroy", "kiops_epirk_workspace_bytes", "kiops_epirk_create", "kiops_epirk_step",
+                     "kiops_epirk_record_history", "kiops_epirk_history", "kiops_epirk_set_forced_schedule",
                      "kiops_epirk_destroy"):
             getattr(L, name).restype = C.c_int
         _lib = L
@@ -335,6 +350,42 @@ class KiopsEpirk:
             raise KiopsError(s, f"kiops_epirk_step: {msg.decode() if msg else ''}")
         out = {k: getattr(st, k) for k, _ in EpirkStats._fields_ if k != "final_m"}
         out["final_m"] = tuple(st.final_m[i] for i in range(3 if self.scheme in ("epirk5p1", "exprb5s3") else 2))
+        return out
+
+    def record_history(self, on=True):
+        s = lib().kiops_epirk_record_history(self.ctx, 1 if on else 0)
+        if s != 0:
+            raise KiopsError(s, "kiops_epirk_record_history")
+
+    def set_forced_schedules(self, calls):
+        """Test hook (trace replay): calls = iterable of (step, call, [(tau, m, accept), ...])
+        for the next step(); an empty iterable clears every schedule."""
+        lib().kiops_epirk_set_forced_schedule(self.ctx, -1, 0, None, None, None, 0)
+        for step, call, sched in calls:
+            n = len(sched)
+            tau = (C.c_double * n)(*[float(e[0]) for e in sched])
+            m = (C.c_int32 * n)(*[int(e[1]) for e in sched])
+            acc = (C.c_int32 * n)(*[int(e[2]) for e in sched])
+            s = lib().kiops_epirk_set_forced_schedule(self.ctx, int(step), int(call), tau, m, acc, n)
+            if s != 0:
+                raise KiopsError(s, "kiops_epirk_set_forced_schedule")
+
+    def history(self):
+        """Per-call records of the last step() (record_history(True) first): dicts with
+        step, call, final_m, krylov_vectors, substeps, rejections, attempts [(j, accept)]."""
+        rows = C.c_int64(0)
+        lib().kiops_epirk_history(self.ctx, None, 0, C.byref(rows))
+        buf = (EpirkCallRecord * max(1, rows.value))()
+        s = lib().kiops_epirk_history(self.ctx, buf, rows.value, C.byref(rows))
+        if s != 0:
+            raise KiopsError(s, "kiops_epirk_history")
+        out = []
+        for r in buf[:rows.value]:
+            n = min(r.n_attempts, EPIRK_HIST_ATTEMPTS)
+            out.append({"step": r.step, "call": r.call, "final_m": r.final_m, "krylov_vectors": r.krylov_vectors,
+                        "substeps": r.substeps, "rejections": r.rejections, "n_attempts": r.n_attempts,
+                        "attempts": [(r.j[a], r.accept[a]) for a in range(n)],
+                        "m_new": [r.m_new[a] for a in range(n)], "omega": [r.omega[a] for a in range(n)]})
         return out
 
     def close(self):
