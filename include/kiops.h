@@ -81,7 +81,7 @@ typedef struct {
 
 /* Alg. 1 inputs plus the IOP window.  Defaults (kiops_options_default):
  * tol 1e-7, m_init 10, m_min 10, m_max 128, iop_q 2, task1 0, max_attempts 10000,
- * host_staging 0, max_outputs 4. */
+ * host_staging 0, max_outputs 4, corrected 0. */
 typedef struct {
   double tol;             /* Eq. 39 tolerance (absolute, 2-norm of the scaled augmented vector, R18) */
   int32_t m_init, m_min, m_max; /* 1 <= m_min <= m_max <= KIOPS_MAX_M                   */
@@ -91,6 +91,9 @@ typedef struct {
   int64_t max_attempts;   /* accepted + rejected attempts before KIOPS_ERR_NO_CONVERGENCE */
   int32_t host_staging;   /* 1 => workspace also holds device staging for kiops_apply_host */
   int32_t max_outputs;    /* largest n_out kiops_apply_host will be called with (staging)  */
+  int32_t corrected;      /* 1 => Saad's corrected scheme [46]: each output update adds
+                           * beta h_{j+1,j} F(j, j+1) v_{j+1} (v_{j+1}: the last basis vector of
+                           * Alg. 2); decisions (eps, omega, Alg. 4) unchanged.  Default 0 */
 } kiops_options;
 
 /* Statistics of one kiops_apply. */

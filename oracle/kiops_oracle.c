@@ -519,18 +519,31 @@ int or_kiops(const or_operator *op, int p, const double *const *u, int n_out, co
       int n_tau = 0;
       for (int k = l; k < n_out; k++)
         if (fabs(T[k]) < fabs(T_next)) n_tau++; /* Alg. 3 l.6, strict (R16), all tasks (R15) */
+      /* Saad's corrected scheme [46] (option): w = beta V_{j+1} exp(tau Hbar) e_1,
+       * Hbar = [[H_j, 0], [h_{j+1,j} e_j^T, 0]], whose entry (j+1, 1) is h_{j+1,j} tau
+       * e_j^T phi_1(tau H_j) e_1 = h_{j+1,j} F(j, j+1) of exp(tau H~) (Eq. 38): one more
+       * basis vector, v_{j+1}, in the projection.  (No v_{j+1} after a happy breakdown.) */
+      const int corr = o->corrected && !happy;
+      const int jc = corr ? j + 1 : j;
       for (int k = 0; k < n_tau; k++) {
         const double tt = T[l + k] - T_now;              /* l.13 */
-        for (int c = 0; c < j; c++)                       /* H(1:j,1:j) */
-          for (int r = 0; r < j; r++) Ht[CM(r, c, j)] = H[CM(r, c, ldh)];
-        if (or_expm(j, Ht, tt, F2, NULL) != 0) { rc = OR_ERR_NONFINITE; goto out; } /* l.14 */
+        if (corr) {                                       /* exp(tt H~), H~ as in l.17-18 (R1) */
+          if (or_expm(n1, Ht, tt, F2, NULL) != 0) { rc = OR_ERR_NONFINITE; goto out; }
+          for (int c = 0; c < j; c++) f1[c] = F2[CM(c, 0, n1)];
+          f1[j] = h_next * F2[CM(j - 1, j, n1)];
+        } else {
+          for (int c = 0; c < j; c++)                     /* H(1:j,1:j) */
+            for (int r = 0; r < j; r++) Ht[CM(r, c, j)] = H[CM(r, c, ldh)];
+          if (or_expm(j, Ht, tt, F2, NULL) != 0) { rc = OR_ERR_NONFINITE; goto out; } /* l.14 */
+          for (int c = 0; c < j; c++) f1[c] = F2[CM(c, 0, j)];
+        }
         S.expm_calls++;
-        for (int c = 0; c < j; c++) f1[c] = F2[CM(c, 0, j)];
-        project(N, ld, j, V, f1, beta, w[l + k]);         /* l.15 */
+        project(N, ld, jc, V, f1, beta, w[l + k]);        /* l.15 */
       }
       l += n_tau;                                         /* l.17 */
       for (int c = 0; c < j; c++) f1[c] = F[CM(c, 0, n1)];
-      project(N, ld, j, V, f1, beta, wcur);               /* l.20 */
+      if (corr) f1[j] = h_next * F[CM(j - 1, j, n1)];
+      project(N, ld, jc, V, f1, beta, wcur);              /* l.20 */
       T_now = final ? T_end : T_next;                     /* l.24, R11 */
       j = 0;                                              /* l.25 */
       S.substeps++;

@@ -53,6 +53,8 @@ typedef struct {
   const double *forced_tau;
   const int *forced_m;
   const int *forced_accept; /* NULL => every forced attempt accepted; else replay     */
+  int corrected;            /* 1 => Saad's corrected scheme [46]: the output  */
+                            /* update adds beta h_{j+1,j} F(j,j+1) v_{j+1}             */
 } or_options;
 
 typedef struct {

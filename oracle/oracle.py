@@ -43,7 +43,7 @@ class _Opts(C.Structure):
         ("tol", C.c_double), ("m_init", C.c_int), ("m_min", C.c_int), ("m_max", C.c_int),
         ("iop_q", C.c_int), ("task1", C.c_int), ("max_attempts", C.c_int64),
         ("n_forced", C.c_int), ("forced_tau", _dp), ("forced_m", C.POINTER(C.c_int)),
-        ("forced_accept", C.POINTER(C.c_int)),
+        ("forced_accept", C.POINTER(C.c_int)), ("corrected", C.c_int),
     ]
 
 
@@ -233,7 +233,7 @@ def dense_phi_combination(op, u, tau):
 
 
 def kiops(op, u, T, tol=1e-7, m_init=10, m_min=10, m_max=128, iop_q=2, task1=0,
-          max_attempts=10000, forced=None, trace_cap=20000, out=None):
+          max_attempts=10000, forced=None, trace_cap=20000, out=None, corrected=0):
     """Alg. 1: returns (w list, stats dict, trace list of dicts, status string)."""
     op = _as_op(op)
     u, arr = _vec_array(u)
@@ -242,7 +242,7 @@ def kiops(op, u, T, tol=1e-7, m_init=10, m_min=10, m_max=128, iop_q=2, task1=0,
     w = out if out is not None else [np.zeros(op.N) for _ in range(n_out)]
     warr = (_dp * n_out)(*[_ptr(x) for x in w])
     o = _Opts(tol=tol, m_init=m_init, m_min=m_min, m_max=m_max, iop_q=iop_q, task1=task1,
-              max_attempts=max_attempts)
+              max_attempts=max_attempts, corrected=int(corrected))
     if forced:
         ft = np.ascontiguousarray([e[0] for e in forced], dtype=np.float64)
         fm = np.ascontiguousarray([e[1] for e in forced], dtype=np.int32)

@@ -574,7 +574,13 @@ __device__ int pade_expm(const Bk &bk, int n, const double *M, double scale, dou
     bk.sync();
   }
   int mult = 0;
+#ifdef KIOPS_PHASE_DEBUG
+  const long long cA = clock64();
+#endif
   bk.matmul(n, X, X, X2); mult++;
+#ifdef KIOPS_PHASE_DEBUG
+  const long long cB = clock64();
+#endif
   if (deg >= 5) { bk.matmul(n, X2, X2, X4); mult++; }
   if (deg >= 7) { bk.matmul(n, X2, X4, X6); mult++; }
   if (deg == 9) { bk.matmul(n, X4, X4, X8); mult++; }
@@ -645,8 +651,8 @@ __device__ int pade_expm(const Bk &bk, int n, const double *M, double scale, dou
   }
 #ifdef KIOPS_PHASE_DEBUG
   if (bk.gid() == 0)
-    printf("expm n=%d deg=%d s=%d mult=%d cycles: pade %lld solve %lld squaring %lld\n", n, deg, s, mult, c1 - c0,
-           c2 - c1, clock64() - c2);
+    printf("expm n=%d deg=%d s=%d mult=%d cycles: pade %lld (setup+norm %lld, first product %lld) solve %lld squaring %lld\n",
+           n, deg, s, mult, c1 - c0, cA - c0, cB - cA, c2 - c1, clock64() - c2);
 #endif
   return mult;
 }
@@ -841,27 +847,43 @@ __global__ void __cluster_dims__(CTRL_CL, 1, 1) __launch_bounds__(CTRL_THREADS, 
     // Alg. 3: coefficients of the one-pass GEMV.  Rows 0..n_tau-1 are the crossed
     // T_{l+k} (F2 = exp((T_{l+k} - T_now) H_j), l.13-15); the last row is the
     // running solution (F, l.20).  coef[o][c-1] = beta F(c,1) / s_c.
+    // Saad's corrected scheme (options.corrected): the extra basis vector x_{j+1}
+    // (stored by the closing pass) with beta h_{j+1,j} F(j, j+1) / s_{j+1}; F2 then comes
+    // from exp(tt H~) (size j+1, H~ as in Alg. 1 l.17-18) for its entry (j, j+1).
+    const bool corr = P.corrected && !happy;
+    const double h_corr = corr ? P.H[j + (size_t)LDH * (j - 1)] : 0.0;
     const double sc_final = P.task1 ? pow(1.0 / call->T[call->n_out - 1], (double)P.p) : 1.0;
-    if (rank == 0)
+    if (rank == 0) {
       for (int c = threadIdx.x; c < j; c += blockDim.x) {
         const double sg = (c == 0) ? beta : P.sig[c + 1];
         P.coef[(size_t)n_tau * LDH + c] = beta * F[c] / sg * (final_ ? sc_final : 1.0);
       }
+      if (corr && threadIdx.x == 0)
+        P.coef[(size_t)n_tau * LDH + j] = beta * (h_corr * F[(j - 1) + (size_t)LDH * j]) / P.sig[j + 1] *
+                                          (final_ ? sc_final : 1.0);
+    }
     cl_sync();
+    const int nf = corr ? j + 1 : j;
     for (int k = 0; k < n_tau; k++) {
-      for (int e = g0; e < j * j; e += gs) {
-        const int r = e % j, c = e / j;
-        Mh[r + (size_t)LDH * c] = (r >= c - P.q + 1 && r <= c + 1) ? P.H[r + (size_t)LDH * c] : 0.0;
+      for (int e = g0; e < nf * nf; e += gs) {
+        const int r = e % nf, c = e / nf;
+        double v = 0.0;
+        if (r < j && c < j && r >= c - P.q + 1 && r <= c + 1) v = P.H[r + (size_t)LDH * c];
+        if (corr && r == 0 && c == j) v = 1.0;
+        Mh[r + (size_t)LDH * c] = v;
       }
       cl_sync();
       const double tt = call->T[l0 + k] - t_now;
-      const int nm2 = cl_expm(j, Mh, tt, F, scr, sm);
+      const int nm2 = cl_expm(nf, Mh, tt, F, scr, sm);
       const double sc = P.task1 ? pow(1.0 / call->T[l0 + k], (double)P.p) : 1.0;
-      if (rank == 0)
+      if (rank == 0) {
         for (int c = threadIdx.x; c < j; c += blockDim.x) {
           const double sg = (c == 0) ? beta : P.sig[c + 1];
           P.coef[(size_t)k * LDH + c] = beta * F[c] / sg * sc;
         }
+        if (corr && threadIdx.x == 0)
+          P.coef[(size_t)k * LDH + j] = beta * (h_corr * F[(j - 1) + (size_t)LDH * j]) / P.sig[j + 1] * sc;
+      }
       if (lead) {
         st->expm_calls++;
         if (nm2 < 0) st->status = KIOPS_ERR_NONFINITE;
@@ -872,7 +894,7 @@ __global__ void __cluster_dims__(CTRL_CL, 1, 1) __launch_bounds__(CTRL_THREADS, 
       for (int k = 0; k < n_tau; k++) st->gemv_out[k] = call->w[l0 + k];
       st->gemv_out[n_tau] = final_ ? call->w[call->n_out - 1] : P.V;  // V slot 1 = running solution
       st->gemv_nout = n_tau + 1;
-      st->gemv_j = j;
+      st->gemv_j = corr ? j + 1 : j;
       st->gemv_x1 = st->x1;
       st->x1 = P.V;
       st->l = l0 + n_tau;

@@ -101,6 +101,7 @@ kiops_status validate(const kiops_operator_desc *op, int p, const kiops_options 
   if (o->m_init < 1) { err = "m_init must be >= 1"; return KIOPS_ERR_INVALID_ARG; }
   if (o->iop_q < 1 || o->iop_q > o->m_max) { err = "need 1 <= iop_q <= m_max"; return KIOPS_ERR_INVALID_ARG; }
   if (o->max_attempts < 1) { err = "max_attempts must be >= 1"; return KIOPS_ERR_INVALID_ARG; }
+  if (o->corrected != 0 && o->corrected != 1) { err = "corrected must be 0 or 1"; return KIOPS_ERR_INVALID_ARG; }
   if (o->host_staging && (o->max_outputs < 1 || o->max_outputs > KIOPS_MAX_OUT)) {
     err = "max_outputs must be in [1, KIOPS_MAX_OUT]"; return KIOPS_ERR_INVALID_ARG;
   }
@@ -497,6 +498,7 @@ void kiops_options_default(kiops_options *o) {
   o->max_attempts = 10000;
   o->host_staging = 0;
   o->max_outputs = 4;
+  o->corrected = 0;
 }
 
 kiops_status kiops_workspace_bytes(const kiops_operator_desc *op, int p, const kiops_options *o, size_t *bytes) {
@@ -550,6 +552,7 @@ kiops_status kiops_create(const kiops_operator_desc *op, int p, const kiops_opti
   P.tol = o->tol;
   P.m_init = o->m_init; P.m_min = o->m_min; P.m_max = o->m_max;
   P.task1 = o->task1;
+  P.corrected = o->corrected;
   P.max_attempts = o->max_attempts;
   unsigned char *w = c->ws;
   P.V = (double *)(w + L.V);

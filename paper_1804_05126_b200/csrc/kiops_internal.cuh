@@ -94,6 +94,7 @@ struct KParams {
   double *gram;       // generic q: G(i,l) = x_i . x_l, LDH x LDH column-major
   double *qpart;      // generic q: (2 LDH + 2) x QG dot partials
   int no_cond;        // 1: launched outside the graph (host-loop profiling hook)
+  int corrected;      // Saad's corrected scheme (options.corrected): the GEMV also uses x_{j+1}
   // padded mode (3D variable-kappa recompute pass, rc3d.cuh / passrc.cuh): every basis
   // slot is a ghost-padded (nx+4) x (ny+4) x nz grid, and slots m_max+1 .. m_max+p hold
   // copies of B's columns (u_p .. u_1), slot m_max+p+1 a copy of kappa, made by k_setup;

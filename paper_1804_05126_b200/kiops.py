@@ -33,7 +33,7 @@ class OperatorDesc(C.Structure):
 class Options(C.Structure):
     _fields_ = [("tol", C.c_double), ("m_init", C.c_int32), ("m_min", C.c_int32), ("m_max", C.c_int32),
                 ("iop_q", C.c_int32), ("task1", C.c_int32), ("max_attempts", C.c_int64),
-                ("host_staging", C.c_int32), ("max_outputs", C.c_int32)]
+                ("host_staging", C.c_int32), ("max_outputs", C.c_int32), ("corrected", C.c_int32)]
 
 
 class Stats(C.Structure):

@@ -380,3 +380,28 @@ def test_alternative_pass_layouts(env, monkeypatch):
     assert_parity(W.config3(200, 72))
     assert_parity(W.config1())
     assert_replay_parity(W.config4(40, 36, 22))
+
+
+# SURVEY 8(f) row f3, second half: Saad's corrected scheme on every operator kind
+# and pass family (fused q = 2 kernels, the 3D recompute pass, the generic q path)
+@pytest.mark.parametrize("make,strict", [(lambda: W.config1(), True), (lambda: W.config2(), True),
+                                         (lambda: W.config3(200, 72), True), (lambda: W.config5(33, 17, 29), True)])
+def test_corrected_scheme(make, strict):
+    assert_parity(make(), strict=strict, corrected=1)
+
+
+def test_corrected_scheme_3d_and_generic_q():
+    assert_replay_parity_opts(W.config4(24, 20, 16), corrected=1)
+    assert_replay_parity_opts(W.config4(256, 256, 8), corrected=1)
+    assert_parity(W.config3(96, 64), corrected=1, iop_q=3)
+
+
+def assert_replay_parity_opts(cfg, rtol=1e-10, **over):
+    o, os_, ot = oracle_run(cfg, **over)
+    sched = [(r["tau"], r["j"], r["accept"]) for r in ot]
+    g, gs, gt = gpu_run(cfg, forced=sched, **over)
+    assert [(r["j"], r["accept"]) for r in gt] == [(r["j"], r["accept"]) for r in ot]
+    for l in range(len(cfg["T"])):
+        rel = np.linalg.norm(g[l] - o[l]) / max(np.linalg.norm(o[l]), 1e-300)
+        print(f"REPLAY {cfg.get('name', '')} {over}: output {l} rel l2 {rel:.2e}")
+        assert rel <= rtol, (l, rel)

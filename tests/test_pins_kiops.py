@@ -221,3 +221,73 @@ def test_replaying_own_trace_is_bitwise():
     assert rc == rc2 == "OK" and st["rejections"] > 0
     assert all(np.array_equal(a, b) for a, b in zip(w, w2))
     assert [(r["j"], r["accept"]) for r in tr] == [(r["j"], r["accept"]) for r in tr2]
+
+
+def _dense_augmented(A, u):
+    """Theorem 1: A~ = [[A, B],[0, K]], B = [u_p..u_1], K the upper shift, v = [u_0; e_p]."""
+    from scipy.linalg import expm  # noqa: F401
+
+    N, p = A.shape[0], len(u) - 1
+    Bm = np.column_stack([u[p - c] for c in range(p)]) if p else np.zeros((N, 0))
+    At = np.block([[A, Bm], [np.zeros((p, N)), np.eye(p, k=1)]])
+    v = np.r_[u[0], np.zeros(max(p - 1, 0)), [1.0] if p else []]
+    return At, v
+
+
+def test_corrected_scheme_more_accurate_at_fixed_m():
+    """Saad's corrected scheme [46] adds beta h_{m+1,m} (tau e_m^T phi_1(tau H_m)
+    e_1) v_{m+1}, one more Krylov direction: at a fixed, forced m its error against the
+    dense exponential of A~ (Theorem 1) is markedly below the standard scheme's (Eq. 33)."""
+    from scipy.linalg import expm
+
+    rng = np.random.default_rng(21)
+    for _ in range(20):
+        N, p, tau = 30, 2, 0.2
+        A = rng.standard_normal((N, N)) - 3 * np.eye(N)
+        u = [rng.standard_normal(N) for _ in range(p + 1)]
+        At, v = _dense_augmented(A, u)
+        ex = (expm(tau * At) @ v)[:N]
+        err = []
+        for corr in (0, 1):
+            w, st, tr, rc = O.kiops({"kind": "dense", "nx": N, "dense": A}, u, [tau], tol=1e-30, m_init=6, m_min=6,
+                                    m_max=6, forced=[(tau, 6, 1)], corrected=corr)
+            assert rc == "OK"
+            err.append(np.linalg.norm(w[0] - ex) / np.linalg.norm(ex))
+        assert err[1] < 0.5 * err[0], err
+
+
+def test_corrected_scheme_free_run_within_tol_and_same_decisions():
+    """Free-running corrected scheme: within 10 tol (absolute, R18) of the dense
+    exponential at every output time; the first substep takes the standard scheme's
+    decisions (the correction changes only the output update, not eps / omega / Alg. 4)."""
+    from scipy.linalg import expm
+
+    rng = np.random.default_rng(22)
+    for _ in range(8):
+        N, p = 40, 3
+        A = 3 * rng.standard_normal((N, N)) - 5 * np.eye(N)
+        u = [rng.standard_normal(N) for _ in range(p + 1)]
+        At, v = _dense_augmented(A, u)
+        T = [0.3, 1.0]
+        op = {"kind": "dense", "nx": N, "dense": A}
+        w1, s1, t1, rc1 = O.kiops(op, u, T, tol=1e-8, m_init=10, m_min=10, m_max=40, corrected=1)
+        w0, s0, t0, rc0 = O.kiops(op, u, T, tol=1e-8, m_init=10, m_min=10, m_max=40, corrected=0)
+        assert rc1 == rc0 == "OK"
+        # the first substep's attempts are identical (the next substep starts from the
+        # corrected running solution, so later rows may differ)
+        n1 = next(i for i, r in enumerate(t0) if r["accept"]) + 1
+        assert t1[:n1] == t0[:n1]
+        for l, t in enumerate(T):
+            assert np.linalg.norm(w1[l] - (expm(t * At) @ v)[:N]) <= 10 * 1e-8
+
+
+def test_corrected_scheme_equals_standard_on_happy_breakdown():
+    """A = 0: the Krylov space closes (happy breakdown, h_{j+1,j} = 0, no v_{j+1}), so
+    the correction vanishes: corrected == standard bitwise (P8's closed form)."""
+    rng = np.random.default_rng(23)
+    N, p = 25, 3
+    u = [rng.standard_normal(N) for _ in range(p + 1)]
+    op = {"kind": "dense", "nx": N, "dense": np.zeros((N, N))}
+    w0, _, _, _ = O.kiops(op, u, [0.5, 1.0], tol=1e-10, corrected=0)
+    w1, _, _, _ = O.kiops(op, u, [0.5, 1.0], tol=1e-10, corrected=1)
+    assert all(np.array_equal(a, b) for a, b in zip(w0, w1))
