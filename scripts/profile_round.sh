@@ -6,7 +6,7 @@
 #   3. one `ncu --set full` capture of the persistent pass of configs 4 and 3
 # Numbers printed under ncu are never bench values.
 set -u
-R=${1:-r01}
+R=${1:-r02}
 mkdir -p gpurun_out
 for c in 4 3 5 1 2; do
   timeout 400 python bench.py --config $c > gpurun_out/${R}_bench_config$c.json 2> gpurun_out/${R}_bench_config$c.err
