@@ -58,6 +58,11 @@
 #ifndef RC3_PRODUCER
 #define RC3_PRODUCER 0  // the thread that issues the TMA boxes
 #endif
+#ifndef RC3_FFORM
+#define RC3_FFORM 1  // stencil as sum_f k_f x_f - (sum_f k_f) x_c, the diagonal sum F carried to stage 2
+                     // (stage 2 saves the six differences per point: 164.5 vs 167.3 us per pass,
+                     // microbenchmark; folding a0 into the scalars and fma-chain dots measured slower)
+#endif
 #ifndef RC3_SPLIT
 #define RC3_SPLIT 1
 #endif
@@ -277,6 +282,18 @@ __device__ __forceinline__ double face_sum(double f0, double d0, double f1, doub
 #endif
 }
 
+// sum_f kappa_f x_f over the six faces (F form: the diagonal part -(sum_f kappa_f) x_c is
+// applied by the caller); two interleaved partial sums.
+__device__ __forceinline__ double face_prod(double f0, double x0, double f1, double x1, double f2, double x2, double f3,
+                                           double x3, double f4, double x4, double f5, double x5) {
+  double a = f0 * x0, b = f1 * x1;
+  a = fma(f2, x2, a);
+  b = fma(f3, x3, b);
+  a = fma(f4, x4, a);
+  b = fma(f5, x5, b);
+  return a + b;
+}
+
 // Stage-1 results of one plane at this thread's pair, carried to stage 2 of the next
 // step (and its x_{k-1} / kappa centre to stage 1 of the next plane as the z-1 terms).
 struct Rec {
@@ -284,6 +301,7 @@ struct Rec {
   double fl, fi, fr;  // kappa sums of the x faces: left, inside the pair, right
   double2 fs, fn, fm; // kappa sums of the y-, y+, z- faces (per point)
   double2 xc, kc;     // x_{k-1}, kappa centre
+  double2 F;          // RC3_FFORM: sum of the six face kappa sums (the stencil's diagonal, x 2)
 };
 
 // Warp roles.  Warp w runs on scheduler w % 4; interior warps run stage 1 + stage 2,
@@ -423,6 +441,7 @@ __device__ __forceinline__ void march(const Geom &G, const PassArgs<PM> &Q, doub
     ra.kc = ld2(sm + (size_t)sm2 * SLOT + SA + offA);
     ra.xk = ra.bk = ra.fs = ra.fn = ra.fm = make_double2(0.0, 0.0);
     ra.fl = ra.fi = ra.fr = 0.0;
+    ra.F = make_double2(0.0, 0.0);
     rb = ra;
     double2 xq = ld2(sm + (size_t)sl * SLOT + offA), kq = ld2(sm + (size_t)sl * SLOT + SA + offA);  // centre of plane L
     __syncthreads();
@@ -447,6 +466,11 @@ __device__ __forceinline__ void march(const Geom &G, const PassArgs<PM> &Q, doub
       const double2 fs = make_double2(kc.x + ks.x, kc.y + ks.y), fn = make_double2(kc.x + kn.x, kc.y + kn.y);
       const double2 fm = make_double2(kc.x + pv.kc.x, kc.y + pv.kc.y), fp = make_double2(kc.x + kqn.x, kc.y + kqn.y);
       double2 xk = xc;
+      double2 Fn = make_double2(0.0, 0.0);  // RC3_FFORM: face-sum diagonal of plane L
+#if RC3_FFORM
+      if (!UR)  // (k = 1: no stage-1 stencil, but stage 2 of the next plane needs F)
+        Fn = make_double2(((fl + fi) + (fs.x + fn.x)) + (fm.x + fp.x), ((fr + fi) + (fs.y + fn.y)) + (fm.y + fp.y));
+#endif
       if (UR) {
         const double2 xs = ld2(XL - W), xn = ld2(XL + W);
         double xl = __shfl_up_sync(0xffffffffu, xc.y, 1), xr = __shfl_down_sync(0xffffffffu, xc.x, 1);
@@ -460,10 +484,16 @@ __device__ __forceinline__ void march(const Geom &G, const PassArgs<PM> &Q, doub
           bt.y = fma(b.y, btp[c], bt.y);
         }
         const double2 xm = pv.xc;
+#if RC3_FFORM
+        Fn = make_double2(((fl + fi) + (fs.x + fn.x)) + (fm.x + fp.x), ((fr + fi) + (fs.y + fn.y)) + (fm.y + fp.y));
+        const double ra_ = fma(-Fn.x, xc.x, face_prod(fl, xl, fi, xc.y, fs.x, xs.x, fn.x, xn.x, fm.x, xm.x, fp.x, xqn.x));
+        const double rb_ = fma(-Fn.y, xc.y, face_prod(fr, xr, fi, xc.x, fs.y, xs.y, fn.y, xn.y, fm.y, xm.y, fp.y, xqn.y));
+#else
         const double ra_ = face_sum(fl, xl - xc.x, fi, xc.y - xc.x, fs.x, xs.x - xc.x, fn.x, xn.x - xc.x, fm.x,
                                     xm.x - xc.x, fp.x, xqn.x - xc.x);
         const double rb_ = face_sum(fr, xr - xc.y, fi, xc.x - xc.y, fs.y, xs.y - xc.y, fn.y, xn.y - xc.y, fm.y,
                                     xm.y - xc.y, fp.y, xqn.y - xc.y);
+#endif
         const double r0 = fma(ra_, hh, bt.x), r1 = fma(rb_, hh, bt.y);
         xk.x = a0 * r0 - a1 * xc.x;
         xk.y = a0 * r1 - a1 * xc.y;
@@ -490,10 +520,17 @@ __device__ __forceinline__ void march(const Geom &G, const PassArgs<PM> &Q, doub
         if (!shr) xr = E[er + 1].x;
         const double2 xs = E[er - 34], xn = E[er + 34];
         // (the upper face of plane L-1 is the lower face fm of plane L)
+#if RC3_FFORM
+        const double ra_ = fma(-pv.F.x, c0.x, face_prod(pv.fl, xl, pv.fi, c0.y, pv.fs.x, xs.x, pv.fn.x, xn.x, pv.fm.x,
+                                                        xkm.x, fm.x, xk.x));
+        const double rb_ = fma(-pv.F.y, c0.y, face_prod(pv.fr, xr, pv.fi, c0.x, pv.fs.y, xs.y, pv.fn.y, xn.y, pv.fm.y,
+                                                        xkm.y, fm.y, xk.y));
+#else
         const double ra_ = face_sum(pv.fl, xl - c0.x, pv.fi, c0.y - c0.x, pv.fs.x, xs.x - c0.x, pv.fn.x, xn.x - c0.x,
                                     pv.fm.x, xkm.x - c0.x, fm.x, xk.x - c0.x);
         const double rb_ = face_sum(pv.fr, xr - c0.y, pv.fi, c0.x - c0.y, pv.fs.y, xs.y - c0.y, pv.fn.y, xn.y - c0.y,
                                     pv.fm.y, xkm.y - c0.y, fm.y, xk.y - c0.y);
+#endif
         const double r0 = fma(ra_, hh, pv.bk.x), r1 = fma(rb_, hh, pv.bk.y);
         const double2 xm = pv.xc;  // x_{k-1} at L-1
         const double d0 = fma(c0.x, c0.x, c0.y * c0.y), d1 = fma(xm.x, c0.x, xm.y * c0.y);
@@ -516,6 +553,7 @@ __device__ __forceinline__ void march(const Geom &G, const PassArgs<PM> &Q, doub
       cu.fl = fl; cu.fi = fi; cu.fr = fr;
       cu.fs = fs; cu.fn = fn; cu.fm = fm;
       cu.xc = xc; cu.kc = kc;
+      cu.F = Fn;
       xq = xqn;
       kq = kqn;
       sl = sq;
