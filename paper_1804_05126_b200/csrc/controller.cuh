@@ -344,6 +344,15 @@ struct ClusterBk {
 // zero-padded to NP = n rounded up to 8 (products of zero-padded operands keep the
 // padding zero, so the elementwise steps may stay on the n x n part).
 #define SM_LD 52
+#ifndef KIOPS_LU1W_MAXN
+#define KIOPS_LU1W_MAXN 24  // n <= this: the LU by one warp (full-row swaps, no block barrier per
+                            // step): 34.1 vs 38.6 k cycles per exponential at n = 12, 55 vs 59 k at
+                            // n = 20, slower from n ~ 36 (scripts/mb_expm.cu)
+#endif
+#ifndef KIOPS_SOLVE2
+#define KIOPS_SOLVE2 1  // small-n substitution: unit upper U', two right-hand sides per warp
+                        // (114.7 vs 122.1 k cycles per exponential at n = 36)
+#endif
 struct SmemBk {
   double *base;   // 10 matrices of SM_LD x SMALL_N (ld = SM_LD) + reduction scratch
   int n_;
@@ -459,6 +468,62 @@ struct SmemBk {
       if (lane == 0) { s_piv[k] = bi; s_rd[k] = rp; }
       __syncwarp();
     };
+if (n <= KIOPS_LU1W_MAXN) {
+    // one warp, everything in shared memory, no block barrier per step: pivot search (first
+    // maximal |pivot|, as the block version), LAPACK-style swap of the FULL rows k and pivot
+    // (L's columns included, so no reordering afterwards), multipliers by the reciprocal
+    // pivot, rank-1 update of the trailing block with each lane owning rows r, r + 32
+    if (warp == 0) {
+      for (int k = 0; k < n; k++) {
+        const double *C = Q + SM_LD * k;
+        const int ra = k + lane, rb = ra + 32;
+        const double va = ra < n ? fabs(C[ra]) : -1.0, vb = rb < n ? fabs(C[rb]) : -1.0;
+        const bool useb = vb > va;
+        const double v = useb ? vb : va;
+        const int rv = useb ? rb : ra;
+        const unsigned long long bits = v >= 0.0 ? (unsigned long long)__double_as_longlong(v) : 0ull;
+        const unsigned hi = (unsigned)(bits >> 32), lo = (unsigned)bits;
+        const unsigned mhi = __reduce_max_sync(0xffffffffu, v >= 0.0 ? hi : 0u);
+        const bool onhi = v >= 0.0 && hi == mhi;
+        const unsigned mlo = __reduce_max_sync(0xffffffffu, onhi ? lo : 0u);
+        const bool top = onhi && lo == mlo;
+        const int bi = (int)__reduce_min_sync(0xffffffffu, top ? (unsigned)rv : 0x7fffffffu);
+        const double best = __longlong_as_double((long long)(((unsigned long long)mhi << 32) | mlo));
+        if (!(best > 0.0) || bi >= n) {
+          if (lane == 0) s_bad = 1;
+          break;
+        }
+        if (bi != k)
+          for (int c = lane; c < n; c += 32) {
+            const double t = Q[k + SM_LD * c];
+            Q[k + SM_LD * c] = Q[bi + SM_LD * c];
+            Q[bi + SM_LD * c] = t;
+          }
+        __syncwarp();
+        const double rp = __drcp_rn(Q[k + SM_LD * k]);
+        const int r0 = k + 1 + lane, r1 = r0 + 32;
+        const double l0 = r0 < n ? Q[r0 + SM_LD * k] * rp : 0.0, l1 = r1 < n ? Q[r1 + SM_LD * k] * rp : 0.0;
+        if (r0 < n) Q[r0 + SM_LD * k] = l0;
+        if (r1 < n) Q[r1 + SM_LD * k] = l1;
+        if (lane == 0) { s_piv[k] = bi; s_rd[k] = rp; }
+#pragma unroll 4
+        for (int c = k + 1; c < n; c++) {
+          double *Xc = Q + SM_LD * c;
+          const double u = Xc[k];
+          if (r0 < n) Xc[r0] = fma(-l0, u, Xc[r0]);
+          if (r1 < n) Xc[r1] = fma(-l1, u, Xc[r1]);
+        }
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    if (s_bad) return -1;
+    if (threadIdx.x == 0) {  // row i of P Q is row perm[i] of Q
+      for (int i = 0; i < n; i++) s_perm[i] = i;
+      for (int k = 0; k < n; k++) { const int pk = s_piv[k], t = s_perm[k]; s_perm[k] = s_perm[pk]; s_perm[pk] = t; }
+    }
+    __syncthreads();
+} else {
     if (warp == 0) pivot(0);
     __syncthreads();
     for (int k = 0; k < n; k++) {
@@ -499,6 +564,52 @@ struct SmemBk {
       for (int k = 0; k < n; k++) { const int pk = s_piv[k], t = s_perm[k]; s_perm[k] = s_perm[pk]; s_perm[pk] = t; }
     }
     __syncthreads();
+}
+#if KIOPS_SOLVE2
+    // U' = D^-1 U: row k of U scaled by 1/u_kk (the reciprocal pivots), so the back
+    // substitution is unit upper triangular and no multiply sits on its dependency chain
+    for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+      const int r = e % n, c = e / n;
+      if (c > r) Q[r + SM_LD * c] *= s_rd[r];
+    }
+    __syncthreads();
+    // two right-hand-side columns per warp (two independent substitution chains);
+    // operands loaded as zeros where the triangle has none, so the updates are branch free
+    for (int c0 = 2 * warp; c0 < n; c0 += 2 * nw) {
+      const bool two = c0 + 1 < n;
+      double *Ra = R + SM_LD * c0, *Rb = R + SM_LD * (two ? c0 + 1 : c0);
+      double a0 = lane < n ? Ra[s_perm[lane]] : 0.0, a1 = lane + 32 < n ? Ra[s_perm[lane + 32]] : 0.0;
+      double b0 = lane < n ? Rb[s_perm[lane]] : 0.0, b1 = lane + 32 < n ? Rb[s_perm[lane + 32]] : 0.0;
+#pragma unroll 4
+      for (int k = 0; k < n; k++) {  // L y = P b (unit lower)
+        const double *Lk = Q + SM_LD * k;
+        const double l0 = (lane > k && lane < n) ? Lk[lane] : 0.0;
+        const double l1 = (lane + 32 > k && lane + 32 < n) ? Lk[lane + 32] : 0.0;
+        const double ya = __shfl_sync(0xffffffffu, k < 32 ? a0 : a1, k & 31);
+        const double yb = __shfl_sync(0xffffffffu, k < 32 ? b0 : b1, k & 31);
+        a0 = fma(-l0, ya, a0); a1 = fma(-l1, ya, a1);
+        b0 = fma(-l0, yb, b0); b1 = fma(-l1, yb, b1);
+      }
+      const double d0 = lane < n ? s_rd[lane] : 0.0, d1 = lane + 32 < n ? s_rd[lane + 32] : 0.0;
+      a0 *= d0; a1 *= d1; b0 *= d0; b1 *= d1;
+#pragma unroll 4
+      for (int k = n - 1; k >= 0; k--) {  // U' x = D^-1 y (unit upper)
+        const double *Uk = Q + SM_LD * k;
+        const double u0 = lane < k ? Uk[lane] : 0.0, u1 = lane + 32 < k ? Uk[lane + 32] : 0.0;
+        const double xa = __shfl_sync(0xffffffffu, k < 32 ? a0 : a1, k & 31);
+        const double xb = __shfl_sync(0xffffffffu, k < 32 ? b0 : b1, k & 31);
+        a0 = fma(-u0, xa, a0); a1 = fma(-u1, xa, a1);
+        b0 = fma(-u0, xb, b0); b1 = fma(-u1, xb, b1);
+      }
+      __syncwarp();
+      if (lane < n) Ra[lane] = a0;
+      if (lane + 32 < n) Ra[lane + 32] = a1;
+      if (two) {
+        if (lane < n) Rb[lane] = b0;
+        if (lane + 32 < n) Rb[lane + 32] = b1;
+      }
+    }
+#else
     for (int c = warp; c < n; c += nw) {
       double *Rc = R + SM_LD * c;
       double x0 = lane < n ? Rc[s_perm[lane]] : 0.0, x1 = lane + 32 < n ? Rc[s_perm[lane + 32]] : 0.0;
@@ -519,6 +630,7 @@ struct SmemBk {
       if (lane < n) Rc[lane] = x0;
       if (lane + 32 < n) Rc[lane + 32] = x1;
     }
+#endif
     __syncthreads();
     return 0;
   }
