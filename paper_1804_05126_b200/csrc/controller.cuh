@@ -331,6 +331,9 @@ struct ClusterBk {
   __device__ int gid() const { return cl_gtid(); }
   __device__ int gsz() const { return cl_gsize(); }
   __device__ void sync() const { cl_sync(); }
+  // elementwise loops: e in [0, ecount) -> (i, j); false: not an element
+  __device__ int ecount(int n) const { return n * n; }
+  __device__ bool eindex(int n, int e, int &i, int &j) const { j = e / n; i = e - j * n; return true; }
   __device__ void matmul(int n, const double *A, const double *B, double *C) const { cl_matmul(n, A, B, C, sm); }
   __device__ double norm1(int n, const double *A) const { return cta_norm1(n, A, sm); }
   __device__ int solve(int n, const double *Q, double *R) const {
@@ -349,6 +352,13 @@ struct ClusterBk {
                             // step): 34.1 vs 38.6 k cycles per exponential at n = 12, 55 vs 59 k at
                             // n = 20, slower from n ~ 36 (scripts/mb_expm.cu)
 #endif
+#ifndef KIOPS_SMALL_MM_INLINE
+#define KIOPS_SMALL_MM_INLINE __noinline__  // one copy of the small product for the 10+ call sites of
+                                            // pade_expm (instruction-cache footprint)
+#endif
+#ifndef KIOPS_SOLVE3
+#define KIOPS_SOLVE3 1  // small-n solve with the augmented matrix in registers (solve3 below)
+#endif
 #ifndef KIOPS_SOLVE2
 #define KIOPS_SOLVE2 1  // small-n substitution: unit upper U', two right-hand sides per warp
                         // (114.7 vs 122.1 k cycles per exponential at n = 36)
@@ -361,6 +371,10 @@ struct SmemBk {
   __device__ int gid() const { return threadIdx.x; }
   __device__ int gsz() const { return blockDim.x; }
   __device__ void sync() const { __syncthreads(); }
+  // elementwise loops run over the stored columns (constant leading dimension: no
+  // runtime integer division per element); padding rows are skipped
+  __device__ int ecount(int n) const { return SM_LD * n; }
+  __device__ bool eindex(int n, int e, int &i, int &j) const { j = e / SM_LD; i = e - j * SM_LD; return i < n; }
   // zero the 10 matrices (padding included); call before the first use for this n
   __device__ void clear() const {
     for (int e = threadIdx.x; e < 10 * SM_LD * SMALL_N; e += blockDim.x) base[e] = 0.0;
@@ -369,7 +383,7 @@ struct SmemBk {
   // C = A B on the FP64 tensor cores: one warp per 8 x 8 output tile (up to 3 tiles
   // per warp interleaved), k in steps of 4.  Fragments (PTX m8n8k4 .f64): A row
   // g = lane/4, col t = lane%4; B row t, col g; C row g, cols 2t, 2t+1.
-  __device__ void matmul(int n, const double *A, const double *B, double *C) const {
+  __device__ KIOPS_SMALL_MM_INLINE void matmul(int n, const double *A, const double *B, double *C) const {
     const int np = (n + 7) & ~7, nt = np >> 3, ntile = nt * nt;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const int g = lane >> 2, tq = lane & 3;
@@ -377,12 +391,16 @@ struct SmemBk {
       double c[3][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
       int ti[3], tj[3];
       bool on[3];
+      const float rnt = __frcp_rn((float)nt);
 #pragma unroll
       for (int u = 0; u < 3; u++) {
         const int tt = t0 + u * nw;
         on[u] = tt < ntile;
-        ti[u] = on[u] ? (tt % nt) * 8 : 0;
-        tj[u] = on[u] ? (tt / nt) * 8 : 0;
+        // tt / nt for tt < 64, nt <= 8 without an integer division: (tt + 1/2) / nt is at
+        // least 1 / (2 nt) away from an integer
+        const int qd = __float2int_rz(((float)tt + 0.5f) * rnt);
+        ti[u] = on[u] ? (tt - qd * nt) * 8 : 0;
+        tj[u] = on[u] ? qd * 8 : 0;
       }
       for (int k0 = 0; k0 < np; k0 += 4) {
 #pragma unroll
@@ -402,11 +420,14 @@ struct SmemBk {
     }
     __syncthreads();
   }
+  // (column sums in ascending row order, as the oracle's: the degree / scaling decision
+  // compares this norm with the theta thresholds)
   __device__ double norm1(int n, const double *A) const {
     double *red = base + 10 * (size_t)SM_LD * SMALL_N;
     double best = 0.0;
     for (int j = threadIdx.x; j < n; j += blockDim.x) {
       double s = 0.0;
+#pragma unroll 8
       for (int i = 0; i < n; i++) s += fabs(A[i + SM_LD * j]);
       best = (s > best || s != s) ? s : best;
     }
@@ -414,27 +435,194 @@ struct SmemBk {
       const double x = __shfl_xor_sync(0xffffffffu, best, o);
       best = (x > best || x != x) ? x : best;
     }
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = best;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    if (lane == 0) red[warp] = best;
     __syncthreads();
-    if (threadIdx.x == 0) {
-      double bb = 0.0;
-      for (int w = 0; w < (int)((blockDim.x + 31) >> 5); w++) bb = (red[w] > bb || red[w] != red[w]) ? red[w] : bb;
-      red[32] = bb;
+    double bb = lane < nw ? red[lane] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) {
+      const double x = __shfl_xor_sync(0xffffffffu, bb, o);
+      bb = (x > bb || x != x) ? x : bb;
     }
     __syncthreads();
-    const double r = red[32];
-    __syncthreads();
-    return r;
+    return bb;
   }
-  // Q X = R in place (R <- X), n <= SMALL_N, everything in CTA 0's shared memory.  The
-  // same scheme as cl_solve: factor Q = P L U in place with partial pivoting (first
-  // maximal |pivot|), static column ownership (warp c mod nw owns column c; swaps and
-  // updates need only __syncwarp), one __syncthreads per step, the owner of column k+1
-  // searching step k+1's pivot right after its update; L brought into final row order;
-  // then one warp per right-hand-side column: P b, L y = P b, U x = y with the column in
-  // registers (rows lane, lane + 32) and pivots broadcast by shuffles.  Q is destroyed.
-  // Returns 0 or -1 (zero pivot), all threads.
+  // Register-resident solve (KIOPS_SOLVE3, the default): Gaussian elimination with
+  // partial pivoting of the augmented matrix [Q | R], columns dealt to the warps (Q
+  // column c and R column c in warp c mod 16, up to 3 + 3 per warp for n <= 48),
+  // lane = row (rows lane, lane + 32), every entry in registers.  Rows are never moved:
+  // each lane knows the step at which its rows were pivoted (implicit pivoting: the
+  // maximal |value| among the rows not yet pivoted; exactly equal |values| -- which a
+  // swapped scheme would break by position -- are broken by the lowest row index).  Step k: the owner of column k
+  // updates that column first, finds the pivot (one 32-bit max reduction in the common
+  // case), publishes the multipliers by row and the pivot row in shared memory and
+  // ARRIVES at a named barrier (bar.arrive, non-blocking); the other warps bar.sync on
+  // it, read the multipliers and update all their columns with one shuffle (the pivot
+  // row's entry) per column, branch free (finished columns and finished rows see zero
+  // multipliers).  So the dependency chain of a step is the owner's column update +
+  // search only; the remaining updates overlap the next step's chain.  Eliminating
+  // [Q | R] together is the forward substitution L y = P b.  Then U is scaled to unit
+  // diagonal and written to shared memory (over Q), and every warp back substitutes
+  // its right-hand-side columns from registers (one shuffle + one fma per step and
+  // column on the dependency chain).  Same operations as LU + substitution.
+  // Q is destroyed.  Returns 0 or -1 (zero / non-finite pivot column), all threads.
+  // Requires 16 warps (CTRL_THREADS = 512).
+  static __device__ __forceinline__ void nb_sync(int id) { asm volatile("bar.sync %0, 512;" ::"r"(id) : "memory"); }
+  static __device__ __forceinline__ void nb_arrive(int id) { asm volatile("bar.arrive %0, 512;" ::"r"(id) : "memory"); }
+  // shared-memory accesses by 32-bit shared address (the step chain carries no generic
+  // address arithmetic)
+  static __device__ __forceinline__ double lds_f64(unsigned a) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a) : "memory");
+    return v;
+  }
+  static __device__ __forceinline__ int lds_s32(unsigned a) {
+    int v;
+    asm volatile("ld.shared.s32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+    return v;
+  }
+  static __device__ __forceinline__ void sts_f64(unsigned a, double v) {
+    asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
+  }
+  static __device__ __forceinline__ void sts_s32(unsigned a, int v) {
+    asm volatile("st.shared.s32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+  }
+  __device__ __noinline__ int solve3(int n, double *Q, double *R) const {
+    constexpr int NS = 3, NW = 16;
+    // per-step publication, double buffered: [buf][0..63] multipliers by row, [buf][64] pivot row
+    __shared__ __align__(16) double s_pub[2][66];
+    __shared__ double s_rd3[SMALL_N];
+    __shared__ int s_prow[SMALL_N];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const bool r0ok = lane < n, r1ok = lane + 32 < n;
+    unsigned pub0 = (unsigned)__cvta_generic_to_shared(&s_pub[0][0]);
+    asm volatile("" : "+r"(pub0));  // (opaque: not rematerialised inside the step chain)
+    const unsigned pubsz = 66 * 8;
+    double q0[NS], q1[NS], y0[NS], y1[NS];  // Q and R columns warp + 16 i, rows lane / lane + 32
+#pragma unroll
+    for (int i = 0; i < NS; i++) {
+      const int c = warp + NW * i;
+      q0[i] = (c < n && r0ok) ? Q[lane + SM_LD * c] : 0.0;
+      q1[i] = (c < n && r1ok) ? Q[lane + 32 + SM_LD * c] : 0.0;
+      y0[i] = (c < n && r0ok) ? R[lane + SM_LD * c] : 0.0;
+      y1[i] = (c < n && r1ok) ? R[lane + 32 + SM_LD * c] : 0.0;
+    }
+    // live0/1: my rows not yet pivoted (rows >= n never are); ps0/1: their pivot steps
+    bool live0 = r0ok, live1 = r1ok;
+    int ps0 = 0x7fffffff, ps1 = 0x7fffffff;
+    // pivot search of step k on column values x0, x1 (owner warp): first maximal |value|
+    // among the live rows (ties: the lowest row), published into buffer k & 1
+    auto search = [&](int k, double x0, double x1) {
+      const double v0 = live0 ? fabs(x0) : -1.0, v1 = live1 ? fabs(x1) : -1.0;
+      const bool useb = v1 > v0;
+      const double v = useb ? v1 : v0;
+      const bool ok = v >= 0.0;  // (false for NaN and for rows already pivoted)
+      const unsigned hi = ok ? (unsigned)__double2hiint(v) : 0u;
+      const unsigned mhi = __reduce_max_sync(0xffffffffu, hi);
+      bool cand = ok && hi == mhi;
+      unsigned m = __ballot_sync(0xffffffffu, cand);
+      if (m & (m - 1)) {  // several lanes share the high word
+        const unsigned lo = cand ? (unsigned)__double2loint(v) : 0u;
+        const unsigned mlo = __reduce_max_sync(0xffffffffu, lo);
+        cand = cand && lo == mlo;
+        m = __ballot_sync(0xffffffffu, cand);
+        const unsigned ma = __ballot_sync(0xffffffffu, cand && !useb);  // equal |values|: rows < 32 first
+        if (ma) m = ma;
+      }
+      const int wl = m ? __ffs(m) - 1 : 0;
+      const double piv = __shfl_sync(0xffffffffu, useb ? x1 : x0, wl);
+      const int rp = wl + (__shfl_sync(0xffffffffu, (int)useb, wl) ? 32 : 0);
+      const bool good = m != 0 && fabs(piv) > 0.0 && fabs(piv) <= 1.7976931348623157e308;
+      const double rpiv = __drcp_rn(piv);
+      const unsigned pb = pub0 + (k & 1) * pubsz;
+      sts_f64(pb + lane * 8, (live0 && lane != rp) ? x0 * rpiv : 0.0);
+      sts_f64(pb + (lane + 32) * 8, (live1 && lane + 32 != rp) ? x1 * rpiv : 0.0);
+      if (lane == 0) sts_s32(pb + 64 * 8, good ? rp : -1);
+      __syncwarp();
+      nb_arrive(1 + (k & 1));
+      if (lane == 0) {
+        s_rd3[k] = rpiv;
+        s_prow[k] = rp;
+      }
+    };
+    if (warp == 0) search(0, q0[0], q1[0]);
+    int bad = 0;
+    // step k (k1 = k + 1); IO = k1 / 16, the register slot of column k1 in its owner warp
+    auto step = [&](int k1, auto iotag) {
+      constexpr int IO = decltype(iotag)::value;
+      const int k = k1 - 1;
+      if ((k & (NW - 1)) != warp) nb_sync(1 + (k & 1));  // (the owner published L_k itself)
+      const unsigned pb = pub0 + (k & 1) * pubsz;
+      const int rp = lds_s32(pb + 64 * 8);
+      const double l0 = lds_f64(pb + lane * 8), l1 = lds_f64(pb + (lane + 32) * 8);
+      if (rp < 0) { bad = 1; return; }
+      const int sl = rp & 31;
+      const bool hi = rp >= 32;
+      if (lane == sl) {
+        if (hi) { live1 = false; ps1 = k; } else { live0 = false; ps0 = k; }
+      }
+      if (k1 < n && (k1 & (NW - 1)) == warp) {  // column k1 first, then its pivot search
+        const double xp = __shfl_sync(0xffffffffu, hi ? q1[IO] : q0[IO], sl);
+        search(k1, fma(-l0, xp, q0[IO]), fma(-l1, xp, q1[IO]));
+      }
+#pragma unroll
+      for (int i = 0; i < NS; i++) {
+        const double xq = __shfl_sync(0xffffffffu, hi ? q1[i] : q0[i], sl);
+        const double xy = __shfl_sync(0xffffffffu, hi ? y1[i] : y0[i], sl);
+        // (a column c <= k keeps its U entries: their rows were pivoted, l = 0)
+        q0[i] = fma(-l0, xq, q0[i]);
+        q1[i] = fma(-l1, xq, q1[i]);
+        y0[i] = fma(-l0, xy, y0[i]);
+        y1[i] = fma(-l1, xy, y1[i]);
+      }
+    };
+    for (int k1 = 1; k1 <= n && k1 < NW && !bad; k1++) step(k1, std::integral_constant<int, 0>{});
+    for (int k1 = NW; k1 <= n && k1 < 2 * NW && !bad; k1++) step(k1, std::integral_constant<int, 1>{});
+    for (int k1 = 2 * NW; k1 <= n && !bad; k1++) step(k1, std::integral_constant<int, 2>{});
+    __syncthreads();
+    if (bad) return -1;
+    // unit-diagonal U' = D^-1 U (row scaling by the reciprocal pivot of the row's step) to
+    // shared memory over Q; y' = D^-1 y stays in registers
+    const double d0 = r0ok ? s_rd3[ps0] : 0.0, d1 = r1ok ? s_rd3[ps1] : 0.0;
+#pragma unroll
+    for (int i = 0; i < NS; i++) {
+      const int c = warp + NW * i;
+      y0[i] *= d0;
+      y1[i] *= d1;
+      if (c < n) {
+        if (r0ok) Q[lane + SM_LD * c] = q0[i] * d0;
+        if (r1ok) Q[lane + 32 + SM_LD * c] = q1[i] * d1;
+      }
+    }
+    __syncthreads();
+    // back substitution, column oriented: x_k = y'(row of step k); rows of earlier steps
+    // subtract U'(row, k) x_k
+#pragma unroll 4
+    for (int k = n - 1; k >= 0; k--) {
+      const int rp = s_prow[k], sl = rp & 31;
+      const bool hi = rp >= 32;
+      const double u0 = ps0 < k ? Q[lane + SM_LD * k] : 0.0, u1 = ps1 < k ? Q[lane + 32 + SM_LD * k] : 0.0;
+#pragma unroll
+      for (int i = 0; i < NS; i++) {
+        const double xk = __shfl_sync(0xffffffffu, hi ? y1[i] : y0[i], sl);
+        y0[i] = fma(-u0, xk, y0[i]);
+        y1[i] = fma(-u1, xk, y1[i]);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < NS; i++) {
+      const int c = warp + NW * i;
+      if (c < n) {
+        if (r0ok) R[ps0 + SM_LD * c] = y0[i];
+        if (r1ok) R[ps1 + SM_LD * c] = y1[i];
+      }
+    }
+    __syncthreads();
+    return 0;
+  }
   __device__ int solve(int n, double *Q, double *R) const {
+#if KIOPS_SOLVE3
+    if (blockDim.x == 512 && n <= SMALL_N) return solve3(n, Q, R);
+#endif
     __shared__ int s_bad, s_piv[SMALL_N], s_perm[SMALL_N];
     __shared__ double s_rd[SMALL_N];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -661,15 +849,19 @@ __device__ int pade_expm(const Bk &bk, int n, const double *M, double scale, dou
          *V = bk.mat(6), *T = bk.mat(7);
   // [m/m] Pade numerator coefficients (kPade, constant memory: a per-thread local
   // table indexed through a runtime pointer costs local-memory round trips).
-  const int nn = n * n, g0 = bk.gid(), gs = bk.gsz();
+  const int g0 = bk.gid(), gs = bk.gsz(), cnt = bk.ecount(n);
+  // f(i, j, q) on every element (q = i + ld j), then a barrier
+  auto each = [&](auto f) {
+    for (int e = g0; e < cnt; e += gs) {
+      int i, j;
+      if (bk.eindex(n, e, i, j)) f(i, j, (size_t)i + (size_t)ld * j);
+    }
+    bk.sync();
+  };
 #ifdef KIOPS_PHASE_DEBUG
   const long long c0 = clock64();
 #endif
-  for (int e = g0; e < nn; e += gs) {
-    const int i = e % n, j = e / n;
-    X[i + (size_t)ld * j] = scale * M[i + (size_t)ld * j];
-  }
-  bk.sync();
+  each([&](int, int, size_t q) { X[q] = scale * M[q]; });
   const double nrm = bk.norm1(n, X);
   if (!isfinite(nrm)) return -1;
   int deg, s = 0;
@@ -682,8 +874,7 @@ __device__ int pade_expm(const Bk &bk, int n, const double *M, double scale, dou
     s = ceil_log2_exact(nrm / 5.371920351148152e0);
     if (s < 0) s = 0;
     const double f = ldexp(1.0, -s);
-    for (int e = g0; e < nn; e += gs) X[(e % n) + (size_t)ld * (e / n)] *= f;
-    bk.sync();
+    each([&](int, int, size_t q) { X[q] *= f; });
   }
   int mult = 0;
 #ifdef KIOPS_PHASE_DEBUG
@@ -698,9 +889,7 @@ __device__ int pade_expm(const Bk &bk, int n, const double *M, double scale, dou
   if (deg == 9) { bk.matmul(n, X4, X4, X8); mult++; }
   if (deg < 13) {
     const double *b = kPade[deg == 3 ? 0 : deg == 5 ? 1 : deg == 7 ? 2 : 3];
-    for (int e = g0; e < nn; e += gs) {
-      const int i = e % n, j = e / n;
-      const size_t q = i + (size_t)ld * j;
+    each([&](int i, int j, size_t q) {
       const double id = (i == j) ? 1.0 : 0.0;
       double odd = b[1] * id + b[3] * X2[q], even = b[0] * id + b[2] * X2[q];
       if (deg >= 5) { odd += b[5] * X4[q]; even += b[4] * X4[q]; }
@@ -708,41 +897,33 @@ __device__ int pade_expm(const Bk &bk, int n, const double *M, double scale, dou
       if (deg >= 9) { odd += b[9] * X8[q]; even += b[8] * X8[q]; }
       T[q] = odd;
       V[q] = even;
-    }
-    bk.sync();
+    });
     bk.matmul(n, X, T, U); mult++;   // U = X * odd part
+    // (V - U) F = (V + U)
+    each([&](int, int, size_t q) {
+      T[q] = V[q] - U[q];
+      F[q] = V[q] + U[q];
+    });
   } else {
     const double *b = kPade[4];
-    for (int e = g0; e < nn; e += gs) {
-      const size_t q = (e % n) + (size_t)ld * (e / n);
+    each([&](int, int, size_t q) {
       T[q] = b[13] * X6[q] + b[11] * X4[q] + b[9] * X2[q];
       X8[q] = b[12] * X6[q] + b[10] * X4[q] + b[8] * X2[q];
-    }
-    bk.sync();
+    });
     bk.matmul(n, X6, T, U); mult++;
     bk.matmul(n, X6, X8, V); mult++;
-    for (int e = g0; e < nn; e += gs) {
-      const int i = e % n, j = e / n;
-      const size_t q = i + (size_t)ld * j;
+    each([&](int i, int j, size_t q) {
       const double id = (i == j) ? 1.0 : 0.0;
       U[q] += b[7] * X6[q] + b[5] * X4[q] + b[3] * X2[q] + b[1] * id;
       V[q] += b[6] * X6[q] + b[4] * X4[q] + b[2] * X2[q] + b[0] * id;
-    }
-    bk.sync();
-    bk.matmul(n, X, U, T); mult++;   // odd part: X [ ... ]
-    for (int e = g0; e < nn; e += gs) {
-      const size_t q = (e % n) + (size_t)ld * (e / n);
-      U[q] = T[q];
-    }
-    bk.sync();
+    });
+    bk.matmul(n, X, U, X8); mult++;   // odd part: X [ ... ]
+    // (V - U) F = (V + U)
+    each([&](int, int, size_t q) {
+      T[q] = V[q] - X8[q];
+      F[q] = V[q] + X8[q];
+    });
   }
-  // (V - U) F = (V + U)
-  for (int e = g0; e < nn; e += gs) {
-    const size_t q = (e % n) + (size_t)ld * (e / n);
-    T[q] = V[q] - U[q];
-    F[q] = V[q] + U[q];
-  }
-  bk.sync();
 #ifdef KIOPS_PHASE_DEBUG
   const long long c1 = clock64();
 #endif
@@ -755,11 +936,7 @@ __device__ int pade_expm(const Bk &bk, int n, const double *M, double scale, dou
     bk.matmul(n, src, src, dst); mult++;
   }
   if (s & 1) {  // result in T
-    for (int e = g0; e < nn; e += gs) {
-      const size_t q = (e % n) + (size_t)ld * (e / n);
-      F[q] = T[q];
-    }
-    bk.sync();
+    each([&](int, int, size_t q) { F[q] = T[q]; });
   }
 #ifdef KIOPS_PHASE_DEBUG
   if (bk.gid() == 0)
