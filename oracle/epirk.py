@@ -149,6 +149,94 @@ class ReactionDiffusion2D:
                 "w": [wa, wa, wa, wa, -4.0 * wa], "diag": h * self.dR(y)}
 
 
+class ReactionDiffusionCSR:
+    """u' = L u + R(u) with a general constant linear part L (CSR: row_ptr, col_idx,
+    vals; every row holds its diagonal entry) and the pointwise cubic R(u) = c0 + c1 u +
+    c2 u^2 + c3 u^3.  J(u) = L + diag(R'(u)); the remainder of P:85 is pointwise as for
+    ReactionDiffusion2D (reading E7).  Plain loops / numpy only."""
+
+    def __init__(self, row_ptr, col_idx, vals, coef):
+        self.row_ptr = np.asarray(row_ptr, dtype=np.int64)
+        self.col_idx = np.asarray(col_idx, dtype=np.int32)
+        self.vals = np.asarray(vals, dtype=np.float64)
+        self.dim = len(self.row_ptr) - 1
+        self.c = tuple(float(c) for c in coef)
+        rows = np.repeat(np.arange(self.dim), np.diff(self.row_ptr))
+        self._rows = rows
+        self.diag_pos = np.full(self.dim, -1, dtype=np.int64)
+        on = np.nonzero(self.col_idx == rows)[0]
+        self.diag_pos[rows[on]] = on
+        if np.any(self.diag_pos < 0):
+            raise ValueError("every row of L must hold its diagonal entry")
+
+    def lmul(self, u):
+        out = np.zeros(self.dim)
+        np.add.at(out, self._rows, self.vals * u[self.col_idx])  # row sums in storage order
+        return out
+
+    def R(self, u):
+        c0, c1, c2, c3 = self.c
+        return c0 + u * (c1 + u * (c2 + u * c3))
+
+    def dR(self, u):
+        _, c1, c2, c3 = self.c
+        return c1 + u * (2.0 * c2 + u * 3.0 * c3)
+
+    def f(self, y):
+        return self.lmul(y) + self.R(y)
+
+    def jmul(self, y, x):
+        return self.lmul(x) + self.dR(y) * x
+
+    def remainder(self, yn, y):
+        return self.R(y) - self.R(yn) - self.dR(yn) * (y - yn)
+
+    def kiops_op(self, y, h):
+        v = self.vals.copy()
+        v[self.diag_pos] += self.dR(y)
+        return {"kind": "csr", "nx": self.dim, "ny": 1, "nz": 1, "row_ptr": self.row_ptr,
+                "col_idx": self.col_idx, "vals": h * v}
+
+
+def adr_neumann(nx, ny=None, eps=0.01, alpha=-10.0, gamma=100.0):
+    """The ADR 2D problem of Sec. 4: u_t = eps lap(u) - alpha (u_x + u_y) +
+    gamma u (u - 1/2)(1 - u) on [0, 1]^2 with homogeneous Neumann boundaries, u_0 =
+    256 (x y (1-x)(1-y))^2 + 0.3.  Discretisation (reading E10): nodes x_i = i dx,
+    i = 0..nx-1, dx = 1/(nx-1) (boundary nodes included), second-order central
+    differences for both the Laplacian and the advection term, the Neumann condition by
+    the mirrored ghost node u_{-1} = u_{1} (so the boundary Laplacian row is
+    (2 u_1 - 2 u_0)/dx^2 and the central first difference vanishes there).  Returns
+    (problem, u0); rows in lexicographic order (x fastest), ascending columns."""
+    ny = ny or nx
+    dx, dy = 1.0 / (nx - 1), 1.0 / (ny - 1)
+    row_ptr, col, val = [0], [], []
+    for j in range(ny):
+        for i in range(nx):
+            ent = {}
+
+            def add(ii, jj, w):
+                ii = -ii if ii < 0 else (2 * (nx - 1) - ii if ii > nx - 1 else ii)  # mirror
+                jj = -jj if jj < 0 else (2 * (ny - 1) - jj if jj > ny - 1 else jj)
+                k = ii + nx * jj
+                ent[k] = ent.get(k, 0.0) + w
+
+            add(i, j, -2.0 * eps / dx ** 2 - 2.0 * eps / dy ** 2)
+            add(i - 1, j, eps / dx ** 2 + alpha / (2.0 * dx))
+            add(i + 1, j, eps / dx ** 2 - alpha / (2.0 * dx))
+            add(i, j - 1, eps / dy ** 2 + alpha / (2.0 * dy))
+            add(i, j + 1, eps / dy ** 2 - alpha / (2.0 * dy))
+            for k in sorted(ent):
+                col.append(k)
+                val.append(ent[k])
+            row_ptr.append(len(col))
+    prob = ReactionDiffusionCSR(row_ptr, col, val, (0.0, -0.5 * gamma, 1.5 * gamma, -gamma))
+    prob.nx, prob.ny = nx, ny
+    xs, ys = dx * np.arange(nx), dy * np.arange(ny)
+    X, Y = np.meshgrid(xs, ys, indexing="xy")
+    u0 = (256.0 * (X * Y * (1.0 - X) * (1.0 - Y)) ** 2 + 0.3).ravel()
+    return prob, u0
+
+
 # ---------------------------------------------------------------------------
 # one step / integration
 # ---------------------------------------------------------------------------

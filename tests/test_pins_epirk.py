@@ -241,3 +241,83 @@ def test_stiff_orders_on_the_semilinear_problem():
     print(f"exprb5s3: {['%.2e' % e for e in e5]} order {s5:.2f}; epirk5p1: {['%.2e' % e for e in e1]} order {s1:.2f}")
     assert 4.6 <= s5 <= 5.4, (s5, e5)
     assert 2.6 <= s1 <= 3.6, (s1, e1)
+
+
+# ---------------------------------------------------------------------------
+# ADR 2D with homogeneous Neumann boundaries (reading E10): the general
+# CSR linear part of ReactionDiffusionCSR
+# ---------------------------------------------------------------------------
+def _adr_f_reference(u, nx, ny, eps, alpha, gamma):
+    """f(u) by an independent formulation: numpy's reflect padding IS the mirrored ghost
+    node u_{-1} = u_{1}; central differences on the padded array."""
+    U = u.reshape(ny, nx)
+    dx, dy = 1.0 / (nx - 1), 1.0 / (ny - 1)
+    P = np.pad(U, 1, mode="reflect")
+    c, w, e, s, n = P[1:-1, 1:-1], P[1:-1, :-2], P[1:-1, 2:], P[:-2, 1:-1], P[2:, 1:-1]
+    lap = (w - 2 * c + e) / dx ** 2 + (s - 2 * c + n) / dy ** 2
+    adv = (e - w) / (2 * dx) + (n - s) / (2 * dy)
+    return (eps * lap - alpha * adv + gamma * c * (c - 0.5) * (1.0 - c)).ravel()
+
+
+def test_adr_neumann_matches_reflect_padded_differences():
+    rng = np.random.default_rng(3)
+    for nx, ny in ((9, 9), (12, 7)):
+        prob, u0 = E.adr_neumann(nx, ny)
+        u = u0 + 0.2 * rng.standard_normal(prob.dim)
+        ref = _adr_f_reference(u, nx, ny, 0.01, -10.0, 100.0)
+        assert np.linalg.norm(prob.f(u) - ref) <= 1e-12 * np.linalg.norm(ref)
+        # constants are in the kernel of the linear part (no-flux boundaries, central advection)
+        assert np.abs(prob.lmul(np.ones(prob.dim))).max() <= 1e-10
+        # initial condition as printed (P:609): 0.3 on the boundary, 256/4^4 + 0.3 = 1.3 at the centre
+        assert np.allclose(u0.reshape(ny, nx)[0], 0.3) and np.allclose(u0.reshape(ny, nx)[:, -1], 0.3)
+    prob, u0 = E.adr_neumann(9, 9)
+    assert abs(u0.reshape(9, 9)[4, 4] - 1.3) <= 1e-15
+
+
+def test_adr_jacobian_and_remainder():
+    rng = np.random.default_rng(9)
+    prob, u0 = E.adr_neumann(10, 8)
+    y = u0 + 0.05 * rng.standard_normal(prob.dim)
+    x = rng.standard_normal(prob.dim)
+    h = 1e-6
+    fd = (prob.f(y + h * x) - prob.f(y - h * x)) / (2 * h)
+    jx = prob.jmul(y, x)
+    assert np.linalg.norm(fd - jx) <= 1e-6 * np.linalg.norm(jx)
+    full = prob.f(y) - prob.f(u0) - prob.jmul(u0, y - u0)
+    assert np.linalg.norm(prob.remainder(u0, y) - full) <= 1e-10 * np.linalg.norm(full)
+    # the KIOPS operator h J(y) as CSR against the dense Jacobian
+    import scipy.sparse as sp
+
+    op = prob.kiops_op(y, 0.01)
+    A = sp.csr_matrix((op["vals"], op["col_idx"], op["row_ptr"]), shape=(prob.dim, prob.dim)).toarray()
+    J = np.column_stack([prob.jmul(y, e) for e in np.eye(prob.dim)])
+    assert np.abs(A - 0.01 * J).max() <= 1e-12 * np.abs(J).max()
+
+
+@pytest.mark.parametrize("scheme", E.SCHEMES)
+def test_adr_order_four_against_an_independent_integrator(scheme):
+    # reference: scipy's implicit Radau at tight tolerances on the same semi-discrete system
+    from scipy.integrate import solve_ivp
+
+    prob, u0 = E.adr_neumann(10, 10)
+    T = 0.02
+    ref = solve_ivp(lambda t, y: prob.f(y), (0.0, T), u0, method="Radau", rtol=1e-12, atol=1e-13,
+                    jac=lambda t, y: np.column_stack([prob.jmul(y, e) for e in np.eye(prob.dim)])).y[:, -1]
+    steps = [2, 4, 8, 16]
+    errs = []
+    for n in steps:
+        y, _ = E.integrate(prob, scheme, u0, 0.0, T, n, tol=1e-13)
+        errs.append(np.linalg.norm(y - ref) / np.linalg.norm(ref))
+    slope = np.polyfit(np.log([1.0 / n for n in steps]), np.log(errs), 1)[0]
+    print(f"ADR {scheme}: errors {['%.2e' % e for e in errs]}, observed order {slope:.2f}")
+    assert 3.6 <= slope <= 4.6, (slope, errs)
+
+
+@pytest.mark.parametrize("scheme", E.SCHEMES)
+def test_adr_grouped_step_equals_naive_per_term_evaluation(scheme):
+    prob, y = E.adr_neumann(7, 6)
+    h = 0.004
+    J = np.column_stack([prob.jmul(y, e) for e in np.eye(prob.dim)])
+    got, _, _ = E.step(prob, scheme, y, h, tol=1e-13)
+    ref = naive_step(prob, scheme, y, h, J)
+    assert np.linalg.norm(got - ref) <= 1e-9 * np.linalg.norm(ref), (scheme, np.linalg.norm(got - ref))
