@@ -204,6 +204,13 @@ kiops_status kiops_set_forced_schedule(kiops_ctx c, const double *tau, const int
  * *npass: number of basis vectors formed in the current substep. */
 kiops_status kiops_debug_basis(kiops_ctx c, double *h, double *sig, int32_t *npass);
 
+/* The operator's value arrays (diag, kappa, CSR vals; DEVICE, borrowed) may be rewritten
+ * by the caller between applies (e.g. a new Jacobian per time step, Sec. 3.6).  Stencil
+ * operators read them at every apply; a CSR operator is applied from the SELL-32 copy
+ * made at kiops_create, which this call rebuilds from the current vals (same sparsity
+ * pattern; asynchronous on the ctx stream).  No-op for the other kinds. */
+kiops_status kiops_refresh_operator(kiops_ctx c);
+
 /* Destroys the ctx (graph, host state).  The workspace stays owned by the caller. */
 kiops_status kiops_destroy(kiops_ctx c);
 
@@ -224,9 +231,9 @@ const char *kiops_last_error(kiops_ctx c);
  *   call 2 (Task II): phi_1(hJ_n) h f + phi_3(hJ_n) b_3 + phi_4(hJ_n) b_4 (p = 4, T = 1);
  *   u_{n+1} = u_n + (call-2 output).
  * Each call's m starts from the same call's final m of the previous step (Sec. 3.6).
- * Problem class: u' = L u + R(u) on a periodic nx x ny grid, L a constant 5-point
- * stencil, R a cubic polynomial applied pointwise (Allen-Cahn: alpha lap(u) + u - u^3,
- * P:593-597).  J(u) = L + diag(R'(u)); for this class the remainder
+ * Problem class: u' = L u + R(u), R a cubic polynomial applied pointwise, L constant:
+ * a 5-point stencil on a periodic nx x ny grid (Allen-Cahn: alpha lap(u) + u - u^3,
+ * P:593-597) or a general CSR matrix (ADR with Neumann boundaries).  J(u) = L + diag(R'(u)); for this class the remainder
  * r(U) = f(U) - f(u_n) - J_n (U - u_n) equals R(U) - R(u_n) - R'(u_n)(U - u_n)
  * exactly (the linear terms cancel), which is what the stage kernel evaluates.
  * =========================================================================== */
@@ -236,6 +243,17 @@ typedef struct {
   int64_t nx, ny;          /* periodic grid, N = nx*ny, x fastest                          */
   double w[5];             /* L: {W, E, S, N, C} weights (alpha lap: alpha/dx^2 {1,1,1,1,-4}) */
   double c[4];             /* R(u) = c[0] + c[1] u + c[2] u^2 + c[3] u^3                   */
+  /* Optional general linear part (non-periodic boundaries, advection, ...; e.g. the ADR
+   * problem with homogeneous Neumann boundaries): when L_row_ptr != NULL, L
+   * is this CSR matrix with N = nx*ny rows (DEVICE arrays, borrowed for the ctx's life,
+   * constant; int64 row_ptr[N+1], int32 col_idx[nnz], fp64 vals[nnz]) and w is ignored.
+   * Every row must hold its diagonal entry (kiops_epirk_create checks: INVALID_ARG).
+   * The KIOPS operator h J_n = h (L + diag R'(u_n)) is then a KIOPS_OP_CSR operator whose
+   * values the driver rewrites every step (kiops_refresh_operator).                    */
+  const int64_t *L_row_ptr;
+  const int32_t *L_col_idx;
+  const double *L_vals;
+  int64_t L_nnz;
 } kiops_rd_problem;
 
 typedef struct {

@@ -20,6 +20,10 @@ struct EpProblem {
   double w[5];  // {W, E, S, N, C}
   double c[4];  // R(u) = c0 + c1 u + c2 u^2 + c3 u^3
   double h;
+  // general linear part (kiops_rd_problem.L_*): CSR, NULL for the periodic stencil
+  const long long *rp;
+  const int *ci;
+  const double *lv;
 };
 
 __device__ __forceinline__ double ep_R(const EpProblem &q, double u) {
@@ -41,6 +45,29 @@ __global__ void __launch_bounds__(256) k_ep_f(EpProblem q, const double *__restr
     const double f = Lu + ep_R(q, uc);
     d[i] = q.h * ep_dR(q, uc);
     b1[i] = q.h * f;
+  }
+}
+
+// CSR linear part: f_n = L u + R(u), b1 = h f_n, and the values of the KIOPS operator
+// h J_n = h (L + diag R'(u_n)) on L's pattern (jv), one row per thread (row sums in
+// storage order, as the oracle's).  bad: counts rows without a diagonal entry.
+__global__ void __launch_bounds__(256) k_ep_f_csr(EpProblem q, const double *__restrict__ u, double *__restrict__ jv,
+                                                  double *__restrict__ b1, int *__restrict__ bad) {
+  const long long N = q.nx * q.ny;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < N; i += (long long)gridDim.x * blockDim.x) {
+    const double uc = u[i], hd = q.h * ep_dR(q, uc);
+    double Lu = 0.0;
+    bool has = false;
+    for (long long e = q.rp[i]; e < q.rp[i + 1]; e++) {
+      const int c = q.ci[e];
+      const double v = q.lv[e];
+      Lu += v * u[c];
+      const bool dg = c == (int)i;
+      has = has || dg;
+      if (jv) jv[e] = dg ? q.h * v + hd : q.h * v;
+    }
+    if (b1) b1[i] = q.h * (Lu + ep_R(q, uc));
+    if (!has && bad) atomicAdd(bad, 1);
   }
 }
 
@@ -146,6 +173,7 @@ struct kiops_epirk_s {
   cudaStream_t stream = nullptr;
   double *d = nullptr, *b1 = nullptr, *zero = nullptr, *o1[3] = {}, *o2[2] = {}, *o3 = nullptr, *t1 = nullptr,
          *t2 = nullptr;
+  double *jv = nullptr;          // CSR linear part: the values of h J_n (L_nnz doubles)
   int m[3] = {0, 0, 0};          // warm start of calls 1-3 (Sec. 3.6, reading E1)
   bool record = false;           // kiops_epirk_record_history
   struct Forced {
@@ -161,14 +189,25 @@ struct kiops_epirk_s {
 namespace {
 constexpr int EP_VECS = 11;  // d, b1, zero, o1[3], o2[2], o3, t1, t2
 
-kiops_operator_desc ep_desc(const kiops_rd_problem *pb, double h, const double *d) {
+kiops_operator_desc ep_desc(const kiops_rd_problem *pb, double h, const double *d, const double *jv = nullptr) {
   kiops_operator_desc o{};
+  if (pb->L_row_ptr) {  // h J_n as a CSR operator on L's pattern; the driver rewrites jv every step
+    o.kind = KIOPS_OP_CSR;
+    o.periodic = 1;
+    o.nx = pb->nx * pb->ny; o.ny = 1; o.nz = 1;
+    o.row_ptr = pb->L_row_ptr; o.col_idx = pb->L_col_idx; o.vals = jv ? jv : pb->L_vals; o.nnz = pb->L_nnz;
+    return o;
+  }
   o.kind = KIOPS_OP_STENCIL2D5;
   o.periodic = 1;
   o.nx = pb->nx; o.ny = pb->ny; o.nz = 1;
   for (int i = 0; i < 5; i++) o.w[i] = h * pb->w[i];  // the matrix argument is h J_n
   o.diag = d;
   return o;
+}
+
+size_t ep_jv_bytes(const kiops_rd_problem *pb) {
+  return pb->L_row_ptr ? (((size_t)pb->L_nnz * sizeof(double) + 255) & ~(size_t)255) : 0;
 }
 
 bool ep_uses(int scheme, int which) {  // 0: kA, 1: kB, 2: kC
@@ -179,6 +218,7 @@ bool ep_uses(int scheme, int which) {  // 0: kA, 1: kB, 2: kC
 
 kiops_status ep_sizes(const kiops_rd_problem *pb, int scheme, const kiops_options *o, size_t b[3], size_t *vec) {
   if (!pb || !o || pb->nx < 1 || pb->ny < 1) return KIOPS_ERR_INVALID_ARG;
+  if (pb->L_row_ptr && (!pb->L_col_idx || !pb->L_vals || pb->L_nnz < pb->nx * pb->ny)) return KIOPS_ERR_INVALID_ARG;
   const double fake = 0.0;
   kiops_operator_desc dsc = ep_desc(pb, 1.0, &fake);
   const int pk[3] = {1, 4, 3}, t1[3] = {1, 0, 1};
@@ -203,7 +243,7 @@ kiops_status kiops_epirk_workspace_bytes(const kiops_rd_problem *pb, int scheme,
   size_t b[3], vec;
   const kiops_status s = ep_sizes(pb, scheme, o, b, &vec);
   if (s != KIOPS_OK) return s;
-  *bytes = b[0] + b[1] + b[2] + EP_VECS * vec;
+  *bytes = b[0] + b[1] + b[2] + EP_VECS * vec + ep_jv_bytes(pb);
   return KIOPS_OK;
 }
 
@@ -217,7 +257,8 @@ kiops_status kiops_epirk_create(const kiops_rd_problem *pb, int scheme, double h
   kiops_status s = ep_sizes(pb, scheme, o, b, &vec);
   if (s != KIOPS_OK) return s;
   const size_t kb = b[0] + b[1] + b[2];
-  if (!workspace || ((uintptr_t)workspace & 255) || workspace_bytes < kb + EP_VECS * vec) return KIOPS_ERR_WORKSPACE;
+  if (!workspace || ((uintptr_t)workspace & 255) || workspace_bytes < kb + EP_VECS * vec + ep_jv_bytes(pb))
+    return KIOPS_ERR_WORKSPACE;
   kiops_epirk_ctx e = new (std::nothrow) kiops_epirk_s();
   if (!e) return KIOPS_ERR_WORKSPACE;
   e->scheme = scheme;
@@ -231,7 +272,28 @@ kiops_status kiops_epirk_create(const kiops_rd_problem *pb, int scheme, double h
   double **vp[EP_VECS] = {&e->d, &e->b1, &e->zero, &e->o1[0], &e->o1[1], &e->o1[2], &e->o2[0], &e->o2[1],
                           &e->o3, &e->t1, &e->t2};
   for (int i = 0; i < EP_VECS; i++) *vp[i] = (double *)(ws + kb + (size_t)i * vec);
-  const kiops_operator_desc dsc = ep_desc(pb, h, e->d);
+  if (pb->L_row_ptr) {  // general linear part: check the diagonals, give jv valid values (h L)
+    e->q.rp = (const long long *)pb->L_row_ptr;
+    e->q.ci = (const int *)pb->L_col_idx;
+    e->q.lv = pb->L_vals;
+    e->jv = (double *)(ws + kb + (size_t)EP_VECS * vec);
+    const long long N = pb->nx * pb->ny;
+    const int grid = (int)std::min<long long>((N + 255) / 256, SM_COUNT_HINT * 8);
+    int *bad = (int *)e->t1, hbad = -1;
+    cudaError_t ce = cudaMemsetAsync(e->zero, 0, vec, e->stream);  // (u = 0 for this pass)
+    if (ce == cudaSuccess) ce = cudaMemsetAsync(bad, 0, sizeof(int), e->stream);
+    if (ce == cudaSuccess) {
+      k_ep_f_csr<<<grid, 256, 0, e->stream>>>(e->q, e->zero, e->jv, nullptr, bad);
+      ce = cudaGetLastError();
+    }
+    if (ce == cudaSuccess) ce = cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, e->stream);
+    if (ce == cudaSuccess) ce = cudaStreamSynchronize(e->stream);
+    if (ce != cudaSuccess || hbad != 0) {
+      delete e;
+      return ce != cudaSuccess ? KIOPS_ERR_CUDA : KIOPS_ERR_INVALID_ARG;  // a row of L without its diagonal
+    }
+  }
+  const kiops_operator_desc dsc = ep_desc(pb, h, e->d, e->jv);
   const int pk[3] = {1, 4, 3}, t1[3] = {1, 0, 1};
   kiops_ctx *kc[3] = {&e->kA, &e->kB, &e->kC};
   size_t off = 0;
@@ -323,8 +385,19 @@ kiops_status kiops_epirk_step(kiops_epirk_ctx e, double *u, int nsteps, kiops_ep
   if (cudaGetLastError() != cudaSuccess) { e->err = name " launch"; return KIOPS_ERR_CUDA; }
   for (int n = 0; n < nsteps; n++) {
     kiops_status s;
-    k_ep_f<<<grid, 256, 0, e->stream>>>(e->q, u, e->d, e->b1);
-    EP_LAUNCHED("k_ep_f");
+    if (e->jv) {  // CSR linear part: new values of h J_n, then the SELL copies of the contexts
+      k_ep_f_csr<<<grid, 256, 0, e->stream>>>(e->q, u, e->jv, e->b1, nullptr);
+      EP_LAUNCHED("k_ep_f_csr");
+      kiops_ctx kc[3] = {e->kA, e->kB, e->kC};
+      for (int i = 0; i < 3; i++)
+        if (kc[i] && (s = kiops_refresh_operator(kc[i])) != KIOPS_OK) {
+          e->err = std::string("operator refresh: ") + kiops_last_error(kc[i]);
+          return s;
+        }
+    } else {
+      k_ep_f<<<grid, 256, 0, e->stream>>>(e->q, u, e->d, e->b1);
+      EP_LAUNCHED("k_ep_f");
+    }
     const double *uf[2] = {z, e->b1};
     if (e->scheme == KIOPS_EPIRK4S3 || e->scheme == KIOPS_EPIRK4S3A) {
       const bool asc = e->c2 < e->c3;  // call-1 outputs come in ascending T

@@ -848,6 +848,17 @@ kiops_status kiops_debug_basis(kiops_ctx c, double *h, double *sig, int32_t *npa
   return KIOPS_OK;
 }
 
+kiops_status kiops_refresh_operator(kiops_ctx c) {
+  if (!c) return KIOPS_ERR_INVALID_ARG;
+  if (c->op.kind != KIOPS_OP_CSR) return KIOPS_OK;  // stencil kinds read diag / kappa at every apply
+  const KParams &P = c->P;
+  k_sell_build<<<sm_count() * 8, 256, 0, c->stream>>>(P.N, P.row_ptr, P.col_idx, P.vals, P.sell_off, (int *)P.sell_col,
+                                                         (double *)P.sell_val);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(c, e, "SELL rebuild");
+  return KIOPS_OK;
+}
+
 kiops_status kiops_destroy(kiops_ctx c) {
   if (!c) return KIOPS_ERR_INVALID_ARG;
   if (c->exec) cudaGraphExecDestroy(c->exec);

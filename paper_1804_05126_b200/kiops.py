@@ -59,7 +59,8 @@ SYMBOLS = ["kiops_options_default", "kiops_workspace_bytes", "kiops_create", "ki
 
 
 class RDProblem(C.Structure):
-    _fields_ = [("nx", C.c_int64), ("ny", C.c_int64), ("w", C.c_double * 5), ("c", C.c_double * 4)]
+    _fields_ = [("nx", C.c_int64), ("ny", C.c_int64), ("w", C.c_double * 5), ("c", C.c_double * 4),
+                ("L_row_ptr", C.c_void_p), ("L_col_idx", C.c_void_p), ("L_vals", C.c_void_p), ("L_nnz", C.c_int64)]
 
 
 class EpirkStats(C.Structure):
@@ -105,6 +106,7 @@ def lib():
                                                 C.c_int]
         L.kiops_debug_basis.argtypes = [C.c_void_p, _dp, _dp, C.POINTER(C.c_int32)]
         L.kiops_set_m_init.argtypes = [C.c_void_p, C.c_int]
+        L.kiops_refresh_operator.argtypes = [C.c_void_p]
         L.kiops_epirk_workspace_bytes.argtypes = [C.POINTER(RDProblem), C.c_int, C.POINTER(Options),
                                                   C.POINTER(C.c_size_t)]
         L.kiops_epirk_create.argtypes = [C.POINTER(RDProblem), C.c_int, C.c_double, C.POINTER(Options), C.c_void_p,
@@ -123,7 +125,8 @@ def lib():
         L.kiops_last_error.argtypes = [C.c_void_p]
         L.kiops_last_error.restype = C.c_char_p
         for name in ("kiops_workspace_bytes", "kiops_create", "kiops_apply", "kiops_apply_host", "kiops_apply_hostloop",
-                     "kiops_get_trace", "kiops_set_m_init", "kiops_set_forced_schedule", "kiops_debug_basis",
+                     "kiops_get_trace", "kiops_set_m_init", "kiops_refresh_operator", "kiops_set_forced_schedule",
+                     "kiops_debug_basis",
                      "kiops_destroy", "kiops_epirk_workspace_bytes", "kiops_epirk_create", "kiops_epirk_step",
                      "kiops_epirk_record_history", "kiops_epirk_history", "kiops_epirk_set_forced_schedule",
                      "kiops_epirk_destroy"):
@@ -209,6 +212,13 @@ class Kiops:
             raise KiopsError(s, "kiops_create")
         self.ctx = ctx
         self.last_stats = None
+
+    def refresh_operator(self):
+        """After rewriting the operator's device value arrays in place (diag, kappa, CSR
+        vals): rebuilds the SELL-32 copy of a CSR operator (no-op for the stencil kinds)."""
+        s = lib().kiops_refresh_operator(self.ctx)
+        if s != 0:
+            raise KiopsError(s, "kiops_refresh_operator")
 
     def close(self):
         if getattr(self, "ctx", None):
@@ -307,7 +317,9 @@ def _host_ptr(x):
 class KiopsEpirk:
     """EPIRK4s3 / EPIRK4s3A (Eqs. 50-51) for u' = L u + R(u) on a periodic grid through
     the kiops_epirk_* C ABI: problem {"nx", "ny", "w": 5 stencil weights {W,E,S,N,C},
-    "c": 4 cubic reaction coefficients}, constant step h, KIOPS options."""
+    "c": 4 cubic reaction coefficients}, constant step h, KIOPS options.  A general
+    linear part (e.g. Neumann boundaries, advection) is given instead of "w" as
+    "L": {"row_ptr", "col_idx", "vals"} (CSR, numpy or torch; copied to the device)."""
 
     def __init__(self, problem: dict, scheme: str, h: float, device="cuda:0", stream=None, **options):
         import torch
@@ -321,9 +333,20 @@ class KiopsEpirk:
         pb = RDProblem()
         pb.nx, pb.ny = int(problem["nx"]), int(problem["ny"])
         for i in range(5):
-            pb.w[i] = float(problem["w"][i])
+            pb.w[i] = float(problem["w"][i]) if "w" in problem else 0.0
         for i in range(4):
             pb.c[i] = float(problem["c"][i])
+        self._L = None
+        if problem.get("L") is not None:
+            Lm = problem["L"]
+            rp = torch.as_tensor(Lm["row_ptr"]).to(device=self.device, dtype=torch.int64).contiguous()
+            ci = torch.as_tensor(Lm["col_idx"]).to(device=self.device, dtype=torch.int32).contiguous()
+            lv = torch.as_tensor(Lm["vals"]).to(device=self.device, dtype=torch.float64).contiguous()
+            if rp.numel() != self.N + 1 or ci.numel() != lv.numel():
+                raise ValueError("L: row_ptr needs N + 1 entries, col_idx and vals nnz each")
+            self._L = (rp, ci, lv)  # borrowed by the ctx for its life
+            pb.L_row_ptr, pb.L_col_idx, pb.L_vals = rp.data_ptr(), ci.data_ptr(), lv.data_ptr()
+            pb.L_nnz = int(lv.numel())
         self.pb = pb
         self.opts = default_options(**options)
         nb = C.c_size_t(0)
