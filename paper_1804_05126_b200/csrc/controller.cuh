@@ -1034,6 +1034,12 @@ __global__ void __cluster_dims__(CTRL_CL, 1, 1) __launch_bounds__(CTRL_THREADS, 
   const unsigned rank = cl_rank();
   const bool lead = rank == 0 && threadIdx.x == 0;
   const unsigned long long t_start = gtimer();
+#ifdef KIOPS_PHASE_DEBUG
+  unsigned long long tph[8] = {t_start, 0, 0, 0, 0, 0, 0, 0};
+#define CTRL_STAMP(i) tph[i] = gtimer()
+#else
+#define CTRL_STAMP(i) do { } while (0)
+#endif
 
   // phase 0: every thread reads the same state
   const int stop = (st->status != 0 || st->npass < 1) ? 1 : (st->zero_start ? 2 : 0);
@@ -1043,6 +1049,7 @@ __global__ void __cluster_dims__(CTRL_CL, 1, 1) __launch_bounds__(CTRL_THREADS, 
   const double tau = final_ ? rem0 : st->tau;
   const int j = st->npass - 1, happy = st->happy, l0 = st->l;
   cl_sync();  // nobody writes the state before everyone has read it
+  CTRL_STAMP(1);
 
   if (stop == 1) {
     if (lead) {
@@ -1076,8 +1083,10 @@ __global__ void __cluster_dims__(CTRL_CL, 1, 1) __launch_bounds__(CTRL_THREADS, 
     Mh[r + (size_t)LDH * c] = v;
   }
   cl_sync();
+  CTRL_STAMP(2);
   const unsigned long long t_e0 = gtimer();
   const int nm = cl_expm(n1, Mh, tau, F, scr, sm);  // Alg. 1 l.18
+  CTRL_STAMP(3);
   if (lead) {
     st->ns_expm += gtimer() - t_e0;
     st->tau = tau;
@@ -1130,8 +1139,10 @@ __global__ void __cluster_dims__(CTRL_CL, 1, 1) __launch_bounds__(CTRL_THREADS, 
     st->bc_accept = accept;
     st->bc_ntau = n_tau;
   }
+  CTRL_STAMP(4);
   cl_sync();
   const int accept = st->bc_accept, n_tau = st->bc_ntau;
+  CTRL_STAMP(5);
   if (accept) {
     // Alg. 3: coefficients of the one-pass GEMV.  Rows 0..n_tau-1 are the crossed
     // T_{l+k} (F2 = exp((T_{l+k} - T_now) H_j), l.13-15); the last row is the
@@ -1193,6 +1204,7 @@ __global__ void __cluster_dims__(CTRL_CL, 1, 1) __launch_bounds__(CTRL_THREADS, 
       write_exact_tail(P, st->t_now, st->mu, P.tails + 1 * KMAXP);  // next substep's exact tail (Eq. 47)
     }
   }
+  CTRL_STAMP(6);
   if (lead) {
     const bool more = st->status == 0 && st->t_now < st->t_end;
     const bool cont = more && st->attempt < P.max_attempts;
@@ -1201,7 +1213,14 @@ __global__ void __cluster_dims__(CTRL_CL, 1, 1) __launch_bounds__(CTRL_THREADS, 
     set_cond(P, COND_INNER, (cont && st->npass < st->m + 1) ? 1u : 0u);
     set_cond(P, COND_ACCEPT, accept ? 1u : 0u);
     st->ns_ctrl += gtimer() - t_start;
+#ifdef KIOPS_PHASE_DEBUG
+    CTRL_STAMP(7);
+    printf("CTRL j=%d accept=%d ns: read+sync %llu assemble+sync %llu expm %llu lead %llu sync %llu accept-path %llu tail %llu total %llu\n",
+           j, accept, tph[1] - tph[0], tph[2] - tph[1], tph[3] - tph[2], tph[4] - tph[3], tph[5] - tph[4], tph[6] - tph[5],
+           tph[7] - tph[6], tph[7] - tph[0]);
+#endif
   }
+#undef CTRL_STAMP
 }
 
 // ---------------------------------------------------------------------------
