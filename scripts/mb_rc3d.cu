@@ -15,6 +15,13 @@
 
 #include "../paper_1804_05126_b200/csrc/rc3d.cuh"
 
+#ifndef MB_XALIGN
+#define MB_XALIGN 1   // padded row pitch rounded up to a multiple of this many doubles
+#endif
+#define XPITCH(nx) (((nx) + 4 + MB_XALIGN - 1) / MB_XALIGN * MB_XALIGN)
+#ifndef MB_L2PROMO
+#define MB_L2PROMO CU_TENSOR_MAP_L2_PROMOTION_L2_256B
+#endif
 #ifndef MB_HM
 #define MB_HM 7
 #endif
@@ -53,7 +60,7 @@ __host__ __device__ inline double hval(int slot, long long i) {
 
 // fill slot s over the padded grid: value of the periodic image (ghosts = copies)
 __global__ void k_fill(double *V, long long ldN, int s, int nx, int ny, int nz) {
-  const int Xp = nx + 4, Yp = ny + 4;
+  const int Xp = XPITCH(nx), Yp = ny + 4;
   const long long np = (long long)Xp * Yp * nz;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < np; i += (long long)gridDim.x * blockDim.x) {
     const int xp = (int)(i % Xp), yp = (int)((i / Xp) % Yp), z = (int)(i / ((long long)Xp * Yp));
@@ -62,11 +69,15 @@ __global__ void k_fill(double *V, long long ldN, int s, int nx, int ny, int nz) 
   }
 }
 
+__global__ void k_scale(double *a, long long n, double f) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) a[i] *= f;
+}
+
 __device__ __forceinline__ double at(const double *V, long long ldN, int s, int nx, int ny, int nz, int x, int y, int z) {
   x = (x % nx + nx) % nx;
   y = (y % ny + ny) % ny;
   z = (z % nz + nz) % nz;
-  return V[(size_t)s * ldN + (x + 2) + (long long)(nx + 4) * ((y + 2) + (long long)(ny + 4) * z)];
+  return V[(size_t)s * ldN + (x + 2) + (long long)XPITCH(nx) * ((y + 2) + (long long)(ny + 4) * z)];
 }
 __device__ double Aop(const double *V, long long ldN, int s, int nx, int ny, int nz, int x, int y, int z, double hh,
                       const double *U, long long ldU) {
@@ -109,11 +120,12 @@ __global__ void k_ref_dots(const double *V, long long ldN, int nx, int ny, int n
   for (int q = 0; q < 5; q++) atomicAdd(dots + q, s[q]);
 }
 __global__ void k_check(const double *XO, const double *XK, int nx, int ny, int nz, double *err) {
-  const int Xp = nx + 4, Yp = ny + 4;
+  const int Xp = XPITCH(nx), Yp = ny + 4;
   const long long np = (long long)Xp * Yp * nz;
   double e1 = 0.0, e2 = 0.0;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < np; i += (long long)gridDim.x * blockDim.x) {
     const int xp = (int)(i % Xp), yp = (int)((i / Xp) % Yp), z = (int)(i / ((long long)Xp * Yp));
+    if (xp >= nx + 4) continue;  // pitch padding
     const int x = (xp - 2 + nx) % nx, y = (yp - 2 + ny) % ny;
     const double ref = XK[x + (long long)nx * (y + (long long)ny * z)];
     const double d = fabs(XO[i] - ref);
@@ -201,7 +213,7 @@ int main(int argc, char **argv) {
   int dev = 0, sms = 0;
   CKR(cudaSetDevice(dev));
   CKR(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  const int Xp = nx + 4, Yp = ny + 4;
+  const int Xp = XPITCH(nx), Yp = ny + 4;
   const long long ldN = ((long long)Xp * Yp * nz + 31) / 32 * 32;
   const int nslot = MB_ROT ? 13 : 6;  // 0 x_{k-1}, 1 x_{k-2}, 2 kappa, 3-4 B, 5 x_k (MB_ROT: 5..12 basis ring)
   double *V;
@@ -219,7 +231,7 @@ int main(int argc, char **argv) {
   for (int m = 0; m < 2; m++) {
     cuuint32_t box[4] = {68, (cuuint32_t)(m == 0 ? C::RA : C::RB), 1, 1};
     CUresult r = enc(&maps[m], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, V, gdim, gstr, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                     CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                     CU_TENSOR_MAP_SWIZZLE_NONE, MB_L2PROMO, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) { fprintf(stderr, "encode failed %d\n", (int)r); return 1; }
   }
   void *dmaps;
@@ -233,6 +245,12 @@ int main(int argc, char **argv) {
   G.V = V;
   const double h = 1.0 / nx;
   G.hh = 0.5 / (h * h);
+#if RC3_KSCALED  // the kappa slot holds hh kappa; the references then use hh = 1
+  k_scale<<<1184, 256>>>(V + 2 * (size_t)ldN, (long long)XPITCH(nx) * (ny + 4) * nz, G.hh);
+  const double hh_ref = 1.0;
+#else
+  const double hh_ref = G.hh;
+#endif
   rc3::PassArgs<PM> Q{};
   Q.k = 3; Q.slot_prev = 0; Q.slot_pp = 1; Q.xout = V + 5 * ldN;
   Q.a0 = 1.0 / 3000.0; Q.a1 = 0.3; Q.a2 = 0.2; Q.btp[0] = 0.7; Q.btp[1] = -0.4; Q.btc[0] = 0.25; Q.btc[1] = 0.6; Q.use_r = 1;
@@ -253,9 +271,9 @@ int main(int argc, char **argv) {
   CKR(cudaGetLastError());
   CKR(cudaDeviceSynchronize());
   // k = 3 is odd: parts with part ^ 1 odd march down -- same values either way up to rounding order of r
-  k_ref_xk<<<1184, 256>>>(V, ldN, nx, ny, nz, G.hh, Q.a0, Q.a1, Q.a2, Q.btp[0], Q.btp[1], XK);
+  k_ref_xk<<<1184, 256>>>(V, ldN, nx, ny, nz, hh_ref, Q.a0, Q.a1, Q.a2, Q.btp[0], Q.btp[1], XK);
   CKR(cudaMemset(rdots, 0, 5 * sizeof(double)));
-  k_ref_dots<<<1184, 256>>>(V, ldN, nx, ny, nz, G.hh, Q.btc[0], Q.btc[1], XK, rdots);
+  k_ref_dots<<<1184, 256>>>(V, ldN, nx, ny, nz, hh_ref, Q.btc[0], Q.btc[1], XK, rdots);
   CKR(cudaMemset(err, 0, 2 * sizeof(double)));
   k_check<<<1184, 256>>>(V + 5 * ldN, XK, nx, ny, nz, err);
   CKR(cudaDeviceSynchronize());
