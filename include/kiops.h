@@ -204,6 +204,14 @@ kiops_status kiops_set_forced_schedule(kiops_ctx c, const double *tau, const int
  * *npass: number of basis vectors formed in the current substep. */
 kiops_status kiops_debug_basis(kiops_ctx c, double *h, double *sig, int32_t *npass);
 
+/* TEST HOOK: f = exp(scale * m) by the controller's own projected exponential (Pade-13
+ * scaling and squaring, reading R17; the single-CTA shared-memory path for
+ * n <= 48, the cluster path above), so that it can be compared with the oracle's directly.
+ * m, f: HOST, n x n doubles, column-major, leading dimension n; 1 <= n <= m_max_cap + 1
+ * (129).  *products (may be NULL): the number of dense products.  Uses the ctx's scratch:
+ * not concurrently with kiops_apply.  NONFINITE for a zero pivot / non-finite norm. */
+kiops_status kiops_debug_expm(kiops_ctx c, int n, const double *m, double scale, double *f, int32_t *products);
+
 /* The operator's value arrays (diag, kappa, CSR vals; DEVICE, borrowed) may be rewritten
  * by the caller between applies (e.g. a new Jacobian per time step, Sec. 3.6).  Stencil
  * operators read them at every apply; a CSR operator is applied from the SELL-32 copy

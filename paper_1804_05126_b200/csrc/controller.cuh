@@ -1232,6 +1232,21 @@ __global__ void __cluster_dims__(CTRL_CL, 1, 1) __launch_bounds__(CTRL_THREADS, 
 // running solution (basis slot 1) is written on the whole padded grid -- its ghosts
 // are the same combination of the basis ghosts, i.e. again the periodic images -- and
 // the caller's outputs on the interior points only, in their natural layout.
+// TEST HOOK (kiops_debug_expm): F = exp(scale M) by the controller's own exponential
+// (cl_expm: the single-CTA shared-memory path for n <= SMALL_N, the cluster path above),
+// on the ctx's scratch.  M, F: global, n x n column-major with leading dimension n.
+__global__ void __cluster_dims__(CTRL_CL, 1, 1) __launch_bounds__(CTRL_THREADS, 1)
+    k_debug_expm(KParams P, int n, const double *M, double scale, double *Fout, int *rc) {
+  extern __shared__ double sm[];
+  double *Mh = P.scratch + 8 * (size_t)LDH * LDH, *F = P.scratch + 9 * (size_t)LDH * LDH;
+  for (int e = cl_gtid(); e < n * n; e += cl_gsize()) Mh[(e % n) + (size_t)LDH * (e / n)] = M[e];
+  cl_sync();
+  const int nm = cl_expm(n, Mh, scale, F, P.scratch, sm);
+  cl_sync();
+  for (int e = cl_gtid(); e < n * n; e += cl_gsize()) Fout[e] = F[(e % n) + (size_t)LDH * (e / n)];
+  if (cl_gtid() == 0) *rc = nm;
+}
+
 __device__ __forceinline__ void gemv_padded(const KParams &P, int j, int nout, const double *x1) {
   DevState *st = P.st;
   __shared__ double sc[GEMV_OCHUNK * LDH];

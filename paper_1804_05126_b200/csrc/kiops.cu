@@ -848,6 +848,32 @@ kiops_status kiops_debug_basis(kiops_ctx c, double *h, double *sig, int32_t *npa
   return KIOPS_OK;
 }
 
+kiops_status kiops_debug_expm(kiops_ctx c, int n, const double *m, double scale, double *f, int32_t *products) {
+  if (!c || !m || !f || n < 1 || n > KMAXM + 1) return KIOPS_ERR_INVALID_ARG;
+  double *dm = nullptr;
+  int *drc = nullptr;
+  const size_t nb = sizeof(double) * (size_t)n * n;
+  CK(cudaMalloc(&dm, 2 * nb + 16), "debug alloc");
+  drc = (int *)((unsigned char *)dm + 2 * nb);
+  kiops_status s = KIOPS_OK;
+  int hrc = -1;
+  cudaError_t e = cudaMemcpyAsync(dm, m, nb, cudaMemcpyHostToDevice, c->stream);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute((void *)k_debug_expm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctrl_smem_bytes());
+  if (e == cudaSuccess) {
+    k_debug_expm<<<CTRL_CL, CTRL_THREADS, ctrl_smem_bytes(), c->stream>>>(c->P, n, dm, scale, dm + (size_t)n * n, drc);
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) e = cudaMemcpyAsync(f, dm + (size_t)n * n, nb, cudaMemcpyDeviceToHost, c->stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&hrc, drc, sizeof(int), cudaMemcpyDeviceToHost, c->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+  if (e != cudaSuccess) s = cuda_fail(c, e, "debug expm");
+  cudaFree(dm);
+  if (products) *products = hrc;
+  if (s == KIOPS_OK && hrc < 0) return KIOPS_ERR_NONFINITE;
+  return s;
+}
+
 kiops_status kiops_refresh_operator(kiops_ctx c) {
   if (!c) return KIOPS_ERR_INVALID_ARG;
   if (c->op.kind != KIOPS_OP_CSR) return KIOPS_OK;  // stencil kinds read diag / kappa at every apply

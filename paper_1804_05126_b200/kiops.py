@@ -107,6 +107,7 @@ def lib():
         L.kiops_debug_basis.argtypes = [C.c_void_p, _dp, _dp, C.POINTER(C.c_int32)]
         L.kiops_set_m_init.argtypes = [C.c_void_p, C.c_int]
         L.kiops_refresh_operator.argtypes = [C.c_void_p]
+        L.kiops_debug_expm.argtypes = [C.c_void_p, C.c_int, _dp, C.c_double, _dp, C.POINTER(C.c_int32)]
         L.kiops_epirk_workspace_bytes.argtypes = [C.POINTER(RDProblem), C.c_int, C.POINTER(Options),
                                                   C.POINTER(C.c_size_t)]
         L.kiops_epirk_create.argtypes = [C.POINTER(RDProblem), C.c_int, C.c_double, C.POINTER(Options), C.c_void_p,
@@ -125,7 +126,8 @@ def lib():
         L.kiops_last_error.argtypes = [C.c_void_p]
         L.kiops_last_error.restype = C.c_char_p
         for name in ("kiops_workspace_bytes", "kiops_create", "kiops_apply", "kiops_apply_host", "kiops_apply_hostloop",
-                     "kiops_get_trace", "kiops_set_m_init", "kiops_refresh_operator", "kiops_set_forced_schedule",
+                     "kiops_get_trace", "kiops_set_m_init", "kiops_refresh_operator", "kiops_debug_expm",
+                     "kiops_set_forced_schedule",
                      "kiops_debug_basis",
                      "kiops_destroy", "kiops_epirk_workspace_bytes", "kiops_epirk_create", "kiops_epirk_step",
                      "kiops_epirk_record_history", "kiops_epirk_history", "kiops_epirk_set_forced_schedule",
@@ -212,6 +214,18 @@ class Kiops:
             raise KiopsError(s, "kiops_create")
         self.ctx = ctx
         self.last_stats = None
+
+    def debug_expm(self, M, scale=1.0):
+        """TEST HOOK: exp(scale * M) by the controller's projected exponential; M: (n, n) numpy."""
+        M = np.asfortranarray(M, dtype=np.float64)
+        n = M.shape[0]
+        mf = M.ravel(order="F").copy()
+        f = np.zeros(n * n)
+        nm = C.c_int32(0)
+        s = lib().kiops_debug_expm(self.ctx, n, mf.ctypes.data_as(_dp), float(scale), f.ctypes.data_as(_dp), C.byref(nm))
+        if s != 0:
+            raise KiopsError(s, "kiops_debug_expm")
+        return f.reshape((n, n), order="F"), nm.value
 
     def refresh_operator(self):
         """After rewriting the operator's device value arrays in place (diag, kappa, CSR
