@@ -26,6 +26,11 @@ __device__ __forceinline__ unsigned cl_rank() {
 __device__ __forceinline__ int cl_gtid() { return (int)(cl_rank() * blockDim.x + threadIdx.x); }
 __device__ __forceinline__ int cl_gsize() { return (int)(CTRL_CL * blockDim.x); }
 
+// Named barriers of one 512-thread CTA (ids 1, 2): bar.arrive by the warp that publishes,
+// bar.sync by the warps that consume (split hand-off instead of a __syncthreads).
+__device__ __forceinline__ void nb_sync512(int id) { asm volatile("bar.sync %0, 512;" ::"r"(id) : "memory"); }
+__device__ __forceinline__ void nb_arrive512(int id) { asm volatile("bar.arrive %0, 512;" ::"r"(id) : "memory"); }
+
 // D += A B for one 8x8x4 FP64 tensor-core tile (mma.sync m8n8k4 .f64): fragments per
 // lane g = lane/4, t = lane%4: A(g, t), B(t, g), C(g, 2t), C(g, 2t+1).
 __device__ __forceinline__ void dmma_8x8x4(double (&c)[2], double a, double b) {
@@ -201,7 +206,15 @@ __device__ int cl_solve(int n, const double *Qg, double *R, double *LUg, int *pi
   }
     if (warp == 0) pivot(0);
     __syncthreads();
+    // Step k needs column k (multipliers) and s_piv[k], final once its owner has run
+    // pivot(k); every other column is written by its own warp only.  So the hand-off is
+    // split: the owner of column k+1 ARRIVES at a named barrier right after pivot(k+1) and
+    // only then updates its other columns; the other warps wait for it at the top of step
+    // k+1.  The step chain is update(column k+1) + pivot(k+1), not the slowest warp's
+    // whole trailing update (blockDim.x = 512: 15 warps sync, the owner arrives).
+    const bool split = blockDim.x == 512;
     for (int k = 0; k < n; k++) {
+      if (split && k > 0 && (k % nw) != warp) nb_sync512(1 + (k & 1));
       if (s_bad) break;
       const int pv = s_piv[k];
       double l[CL_RS];
@@ -214,11 +227,14 @@ __device__ int cl_solve(int n, const double *Qg, double *R, double *LUg, int *pi
       if (c == k + 1 && c < n) {
         CL_UPDATE(sQ + n * c);
         pivot(k + 1);
+        __syncwarp();
+        if (split) nb_arrive512(1 + ((k + 1) & 1));
         c += nw;
       }
       for (; c < n; c += nw) CL_UPDATE(sQ + n * c);
-      __syncthreads();
+      if (!split) __syncthreads();
     }
+    __syncthreads();
 #undef CL_UPDATE
 #ifdef KIOPS_PHASE_DEBUG
     if (threadIdx.x == 0) printf("cl_solve n=%d factor cycles %lld\n", n, clock64() - f0);
@@ -466,8 +482,8 @@ struct SmemBk {
   // column on the dependency chain).  Same operations as LU + substitution.
   // Q is destroyed.  Returns 0 or -1 (zero / non-finite pivot column), all threads.
   // Requires 16 warps (CTRL_THREADS = 512).
-  static __device__ __forceinline__ void nb_sync(int id) { asm volatile("bar.sync %0, 512;" ::"r"(id) : "memory"); }
-  static __device__ __forceinline__ void nb_arrive(int id) { asm volatile("bar.arrive %0, 512;" ::"r"(id) : "memory"); }
+  static __device__ __forceinline__ void nb_sync(int id) { nb_sync512(id); }
+  static __device__ __forceinline__ void nb_arrive(int id) { nb_arrive512(id); }
   // shared-memory accesses by 32-bit shared address (the step chain carries no generic
   // address arithmetic)
   static __device__ __forceinline__ double lds_f64(unsigned a) {
