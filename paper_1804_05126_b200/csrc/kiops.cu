@@ -368,7 +368,6 @@ static kiops_status build_graph(kiops_ctx c) {
   KParams &P = c->P;
   CK(cudaGraphCreate(&c->graph, 0), "cudaGraphCreate");
   CK(cudaGraphConditionalHandleCreate(&P.h_outer, c->graph, 1, cudaGraphCondAssignDefault), "handle outer");
-  CK(cudaGraphConditionalHandleCreate(&P.h_inner, c->graph, 1, cudaGraphCondAssignDefault), "handle inner");
   CK(cudaGraphConditionalHandleCreate(&P.h_accept, c->graph, 0, cudaGraphCondAssignDefault), "handle accept");
 
   void *fpass = nullptr;
@@ -455,10 +454,25 @@ static kiops_status build_graph(kiops_ctx c) {
   CK(cudaFuncSetAttribute((void *)k_ctrl, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctrl_smem_bytes()),
      "smem attr ctrl");
 
+  // (set before any node is added: every kernel node copies P)
+  const char *fe = getenv("KIOPS_FLAT");  // 0: keep the inner WHILE node around the persistent kernel (A/B switch)
+  const bool flat = finner && P.q == 2 && c->op.kind != KIOPS_OP_CSR && !(fe && fe[0] == '0');
+  P.flat_inner = flat ? 1 : 0;
+  if (!flat) CK(cudaGraphConditionalHandleCreate(&P.h_inner, c->graph, 1, cudaGraphCondAssignDefault), "handle inner");
   cudaGraphNode_t n_setup, n_outer, n_inner, n_ctrl, n_if, n_a, n_b, n_gemv;
   cudaGraph_t b_outer, b_inner, b_if;
   CK(add_kernel(c->graph, &n_setup, nullptr, 0, (void *)k_setup, c->L.grid_setup, 256, 0, &P), "node setup");
   CK(add_cond(c->graph, &n_outer, &n_setup, 1, P.h_outer, cudaGraphCondTypeWhile, &b_outer), "node outer");
+  // persistent inner loop: ONE launch runs every pass of the attempt, so the kernel is a plain
+  // node of the outer loop's body (it returns at once when the attempt needs no pass); the other
+  // paths launch per pass inside an inner WHILE node
+  if (flat) {
+    CK(add_kernel(b_outer, &n_a, nullptr, 0, finner, c->L.grid_pass, c->L.block_pass, c->L.smem_pass, &P), "node inner");
+    cudaLaunchAttributeValue av = {};
+    av.cooperative = 1;
+    CK(cudaGraphKernelNodeSetAttribute(n_a, cudaLaunchAttributeCooperative, &av), "cooperative attr");
+    n_inner = n_a;
+  } else {
   CK(add_cond(b_outer, &n_inner, nullptr, 0, P.h_inner, cudaGraphCondTypeWhile, &b_inner), "node inner");
   if (P.q != 2) {  // generic IOP window (passq.cuh): form, apply, window dots, finalise
     cudaGraphNode_t n_c, n_d;
@@ -477,6 +491,7 @@ static kiops_status build_graph(kiops_ctx c) {
     CK(cudaGraphKernelNodeSetAttribute(n_a, cudaLaunchAttributeCooperative, &av), "cooperative attr");
   } else {
     CK(add_kernel(b_inner, &n_a, nullptr, 0, fpass, c->L.grid_pass, c->L.block_pass, c->L.smem_pass, &P), "node pass");
+  }
   }
   CK(add_kernel(b_outer, &n_ctrl, &n_inner, 1, (void *)k_ctrl, CTRL_CL, CTRL_THREADS, ctrl_smem_bytes(), &P), "node ctrl");
   CK(add_cond(b_outer, &n_if, &n_ctrl, 1, P.h_accept, cudaGraphCondTypeIf, &b_if), "node if");

@@ -94,6 +94,8 @@ struct KParams {
   double *gram;       // generic q: G(i,l) = x_i . x_l, LDH x LDH column-major
   double *qpart;      // generic q: (2 LDH + 2) x QG dot partials
   int no_cond;        // 1: launched outside the graph (host-loop profiling hook)
+  int flat_inner;     // 1: the persistent inner kernel is a plain node of the outer WHILE body (no inner
+                      //    WHILE node): COND_INNER only lives in st->cond, the kernel checks for work itself
   int corrected;      // Saad's corrected scheme (options.corrected): the GEMV also uses x_{j+1}
   // padded mode (3D variable-kappa recompute pass, rc3d.cuh / passrc.cuh): every basis
   // slot is a ghost-padded (nx+4) x (ny+4) x nz grid, and slots m_max+1 .. m_max+p hold
@@ -142,7 +144,7 @@ __device__ __forceinline__ void block_sum(double (&v)[NV], double *red /* smem N
 }
 
 __device__ __forceinline__ void set_cond(const KParams &P, int which, unsigned v) {
-  if (!P.no_cond)
+  if (!P.no_cond && !(P.flat_inner && which == COND_INNER))
     cudaGraphSetConditional(which == COND_OUTER ? P.h_outer : which == COND_INNER ? P.h_inner : P.h_accept, v);
   P.st->cond[which] = v;
 }
