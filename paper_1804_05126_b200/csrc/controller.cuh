@@ -985,6 +985,36 @@ __device__ int cl_expm(int n, const double *M, double scale, double *F, double *
   return reinterpret_cast<int *>(scr + 11 * (size_t)LDH * LDH)[LDH + 1];
 }
 
+// The same with the matrix given by fill(r, c) (every participant, identical values):
+// n <= SMALL_N assembles it directly in CTA 0's shared memory (no global round trip, no
+// cluster barrier before the exponential); larger n through the global scratch Mh.
+template <class Fill>
+__device__ int cl_expm_fill(int n, Fill fill, double *Mh, double scale, double *F, double *scr, double *sm) {
+  if (n > SMALL_N) {
+    for (int e = cl_gtid(); e < n * n; e += cl_gsize()) {
+      const int c = e / n, r = e - c * n;
+      Mh[r + (size_t)LDH * c] = fill(r, c);
+    }
+    cl_sync();
+    ClusterBk bk{scr, sm};
+    return pade_expm(bk, n, Mh, scale, F);
+  }
+  if (cl_rank() == 0) {
+    SmemBk bk{sm, n};
+    double *Ms = bk.mat(8), *Fs = bk.mat(9);
+    bk.clear();
+    for (int j = threadIdx.x >> 6; j < n; j += blockDim.x >> 6)
+      for (int i = threadIdx.x & 63; i < n; i += 64) Ms[i + SM_LD * j] = fill(i, j);
+    __syncthreads();
+    const int r = pade_expm(bk, n, Ms, scale, Fs);
+    for (int j = threadIdx.x >> 6; j < n; j += blockDim.x >> 6)
+      for (int i = threadIdx.x & 63; i < n; i += 64) F[i + (size_t)LDH * j] = Fs[i + SM_LD * j];
+    if (threadIdx.x == 0) reinterpret_cast<int *>(scr + 11 * (size_t)LDH * LDH)[LDH + 1] = r;
+  }
+  cl_sync();
+  return reinterpret_cast<int *>(scr + 11 * (size_t)LDH * LDH)[LDH + 1];
+}
+
 // ---------------------------------------------------------------------------
 // Alg. 4 with readings R4-R10.  Thread 0 only.
 // ---------------------------------------------------------------------------
@@ -1089,19 +1119,17 @@ __global__ void __cluster_dims__(CTRL_CL, 1, 1) __launch_bounds__(CTRL_THREADS, 
     }
     return;
   }
-  const int n1 = j + 1, g0 = cl_gtid(), gs = cl_gsize();
+  const int n1 = j + 1;
   // R1 / Eq. 37: H~ = [[H(1:j,1:j), e_1],[0, 0]] from the IOP band (rows c-q+1 .. c+1)
-  for (int e = g0; e < n1 * n1; e += gs) {
-    const int r = e % n1, c = e / n1;
+  auto htilde = [&](int r, int c) -> double {
     double v = 0.0;
     if (r < j && c < j && r >= c - P.q + 1 && r <= c + 1) v = P.H[r + (size_t)LDH * c];  // IOP band
     if (r == 0 && c == j) v = 1.0;
-    Mh[r + (size_t)LDH * c] = v;
-  }
-  cl_sync();
+    return v;
+  };
   CTRL_STAMP(2);
   const unsigned long long t_e0 = gtimer();
-  const int nm = cl_expm(n1, Mh, tau, F, scr, sm);  // Alg. 1 l.18
+  const int nm = cl_expm_fill(n1, htilde, Mh, tau, F, scr, sm);  // Alg. 1 l.18
   CTRL_STAMP(3);
   if (lead) {
     st->ns_expm += gtimer() - t_e0;
@@ -1181,16 +1209,14 @@ __global__ void __cluster_dims__(CTRL_CL, 1, 1) __launch_bounds__(CTRL_THREADS, 
     cl_sync();
     const int nf = corr ? j + 1 : j;
     for (int k = 0; k < n_tau; k++) {
-      for (int e = g0; e < nf * nf; e += gs) {
-        const int r = e % nf, c = e / nf;
+      auto hj = [&](int r, int c) -> double {  // H_j, or H~ for the corrected scheme
         double v = 0.0;
         if (r < j && c < j && r >= c - P.q + 1 && r <= c + 1) v = P.H[r + (size_t)LDH * c];
         if (corr && r == 0 && c == j) v = 1.0;
-        Mh[r + (size_t)LDH * c] = v;
-      }
-      cl_sync();
+        return v;
+      };
       const double tt = call->T[l0 + k] - t_now;
-      const int nm2 = cl_expm(nf, Mh, tt, F, scr, sm);
+      const int nm2 = cl_expm_fill(nf, hj, Mh, tt, F, scr, sm);
       const double sc = P.task1 ? pow(1.0 / call->T[l0 + k], (double)P.p) : 1.0;
       if (rank == 0) {
         for (int c = threadIdx.x; c < j; c += blockDim.x) {
