@@ -54,7 +54,7 @@ struct InnerCarry {
   double skm1, iskm1, R2km1;      // sig[k-1], 1 / sig[k-1], R2[k-1]
   double nu;
   const double *x1;
-  int m, status_in, go, trip, idle;
+  int m, status_in, go, trip;
   unsigned long long launches;
 };
 // State counters CTA 0 keeps in registers and stores (never read back) every pass.
@@ -244,18 +244,21 @@ __device__ __forceinline__ void inner_loop(const KParams &P, Body &&body, Hooks 
     // loop guard (pass_guard), evaluated identically by every CTA
     C.launches = st->launches + 1;
     const unsigned long long cap = (unsigned long long)(P.max_attempts + 2) * (unsigned long long)(P.m_max + 2);
+    // No pass to run in this attempt (a rejection that only shrank tau: the basis stands,
+    // also the full basis npass = m_max + 1) or an error status -- what an inner WHILE
+    // node's condition would express: the launch ends through the S.k = 0 exit below, so
+    // that the kernel can be a plain node of the outer loop body (flat_inner, kiops.cu).
+    const bool idle = st->npass >= st->m + 1 || st->status != 0;
+    C.trip = (C.launches > cap || (st->npass > P.m_max && !idle)) ? 1 : 0;
     C.status_in = st->status;
     C.m = st->m;
-    // no pass to run in this attempt (a rejection that only shrank tau: the basis stands):
-    // what the inner WHILE's condition expresses; checked here so that the kernel can be a
-    // plain node of the outer loop body (flat_inner)
-    C.idle = (st->npass >= st->m + 1 || st->status != 0) ? 1 : 0;
-    // (a full basis, npass = m_max + 1, is a legitimate idle state; beyond it, or with a
-    // pass to run, npass > m_max is the guard's business)
-    C.trip = (C.launches > cap || (st->npass > P.m_max && !(C.idle && st->npass <= P.m_max + 1))) ? 1 : 0;
     C.nu = st->nu;
     C.x1 = st->x1;
     load_pass_scalars(P, S);
+    if (idle) {
+      S.k = 0;
+      if (blockIdx.x == 0) set_cond(P, COND_INNER, 0u);
+    }
     const int k = S.k;
     if (k >= 1) {
       for (int c = 0; c < KMAXP; c++) {
@@ -272,10 +275,6 @@ __device__ __forceinline__ void inner_loop(const KParams &P, Body &&body, Hooks 
   // one grid barrier per launch: every CTA has read the launch and pass counters
   grid_sync(st, nb, gen);
   if (lead) st->launches = C.launches;
-  if (C.idle && !C.trip) {
-    if (lead) set_cond(P, COND_INNER, 0u);
-    return;
-  }
   if (C.trip || S.k == 0) {
     if (lead && C.trip) {
       st->status = KIOPS_ERR_CUDA;
