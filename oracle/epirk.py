@@ -237,6 +237,36 @@ def adr_neumann(nx, ny=None, eps=0.01, alpha=-10.0, gamma=100.0):
     return prob, u0
 
 
+def allen_cahn_noflow(nx, ny=None, alpha=0.1):
+    """Allen-Cahn 2D as printed: u_t = alpha lap(u) + u - u^3 on [-1, 1]^2 with
+    NO-FLOW (homogeneous Neumann) boundaries, u_0 = 0.1 + 0.1 cos(2 pi x) cos(2 pi y).
+    Same discretisation as adr_neumann (reading E10): nodes x_i = -1 + i dx, dx = 2/(nx-1),
+    mirrored ghost nodes.  (ReactionDiffusion2D is the periodic variant, reading E4.)
+    Returns (problem, u0)."""
+    ny = ny or nx
+    dx, dy = 2.0 / (nx - 1), 2.0 / (ny - 1)
+    row_ptr, col, val = [0], [], []
+    for j in range(ny):
+        for i in range(nx):
+            ent = {}
+            for ii, jj, w in ((i, j, -2.0 * alpha / dx ** 2 - 2.0 * alpha / dy ** 2), (i - 1, j, alpha / dx ** 2),
+                              (i + 1, j, alpha / dx ** 2), (i, j - 1, alpha / dy ** 2), (i, j + 1, alpha / dy ** 2)):
+                ii = -ii if ii < 0 else (2 * (nx - 1) - ii if ii > nx - 1 else ii)  # mirror
+                jj = -jj if jj < 0 else (2 * (ny - 1) - jj if jj > ny - 1 else jj)
+                k = ii + nx * jj
+                ent[k] = ent.get(k, 0.0) + w
+            for k in sorted(ent):
+                col.append(k)
+                val.append(ent[k])
+            row_ptr.append(len(col))
+    prob = ReactionDiffusionCSR(row_ptr, col, val, (0.0, 1.0, 0.0, -1.0))
+    prob.nx, prob.ny = nx, ny
+    xs, ys = -1.0 + dx * np.arange(nx), -1.0 + dy * np.arange(ny)
+    X, Y = np.meshgrid(xs, ys, indexing="xy")
+    u0 = (0.1 + 0.1 * np.cos(2 * np.pi * X) * np.cos(2 * np.pi * Y)).ravel()
+    return prob, u0
+
+
 # ---------------------------------------------------------------------------
 # one step / integration
 # ---------------------------------------------------------------------------

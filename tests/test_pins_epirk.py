@@ -321,3 +321,37 @@ def test_adr_grouped_step_equals_naive_per_term_evaluation(scheme):
     got, _, _ = E.step(prob, scheme, y, h, tol=1e-13)
     ref = naive_step(prob, scheme, y, h, J)
     assert np.linalg.norm(got - ref) <= 1e-9 * np.linalg.norm(ref), (scheme, np.linalg.norm(got - ref))
+
+
+def test_allen_cahn_noflow_matches_reflect_padded_differences():
+    # Allen-Cahn with the paper's no-flow boundaries through the CSR linear part
+    rng = np.random.default_rng(4)
+    for nx, ny in ((9, 9), (11, 6)):
+        prob, u0 = E.allen_cahn_noflow(nx, ny)
+        u = u0 + 0.3 * rng.standard_normal(prob.dim)
+        U = u.reshape(ny, nx)
+        dx, dy = 2.0 / (nx - 1), 2.0 / (ny - 1)
+        P = np.pad(U, 1, mode="reflect")
+        c, w, e, s_, n = P[1:-1, 1:-1], P[1:-1, :-2], P[1:-1, 2:], P[:-2, 1:-1], P[2:, 1:-1]
+        ref = (0.1 * ((w - 2 * c + e) / dx ** 2 + (s_ - 2 * c + n) / dy ** 2) + c - c ** 3).ravel()
+        assert np.linalg.norm(prob.f(u) - ref) <= 1e-12 * np.linalg.norm(ref)
+        assert np.abs(prob.lmul(np.ones(prob.dim))).max() <= 1e-10
+    prob, u0 = E.allen_cahn_noflow(9, 9)
+    assert abs(u0.reshape(9, 9)[4, 4] - 0.2) <= 1e-15 and abs(u0[0] - 0.2) <= 1e-15  # cos(0) = cos(2 pi) = 1
+
+
+@pytest.mark.parametrize("scheme", E.SCHEMES)
+def test_allen_cahn_noflow_order_four(scheme):
+    from scipy.integrate import solve_ivp
+
+    prob, u0 = E.allen_cahn_noflow(10, 10)
+    T = 1.0
+    ref = solve_ivp(lambda t, y: prob.f(y), (0.0, T), u0, method="Radau", rtol=1e-12, atol=1e-13,
+                    jac=lambda t, y: np.column_stack([prob.jmul(y, e) for e in np.eye(prob.dim)])).y[:, -1]
+    steps, errs = [2, 4, 8, 16], []
+    for n in steps:
+        y, _ = E.integrate(prob, scheme, u0, 0.0, T, n, tol=1e-13)
+        errs.append(np.linalg.norm(y - ref) / np.linalg.norm(ref))
+    slope = np.polyfit(np.log([1.0 / n for n in steps]), np.log(errs), 1)[0]
+    print(f"Allen-Cahn no-flow {scheme}: errors {['%.2e' % e for e in errs]}, observed order {slope:.2f}")
+    assert 3.5 <= slope <= 4.8, (slope, errs)
