@@ -20,7 +20,7 @@ import torch  # noqa: E402
 from paper_1804_05126_b200 import KiopsEpirk  # noqa: E402
 
 ap = argparse.ArgumentParser()
-ap.add_argument("--problem", default="allen_cahn", choices=["allen_cahn", "adr"])
+ap.add_argument("--problem", default="allen_cahn", choices=["allen_cahn", "adr", "allen_cahn_noflow"])
 ap.add_argument("--n", type=int, default=1024)
 ap.add_argument("--scheme", default="epirk4s3", choices=["epirk4s3", "epirk4s3a", "epirk5p1", "exprb5s3"])
 ap.add_argument("--h", type=float, default=0.01)
@@ -37,6 +37,12 @@ if a.problem == "adr":
     prob, u0 = E0.adr_neumann(n, n)
     pb = {"nx": n, "ny": n, "c": list(prob.c), "L": {"row_ptr": prob.row_ptr, "col_idx": prob.col_idx, "vals": prob.vals}}
     wname, dname = f"adr_neumann_2d_{n}x{n}", "ADR 2D, homogeneous Neumann (CSR linear part)"
+elif a.problem == "allen_cahn_noflow":
+    from oracle import epirk as E0
+
+    prob, u0 = E0.allen_cahn_noflow(n, n)
+    pb = {"nx": n, "ny": n, "c": list(prob.c), "L": {"row_ptr": prob.row_ptr, "col_idx": prob.col_idx, "vals": prob.vals}}
+    wname, dname = f"allen_cahn_noflow_2d_{n}x{n}", "Allen-Cahn 2D, no-flow boundaries (CSR linear part)"
 else:
     alpha = 0.1
     dx = 2.0 / n
@@ -71,7 +77,7 @@ line = {"metric": f"{a.scheme} step time, {dname} (EPIRK driver, f1)", "value": 
 if a.oracle_steps > 0:
     from oracle import epirk as E
 
-    if a.problem != "adr":
+    if a.problem == "allen_cahn":
         prob = E.ReactionDiffusion2D(n, alpha=alpha)
     y = u0.copy()
     t0 = time.perf_counter()

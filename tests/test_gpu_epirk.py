@@ -193,3 +193,31 @@ def test_refresh_operator_csr_values():
     assert np.linalg.norm(w1[0].cpu().numpy() - ref1) <= 1e-10 * np.linalg.norm(ref1)
     assert np.linalg.norm(ref1 - ref0) > 1e-3 * np.linalg.norm(ref0)  # (the two operators differ)
     k.close()
+
+
+@pytest.mark.parametrize("scheme", E.SCHEMES + E.SCHEMES5)
+def test_epirk_allen_cahn_noflow_matches_oracle(scheme):
+    # the paper's Allen-Cahn problem with its no-flow boundaries through the CSR linear part
+    from paper_1804_05126_b200 import KiopsEpirk
+
+    nx, ny = 30, 22
+    prob, u0 = E.allen_cahn_noflow(nx, ny)
+    pb = {"nx": nx, "ny": ny, "c": list(prob.c),
+          "L": {"row_ptr": prob.row_ptr, "col_idx": prob.col_idx, "vals": prob.vals}}
+    h, n, tol = 0.0625, 3, 1e-12
+    yo, so = E.integrate(prob, scheme, u0, 0.0, n * h, n, tol=tol)
+    k = KiopsEpirk(pb, scheme, h, device=DEV, tol=tol)
+    k.record_history(True)
+    k.set_forced_schedules([(oc["step"], oc["call"], [(r["tau"], r["j"], r["accept"]) for r in oc["trace"]])
+                            for oc in so["calls"]])
+    u = torch.as_tensor(u0.copy(), device=DEV)
+    st = k.step(u, n)
+    torch.cuda.synchronize()
+    rel = np.linalg.norm(u.cpu().numpy() - yo) / np.linalg.norm(yo)
+    hist = k.history()
+    assert len(hist) == len(so["calls"])
+    for gc, oc in zip(hist, so["calls"]):
+        assert gc["attempts"] == [(r["j"], r["accept"]) for r in oc["trace"]], (scheme, oc["step"], oc["call"])
+    assert st["krylov_vectors"] == so["krylov_vectors"]
+    assert rel <= 1e-12, rel
+    k.close()
