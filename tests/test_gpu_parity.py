@@ -405,3 +405,24 @@ def assert_replay_parity_opts(cfg, rtol=1e-10, **over):
         rel = np.linalg.norm(g[l] - o[l]) / max(np.linalg.norm(o[l]), 1e-300)
         print(f"REPLAY {cfg.get('name', '')} {over}: output {l} rel l2 {rel:.2e}")
         assert rel <= rtol, (l, rel)
+
+
+# Random geometries of the 3D recompute pass (seeded): tile columns narrower than 64 points,
+# several tile columns with a ragged last one, bands of 1-7 rows, z columns shorter than the
+# TMA ring, every p of the PM templates.  Replay parity against the oracle, as above.
+def _rc_geometries():
+    rng = np.random.default_rng(2024)
+    out = []
+    for _ in range(14):
+        nx = 2 * int(rng.integers(2, 76))     # even, 4 .. 150
+        ny = int(rng.integers(4, 60))
+        nz = int(rng.integers(2, 20))
+        p = int(rng.integers(0, 5))
+        out.append(((nx, ny, nz), p))
+    out += [((4, 6, 3), 2), ((130, 5, 3), 1), ((66, 7, 2), 4), ((128, 4, 5), 0), ((64, 148, 2), 2)]
+    return out
+
+
+@pytest.mark.parametrize("dims,p", _rc_geometries())
+def test_config4_random_geometries(dims, p):
+    assert_replay_parity(config4_p(dims, p))
