@@ -426,3 +426,33 @@ def _rc_geometries():
 @pytest.mark.parametrize("dims,p", _rc_geometries())
 def test_config4_random_geometries(dims, p):
     assert_replay_parity(config4_p(dims, p))
+
+
+# Random 2D / 1D geometries of the lazy pair pass and the persistent loop (seeded): strips
+# narrower than 60 points, a ragged last strip, fewer rows than a strip marches, odd nx (the
+# generic tile kernel), every p.  Config-2 type (advection: non-symmetric stencil, diagonal)
+# and config-3 type operators; trace replay against the oracle.
+def _cfg2d(kind, nx, ny, p, seed):
+    c = (W.config2 if kind == 2 else W.config3)(nx, ny)
+    rng = np.random.default_rng(seed)
+    c["u"] = [c["u"][k] if k < len(c["u"]) else rng.standard_normal(c["N"]) for k in range(p + 1)]
+    c["p"] = p
+    c["name"] += f"_p{p}"
+    return c
+
+
+def _geometries_2d():
+    rng = np.random.default_rng(77)
+    out = []
+    for i in range(12):
+        nx = int(rng.integers(2, 200)) * (2 if i % 4 else 1)  # mostly even, some odd
+        ny = int(rng.integers(1, 120))
+        kind, p = 2 + i % 2, int(rng.integers(0, 5))
+        out.append((kind, max(nx, 3), ny, max(p, 1) if kind == 2 else p, 500 + i))  # (config 2: u_0 = 0, so p >= 1)
+    out += [(2, 4, 1, 3, 1), (3, 8, 3, 3, 5), (2, 62, 9, 1, 2), (3, 60, 8, 0, 3), (3, 122, 2, 4, 4)]
+    return out
+
+
+@pytest.mark.parametrize("kind,nx,ny,p,seed", _geometries_2d())
+def test_2d_random_geometries(kind, nx, ny, p, seed):
+    assert_replay_parity(_cfg2d(kind, nx, ny, p, seed))
