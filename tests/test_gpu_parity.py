@@ -456,3 +456,15 @@ def _geometries_2d():
 @pytest.mark.parametrize("kind,nx,ny,p,seed", _geometries_2d())
 def test_2d_random_geometries(kind, nx, ny, p, seed):
     assert_replay_parity(_cfg2d(kind, nx, ny, p, seed))
+
+
+# CSR (SELL-32) path on random small shapes: rows not a multiple of the 32-row slice, p = 0..4.
+@pytest.mark.parametrize("dims,p", [((5, 3, 2), 2), ((9, 7, 5), 0), ((31, 1, 1), 1), ((33, 2, 1), 4), ((12, 11, 3), 3),
+                                    ((40, 8, 2), 4)])
+def test_csr_random_shapes(dims, p):
+    c = W.config5(*dims)
+    rng = np.random.default_rng(900 + p)
+    c["u"] = [c["u"][k] if k < len(c["u"]) else rng.standard_normal(c["N"]) for k in range(p + 1)][: p + 1]
+    c["p"] = p
+    c["name"] += f"_p{p}"
+    assert_replay_parity(c)
