@@ -1113,8 +1113,7 @@ __global__ void __cluster_dims__(CTRL_CL, 1, 1) __launch_bounds__(CTRL_THREADS, 
       st->gemv_x1 = st->x1;
       st->l = call->n_out - 1;
       st->t_now = st->t_end;
-      st->substeps++;
-      st->attempt++;
+      // (no attempt took place: counters and trace stay as the oracle's, R27)
       set_cond(P, COND_OUTER, 0u); set_cond(P, COND_INNER, 0u); set_cond(P, COND_ACCEPT, 1u);
     }
     return;

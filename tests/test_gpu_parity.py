@@ -193,6 +193,11 @@ def test_zero_start_and_happy_breakdown():
            "m_max": 128, "iop_q": 2, "N": N}
     g, st, tr = gpu_run(cfg)
     assert not np.any(g[0])
+    # R27: no attempt takes place -- counters and trace as the oracle's
+    wo, sto, tro, rc = O.kiops(z, cfg["u"], cfg["T"], tol=cfg["tol"])
+    assert rc == "OK" and tro == [] and tr == []
+    for key in ("substeps", "rejections", "krylov_vectors", "expm_calls", "happy_breakdowns"):
+        assert st[key] == sto[key] == 0, (key, st[key], sto[key])
     cfg["u"] = [rng.standard_normal(N), rng.standard_normal(N)]
     cfg["p"] = 1
     g, st, tr = assert_parity(cfg)
