@@ -473,3 +473,16 @@ def test_csr_random_shapes(dims, p):
     c["p"] = p
     c["name"] += f"_p{p}"
     assert_replay_parity(c)
+
+
+# Many output times (Alg. 3 l.2-15: several outputs crossed inside one substep, outputs on
+# both sides of substep boundaries, the last one at T_end), Task I and Task II, on a 2D and
+# on a 3D (padded GEMV) operator; trace replay.  64 = KIOPS_MAX_OUT.
+@pytest.mark.parametrize("which,n_out,task1", [("c3", 7, 0), ("c3", 7, 1), ("c3", 64, 1), ("c4", 9, 0), ("c4", 5, 1),
+                                               ("c2", 12, 0)])
+def test_many_output_times(which, n_out, task1):
+    c = {"c3": lambda: W.config3(96, 40), "c4": lambda: W.config4(24, 20, 16), "c2": lambda: W.config2(50, 30)}[which]()
+    rng = np.random.default_rng(n_out + 10 * task1)
+    T_end = float(c["T"][-1])
+    c["T"] = np.sort(np.r_[T_end * rng.uniform(0.02, 0.98, n_out - 1), T_end])
+    assert_replay_parity_opts(c, task1=task1)
