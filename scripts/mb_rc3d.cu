@@ -22,6 +22,9 @@
 #ifndef MB_L2PROMO
 #define MB_L2PROMO CU_TENSOR_MAP_L2_PROMOTION_L2_256B
 #endif
+#ifndef MB_CPS
+#define MB_CPS (RC3_TWP == 16 ? 2 : 1)
+#endif
 #ifndef MB_HM
 #define MB_HM 7
 #endif
@@ -141,7 +144,7 @@ __device__ unsigned long long mb_count;  // grid barrier (MB_GRID): monotonic ar
 __device__ rc3::Geom mb_G;
 __device__ rc3::PassArgs<PM> mb_Q;
 #if MB_QREG  // geometry and pass scalars in registers (as in the product), not kernel parameters
-__global__ void __launch_bounds__(C::NT, 1) k_mb(rc3::Geom G0, rc3::PassArgs<PM> Q0, double *dots, int reps) {
+__global__ void __launch_bounds__(C::NT, MB_CPS) k_mb(rc3::Geom G0, rc3::PassArgs<PM> Q0, double *dots, int reps) {
 #if MB_QREG == 1
   rc3::Geom G;
   memcpy(&G, (const void *)&mb_G, sizeof(G));
@@ -229,7 +232,7 @@ int main(int argc, char **argv) {
   cuuint64_t gstr[3] = {(cuuint64_t)Xp * 8, (cuuint64_t)Xp * Yp * 8, (cuuint64_t)ldN * 8};
   cuuint32_t es[4] = {1, 1, 1, 1};
   for (int m = 0; m < 2; m++) {
-    cuuint32_t box[4] = {68, (cuuint32_t)(m == 0 ? C::RA : C::RB), 1, 1};
+    cuuint32_t box[4] = {(cuuint32_t)C::W, (cuuint32_t)(m == 0 ? C::RA : C::RB), 1, 1};
     CUresult r = enc(&maps[m], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, V, gdim, gstr, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
                      CU_TENSOR_MAP_SWIZZLE_NONE, MB_L2PROMO, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) { fprintf(stderr, "encode failed %d\n", (int)r); return 1; }
@@ -239,7 +242,8 @@ int main(int argc, char **argv) {
   CKR(cudaMemcpy(dmaps, maps, sizeof(maps), cudaMemcpyHostToDevice));
   rc3::Geom G{};
   G.nx = nx; G.ny = ny; G.nz = nz; G.Xp = Xp; G.Yp = Yp; G.ldN = ldN;
-  rc3::tiles(nx, ny, nz, sms, HM, &G.ntx, &G.nb, &G.zsplit);
+  const int ctas = sms * MB_CPS;  // CTAs per SM (RC3_TWP = 16: two 32-point-wide tiles per SM)
+  rc3::tiles(nx, ny, nz, ctas, HM, &G.ntx, &G.nb, &G.zsplit);
   G.slot_kappa = 2; G.slot_B = 3;
   G.mapA = dmaps; G.mapB = (char *)dmaps + sizeof(CUtensorMap);
   G.V = V;
@@ -254,7 +258,7 @@ int main(int argc, char **argv) {
   rc3::PassArgs<PM> Q{};
   Q.k = 3; Q.slot_prev = 0; Q.slot_pp = 1; Q.xout = V + 5 * ldN;
   Q.a0 = 1.0 / 3000.0; Q.a1 = 0.3; Q.a2 = 0.2; Q.btp[0] = 0.7; Q.btp[1] = -0.4; Q.btc[0] = 0.25; Q.btc[1] = 0.6; Q.use_r = 1;
-  const int grid = std::min(sms, G.ntx * G.nb * G.zsplit);
+  const int grid = std::min(ctas, G.ntx * G.nb * G.zsplit);
   CKR(cudaMemcpyToSymbol(mb_G, &G, sizeof(G)));
   CKR(cudaMemcpyToSymbol(mb_Q, &Q, sizeof(Q)));
   CKR(cudaFuncSetAttribute(k_mb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::smem_bytes));
