@@ -23,7 +23,7 @@
 #define MB_L2PROMO CU_TENSOR_MAP_L2_PROMOTION_L2_256B
 #endif
 #ifndef MB_CPS
-#define MB_CPS (RC3_TWP == 16 ? 2 : 1)
+#define MB_CPS 1  // CTAs per SM (2 for the 32-point-wide tile prototype, profiles/r02_kernel_evolution.md)
 #endif
 #ifndef MB_HM
 #define MB_HM 7
@@ -242,7 +242,7 @@ int main(int argc, char **argv) {
   CKR(cudaMemcpy(dmaps, maps, sizeof(maps), cudaMemcpyHostToDevice));
   rc3::Geom G{};
   G.nx = nx; G.ny = ny; G.nz = nz; G.Xp = Xp; G.Yp = Yp; G.ldN = ldN;
-  const int ctas = sms * MB_CPS;  // CTAs per SM (RC3_TWP = 16: two 32-point-wide tiles per SM)
+  const int ctas = sms * MB_CPS;
   rc3::tiles(nx, ny, nz, ctas, HM, &G.ntx, &G.nb, &G.zsplit);
   G.slot_kappa = 2; G.slot_B = 3;
   G.mapA = dmaps; G.mapB = (char *)dmaps + sizeof(CUtensorMap);
