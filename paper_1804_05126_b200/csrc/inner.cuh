@@ -376,3 +376,82 @@ template <int PM, int TYM, int CPS, int DD, int NH = 1>
 __global__ void __launch_bounds__(LazyQ<PM, TYM, CPS, DD, NH>::BLOCK, CPS / NH) k_inner_3d_lazyq(KParams P) {
   inner_loop(P, [&](const PassScalars &S, double (&v)[NDOT]) { body_3d_lazyq<PM, TYM, CPS, DD, NH>(P, S, v); });
 }
+
+// ---------------------------------------------------------------------------
+// Persistent inner loop of the CSR path for SMALL matrices (where a pass takes a few
+// microseconds and the two launches + WHILE iteration per pass dominate: the EPIRK driver's
+// CSR Jacobians, reduced grids).  Per pass: the pointwise formation of x_k (k_csr_form's),
+// ONE grid barrier (x_k complete and visible), the SELL-32 SpMV with the five dots
+// (k_sell_spmv's), then the loop's record reduction and finalisation.  x_k is gathered with
+// L2 loads (.cg): it was written in this launch by other CTAs, so the non-coherent path the
+// per-pass SpMV uses for its gathers is not allowed -- which is why the large matrices
+// (config 5) keep the per-pass kernels.  Every thread forms and later reads r, x_{k-1},
+// x_k at its own rows (the same grid-stride map in both loops).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void grid_sync2(DevState *st, unsigned nb, unsigned &gen) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (nb > 1) {
+      __threadfence();
+      if (atomicAdd(&st->bar2_count, 1u) == nb - 1) {
+        st->bar2_count = 0;
+        __threadfence();
+        atomicAdd(&st->bar2_gen, 1u);
+      } else {
+        while (ld_acquire_u32(&st->bar2_gen) == gen) {
+        }
+      }
+      __threadfence();
+    }
+    gen++;
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(256) k_inner_csr(KParams P) {
+  unsigned gen2 = 0;
+  if (threadIdx.x == 0) gen2 = ld_acquire_u32(&P.st->bar2_gen);  // (before this CTA's first arrival)
+  inner_loop(P, [&](const PassScalars &S, double (&v)[NDOT]) {
+    const int k = S.k, p = P.p;
+    const long long i0 = blockIdx.x * (long long)blockDim.x + threadIdx.x, di = (long long)gridDim.x * blockDim.x;
+    if (k >= 2) {  // x_k = a0 r_{k-1} - a1 x_{k-1} - a2 x_{k-2}  (Alg. 2 l.7-10, l.17 folded)
+      const double *r = P.r;
+      for (long long i = i0; i < P.N; i += di) {
+        double xk = S.a0 * r[i] - S.a1 * S.xprev[i];
+        if (S.xpp) xk -= S.a2 * S.xpp[i];
+        S.xout[i] = xk;
+      }
+    }
+    grid_sync2(P.st, gridDim.x, gen2);
+    const double *xk = (k == 1) ? S.xprev : S.xout;
+    const double *xm = S.xprev;
+    const double *__restrict__ sval = P.sell_val;
+    const int *__restrict__ scol = P.sell_col;
+    const long long *__restrict__ soff = P.sell_off;
+    for (long long r = i0; r < P.N; r += di) {
+      const long long sl = r >> 5, o0 = soff[sl] + (r & 31), len = (soff[sl + 1] - soff[sl]) >> 5;
+      double a0 = 0.0, a1 = 0.0;
+      long long q = o0;
+      int kk = 0;
+#pragma unroll 4
+      for (; kk + 1 < len; kk += 2, q += 64) {
+        const double va = __ldg(sval + q), vb = __ldg(sval + q + 32);
+        const int ca = __ldg(scol + q), cb = __ldg(scol + q + 32);
+        a0 = fma(va, __ldcg(xk + ca), a0);
+        a1 = fma(vb, __ldcg(xk + cb), a1);
+      }
+      if (kk < len) a0 = fma(__ldg(sval + q), __ldcg(xk + __ldg(scol + q)), a0);
+      double rr = a0 + a1;
+#pragma unroll
+      for (int c = 0; c < KMAXP; c++)
+        if (c < p) rr += S.B[c][r] * S.btc[c];
+      const double x = xk[r], y = xm[r];
+      v[0] += x * x;
+      v[1] += y * x;
+      v[2] += y * rr;
+      v[3] += x * rr;
+      v[4] += rr * rr;
+      P.r[r] = rr;
+    }
+  });
+}

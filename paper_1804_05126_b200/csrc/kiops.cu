@@ -450,13 +450,36 @@ static kiops_status build_graph(kiops_ctx c) {
       if ((long long)per_sm * sms < c->L.grid_pass) finner = nullptr;  // not co-resident: per-pass launches
     }
   }
+  // CSR: the persistent loop for small matrices only (inner.cuh, k_inner_csr); KIOPS_CSR_PERSIST=0|1
+  // forces per-pass launches / the persistent loop
+  if (P.q == 2 && c->op.kind == KIOPS_OP_CSR && !(pe && pe[0] == '0')) {
+    const char *ce = getenv("KIOPS_CSR_PERSIST");
+    const bool want = ce ? ce[0] != '0' : (c->P.N <= (1LL << 20));
+    if (want) {
+      int dev = 0, sms = 0, per_sm = 0;
+      CK(cudaGetDevice(&dev), "cudaGetDevice");
+      CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "SM count");
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (void *)k_inner_csr, 256, 0), "occupancy csr");
+      if (per_sm >= 1) {
+        finner = (void *)k_inner_csr;
+        // few CTAs: every pass ends in two grid barriers and every CTA reads every CTA's dot record
+        // (measured, EPIRK4s3 steps: ADR 400^2 1.14 / 1.02 / 1.26 ms and Allen-Cahn 500^2 5.99 / 4.46 / 5.14 ms
+        // with 1 / 2 / 4 CTAs per SM; per-pass launches: 1.43 and 5.84)
+        const char *ge = getenv("KIOPS_CSR_CPS");  // CTAs per SM of the persistent CSR loop (default 2)
+        const int cps = std::max(1, std::min(per_sm, ge ? atoi(ge) : 2));
+        c->L.grid_pass = (int)std::min<long long>(c->L.grid_pass, (long long)cps * sms);
+        c->L.block_pass = 256;
+        c->L.smem_pass = 0;
+      }
+    }
+  }
   c->finner = finner;
   CK(cudaFuncSetAttribute((void *)k_ctrl, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctrl_smem_bytes()),
      "smem attr ctrl");
 
   // (set before any node is added: every kernel node copies P)
   const char *fe = getenv("KIOPS_FLAT");  // 0: keep the inner WHILE node around the persistent kernel (A/B switch)
-  const bool flat = finner && P.q == 2 && c->op.kind != KIOPS_OP_CSR && !(fe && fe[0] == '0');
+  const bool flat = finner && P.q == 2 && !(fe && fe[0] == '0');
   P.flat_inner = flat ? 1 : 0;
   if (!flat) CK(cudaGraphConditionalHandleCreate(&P.h_inner, c->graph, 1, cudaGraphCondAssignDefault), "handle inner");
   cudaGraphNode_t n_setup, n_outer, n_inner, n_ctrl, n_if, n_a, n_b, n_gemv;
@@ -480,15 +503,15 @@ static kiops_status build_graph(kiops_ctx c) {
     CK(add_kernel(b_inner, &n_b, &n_a, 1, (void *)k_q_apply, QG, 256, 0, &P), "node q apply");
     CK(add_kernel(b_inner, &n_c, &n_b, 1, (void *)k_q_dots, QG, 256, 0, &P, P.q), "node q dots");
     CK(add_kernel(b_inner, &n_d, &n_c, 1, (void *)k_q_finalize, 1, 256, 0, &P), "node q finalize");
-  } else if (c->op.kind == KIOPS_OP_CSR) {
-    CK(add_kernel(b_inner, &n_a, nullptr, 0, (void *)k_csr_form, c->L.grid_form, 256, 0, &P), "node form");
-    CK(add_kernel(b_inner, &n_b, &n_a, 1, (void *)k_sell_spmv, c->L.grid_pass, 256, 0, &P), "node spmv");
   } else if (finner) {  // the WHILE body runs once: the kernel loops over the passes itself
     CK(add_kernel(b_inner, &n_a, nullptr, 0, finner, c->L.grid_pass, c->L.block_pass, c->L.smem_pass, &P),
        "node inner");
     cudaLaunchAttributeValue av = {};
     av.cooperative = 1;
     CK(cudaGraphKernelNodeSetAttribute(n_a, cudaLaunchAttributeCooperative, &av), "cooperative attr");
+  } else if (c->op.kind == KIOPS_OP_CSR) {
+    CK(add_kernel(b_inner, &n_a, nullptr, 0, (void *)k_csr_form, c->L.grid_form, 256, 0, &P), "node form");
+    CK(add_kernel(b_inner, &n_b, &n_a, 1, (void *)k_sell_spmv, c->L.grid_pass, 256, 0, &P), "node spmv");
   } else {
     CK(add_kernel(b_inner, &n_a, nullptr, 0, fpass, c->L.grid_pass, c->L.block_pass, c->L.smem_pass, &P), "node pass");
   }
@@ -800,14 +823,14 @@ kiops_status kiops_apply_hostloop(kiops_ctx c, const double *const *u, const dou
         if ((s = launch_plain(c, (void *)k_q_apply, QG, 256, 0, &P)) != KIOPS_OK) return s;
         CK(cudaLaunchKernel((void *)k_q_dots, dim3(QG, P.q), dim3(256), args, 0, c->stream), "k_q_dots");
         if ((s = launch_plain(c, (void *)k_q_finalize, 1, 256, 0, &P)) != KIOPS_OK) return s;
-      } else if (c->op.kind == KIOPS_OP_CSR) {
-        if ((s = launch_plain(c, (void *)k_csr_form, c->L.grid_form, 256, 0, &P)) != KIOPS_OK) return s;
-        if ((s = launch_plain(c, (void *)k_sell_spmv, c->L.grid_pass, 256, 0, &P)) != KIOPS_OK) return s;
       } else if (c->finner) {
         void *args[] = {&P};
         CK(cudaLaunchCooperativeKernel(c->finner, dim3(c->L.grid_pass), dim3(c->L.block_pass), args, c->L.smem_pass,
                                        c->stream),
            "cudaLaunchCooperativeKernel inner");
+      } else if (c->op.kind == KIOPS_OP_CSR) {
+        if ((s = launch_plain(c, (void *)k_csr_form, c->L.grid_form, 256, 0, &P)) != KIOPS_OK) return s;
+        if ((s = launch_plain(c, (void *)k_sell_spmv, c->L.grid_pass, 256, 0, &P)) != KIOPS_OK) return s;
       } else {
         if ((s = launch_plain(c, c->fpass, c->L.grid_pass, c->L.block_pass, c->L.smem_pass, &P)) != KIOPS_OK) return s;
       }

@@ -54,6 +54,7 @@ struct DevState {
   int bc_accept, bc_ntau;        // controller-cluster broadcast (CTA 0 -> all CTAs)
   unsigned int bar_count, bar_gen;  // launch-start grid barrier of the persistent inner loop (inner.cuh)
   unsigned long long pass_count;    // per-pass arrivals of the persistent inner loop (monotonic)
+  unsigned int bar2_count, bar2_gen;  // in-pass grid barrier of the persistent CSR loop (form -> SpMV)
 };
 
 // Frozen per-ctx parameters, passed BY VALUE to every kernel (graph node params).

@@ -486,3 +486,11 @@ def test_many_output_times(which, n_out, task1):
     T_end = float(c["T"][-1])
     c["T"] = np.sort(np.r_[T_end * rng.uniform(0.02, 0.98, n_out - 1), T_end])
     assert_replay_parity_opts(c, task1=task1)
+
+
+# The persistent CSR inner loop (small matrices) and the per-pass CSR kernels: both against the oracle.
+@pytest.mark.parametrize("persist", ["0", "1"])
+@pytest.mark.parametrize("dims", [(40, 40, 40), (33, 17, 29), (12, 11, 3)])
+def test_csr_persistent_and_per_pass(dims, persist, monkeypatch):
+    monkeypatch.setenv("KIOPS_CSR_PERSIST", persist)
+    assert_parity(W.config5(*dims))
