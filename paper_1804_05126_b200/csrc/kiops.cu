@@ -454,7 +454,10 @@ static kiops_status build_graph(kiops_ctx c) {
   // forces per-pass launches / the persistent loop
   if (P.q == 2 && c->op.kind == KIOPS_OP_CSR && !(pe && pe[0] == '0')) {
     const char *ce = getenv("KIOPS_CSR_PERSIST");
-    const bool want = ce ? ce[0] != '0' : (c->P.N <= (1LL << 20));
+    // default: matrices whose pass streams <= 64 MB (12 bytes per nonzero + 8 vectors), i.e. a pass of at
+    // most ~15 us, the order of the per-pass launch overhead it removes
+    const long long pass_bytes = 12LL * (long long)c->op.nnz + 64LL * c->P.N;
+    const bool want = ce ? ce[0] != '0' : (pass_bytes <= (64LL << 20));
     if (want) {
       int dev = 0, sms = 0, per_sm = 0;
       CK(cudaGetDevice(&dev), "cudaGetDevice");
