@@ -61,7 +61,9 @@ bool use_padded(const kiops_operator_desc *op, int p, const kiops_options *o) {
 #define T1D 1, 256, 1, 1
 #define T2D 2, 64, 16, 1
 #define T3D 3, 32, 8, 4
+#ifndef L2YC
 #define L2YC 8
+#endif
 #ifndef Q3Y
 #define Q3Y 7   // lock-step 3D pass: max tile rows (config 4 bands: 6-7 rows)
 #endif
