@@ -86,6 +86,7 @@ struct Layout {
   int block_pass;
   int nh3 = 1;  // 3D pair pass: z-parts per CTA
   int w2d = 8;  // 2D async pass: warps per CTA
+  int yc2d = L2YC;  // 2D lazy pass: rows a warp's strip marches (8; 4 / 2 for small grids)
   size_t smem_pass;
 };
 
@@ -163,7 +164,14 @@ Layout layout(const kiops_operator_desc *op, int p, const kiops_options *o) {
     case KIOPS_OP_STENCIL1D3:
     case KIOPS_OP_STENCIL2D5:
       if (op->nx % 2 == 0 && p <= 4) {  // warp-strip lazy kernel (16-byte pairs)
-        const int yc = L2YC;
+        // strip height: 8 rows; small grids take 4 or 2 so that more warps march shorter strips (the
+        // pass of a small grid is the latency of one warp's march: config 2 passes 0.120 -> 0.091 ms
+        // per call with 2 rows; from ~2^19 points the halo rows' extra loads cost more than they gain,
+        // and 1024^2 needs 8 to stay one co-resident grid).  KIOPS_2D_YC=2|4|8 forces.
+        const char *ey = getenv("KIOPS_2D_YC");
+        const int yc = (ey && (atoi(ey) == 2 || atoi(ey) == 4 || atoi(ey) == 8)) ? atoi(ey)
+                     : (N <= (1LL << 17) ? 2 : N <= (1LL << 19) ? 4 : L2YC);
+        L.yc2d = yc;
         const long long strips = (op->nx + 59) / 60 * ((op->ny + yc - 1) / yc);
         const char *ev = getenv("KIOPS_2D_ASYNC");  // 0: register-prefetch body (A/B switch)
         // warps per CTA: 16 (one 512-thread CTA per SM: half the per-CTA dot records to gather
@@ -374,21 +382,21 @@ static kiops_status build_graph(kiops_ctx c) {
 
   void *fpass = nullptr;
   const bool lazy2d = c->op.nx % 2 == 0 && c->p <= 4;
+// a 2D kernel instantiation by p (0..4) and strip height (Layout::yc2d); VA: the remaining template arguments
+#define SEL2D_P(FN, YC, ...)                                                                                         \
+  (c->p == 0 ? (void *)FN<YC, 0, __VA_ARGS__> : c->p == 1 ? (void *)FN<YC, 1, __VA_ARGS__>                           \
+   : c->p == 2 ? (void *)FN<YC, 2, __VA_ARGS__> : c->p == 3 ? (void *)FN<YC, 3, __VA_ARGS__> : (void *)FN<YC, 4, __VA_ARGS__>)
+#define SEL2D(FN, ...)                                                                                               \
+  (c->L.yc2d == 2 ? SEL2D_P(FN, 2, __VA_ARGS__) : c->L.yc2d == 4 ? SEL2D_P(FN, 4, __VA_ARGS__) : SEL2D_P(FN, L2YC, __VA_ARGS__))
   switch (c->op.kind) {
     case KIOPS_OP_STENCIL1D3:
     case KIOPS_OP_STENCIL2D5:
       if (lazy2d && c->L.smem_pass == 0)  // strip height 8, 2 CTAs/SM: measured best of YC 4/8/16 and 2-3 CTAs/SM
-        fpass = c->p == 0 ? (void *)k_pass_2d_lazy<L2YC, 0, 2> : c->p == 1 ? (void *)k_pass_2d_lazy<L2YC, 1, 2>
-              : c->p == 2 ? (void *)k_pass_2d_lazy<L2YC, 2, 2> : c->p == 3 ? (void *)k_pass_2d_lazy<L2YC, 3, 2>
-                          : (void *)k_pass_2d_lazy<L2YC, 4, 2>;
+        fpass = SEL2D(k_pass_2d_lazy, 2);
       else if (lazy2d && c->L.w2d == 16)
-        fpass = c->p == 0 ? (void *)k_pass_2d_lazy<L2YC, 0, 1, 2, 512> : c->p == 1 ? (void *)k_pass_2d_lazy<L2YC, 1, 1, 2, 512>
-              : c->p == 2 ? (void *)k_pass_2d_lazy<L2YC, 2, 1, 2, 512> : c->p == 3 ? (void *)k_pass_2d_lazy<L2YC, 3, 1, 2, 512>
-                          : (void *)k_pass_2d_lazy<L2YC, 4, 1, 2, 512>;
+        fpass = SEL2D(k_pass_2d_lazy, 1, 2, 512);
       else if (lazy2d)  // cp.async ring, 2 rows in flight per warp
-        fpass = c->p == 0 ? (void *)k_pass_2d_lazy<L2YC, 0, 2, 2> : c->p == 1 ? (void *)k_pass_2d_lazy<L2YC, 1, 2, 2>
-              : c->p == 2 ? (void *)k_pass_2d_lazy<L2YC, 2, 2, 2> : c->p == 3 ? (void *)k_pass_2d_lazy<L2YC, 3, 2, 2>
-                          : (void *)k_pass_2d_lazy<L2YC, 4, 2, 2>;
+        fpass = SEL2D(k_pass_2d_lazy, 2, 2);
       else
         fpass = c->op.kind == KIOPS_OP_STENCIL1D3 ? (void *)k_pass_stencil<T1D> : (void *)k_pass_stencil<T2D>;
       break;
@@ -419,17 +427,11 @@ static kiops_status build_graph(kiops_ctx c) {
   const char *pe = getenv("KIOPS_PERSIST");
   if (P.q == 2 && !(pe && pe[0] == '0')) {
     if (lazy2d && (c->op.kind == KIOPS_OP_STENCIL1D3 || c->op.kind == KIOPS_OP_STENCIL2D5) && c->L.smem_pass == 0)
-      finner = c->p == 0 ? (void *)k_inner_2d_lazy<L2YC, 0, 2> : c->p == 1 ? (void *)k_inner_2d_lazy<L2YC, 1, 2>
-             : c->p == 2 ? (void *)k_inner_2d_lazy<L2YC, 2, 2> : c->p == 3 ? (void *)k_inner_2d_lazy<L2YC, 3, 2>
-                         : (void *)k_inner_2d_lazy<L2YC, 4, 2>;
+      finner = SEL2D(k_inner_2d_lazy, 2);
     else if (lazy2d && (c->op.kind == KIOPS_OP_STENCIL1D3 || c->op.kind == KIOPS_OP_STENCIL2D5) && c->L.w2d == 16)
-      finner = c->p == 0 ? (void *)k_inner_2d_lazy<L2YC, 0, 1, 2, 512> : c->p == 1 ? (void *)k_inner_2d_lazy<L2YC, 1, 1, 2, 512>
-             : c->p == 2 ? (void *)k_inner_2d_lazy<L2YC, 2, 1, 2, 512> : c->p == 3 ? (void *)k_inner_2d_lazy<L2YC, 3, 1, 2, 512>
-                         : (void *)k_inner_2d_lazy<L2YC, 4, 1, 2, 512>;
+      finner = SEL2D(k_inner_2d_lazy, 1, 2, 512);
     else if (lazy2d && (c->op.kind == KIOPS_OP_STENCIL1D3 || c->op.kind == KIOPS_OP_STENCIL2D5))
-      finner = c->p == 0 ? (void *)k_inner_2d_lazy<L2YC, 0, 2, 2> : c->p == 1 ? (void *)k_inner_2d_lazy<L2YC, 1, 2, 2>
-             : c->p == 2 ? (void *)k_inner_2d_lazy<L2YC, 2, 2, 2> : c->p == 3 ? (void *)k_inner_2d_lazy<L2YC, 3, 2, 2>
-                         : (void *)k_inner_2d_lazy<L2YC, 4, 2, 2>;
+      finner = SEL2D(k_inner_2d_lazy, 2, 2);
     else if (c->L.padded)
       finner = c->p == 0 ? (void *)k_inner_3d_rc<0> : c->p == 1 ? (void *)k_inner_3d_rc<1> : c->p == 2 ? (void *)k_inner_3d_rc<2>
              : c->p == 3 ? (void *)k_inner_3d_rc<3> : (void *)k_inner_3d_rc<4>;
