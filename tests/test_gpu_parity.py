@@ -494,3 +494,20 @@ def test_many_output_times(which, n_out, task1):
 def test_csr_persistent_and_per_pass(dims, persist, monkeypatch):
     monkeypatch.setenv("KIOPS_CSR_PERSIST", persist)
     assert_parity(W.config5(*dims))
+
+
+# Every strip height of the 2D lazy pass (2 / 4 / 8 rows, chosen by grid size at create or forced),
+# with the 8- and 16-warp CTAs; and a grid in the 4-row range of the default rule.
+@pytest.mark.parametrize("yc", ["2", "4", "8"])
+@pytest.mark.parametrize("warps", ["8", "16"])
+def test_2d_strip_heights(yc, warps, monkeypatch):
+    monkeypatch.setenv("KIOPS_2D_YC", yc)
+    monkeypatch.setenv("KIOPS_2D_WARPS", warps)
+    assert_parity(W.config3(200, 72))
+    assert_replay_parity(_cfg2d(2, 64, 50, 2, 11))
+    assert_parity(W.config1())
+
+
+def test_2d_default_strip_height_mid_size():
+    assert_parity(W.config3(512, 400))   # 2^17 < N <= 2^19: 4-row strips
+    assert_parity(W.config2(600, 500))
