@@ -19,4 +19,8 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_in
   -o gpurun_out/${R}_c4_inner -f python scripts/profile_run.py --config 4 > gpurun_out/${R}_c4_ncu_full.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_inner_2d -s 2 -c 1 \
   -o gpurun_out/${R}_c3_inner -f python scripts/profile_run.py --config 3 > gpurun_out/${R}_c3_ncu_full.log 2>&1
+# summaries on the box (the two reports together exceed what gpurun brings back); KEEP_REPS=1 keeps them
+python scripts/ncu_summary.py gpurun_out/${R}_c4_inner.ncu-rep 20 > gpurun_out/${R}_c4_inner_summary.txt 2>&1
+python scripts/ncu_summary.py gpurun_out/${R}_c3_inner.ncu-rep 20 > gpurun_out/${R}_c3_inner_summary.txt 2>&1
+[ "${KEEP_REPS:-0}" = "1" ] || rm -f gpurun_out/${R}_c4_inner.ncu-rep gpurun_out/${R}_c3_inner.ncu-rep
 echo done
